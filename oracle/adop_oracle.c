@@ -1,0 +1,563 @@
+/*
+ * adop_oracle.c -- plain, slow, single-threaded CPU oracle of ADOP's one-pixel
+ * point rasterizer (Rückert, Franke, Stamminger: "ADOP: Approximate
+ * Differentiable One-Pixel Point Rendering", arXiv 2110.06635).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path may import, link or
+ * execute this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs use it.  It shares no code, header,
+ * table or constant generator with paper_2110_06635_b200/csrc/; the CUDA path
+ * and this file were written separately against the readings R1..R27 listed
+ * in DESIGN.md.
+ *
+ * Citations: "P:Lnnn" = /root/reference/PAPER.md line nnn (section/equation
+ * named alongside).  Readings "Rnn" = DESIGN.md §Readings.
+ *
+ * Precision: every quantity that DECIDES an integer (pixel index, bounds,
+ * depth key, discard/ghost bits, fuzzy-test and Eq. 11 case choices) is
+ * computed in IEEE fp32 with the pinned operation order of R1/R2/R6/R9/R10/R14
+ * (compile with -ffp-contract=off, no fast-math), because the task requires
+ * both sides to take such decisions in the same precision.  Every continuous
+ * result (blend sums, means, gradients, Jacobians) is accumulated in fp64.
+ *
+ * Loops follow the paper's order: per view, per layer/point: project (Eq. 2),
+ * round (Eq. 3), bounds (Eq. 4), stochastic discard (Eq. 12), depth-only pass
+ * (§4.5), fuzzy test (Eq. 6), blend mean (Eq. 7); backward: texture gradient
+ * (§4.2 "straightforward"), ghost image-space gradient (Eqs. 9-11, §4.3),
+ * chain rule to points and tangent-space pose (Eq. 8, Eq. 17).
+ *
+ * Parity pins: tests/test_oracle_*.py (closed forms, brute force, finite
+ * differences, worked values).  Parity unpinned: none of the functions below
+ * is unpinned; the *usefulness* of ghost gradients (paper §6.2) is not a
+ * parity claim.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+
+typedef struct {
+    int32_t width, height, model; /* model 0 = pinhole, 1 = OpenCV rational 8-coefficient (R6) */
+    float fx, fy, cx, cy;
+    float k[6];
+    float p[2];
+    float r2_max;
+} orc_camera;
+
+typedef struct {
+    float R[9]; /* world -> camera rotation, row-major: Xc = R x + t (Eq. 2) */
+    float t[3];
+} orc_pose;
+
+typedef struct {
+    int32_t layers;
+    float alpha;        /* fuzzy depth threshold, Eq. 6 */
+    int32_t discard;    /* stochastic point discarding on/off, §4.4 */
+    float gamma;        /* Eq. 12 */
+    float ghost_rate;   /* dropout rate of the ghost split, §4.3 (R13) */
+    float z_near;       /* R7 */
+    uint64_t seed;
+    int32_t view_id_base;
+} orc_params;
+
+typedef struct {
+    int64_t n;
+    int64_t global_offset; /* global index of point 0 (R25) */
+    int64_t pos_stride;    /* x row at pos[0..n), y row at pos[stride..], z row at pos[2*stride..] */
+    const float *pos;
+    const float *radius;   /* [n] or NULL -> radius_uniform */
+    float radius_uniform;
+    const float *feat;     /* [n][C] */
+    int32_t channels;
+} orc_points;
+
+#define ORC_SENTINEL 0x7FFFFFFFFFFFFFFFULL /* R8: empty pixel */
+#define ORC_STREAM_GHOST 1u
+#define ORC_STREAM_DISCARD 2u
+
+/* ------------------------------------------------------------------------- */
+/* Layer geometry (R5): w_l = ceil(w / 2^l), h_l = ceil(h / 2^l).             */
+/* ------------------------------------------------------------------------- */
+static int32_t layer_w(int32_t w, int l) { return (int32_t)((w + (1 << l) - 1) >> l); }
+
+int64_t orc_pyramid_pixels(int32_t w, int32_t h, int32_t layers)
+{
+    int64_t total = 0;
+    for (int l = 0; l < layers; ++l) total += (int64_t)layer_w(w, l) * layer_w(h, l);
+    return total;
+}
+
+static int64_t layer_offset(int32_t w, int32_t h, int l)
+{
+    return orc_pyramid_pixels(w, h, l);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Counter-based hash (R11, R13).  Both sides implement this same published  */
+/* integer finalizer independently (the task allows "each side implements    */
+/* the same counter-based generator").                                       */
+/* ------------------------------------------------------------------------- */
+static uint32_t mix32(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+static uint32_t stream_salt(uint64_t seed, uint32_t stream, uint32_t view)
+{
+    uint32_t s = mix32((uint32_t)seed + 0x9E3779B9U * (stream + 1U));
+    s = mix32(s ^ (uint32_t)(seed >> 32));
+    return mix32(s + 0x85EBCA6BU * (view + 1U));
+}
+
+/* Top 24 bits of the hash of global point index i for (seed, stream, view). */
+uint32_t orc_h24(uint64_t seed, uint32_t stream, uint32_t view, uint32_t i)
+{
+    return mix32(i ^ stream_salt(seed, stream, view)) >> 8;
+}
+
+static uint32_t ghost_threshold(float rate)
+{
+    /* floor(rho * 2^24); rho in [0,1) */
+    return (uint32_t)floor((double)rate * 16777216.0);
+}
+
+/* R13: point is a ghost (dropout set of §4.3). */
+int orc_is_ghost(const orc_params *pr, uint32_t gi)
+{
+    uint32_t thr = ghost_threshold(pr->ghost_rate);
+    return thr != 0 && orc_h24(pr->seed, ORC_STREAM_GHOST, 0u, gi) < thr;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Projection P_0 = C(R x + t)   (Eq. 2; camera model R6)        */
+/* Pinned fp32 order (R1, R2, R6).  Returns 1 if the point is valid (R7).    */
+/* out: [0..2] = Xc, [3] = u0, [4] = v0, [5] = 1/z                            */
+/* ------------------------------------------------------------------------- */
+int orc_project(const orc_camera *c, const orc_pose *P, float x, float y, float z, float z_near, float *out)
+{
+    const float *R = P->R, *t = P->t;
+    float X = ((R[0] * x + R[1] * y) + R[2] * z) + t[0];
+    float Y = ((R[3] * x + R[4] * y) + R[5] * z) + t[1];
+    float Z = ((R[6] * x + R[7] * y) + R[8] * z) + t[2];
+    out[0] = X; out[1] = Y; out[2] = Z;
+    if (!(Z > z_near && Z <= FLT_MAX)) return 0; /* behind camera / non-finite: culled (R7) */
+    float iz = 1.0f / Z;
+    float xn = X * iz, yn = Y * iz;
+    float xd = xn, yd = yn;
+    if (c->model == 1) {
+        float xx = xn * xn, yy = yn * yn, xy = xn * yn;
+        float r2 = xx + yy;
+        if (!(r2 <= c->r2_max)) return 0; /* outside the camera's valid radius (R6) */
+        float r4 = r2 * r2, r6 = r4 * r2;
+        float num = ((1.0f + c->k[0] * r2) + c->k[1] * r4) + c->k[2] * r6;
+        float den = ((1.0f + c->k[3] * r2) + c->k[4] * r4) + c->k[5] * r6;
+        if (!(den > 0.0f)) return 0;
+        float radial = num / den;
+        float a1 = 2.0f * xy;
+        float a2 = r2 + 2.0f * xx;
+        float a3 = r2 + 2.0f * yy;
+        xd = (xn * radial + c->p[0] * a1) + c->p[1] * a2;
+        yd = (yn * radial + c->p[0] * a3) + c->p[1] * a1;
+    }
+    out[3] = c->fx * xd + c->cx;
+    out[4] = c->fy * yd + c->cy;
+    out[5] = iz;
+    return 1;
+}
+
+/* Eq. 3 + Eq. 4: round half away from zero (R3) and
+ * bounds-test the rounded float.  Returns the layer-local linear index or -1. */
+static int64_t layer_pixel(const orc_camera *c, float u0, float v0, int l)
+{
+    float s = ldexpf(1.0f, -l);         /* 1/2^l of Eq. 2 */
+    float ru = roundf(u0 * s), rv = roundf(v0 * s);
+    int32_t wl = layer_w(c->width, l), hl = layer_w(c->height, l);
+    if (!(ru >= 0.0f && ru < (float)wl && rv >= 0.0f && rv < (float)hl)) return -1;
+    return (int64_t)rv * wl + (int64_t)ru;
+}
+
+/* Eq. 12, R10/R11: number of leading layers at which the point is
+ * kept.  keep_l <=> (gamma * r_screen_l)^2 > 1 - beta, beta per (view, point). */
+static int keep_layers(const orc_params *pr, const orc_camera *c, float rw, float iz, uint32_t view, uint32_t gi)
+{
+    if (!pr->discard) return pr->layers;
+    float feff = (c->fx + c->fy) * 0.5f;
+    float rs0 = (rw * feff) * iz;                      /* r_world projected to pixels, layer 0 */
+    uint32_t h = orc_h24(pr->seed, ORC_STREAM_DISCARD, view, gi);
+    float one_minus_beta = (float)(16777216u - h) * (1.0f / 16777216.0f);
+    int l;
+    for (l = 0; l < pr->layers; ++l) {
+        float rl = rs0 * ldexpf(1.0f, -l);
+        float a = pr->gamma * rl;
+        if (!(a * a > one_minus_beta)) break;
+    }
+    return l;
+}
+
+static float point_radius(const orc_points *pts, int64_t i)
+{
+    return pts->radius ? pts->radius[i] : pts->radius_uniform;
+}
+
+/* Per point, per view: bit l = valid & in-bounds at l & kept at l (discard);
+ * bit 7 = ghost.  The render set at layer l is bit l and not bit 7. */
+static unsigned point_mask(const orc_points *pts, int64_t i, const orc_camera *c, const orc_pose *P,
+                           const orc_params *pr, uint32_t view, int64_t *pix /*[layers]*/, float *proj /*[6]*/)
+{
+    uint32_t gi = (uint32_t)(pts->global_offset + i);
+    const float *pos = pts->pos;
+    float x = pos[i], y = pos[pts->pos_stride + i], z = pos[2 * pts->pos_stride + i];
+    unsigned m = orc_is_ghost(pr, gi) ? 0x80u : 0u;
+    if (!orc_project(c, P, x, y, z, pr->z_near, proj)) return m;
+    int nk = keep_layers(pr, c, point_radius(pts, i), proj[5], view, gi);
+    for (int l = 0; l < pr->layers; ++l) {
+        pix[l] = layer_pixel(c, proj[3], proj[4], l);
+        if (l < nk && pix[l] >= 0) m |= 1u << l;
+    }
+    return m;
+}
+
+void orc_point_masks(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
+                     const orc_params *pr, uint8_t *mask /*[V][n]*/)
+{
+    int64_t pix[8];
+    float proj[6];
+    for (int v = 0; v < n_views; ++v)
+        for (int64_t i = 0; i < pts->n; ++i)
+            mask[(int64_t)v * pts->n + i] =
+                (uint8_t)point_mask(pts, i, &cams[v], &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
+}
+
+static uint64_t depth_key(float Z, uint32_t gi)
+{
+    uint32_t zb;
+    memcpy(&zb, &Z, 4);
+    return ((uint64_t)zb << 32) | gi; /* R8 */
+}
+
+static float key_depth(uint64_t key)
+{
+    uint32_t zb = (uint32_t)(key >> 32);
+    float m;
+    memcpy(&m, &zb, 4);
+    return m;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Forward pass 1: depth-only render pass (§4.5) = per-pixel min of  */
+/* the packed keys over the render set (Eq. 6's min_z with R8 tie rule).     */
+/* keys: [V][P], set to the sentinel first.                                  */
+/* ------------------------------------------------------------------------- */
+void orc_forward_depth(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
+                       const orc_params *pr, uint64_t *keys)
+{
+    int64_t pix[8];
+    float proj[6];
+    for (int v = 0; v < n_views; ++v) {
+        const orc_camera *c = &cams[v];
+        int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
+        uint64_t *kv = keys + (int64_t)v * P;
+        for (int64_t p = 0; p < P; ++p) kv[p] = ORC_SENTINEL;
+        for (int64_t i = 0; i < pts->n; ++i) {
+            unsigned m = point_mask(pts, i, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
+            if (m & 0x80u) continue; /* ghosts are not rendered */
+            uint64_t key = depth_key(proj[2], (uint32_t)(pts->global_offset + i));
+            for (int l = 0; l < pr->layers; ++l) {
+                if (!(m & (1u << l))) continue;
+                int64_t q = layer_offset(c->width, c->height, l) + pix[l];
+                if (key < kv[q]) kv[q] = key;
+            }
+        }
+    }
+}
+
+/* Fuzzy depth test, Eq. 6, pinned as R9: z <= fl(fl(1+alpha) * m). */
+static int fuzzy_pass(float z, uint64_t key, float alpha)
+{
+    float onepa = 1.0f + alpha;
+    float thr = onepa * key_depth(key);
+    return z <= thr;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Forward pass 2: accumulate tau and |Lambda| for points passing the fuzzy  */
+/* test (§4.5).  accum [V][P][C] fp64, count [V][P] fp64; both   */
+/* are zeroed first.                                                         */
+/* ------------------------------------------------------------------------- */
+void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
+                       const orc_params *pr, const uint64_t *keys, double *accum, double *count)
+{
+    int64_t pix[8];
+    float proj[6];
+    const int C = pts->channels;
+    for (int v = 0; v < n_views; ++v) {
+        const orc_camera *c = &cams[v];
+        int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
+        const uint64_t *kv = keys + (int64_t)v * P;
+        double *av = accum + (int64_t)v * P * C;
+        double *cv = count + (int64_t)v * P;
+        memset(av, 0, sizeof(double) * (size_t)(P * C));
+        memset(cv, 0, sizeof(double) * (size_t)P);
+        for (int64_t i = 0; i < pts->n; ++i) {
+            unsigned m = point_mask(pts, i, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
+            if (m & 0x80u) continue;
+            for (int l = 0; l < pr->layers; ++l) {
+                if (!(m & (1u << l))) continue;
+                int64_t q = layer_offset(c->width, c->height, l) + pix[l];
+                if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
+                for (int ch = 0; ch < C; ++ch) av[q * C + ch] += (double)pts->feat[i * C + ch];
+                cv[q] += 1.0;
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Forward pass 3: Eq. 7: mean of tau over Lambda, or the       */
+/* background E (constant vector, R18) when Lambda is empty.  image layout:  */
+/* [V][C*P], layer l planar [C][h_l][w_l] starting at C*off_l.               */
+/* ------------------------------------------------------------------------- */
+void orc_forward_resolve(int32_t n_views, const orc_camera *cams, const orc_params *pr, int32_t C,
+                         const double *accum, const double *count, const float *bg, double *image)
+{
+    for (int v = 0; v < n_views; ++v) {
+        const orc_camera *c = &cams[v];
+        int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
+        for (int l = 0; l < pr->layers; ++l) {
+            int64_t off = layer_offset(c->width, c->height, l);
+            int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
+            for (int64_t j = 0; j < hw; ++j) {
+                int64_t q = off + j;
+                double n = count[(int64_t)v * P + q];
+                for (int ch = 0; ch < C; ++ch) {
+                    double val = n > 0.0 ? accum[((int64_t)v * P + q) * C + ch] / n : (bg ? (double)bg[ch] : 0.0);
+                    image[(int64_t)v * C * P + C * off + ch * hw + j] = val;
+                }
+            }
+        }
+    }
+}
+
+/* Full forward: Eq. 1 I_l = Phi_l(...) for all layers and views. */
+void orc_forward(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
+                 const orc_params *pr, const float *bg, uint64_t *keys, double *accum, double *count, double *image)
+{
+    orc_forward_depth(pts, n_views, cams, poses, pr, keys);
+    orc_forward_blend(pts, n_views, cams, poses, pr, keys, accum, count);
+    orc_forward_resolve(n_views, cams, pr, pts->channels, accum, count, bg, image);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Eq. 11 with reading R14: induced change of neighbour pixel q */
+/* when the ghost (descriptor tau, depth z) is virtually shifted onto q.     */
+/* Returns the case number 1..4.                                             */
+/* ------------------------------------------------------------------------- */
+int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double n_q, uint64_t key_q,
+                       const double *I_q, double *delta)
+{
+    float onepa = 1.0f + alpha;
+    float m_q = key_depth(key_q);
+    int kase;
+    if (n_q == 0.0) kase = 1;                       /* background neighbour */
+    else if (z > onepa * m_q) kase = 2;             /* shifted point fully behind */
+    else if (z * onepa < m_q) kase = 3;             /* shifted point fully in front */
+    else kase = 4;                                  /* fuzzy co-visible: blend mean changes */
+    for (int ch = 0; ch < C; ++ch) {
+        double t = (double)tau[ch];
+        switch (kase) {
+        case 1: case 3: delta[ch] = t - I_q[ch]; break;
+        case 2: delta[ch] = 0.0; break;
+        default: delta[ch] = (n_q * I_q[ch] + t) / (n_q + 1.0) - I_q[ch]; break;
+        }
+    }
+    return kase;
+}
+
+/* Projection Jacobian d(u0,v0)/dXc (R21), fp64 at the fp32 camera point.   */
+void orc_jacobian(const orc_camera *c, const float *Xc, double *J /* 2x3 row-major */)
+{
+    double X = Xc[0], Y = Xc[1], Z = Xc[2];
+    double xn = X / Z, yn = Y / Z;
+    /* dn/dXc = [[1/Z, 0, -X/Z^2], [0, 1/Z, -Y/Z^2]] */
+    double N[2][3] = {{1.0 / Z, 0.0, -X / (Z * Z)}, {0.0, 1.0 / Z, -Y / (Z * Z)}};
+    double D[2][2] = {{1.0, 0.0}, {0.0, 1.0}};
+    if (c->model == 1) {
+        const double k1 = c->k[0], k2 = c->k[1], k3 = c->k[2], k4 = c->k[3], k5 = c->k[4], k6 = c->k[5];
+        const double p1 = c->p[0], p2 = c->p[1];
+        double r2 = xn * xn + yn * yn;
+        double num = 1.0 + k1 * r2 + k2 * r2 * r2 + k3 * r2 * r2 * r2;
+        double den = 1.0 + k4 * r2 + k5 * r2 * r2 + k6 * r2 * r2 * r2;
+        double dnum = k1 + 2.0 * k2 * r2 + 3.0 * k3 * r2 * r2;
+        double dden = k4 + 2.0 * k5 * r2 + 3.0 * k6 * r2 * r2;
+        double rad = num / den;
+        double drad = (dnum * den - num * dden) / (den * den); /* d radial / d r2 */
+        D[0][0] = rad + 2.0 * xn * xn * drad + 2.0 * p1 * yn + 6.0 * p2 * xn;
+        D[0][1] = 2.0 * xn * yn * drad + 2.0 * p1 * xn + 2.0 * p2 * yn;
+        D[1][0] = 2.0 * xn * yn * drad + 2.0 * p1 * xn + 2.0 * p2 * yn;
+        D[1][1] = rad + 2.0 * yn * yn * drad + 6.0 * p1 * yn + 2.0 * p2 * xn;
+    }
+    double f[2] = {c->fx, c->fy};
+    for (int r = 0; r < 2; ++r)
+        for (int k = 0; k < 3; ++k)
+            J[r * 3 + k] = f[r] * (D[r][0] * N[0][k] + D[r][1] * N[1][k]);
+}
+
+/* Continuous fp64 projection (same camera model) -- used only to check the
+ * Jacobian by finite differences. */
+void orc_project_f64(const orc_camera *c, const double *Xc, double *uv)
+{
+    double xn = Xc[0] / Xc[2], yn = Xc[1] / Xc[2];
+    double xd = xn, yd = yn;
+    if (c->model == 1) {
+        double r2 = xn * xn + yn * yn;
+        double num = 1.0 + c->k[0] * r2 + c->k[1] * r2 * r2 + c->k[2] * r2 * r2 * r2;
+        double den = 1.0 + c->k[3] * r2 + c->k[4] * r2 * r2 + c->k[5] * r2 * r2 * r2;
+        double rad = num / den;
+        xd = xn * rad + 2.0 * c->p[0] * xn * yn + c->p[1] * (r2 + 2.0 * xn * xn);
+        yd = yn * rad + c->p[0] * (r2 + 2.0 * yn * yn) + 2.0 * c->p[1] * xn * yn;
+    }
+    uv[0] = c->fx * xd + c->cx;
+    uv[1] = c->fy * yd + c->cy;
+}
+
+/* Ghost image-space gradient at layer l, pixel (u,v) (Eqs. 9-11, R14-R16):
+ * g = (g_u, g_v) in layer-l pixels; gabs = per-direction sums of |G.Delta|/2. */
+static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, int64_t local, int32_t C,
+                             const float *tau, float z, const uint64_t *kv, const double *cv, const double *img,
+                             const float *Gv, int64_t P, double *g, double *gabs)
+{
+    int32_t wl = layer_w(c->width, l), hl = layer_w(c->height, l);
+    int64_t off = layer_offset(c->width, c->height, l);
+    int64_t hw = (int64_t)wl * hl;
+    int64_t u = local % wl, vv = local / wl;
+    static const int du[4] = {+1, -1, 0, 0}, dv[4] = {0, 0, +1, -1};
+    double d[4], dabs[4];
+    double Iq[32], delta[32];
+    (void)P;
+    for (int k = 0; k < 4; ++k) {
+        int64_t qu = u + du[k], qv = vv + dv[k];
+        d[k] = 0.0; dabs[k] = 0.0;
+        if (qu < 0 || qu >= wl || qv < 0 || qv >= hl) continue; /* neighbour outside: no term (R14) */
+        int64_t qj = qv * wl + qu;
+        for (int ch = 0; ch < C; ++ch) Iq[ch] = img[C * off + ch * hw + qj];
+        orc_induced_change(C, tau, z, pr->alpha, cv[off + qj], kv[off + qj], Iq, delta);
+        for (int ch = 0; ch < C; ++ch) {
+            double gq = (double)Gv[C * off + ch * hw + qj];
+            d[k] += gq * delta[ch];
+            dabs[k] += fabs(gq * delta[ch]);
+        }
+    }
+    g[0] = 0.5 * (d[0] - d[1]);   /* Eq. 10 with the signed central difference (R15) */
+    g[1] = 0.5 * (d[2] - d[3]);
+    gabs[0] = 0.5 * dabs[0]; gabs[1] = 0.5 * dabs[1];
+    gabs[2] = 0.5 * dabs[2]; gabs[3] = 0.5 * dabs[3];
+}
+
+/* ------------------------------------------------------------------------- */
+/* Backward.  Inputs: the forward's keys/count/image (re-render) and */
+/* the upstream gradient G = dL/dI (image layout).  Outputs (overwritten):   */
+/*   dtau [n][C]   texture gradient of rendered points (R24; ghosts 0)       */
+/*   dx   [3][n]   position gradient of ghost points (R17, R22; others 0)    */
+/*   dpose [V][6]  tangent-space pose gradient (w, Xc x w) (R19)             */
+/* and the per-element sums of |terms| used to scale tolerances (R20).       */
+/* Any output pointer may be NULL.                                           */
+/* ------------------------------------------------------------------------- */
+void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
+                  const orc_params *pr, const uint64_t *keys, const double *count, const double *image,
+                  const float *G, double *dtau, double *dx, double *dpose,
+                  double *dtau_abs, double *dx_abs, double *dpose_abs)
+{
+    const int C = pts->channels;
+    const int64_t n = pts->n;
+    int64_t pix[8];
+    float proj[6];
+    if (dtau) memset(dtau, 0, sizeof(double) * (size_t)(n * C));
+    if (dtau_abs) memset(dtau_abs, 0, sizeof(double) * (size_t)(n * C));
+    if (dx) memset(dx, 0, sizeof(double) * (size_t)(3 * n));
+    if (dx_abs) memset(dx_abs, 0, sizeof(double) * (size_t)(3 * n));
+    if (dpose) memset(dpose, 0, sizeof(double) * (size_t)(6 * n_views));
+    if (dpose_abs) memset(dpose_abs, 0, sizeof(double) * (size_t)(6 * n_views));
+    int64_t Gbase = 0;
+    for (int v = 0; v < n_views; ++v) {
+        const orc_camera *c = &cams[v];
+        const orc_pose *Pz = &poses[v];
+        int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
+        const uint64_t *kv = keys + (int64_t)v * P;
+        const double *cv = count + (int64_t)v * P;
+        const double *img = image + Gbase;
+        const float *Gv = G + Gbase;
+        Gbase += (int64_t)C * P;
+        for (int64_t i = 0; i < n; ++i) {
+            unsigned m = point_mask(pts, i, c, Pz, pr, (uint32_t)(pr->view_id_base + v), pix, proj);
+            if (!(m & 0x7Fu)) continue;
+            const float *tau = pts->feat + i * C;
+            if (!(m & 0x80u)) {
+                /* rendered point: texture gradient of Eq. 7, dI/dtau = 1/|Lambda| (R24) */
+                for (int l = 0; l < pr->layers; ++l) {
+                    if (!(m & (1u << l))) continue;
+                    int64_t off = layer_offset(c->width, c->height, l);
+                    int64_t q = off + pix[l];
+                    if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
+                    int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
+                    for (int ch = 0; ch < C; ++ch) {
+                        double t = (double)Gv[C * off + ch * hw + pix[l]] / cv[q];
+                        if (dtau) dtau[i * C + ch] += t;
+                        if (dtau_abs) dtau_abs[i * C + ch] += fabs(t);
+                    }
+                }
+                continue;
+            }
+            /* ghost point: image-space gradient summed over layers in layer-0 pixels (R17) */
+            double gu = 0.0, gv = 0.0, ga[4] = {0, 0, 0, 0};
+            for (int l = 0; l < pr->layers; ++l) {
+                if (!(m & (1u << l))) continue;
+                double g[2], gabs[4];
+                ghost_layer_grad(c, pr, l, pix[l], C, tau, proj[2], kv, cv, img, Gv, P, g, gabs);
+                double s = ldexp(1.0, -l);
+                gu += s * g[0]; gv += s * g[1];
+                for (int k = 0; k < 4; ++k) ga[k] += s * gabs[k];
+            }
+            double J[6];
+            orc_jacobian(c, proj, J);
+            /* w = J^T g = dL/dXc */
+            double w[3], wu[3], wv[3];
+            for (int k = 0; k < 3; ++k) {
+                w[k] = J[k] * gu + J[3 + k] * gv;
+                wu[k] = J[k];
+                wv[k] = J[3 + k];
+            }
+            const float *R = Pz->R;
+            double X[3] = {proj[0], proj[1], proj[2]};
+            for (int k = 0; k < 3; ++k) {
+                /* dx = R^T w (Xc = R x + t) */
+                double a = R[0 + k] * w[0] + R[3 + k] * w[1] + R[6 + k] * w[2];
+                double au = R[0 + k] * wu[0] + R[3 + k] * wu[1] + R[6 + k] * wu[2];
+                double av = R[0 + k] * wv[0] + R[3 + k] * wv[1] + R[6 + k] * wv[2];
+                if (dx) dx[k * n + i] += a;
+                if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * fabs(au) + (ga[2] + ga[3]) * fabs(av);
+            }
+            if (dpose || dpose_abs) {
+                /* Eq. 17 left perturbation: dXc/dxi = [I | -[Xc]x] -> (w, Xc x w) (R19) */
+                double cr[3] = {X[1] * w[2] - X[2] * w[1], X[2] * w[0] - X[0] * w[2], X[0] * w[1] - X[1] * w[0]};
+                double cu[3] = {X[1] * wu[2] - X[2] * wu[1], X[2] * wu[0] - X[0] * wu[2], X[0] * wu[1] - X[1] * wu[0]};
+                double cvv[3] = {X[1] * wv[2] - X[2] * wv[1], X[2] * wv[0] - X[0] * wv[2], X[0] * wv[1] - X[1] * wv[0]};
+                for (int k = 0; k < 3; ++k) {
+                    if (dpose) {
+                        dpose[v * 6 + k] += w[k];
+                        dpose[v * 6 + 3 + k] += cr[k];
+                    }
+                    if (dpose_abs) {
+                        dpose_abs[v * 6 + k] += (ga[0] + ga[1]) * fabs(wu[k]) + (ga[2] + ga[3]) * fabs(wv[k]);
+                        dpose_abs[v * 6 + 3 + k] += (ga[0] + ga[1]) * fabs(cu[k]) + (ga[2] + ga[3]) * fabs(cvv[k]);
+                    }
+                }
+            }
+        }
+    }
+}

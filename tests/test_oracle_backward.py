@@ -1,0 +1,245 @@
+"""Pins for the oracle's backward pass (texture gradient, Eqs. 9-11, ghosts, chain rule) -- CPU only."""
+import dataclasses
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2110_06635_b200 import scene as S
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_values.json")))
+F = np.float32
+IDENT = S.Pose(np.eye(3, dtype=F), np.zeros(3, dtype=F))
+
+
+def _cam(w, h, f, cx, cy):
+    return S.Camera(w, h, S.PINHOLE, float(F(f)), float(F(f)), float(F(cx)), float(F(cy)))
+
+
+def _at_pixel(cam, u, v, z):
+    """World point (identity pose) whose layer-0 projection rounds to pixel (u, v) at depth z."""
+    return [(u - cam.cx) * z / cam.fx, (v - cam.cy) * z / cam.fy, z]
+
+
+def arrange(render, ghost, params, feat_r, feat_g):
+    """Build a cloud whose global indices put `render` points on non-ghost ids and `ghost` points on ghost
+    ids (R13 hash), padding unused ids with points behind the camera.  -> (Points, ghost ids)."""
+    render, ghost = list(render), list(ghost)
+    feat_r, feat_g = list(feat_r), list(feat_g)
+    xyz, feat, gids = [], [], []
+    C = len((feat_r + feat_g)[0])
+    gi = 0
+    while render or ghost:
+        is_g = O.is_ghost(params, gi)
+        if is_g and ghost:
+            xyz.append(ghost.pop(0)); feat.append(feat_g.pop(0)); gids.append(gi)
+        elif not is_g and render:
+            xyz.append(render.pop(0)); feat.append(feat_r.pop(0))
+        else:
+            xyz.append([0.0, 0.0, -1.0]); feat.append([0.0] * C)
+        gi += 1
+    pos = np.asarray(xyz, dtype=F).T.copy()
+    return O.Points(pos, np.full(pos.shape[1], 0.005, F), np.asarray(feat, F)), gids
+
+
+def _grad_image(cam, L, C, fill):
+    P = O.pyramid_pixels(cam.width, cam.height, L)
+    return np.full((1, C * P), fill, dtype=F)
+
+
+# --------------------------------------------------------------------------- #
+# texture gradient (§4.2 "straightforward", R24)
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("case", GOLDEN["texture_grad"])
+def test_texture_grad_worked(case):
+    cam = _cam(16, 16, 8.0, 8.0, 8.0)
+    k = case["points_in_pixel"]
+    pts = O.Points(np.asarray([[0.0, 0.0, 2.0 + 0.001 * i] for i in range(k)], F).T.copy(),
+                   np.full(k, 0.005, F), np.full((k, 1), 0.5, F))
+    prm = S.Params(layers=1, discard=False)
+    fwd = O.forward(pts, [cam], [IDENT], prm)
+    G = _grad_image(cam, 1, 1, 0.0)
+    G[0, 8 * 16 + 8] = case["adjoint"]
+    bwd = O.backward(pts, [cam], [IDENT], prm, fwd, G)
+    assert np.allclose(bwd.dtau[:, 0], case["d_tau_each"])
+
+
+def _loss(pts, cams, poses, prm, G):
+    fwd = O.forward(pts, cams, poses, prm)
+    return float((fwd.image * G.astype(np.float64)).sum()), fwd
+
+
+def test_texture_grad_equals_finite_differences():
+    """I is linear in tau with geometry fixed, so a central FD on tau is exact up to rounding."""
+    rng = np.random.default_rng(0)
+    room = S.make_room(4.0)
+    cloud = S.room_cloud(3000, room, channels=3, seed=11)
+    cams = [S.pinhole(96, 64), S.opencv_camera(96, 64, seed=5)]
+    poses = S.room_poses(2, room, seed=3)
+    pts = O.Points.from_cloud(cloud)
+    pts = O.Points(pts.pos, np.full(pts.n, 0.03, F), pts.feat)
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.2, seed=77)
+    P = O.pyramid_pixels(96, 64, 3)
+    G = (rng.random((2, 3 * P)) * 2 - 1).astype(F)
+    L0, fwd = _loss(pts, cams, poses, prm, G)
+    bwd = O.backward(pts, cams, poses, prm, fwd, G)
+    nz = np.argwhere(bwd.dtau != 0)
+    assert len(nz) > 50
+    picks = list(nz[rng.choice(len(nz), 25, replace=False)]) + [np.argwhere(bwd.dtau == 0)[0]]
+    for i, c in picks:
+        h = F(1.0 / 1024)
+        fp, fm = pts.feat.copy(), pts.feat.copy()
+        fp[i, c] = F(fp[i, c] + h)
+        fm[i, c] = F(fm[i, c] - h)
+        Lp, _ = _loss(O.Points(pts.pos, pts.radius, fp), cams, poses, prm, G)
+        Lm, _ = _loss(O.Points(pts.pos, pts.radius, fm), cams, poses, prm, G)
+        fd = (Lp - Lm) / (float(fp[i, c]) - float(fm[i, c]))
+        assert abs(fd - bwd.dtau[i, c]) < 1e-9 * max(1.0, abs(fd)), (i, c, fd, bwd.dtau[i, c])
+
+
+# --------------------------------------------------------------------------- #
+# Eq. 11 (R14)
+# --------------------------------------------------------------------------- #
+def _key(m, idx=0):
+    if m is None:
+        return O.SENTINEL
+    return (int(np.array([m], F).view(np.uint32)[0]) << 32) | idx
+
+
+@pytest.mark.parametrize("case", GOLDEN["eq11"])
+def test_eq11_worked_values(case):
+    kase, d = O.induced_change([case["tau"]], case["z"], 0.01, case["n"], _key(case["m"]), [case["I"]])
+    assert kase == case["case"]
+    assert abs(d[0] - case["delta"]) < 1e-7
+
+
+def test_eq11_equals_rerender_with_ghost_inserted():
+    """For cases 1-3 and case 4 with z >= min_z, Delta of Eq. 11 is exactly the change of Eq. 7 at the
+    neighbour when the shifted point is rendered there (S:L351 cross-check, generalised)."""
+    rng = np.random.default_rng(1)
+    cam = _cam(8, 4, 4.0, 4.0, 2.0)
+    prm = S.Params(layers=1, discard=False, alpha=0.01)
+    seen = set()
+    for trial in range(400):
+        n = int(rng.integers(0, 4))
+        base_z = rng.uniform(1.0, 2.0)
+        depths = base_z * (1 + rng.uniform(0, 0.012, n))
+        xyz = [_at_pixel(cam, 5, 2, z) for z in depths]
+        tau = rng.random((n, 2)).astype(F)
+        zg = F(base_z * rng.choice([0.9, 0.995, 1.0, 1.004, 1.02, 1.2]))
+        tg = rng.random(2).astype(F)
+        pts = O.Points(np.asarray(xyz, F).reshape(-1, 3).T.copy(), np.full(n, 0.005, F), tau.reshape(n, 2))
+        fwd = O.forward(pts, [cam], [IDENT], prm)
+        q = 2 * 8 + 5
+        Iq = [fwd.image[0, c * 32 + q] for c in range(2)]
+        kase, delta = O.induced_change(tg, zg, prm.alpha, fwd.count[0, q], int(fwd.keys[0, q]), Iq)
+        m_q = np.array([int(fwd.keys[0, q]) >> 32], np.uint32).view(F)[0]
+        if kase == 4 and zg < m_q:
+            continue
+        seen.add(kase)
+        xyz2 = np.asarray(xyz + [_at_pixel(cam, 5, 2, float(zg))], F).reshape(-1, 3).T.copy()
+        assert O.project(cam, IDENT, *xyz2[:, -1])[1][2] == zg
+        pts2 = O.Points(xyz2, np.full(n + 1, 0.005, F), np.vstack([tau.reshape(n, 2), tg[None]]))
+        fwd2 = O.forward(pts2, [cam], [IDENT], prm)
+        for c in range(2):
+            assert abs((fwd2.image[0, c * 32 + q] - Iq[c]) - delta[c]) < 1e-12, (trial, kase)
+    assert seen == {1, 2, 3, 4}
+
+
+# --------------------------------------------------------------------------- #
+# Eqs. 9-10 spatial gradient, ghosts (§4.3), chain rule (Eq. 8, Eq. 17)
+# --------------------------------------------------------------------------- #
+GPRM = S.Params(layers=1, discard=False, alpha=0.01, ghost_rate=0.5, seed=4242)
+
+
+def test_linear_ramp_recovers_gradient():
+    """Rendered row I(u) = c*u at depth 2, ghost in front carrying tau = I(u_g): the signed central
+    difference (R15) gives g_u = -G*c exactly (S:L359 ramp; magnitude G*c, sign from moving right onto a
+    brighter pixel lowering L = sum G*I).  dx = J^T g with J = [fx/Z, 0, -fx X/Z^2] (R21)."""
+    cam = _cam(32, 8, 8.0, 16.0, 4.0)
+    c = 1.0 / 64  # exact in fp32
+    render = [_at_pixel(cam, u, 4, 2.0) for u in range(32)]
+    feats = [[c * u] for u in range(32)]
+    pts, gids = arrange(render, [_at_pixel(cam, 16, 4, 1.0)], GPRM, feats, [[c * 16]])
+    fwd = O.forward(pts, [cam], [IDENT], GPRM)
+    G = _grad_image(cam, 1, 1, 0.0)
+    G[0, 4 * 32: 5 * 32] = 1.0
+    bwd = O.backward(pts, [cam], [IDENT], GPRM, fwd, G)
+    g = gids[0]
+    gu = -1.0 * c
+    np.testing.assert_allclose(bwd.dx[:, g], [8.0 / 1.0 * gu, 0.0, 0.0], atol=1e-9)
+    np.testing.assert_allclose(bwd.dpose[0], [8.0 * gu, 0, 0, 0, 8.0 * gu, 0], atol=1e-9)  # (w, Xc x w), Xc = (0,0,1)
+    # only the ghost gets a spatial gradient, only rendered points get texture gradients (Fig. 4, R22)
+    assert np.count_nonzero(bwd.dx) == 1 and bwd.dtau[g, 0] == 0.0
+    assert np.count_nonzero(bwd.dtau) > 0
+
+
+def test_border_drops_outside_neighbour():
+    """at u = 0 the left term is dropped, g_u = 1/2 <G(1,v), Delta+>."""
+    cam = _cam(8, 4, 4.0, 4.0, 2.0)
+    pts, gids = arrange([], [_at_pixel(cam, 0, 2, 1.0)], GPRM, [], [[0.75]])
+    fwd = O.forward(pts, [cam], [IDENT], GPRM)
+    G = _grad_image(cam, 1, 1, 0.0)
+    G[0, 2 * 8 + 1] = 2.0   # right neighbour: background (case 1), Delta = 0.75 - 0
+    bwd = O.backward(pts, [cam], [IDENT], GPRM, fwd, G)
+    gu = 0.5 * 2.0 * 0.75
+    np.testing.assert_allclose(bwd.dx[:, gids[0]], [4.0 * gu, 0.0, 4.0 * gu], atol=1e-9)  # J_u = [fx/Z, 0, -fx X/Z^2], X=-1
+
+
+def test_uniform_covisible_field_gives_zero():
+    """uniform image, uniform depth, tau = I -> every Delta vanishes (case 4) -> g = 0."""
+    cam = _cam(12, 10, 6.0, 6.0, 5.0)
+    render = [_at_pixel(cam, u, v, 2.0) for v in range(10) for u in range(12)]
+    ghosts = [_at_pixel(cam, u, v, 2.0) for u, v in ((3, 3), (6, 5), (0, 0), (11, 9))]
+    pts, gids = arrange(render, ghosts, GPRM, [[0.5, 0.25]] * len(render), [[0.5, 0.25]] * 4)
+    fwd = O.forward(pts, [cam], [IDENT], GPRM)
+    G = np.random.default_rng(2).uniform(-1, 1, (1, 2 * 120)).astype(F)
+    bwd = O.backward(pts, [cam], [IDENT], GPRM, fwd, G)
+    assert np.abs(bwd.dx).max() < 1e-12 and np.abs(bwd.dpose).max() < 1e-12
+
+
+def test_empty_ghost_set_gives_zero_structural_gradients():
+    room = S.make_room(4.0)
+    pts = O.Points.from_cloud(S.room_cloud(2000, room, 3, seed=5))
+    cams, poses = [S.pinhole(64, 48)], S.room_poses(1, room)
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.0)
+    fwd = O.forward(pts, cams, poses, prm)
+    G = S.grad_pyramid(1, 3, fwd.count.shape[1]).numpy()
+    bwd = O.backward(pts, cams, poses, prm, fwd, G)
+    assert not bwd.dx.any() and not bwd.dpose.any()
+
+
+def _rodrigues(w):
+    th = np.linalg.norm(w)
+    K = np.array([[0, -w[2], w[1]], [w[2], 0, -w[0]], [-w[1], w[0], 0]])
+    if th < 1e-300:
+        return np.eye(3)
+    return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th ** 2 * K @ K
+
+
+def test_pose_gradient_is_left_tangent_chain_rule():
+    """Eq. 17: d/dxi of w . (exp(xi) Xc) at 0 equals (w, Xc x w) (R19); translation part = R dx (Xc = R x + t)."""
+    room = S.make_room(4.0)
+    cloud = S.room_cloud(4000, room, 2, seed=8)
+    pts = O.Points.from_cloud(cloud)
+    pts = O.Points(pts.pos, np.full(pts.n, 0.02, F), pts.feat)
+    cams, poses = [S.pinhole(80, 60)], S.room_poses(1, room, seed=9)
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.3, seed=3)
+    fwd = O.forward(pts, cams, poses, prm)
+    G = S.grad_pyramid(1, 2, fwd.count.shape[1], seed=12).numpy()
+    bwd = O.backward(pts, cams, poses, prm, fwd, G)
+    R = poses[0].R.astype(np.float64)
+    ghosts = np.nonzero(np.abs(bwd.dx).sum(0))[0]
+    assert len(ghosts) > 20
+    w = R @ bwd.dx[:, ghosts]                       # dL/dXc per ghost
+    np.testing.assert_allclose(bwd.dpose[0, :3], w.sum(1), rtol=1e-6, atol=1e-9)  # fp32 R is orthonormal to ~1e-7
+    rot = np.zeros(3)
+    for j, i in enumerate(ghosts):
+        Xc = O.project(cams[0], poses[0], *pts.pos[:, i])[1].astype(np.float64)
+        for k in range(3):                          # FD through the exponential map (rotation part)
+            e = np.zeros(3); e[k] = 1e-6
+            rot[k] += w[:, j] @ (_rodrigues(e) @ Xc - _rodrigues(-e) @ Xc) / 2e-6
+    np.testing.assert_allclose(bwd.dpose[0, 3:], rot, rtol=1e-6, atol=1e-9)
