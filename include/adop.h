@@ -1,0 +1,205 @@
+/*
+ * adop.h -- C-ABI of the B200-native ADOP one-pixel point rasterizer
+ * (Rückert, Franke, Stamminger, "ADOP: Approximate Differentiable One-Pixel
+ * Point Rendering", arXiv 2110.06635).  Library: libadop.so (sm_100a).
+ *
+ * The entry points are the render function of Eq. 1 (PAPER.md L171-177,
+ * §4 "I_l = Phi_l(C, R, t, x, n, E, tau)") split into the three passes of
+ * §4.5 (L356-359: depth-only pass, accumulate with counts, normalize), and
+ * its backward (§4.2-4.3: texture gradient, ghost-geometry
+ * position and tangent-space pose gradients, Eq. 8, Eq. 17).
+ *
+ * Conventions (all entry points):
+ *  - Every pointer inside adop_points / adop_pyramid and every gradient
+ *    pointer is DEVICE memory (cudaMalloc / torch CUDA tensor) on the current
+ *    device; camera, pose and params descriptors (and params->background)
+ *    are HOST memory read during the call.
+ *  - The caller owns every buffer.  The library allocates no device memory;
+ *    scratch comes from the caller's workspace (adop_workspace_size).
+ *  - Work is enqueued on `stream` (a cudaStream_t passed as void*, NULL =
+ *    legacy default stream).  No entry point synchronizes the host.
+ *  - All argument checks run on the host before anything is enqueued; on
+ *    any error nothing runs and adop_last_error() describes it.  Points that
+ *    are behind the camera or non-finite are NOT errors: they are culled
+ *    (PAPER.md L205-207 bounds test; R7).
+ *  - No C++ exception crosses this boundary.
+ *
+ * Layouts:
+ *  - positions: SoA rows x, y, z: pos[0..n), pos[stride..stride+n),
+ *    pos[2*stride..2*stride+n).  Rows 16-byte aligned with stride % 4 == 0
+ *    select the vectorized load path (any 4-byte aligned layout works).
+ *  - features tau: [n][C] fp32 row-major (C contiguous).
+ *  - pyramid of one view, L layers, layer l of size w_l x h_l with
+ *    w_l = ceil(w / 2^l), h_l = ceil(h / 2^l) (R5), pixel offset
+ *    off_l = sum_{k<l} w_k h_k, P = off_L:
+ *      keys  [P]    uint64 packed depth keys (bits(z) << 32 | global index),
+ *                   empty pixel = 0x7FFFFFFFFFFFFFFF (R8)
+ *      count [P]    float, |Lambda_{l,u,v}| (exact integers)
+ *      accum [P][C] float, sum of tau over Lambda (shard-reducible scratch)
+ *      image [C*P]  float, layer l stored planar [C][h_l][w_l] at C*off_l
+ *                   (an NCHW tensor per layer), Eq. 7 output.
+ *  - upstream gradient dL/dI: same layout as image.
+ *  - d_feat [n][C], d_pos [3][n] (SoA rows, stride n), d_pose [V][6] double
+ *    ordered (translation, rotation) of the left tangent increment of Eq. 17.
+ */
+#ifndef ADOP_H
+#define ADOP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ADOP_API __attribute__((visibility("default")))
+#else
+#define ADOP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ADOP_OK = 0,
+    ADOP_ERR_INVALID_ARGUMENT = 1,
+    ADOP_ERR_SHAPE_MISMATCH = 2,
+    ADOP_ERR_UNSUPPORTED = 3,
+    ADOP_ERR_WORKSPACE_TOO_SMALL = 4,
+    ADOP_ERR_CUDA = 5
+} adop_status;
+
+enum { ADOP_PINHOLE = 0, ADOP_OPENCV8 = 1 };
+
+#define ADOP_MAX_LAYERS 8
+#define ADOP_MAX_CHANNELS 32
+
+/* One shard of the point cloud (x, tau and r_world of Eq. 1 / §4.4). */
+typedef struct {
+    int64_t n;              /* points in this shard, >= 0                                  */
+    int64_t global_offset;  /* global index of point 0; keys and hashes use it (R25);
+                               global_offset + n <= 2^32                                  */
+    int64_t pos_stride;     /* elements between the x, y, z rows, >= n                      */
+    const float *pos;       /* device, SoA [3][pos_stride]                                  */
+    const float *radius;    /* device [n] world radius r_world (§4.4), or NULL         */
+    float radius_uniform;   /* used when radius == NULL                                     */
+    const float *feat;      /* device [n][C] neural descriptor tau                         */
+    int32_t channels;       /* C, 1..32                                                     */
+} adop_points;
+
+/* Camera model C of Eq. 2 (R6): pinhole, or OpenCV rational 8-coefficient distortion
+ * on normalized coordinates; points with r^2 > r2_max or a non-positive radial
+ * denominator are culled.  Host memory. */
+typedef struct {
+    int32_t width, height;  /* layer-0 image size, >= 1                                     */
+    int32_t model;          /* ADOP_PINHOLE or ADOP_OPENCV8                                  */
+    float fx, fy, cx, cy;   /* pixels; pixel centres at integer coordinates                 */
+    float k[6];             /* k1..k6 (OpenCV8)                                             */
+    float p[2];             /* p1, p2 (OpenCV8)                                             */
+    float r2_max;           /* validity radius in normalized r^2 (OpenCV8; +inf allowed)   */
+} adop_camera;
+
+/* World -> camera rigid transform (R, t) of Eq. 2: Xc = R x + t, R row-major.  Host. */
+typedef struct {
+    float R[9];
+    float t[3];
+} adop_pose;
+
+/* Method parameters.  Host memory. */
+typedef struct {
+    int32_t layers;         /* L, 1..8 (Eq. 1 l in {0..L-1})                                */
+    float alpha;            /* fuzzy depth threshold of Eq. 6, >= 0 (paper: 0.01, L217)     */
+    int32_t discard;        /* stochastic point discarding of §4.4 on/off                   */
+    float gamma;            /* Eq. 12 gamma > 0 (paper: 1.5, L349)                          */
+    float ghost_rate;       /* rho in [0,1): fraction of points in the ghost set (§4.3)    */
+    float z_near;           /* near plane >= 0; points with z <= z_near are culled (R7)     */
+    uint64_t seed;          /* seeds the ghost split and the per-(view, point) beta (R11)   */
+    int32_t view_id_base;   /* global id of view 0 of this call (beta is keyed by it)       */
+    const float *background;/* host [C] constant environment colour E (R18), NULL = zeros   */
+    int32_t grad_accumulate;/* backward: 0 overwrite d_feat/d_pos/d_pose, 1 add into them   */
+} adop_params;
+
+/* Buffers of one view (device).  See layouts above. */
+typedef struct {
+    float *image;
+    float *count;
+    uint64_t *keys;
+    float *accum;
+} adop_pyramid;
+
+/* Pixels of one pyramid: sum_l ceil(w/2^l) * ceil(h/2^l).  Returns 0 on invalid sizes. */
+ADOP_API int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t layers);
+
+/* Workspace bytes for calls over `n_views` views of `points`.
+ * record_capacity: number of 16-byte survivor records the depth pass may emit
+ * ((point, view, layer) hits of the render set); < 0 selects the worst case
+ * n * n_views * layers.  If a call's survivors exceed the capacity, the blend
+ * pass falls back to re-streaming all points (correct, slower).
+ * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, n_views < 1, bad layers). */
+ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_params *params,
+                                int64_t record_capacity, size_t *bytes);
+
+/* Phase 1, depth-only render pass (§4.5; Eqs. 2-4, 12, min_z of Eq. 6):
+ * sets keys to the sentinel and accum/count to zero for every view, then
+ * atomically min-reduces the packed key of every render-set point into every
+ * layer it lands on, and records the survivors in the workspace.
+ * Caller-run collectives (point sharding) may min-reduce keys (as int64 or
+ * uint64: the sentinel keeps both orders equal) before phase 2.
+ * Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_WORKSPACE_TOO_SMALL, ADOP_ERR_CUDA. */
+ADOP_API adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                               const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
+/* Phase 2, accumulate (§4.5; fuzzy test Eq. 6, sums of Eq. 7):
+ * for every survivor of phase 1 that passes z <= (1+alpha) * min_z against the
+ * (possibly globally reduced) keys, adds tau to accum and 1 to count.
+ * Must follow adop_forward_depth with the same arguments and workspace. */
+ADOP_API adop_status adop_forward_blend(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                               const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
+/* Phase 3, normalize (Eq. 7): image = accum / count where count > 0,
+ * else the background colour; writes the planar image of every layer. */
+ADOP_API adop_status adop_forward_resolve(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                 const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* Phases 1-3 in order (single GPU). */
+ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                   const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                   void *workspace, size_t workspace_bytes, void *stream);
+
+/* Backward (§4.2-4.5): re-renders every point (L361) against the forward's
+ * keys/count/image (which must be unmodified) and the upstream gradient
+ * grad_image[v] (device, image layout) and produces
+ *   d_feat [n][C]: sum over views/layers of G/|Lambda| for rendered points (ghosts 0),
+ *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17),
+ *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment).
+ * Any of d_feat / d_pos / d_pose may be NULL.  params->grad_accumulate selects
+ * overwrite or add.  Points, cameras, poses and params must equal the forward's.
+ * Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_WORKSPACE_TOO_SMALL, ADOP_ERR_CUDA. */
+ADOP_API adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                    const adop_pose *poses, const adop_params *params,
+                                    const adop_pyramid *fwd_views, const float *const *grad_image,
+                                    float *d_feat, float *d_pos, double *d_pose,
+                                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* Debug / parity: per point and view, bit l (l < L) = valid, in bounds and kept
+ * by the discard test at layer l; bit 7 = ghost.  mask: device uint8 [V][n]. */
+ADOP_API adop_status adop_point_masks(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                             const adop_pose *poses, const adop_params *params, uint8_t *mask, void *stream);
+
+/* Survivor statistics of the last depth pass in `workspace` (synchronizes `stream`):
+ * records emitted and whether they overflowed the capacity. */
+ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream,
+                                 int64_t *records, int32_t *overflowed);
+
+/* Thread-local description of the last non-OK status ("" if none). */
+ADOP_API const char *adop_last_error(void);
+
+/* Library version string. */
+ADOP_API const char *adop_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADOP_H */

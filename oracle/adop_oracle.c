@@ -446,11 +446,13 @@ static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, i
         if (qu < 0 || qu >= wl || qv < 0 || qv >= hl) continue; /* neighbour outside: no term (R14) */
         int64_t qj = qv * wl + qu;
         for (int ch = 0; ch < C; ++ch) Iq[ch] = img[C * off + ch * hw + qj];
-        orc_induced_change(C, tau, z, pr->alpha, cv[off + qj], kv[off + qj], Iq, delta);
+        int kase = orc_induced_change(C, tau, z, pr->alpha, cv[off + qj], kv[off + qj], Iq, delta);
+        /* magnitude scale for tolerances: sum_c |G| (|tau| + |I|) times the case factor */
+        double fac = kase == 2 ? 0.0 : (kase == 4 ? 1.0 / (cv[off + qj] + 1.0) : 1.0);
         for (int ch = 0; ch < C; ++ch) {
             double gq = (double)Gv[C * off + ch * hw + qj];
             d[k] += gq * delta[ch];
-            dabs[k] += fabs(gq * delta[ch]);
+            dabs[k] += fabs(gq) * (fabs((double)tau[ch]) + fabs(Iq[ch])) * fac;
         }
     }
     g[0] = 0.5 * (d[0] - d[1]);   /* Eq. 10 with the signed central difference (R15) */

@@ -1,0 +1,342 @@
+"""Thin ctypes binding of libadop.so (include/adop.h) -- argument marshalling only.
+
+Every step of the rasterizer runs in the library's sm_100a kernels; torch is used
+for device memory and streams.  There is no CPU fallback: if libadop.so is
+missing or no CUDA device is present, the calls raise.
+
+Names follow the C-ABI without the `adop_` prefix:
+    pyramid_pixels, workspace_size, forward_depth, forward_blend, forward_resolve,
+    rasterize_forward, rasterize_backward, point_masks, workspace_stats.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import build as _build
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libadop.so")
+MAX_VIEWS = 16
+SENTINEL = 0x7FFFFFFFFFFFFFFF
+
+STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "SHAPE_MISMATCH", 3: "UNSUPPORTED", 4: "WORKSPACE_TOO_SMALL",
+          5: "CUDA"}
+
+
+class AdopError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"adop status {status} ({STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class adop_points(C.Structure):
+    _fields_ = [("n", C.c_int64), ("global_offset", C.c_int64), ("pos_stride", C.c_int64),
+                ("pos", C.c_void_p), ("radius", C.c_void_p), ("radius_uniform", C.c_float),
+                ("feat", C.c_void_p), ("channels", C.c_int32)]
+
+
+class adop_camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("model", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("k", C.c_float * 6), ("p", C.c_float * 2), ("r2_max", C.c_float)]
+
+
+class adop_pose(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3)]
+
+
+class adop_params(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("alpha", C.c_float), ("discard", C.c_int32), ("gamma", C.c_float),
+                ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
+                ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32)]
+
+
+class adop_pyramid(C.Structure):
+    _fields_ = [("image", C.c_void_p), ("count", C.c_void_p), ("keys", C.c_void_p), ("accum", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libadop.so (building it first if the sources are newer).  Raises if it cannot be loaded."""
+    global _lib
+    if _lib is None:
+        if _build.needs_build():
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libadop.so not found at {LIB_PATH}; run python -m paper_2110_06635_b200.build")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        common = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params), P(adop_pyramid),
+                  C.c_void_p, C.c_size_t, C.c_void_p]
+        for name in ("adop_forward_depth", "adop_forward_blend", "adop_forward_resolve", "adop_rasterize_forward"):
+            f = getattr(L, name)
+            f.restype, f.argtypes = C.c_int, common
+        L.adop_rasterize_backward.restype = C.c_int
+        L.adop_rasterize_backward.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose),
+                                              P(adop_params), P(adop_pyramid), P(C.c_void_p), C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.adop_point_masks.restype = C.c_int
+        L.adop_point_masks.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params),
+                                       C.c_void_p, C.c_void_p]
+        L.adop_pyramid_pixels.restype = C.c_int64
+        L.adop_pyramid_pixels.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.adop_workspace_size.restype = C.c_int
+        L.adop_workspace_size.argtypes = [P(adop_points), C.c_int32, P(adop_params), C.c_int64, P(C.c_size_t)]
+        L.adop_workspace_stats.restype = C.c_int
+        L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int32)]
+        L.adop_last_error.restype = C.c_char_p
+        L.adop_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise AdopError(status, lib().adop_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+# --------------------------------------------------------------------------- #
+# descriptors
+# --------------------------------------------------------------------------- #
+class Points:
+    """adop_points over torch CUDA tensors (keeps them alive).  pos: (3, N) or (3, stride) float32."""
+
+    def __init__(self, pos: torch.Tensor, radius: Optional[torch.Tensor], feat: torch.Tensor,
+                 global_offset: int = 0, radius_uniform: float = 0.0, n: Optional[int] = None):
+        assert pos.dtype == torch.float32 and pos.dim() == 2 and pos.shape[0] == 3 and pos.stride(1) == 1
+        assert feat.dtype == torch.float32 and feat.dim() == 2 and feat.is_contiguous()
+        self.pos, self.radius, self.feat = pos, radius, feat
+        self.n = int(feat.shape[0]) if n is None else int(n)
+        self.channels = int(feat.shape[1])
+        s = adop_points()
+        s.n, s.global_offset, s.pos_stride = self.n, int(global_offset), int(pos.stride(0))
+        s.pos, s.radius, s.radius_uniform = _ptr(pos), _ptr(radius), float(radius_uniform)
+        s.feat, s.channels = _ptr(feat), self.channels
+        self.s = s
+
+    @staticmethod
+    def from_cloud(cloud, global_offset: int = 0) -> "Points":
+        return Points(cloud.pos, cloud.radius, cloud.feat, global_offset)
+
+
+def camera_struct(cam) -> adop_camera:
+    s = adop_camera()
+    s.width, s.height, s.model = int(cam.width), int(cam.height), int(cam.model)
+    s.fx, s.fy, s.cx, s.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    for i in range(6):
+        s.k[i] = cam.k[i]
+    s.p[0], s.p[1] = cam.p
+    s.r2_max = cam.r2_max
+    return s
+
+
+def pose_struct(pose) -> adop_pose:
+    s = adop_pose()
+    R = [float(v) for v in torch.as_tensor(pose.R, dtype=torch.float32).reshape(9)]
+    t = [float(v) for v in torch.as_tensor(pose.t, dtype=torch.float32).reshape(3)]
+    for i in range(9):
+        s.R[i] = R[i]
+    for i in range(3):
+        s.t[i] = t[i]
+    return s
+
+
+class Params:
+    def __init__(self, p, channels: int):
+        s = adop_params()
+        s.layers, s.alpha, s.discard, s.gamma = int(p.layers), p.alpha, int(bool(p.discard)), p.gamma
+        s.ghost_rate, s.z_near, s.seed, s.view_id_base = p.ghost_rate, p.z_near, int(p.seed), int(p.view_id_base)
+        bg = p.background if p.background is not None else None
+        self._bg = (C.c_float * channels)(*bg) if bg is not None else None
+        s.background = C.cast(self._bg, C.c_void_p) if self._bg is not None else None
+        s.grad_accumulate = int(getattr(p, "grad_accumulate", 0))
+        self.s = s
+        self.layers = int(p.layers)
+
+
+def pyramid_pixels(width: int, height: int, layers: int) -> int:
+    return int(lib().adop_pyramid_pixels(width, height, layers))
+
+
+@dataclasses.dataclass
+class Pyramid:
+    """Buffers of one view.  accum and count are views of one tensor `ac` so a point-sharded
+    caller can sum-reduce both in a single collective."""
+    image: torch.Tensor   # [C*P] float32
+    count: torch.Tensor   # [P] float32
+    keys: torch.Tensor    # [P] int64 (uint64 bit pattern)
+    accum: torch.Tensor   # [P*C] float32
+    ac: torch.Tensor      # [P*(C+1)] float32 backing accum ++ count
+    width: int
+    height: int
+    layers: int
+
+    def struct(self) -> adop_pyramid:
+        s = adop_pyramid()
+        s.image, s.count, s.keys, s.accum = (self.image.data_ptr(), self.count.data_ptr(), self.keys.data_ptr(),
+                                             self.accum.data_ptr())
+        return s
+
+    def layer_image(self, l: int, channels: int) -> torch.Tensor:
+        """Layer l as a (C, h_l, w_l) view of the planar image (Eq. 1's I_l)."""
+        off = 0
+        for k in range(l):
+            off += -(-self.width // (1 << k)) * -(-self.height // (1 << k))
+        wl, hl = -(-self.width // (1 << l)), -(-self.height // (1 << l))
+        return self.image[channels * off: channels * (off + wl * hl)].view(channels, hl, wl)
+
+
+def alloc_pyramids(cams, layers: int, channels: int, device) -> List[Pyramid]:
+    out = []
+    for cam in cams:
+        P = pyramid_pixels(cam.width, cam.height, layers)
+        ac = torch.empty(P * (channels + 1), dtype=torch.float32, device=device)
+        out.append(Pyramid(torch.empty(channels * P, dtype=torch.float32, device=device),
+                           ac[P * channels:], torch.empty(P, dtype=torch.int64, device=device),
+                           ac[:P * channels], ac, cam.width, cam.height, layers))
+    return out
+
+
+class Workspace:
+    def __init__(self, points: Points, n_views: int, params: Params, device, record_capacity: int = -1):
+        size = C.c_size_t(0)
+        _check(lib().adop_workspace_size(C.byref(points.s), n_views, C.byref(params.s), int(record_capacity),
+                                         C.byref(size)))
+        self.nbytes = int(size.value)
+        self.buf = torch.empty((self.nbytes + 255) // 256 * 256 + 256, dtype=torch.uint8, device=device)
+        base = self.buf.data_ptr()
+        self.ptr = (base + 255) // 256 * 256
+
+    def stats(self, stream=None):
+        rec, of = C.c_int64(0), C.c_int32(0)
+        _check(lib().adop_workspace_stats(self.ptr, self.nbytes, _stream(stream), C.byref(rec), C.byref(of)))
+        return int(rec.value), bool(of.value)
+
+
+def default_record_capacity(n: int, n_views: int, layers: int, discard: bool) -> int:
+    """Worst case n*V*L when affordable (< 4 GiB), else a generous bound: with stochastic discarding
+    the kept points per pixel are bounded (Eq. 12), so the records are far below the worst case;
+    exceeding the capacity is still correct (the blend pass re-streams the points)."""
+    worst = n * n_views * layers
+    if worst * 16 <= (4 << 30) or not discard:
+        return worst
+    return max(1 << 22, worst // 4)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+class _Call:
+    """Marshalled arguments of one call (keeps ctypes arrays alive)."""
+
+    def __init__(self, points: Points, cams, poses, params: Params, pyrs: Optional[Sequence[Pyramid]]):
+        V = len(cams)
+        if V < 1 or V > MAX_VIEWS:
+            raise ValueError(f"1..{MAX_VIEWS} views per call, got {V}")
+        self.V = V
+        self.cams = (adop_camera * V)(*[camera_struct(c) for c in cams])
+        self.poses = (adop_pose * V)(*[pose_struct(p) for p in poses])
+        self.pyrs = (adop_pyramid * V)(*[p.struct() for p in pyrs]) if pyrs is not None else None
+        self.points, self.params = points, params
+
+
+def _phase(fn_name, points, cams, poses, params, pyrs, ws: Workspace, stream=None):
+    c = _Call(points, cams, poses, params, pyrs)
+    fn = getattr(lib(), fn_name)
+    _check(fn(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, ws.ptr, ws.nbytes,
+              _stream(stream)))
+
+
+def forward_depth(points, cams, poses, params, pyrs, ws, stream=None):
+    _phase("adop_forward_depth", points, cams, poses, params, pyrs, ws, stream)
+
+
+def forward_blend(points, cams, poses, params, pyrs, ws, stream=None):
+    _phase("adop_forward_blend", points, cams, poses, params, pyrs, ws, stream)
+
+
+def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None):
+    _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream)
+
+
+def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None):
+    _phase("adop_rasterize_forward", points, cams, poses, params, pyrs, ws, stream)
+
+
+def rasterize_backward(points, cams, poses, params, pyrs, grads: Sequence[torch.Tensor], ws,
+                       d_feat: Optional[torch.Tensor], d_pos: Optional[torch.Tensor],
+                       d_pose: Optional[torch.Tensor], stream=None):
+    c = _Call(points, cams, poses, params, pyrs)
+    g = (C.c_void_p * c.V)(*[t.data_ptr() for t in grads])
+    _check(lib().adop_rasterize_backward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, g,
+                                         _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), ws.ptr, ws.nbytes,
+                                         _stream(stream)))
+
+
+def point_masks(points, cams, poses, params, mask: torch.Tensor, stream=None):
+    c = _Call(points, cams, poses, params, None)
+    _check(lib().adop_point_masks(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), mask.data_ptr(),
+                                  _stream(stream)))
+
+
+def version() -> str:
+    return lib().adop_version().decode()
+
+
+class Renderer:
+    """Convenience owner of the device buffers of one (cloud, views) configuration.
+
+    forward()  -> adop_rasterize_forward into self.pyrs
+    backward(grads) -> adop_rasterize_backward into self.d_feat / self.d_pos / self.d_pose
+    """
+
+    def __init__(self, cloud, cams, poses, params, global_offset: int = 0, record_capacity: Optional[int] = None,
+                 device=None):
+        device = cloud.pos.device if device is None else device
+        self.cams, self.poses, self.sparams = list(cams), list(poses), params
+        self.points = Points.from_cloud(cloud, global_offset)
+        self.C = self.points.channels
+        self.params = Params(params, self.C)
+        self.pyrs = alloc_pyramids(self.cams, params.layers, self.C, device)
+        if record_capacity is None:
+            record_capacity = default_record_capacity(self.points.n, len(self.cams), params.layers, params.discard)
+        self.ws = Workspace(self.points, len(self.cams), self.params, device, record_capacity)
+        self.device = device
+        self.d_feat = self.d_pos = self.d_pose = None
+
+    def forward(self, stream=None):
+        rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream)
+        return self.pyrs
+
+    def alloc_grads(self):
+        n = self.points.n
+        self.d_feat = torch.empty(n, self.C, dtype=torch.float32, device=self.device)
+        self.d_pos = torch.empty(3, n, dtype=torch.float32, device=self.device)
+        self.d_pose = torch.empty(len(self.cams), 6, dtype=torch.float64, device=self.device)
+
+    def backward(self, grads: Sequence[torch.Tensor], stream=None):
+        if self.d_feat is None:
+            self.alloc_grads()
+        rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,
+                           self.d_feat, self.d_pos, self.d_pose, stream)
+        return self.d_feat, self.d_pos, self.d_pose
+
+    def masks(self, stream=None) -> torch.Tensor:
+        m = torch.empty(len(self.cams), self.points.n, dtype=torch.uint8, device=self.device)
+        point_masks(self.points, self.cams, self.poses, self.params, m, stream)
+        return m

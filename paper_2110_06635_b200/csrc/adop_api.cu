@@ -1,0 +1,421 @@
+// adop_api.cu -- host side of the C-ABI (include/adop.h): argument validation,
+// kernel argument blocks, workspace layout and launch sequencing.
+// No exception crosses the ABI; errors are reported as adop_status plus a
+// thread-local message (adop_last_error).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "adop_internal.h"
+
+using namespace adop;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+adop_status fail(adop_status s, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+adop_status ok() {
+    g_err[0] = '\0';
+    return ADOP_OK;
+}
+
+// hash salt (R11, R13): mix of (seed, stream, view)
+uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+uint32_t salt_of(uint64_t seed, uint32_t stream, uint32_t view) {
+    uint32_t s = mix32((uint32_t)seed + 0x9E3779B9U * (stream + 1U));
+    s = mix32(s ^ (uint32_t)(seed >> 32));
+    return mix32(s + 0x85EBCA6BU * (view + 1U));
+}
+constexpr uint32_t kStreamGhost = 1, kStreamDiscard = 2;
+
+constexpr size_t kHeaderBytes = 256;
+constexpr int kMaxBwdBlocks = 2048;
+constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 6 * sizeof(double);
+
+int32_t layer_size(int32_t s, int l) { return (int32_t)((s + (1 << l) - 1) >> l); }
+
+int device_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = sms > 0 ? sms : 148;
+    }
+    return cached[dev];
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+adop_status check_points(const adop_points *pts, bool need_feat) {
+    if (!pts) return fail(ADOP_ERR_INVALID_ARGUMENT, "points is NULL");
+    if (pts->n < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->n = %lld < 0", (long long)pts->n);
+    if (pts->global_offset < 0 || pts->global_offset + pts->n > (int64_t)4294967296LL)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "global_offset + n must be in [0, 2^32]");
+    if (pts->channels < 1 || pts->channels > ADOP_MAX_CHANNELS)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "channels = %d not in [1, %d]", pts->channels, ADOP_MAX_CHANNELS);
+    if (pts->n == 0) return ok();
+    if (!pts->pos) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->pos is NULL");
+    if (!aligned(pts->pos, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->pos not 4-byte aligned");
+    if (pts->pos_stride < pts->n) return fail(ADOP_ERR_INVALID_ARGUMENT, "pos_stride < n");
+    if (pts->radius && !aligned(pts->radius, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "radius not aligned");
+    if (!pts->radius && !(pts->radius_uniform >= 0.0f && std::isfinite(pts->radius_uniform)))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "radius_uniform must be finite and >= 0");
+    if (need_feat && !pts->feat) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->feat is NULL");
+    if (pts->feat && !aligned(pts->feat, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "feat not aligned");
+    return ok();
+}
+
+adop_status check_params(const adop_params *pr) {
+    if (!pr) return fail(ADOP_ERR_INVALID_ARGUMENT, "params is NULL");
+    if (pr->layers < 1 || pr->layers > ADOP_MAX_LAYERS)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "layers = %d not in [1, %d]", pr->layers, ADOP_MAX_LAYERS);
+    if (!(pr->alpha >= 0.0f) || !std::isfinite(pr->alpha)) return fail(ADOP_ERR_INVALID_ARGUMENT, "alpha must be >= 0");
+    if (pr->discard && (!(pr->gamma > 0.0f) || !std::isfinite(pr->gamma)))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "gamma must be > 0 with discard on");
+    if (!(pr->ghost_rate >= 0.0f && pr->ghost_rate < 1.0f))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "ghost_rate must be in [0, 1)");
+    if (!(pr->z_near >= 0.0f) || !std::isfinite(pr->z_near))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "z_near must be finite and >= 0");
+    if (pr->view_id_base < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "view_id_base < 0");
+    return ok();
+}
+
+adop_status check_camera(const adop_camera *c, int v, int layers) {
+    if (c->width < 1 || c->height < 1) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: width/height < 1", v);
+    if (c->model != ADOP_PINHOLE && c->model != ADOP_OPENCV8)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: unknown camera model %d", v, c->model);
+    if (!std::isfinite(c->fx) || !std::isfinite(c->fy) || !std::isfinite(c->cx) || !std::isfinite(c->cy))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite intrinsics", v);
+    if (c->model == ADOP_OPENCV8) {
+        for (int i = 0; i < 6; ++i)
+            if (!std::isfinite(c->k[i])) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite k", v);
+        if (!std::isfinite(c->p[0]) || !std::isfinite(c->p[1]))
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite p", v);
+        if (!(c->r2_max > 0.0f)) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: r2_max must be > 0", v);
+    }
+    int64_t P = adop_pyramid_pixels(c->width, c->height, layers);
+    if (P <= 0 || P >= (int64_t)1 << 31) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: pyramid too large", v);
+    return ok();
+}
+
+adop_status check_views(int32_t n_views, const adop_camera *cams, const adop_pose *poses, const adop_params *pr,
+                        const adop_pyramid *views, int C, bool need_pyr) {
+    if (n_views < 1 || n_views > ADOP_MAX_VIEWS_PER_LAUNCH)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views = %d not in [1, %d]", n_views, ADOP_MAX_VIEWS_PER_LAUNCH);
+    if (!cams || !poses) return fail(ADOP_ERR_INVALID_ARGUMENT, "cameras/poses is NULL");
+    if (need_pyr && !views) return fail(ADOP_ERR_INVALID_ARGUMENT, "views is NULL");
+    for (int v = 0; v < n_views; ++v) {
+        adop_status s = check_camera(&cams[v], v, pr->layers);
+        if (s) return s;
+        for (int i = 0; i < 9; ++i)
+            if (!std::isfinite(poses[v].R[i])) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite R", v);
+        for (int i = 0; i < 3; ++i)
+            if (!std::isfinite(poses[v].t[i])) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite t", v);
+        if (!need_pyr) continue;
+        const adop_pyramid &py = views[v];
+        if (!py.image || !py.count || !py.keys || !py.accum)
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: NULL pyramid buffer", v);
+        if (!aligned(py.keys, 8) || !aligned(py.count, 4) || !aligned(py.image, 4) || !aligned(py.accum, 4))
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: misaligned pyramid buffer", v);
+    }
+    (void)C;
+    return ok();
+}
+
+struct Ws {
+    WsHeader *hdr;
+    double *partials;
+    Record *records;
+    int64_t capacity;
+};
+
+adop_status carve_workspace(void *ws, size_t bytes, Ws &out) {
+    if (!ws) return fail(ADOP_ERR_INVALID_ARGUMENT, "workspace is NULL");
+    if (!aligned(ws, 256)) return fail(ADOP_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
+    if (bytes < kHeaderBytes + kPartialBytes)
+        return fail(ADOP_ERR_WORKSPACE_TOO_SMALL, "workspace of %zu bytes < minimum %zu", bytes,
+                    kHeaderBytes + kPartialBytes);
+    char *b = static_cast<char *>(ws);
+    out.hdr = reinterpret_cast<WsHeader *>(b);
+    out.partials = reinterpret_cast<double *>(b + kHeaderBytes);
+    out.records = reinterpret_cast<Record *>(b + kHeaderBytes + kPartialBytes);
+    out.capacity = (int64_t)((bytes - kHeaderBytes - kPartialBytes) / sizeof(Record));
+    return ok();
+}
+
+void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const adop_camera *cams,
+               const adop_pose *poses, const adop_params *pr, const adop_pyramid *views, const Ws *ws) {
+    std::memset(&a, 0, sizeof(a));
+    a.x = pts->pos;
+    a.y = pts->pos ? pts->pos + pts->pos_stride : nullptr;
+    a.z = pts->pos ? pts->pos + 2 * pts->pos_stride : nullptr;
+    a.radius = pts->radius;
+    a.radius_uniform = pts->radius_uniform;
+    a.feat = pts->feat;
+    a.n = pts->n;
+    a.goff = (uint32_t)pts->global_offset;
+    a.channels = pts->channels;
+    a.layers = pr->layers;
+    a.nviews = n_views;
+    a.onepa = 1.0f + pr->alpha;
+    a.gamma = pr->gamma;
+    a.z_near = pr->z_near;
+    a.discard = pr->discard ? 1 : 0;
+    a.ghost_thr = (uint32_t)std::floor((double)pr->ghost_rate * 16777216.0);
+    a.ghost_salt = salt_of(pr->seed, kStreamGhost, 0u);
+    a.grad_accumulate = pr->grad_accumulate ? 1 : 0;
+    for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
+    if (ws) {
+        a.hdr = ws->hdr;
+        a.records = ws->records;
+        a.rec_capacity = ws->capacity;
+        a.pose_partials = ws->partials;
+    }
+    const float lmax = (float)(1 << (pr->layers - 1));
+    for (int v = 0; v < n_views; ++v) {
+        ViewDesc &d = a.v[v];
+        const adop_camera &c = cams[v];
+        std::memcpy(d.R, poses[v].R, sizeof(d.R));
+        std::memcpy(d.t, poses[v].t, sizeof(d.t));
+        d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+        if (c.model == ADOP_OPENCV8) {
+            std::memcpy(d.k, c.k, sizeof(d.k));
+            std::memcpy(d.p, c.p, sizeof(d.p));
+            d.r2_max = c.r2_max;
+            d.r2cull = std::isinf(c.r2_max) ? c.r2_max : (float)((double)c.r2_max * (1.0 + 1.0 / 4096.0));
+        } else {
+            d.r2_max = INFINITY;
+            d.r2cull = INFINITY;
+        }
+        d.feff = (c.fx + c.fy) * 0.5f;
+        // conservative window over all layers: u0 in (-2^(L-1)/2, w + 2^(L-1)) plus margin
+        d.ulo = -lmax - 2.0f;
+        d.uhi = (float)c.width + lmax + 2.0f;
+        d.vlo = -lmax - 2.0f;
+        d.vhi = (float)c.height + lmax + 2.0f;
+        d.discard_salt = salt_of(pr->seed, kStreamDiscard, (uint32_t)(pr->view_id_base + v));
+        int32_t off = 0;
+        for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {
+            if (l < pr->layers) {
+                d.wl[l] = layer_size(c.width, l);
+                d.hl[l] = layer_size(c.height, l);
+                d.off[l] = off;
+                off += d.wl[l] * d.hl[l];
+            } else {
+                d.wl[l] = d.hl[l] = 0;
+                d.off[l] = off;
+            }
+        }
+        d.pixels = off;
+        if (views) {
+            d.keys = views[v].keys;
+            d.accum = views[v].accum;
+            d.count = views[v].count;
+            d.image = views[v].image;
+        }
+    }
+}
+
+bool vec_path(const adop_points *pts) {
+    return pts->n > 0 && aligned(pts->pos, 16) && pts->pos_stride % 4 == 0 && (!pts->radius || aligned(pts->radius, 16));
+}
+
+adop_status cuda_status(int err, const char *what) {
+    if (err != cudaSuccess) return fail(ADOP_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)err));
+    return ok();
+}
+
+adop_status prologue(const adop_points *points, int32_t n_views, const adop_camera *cameras, const adop_pose *poses,
+                     const adop_params *params, const adop_pyramid *views, void *workspace, size_t workspace_bytes,
+                     bool need_feat, Ws &ws) {
+    adop_status s;
+    if ((s = check_params(params))) return s;
+    if ((s = check_points(points, need_feat))) return s;
+    if ((s = check_views(n_views, cameras, poses, params, views, points->channels, true))) return s;
+    if ((s = carve_workspace(workspace, workspace_bytes, ws))) return s;
+    cudaError_t pending = cudaGetLastError();
+    if (pending != cudaSuccess) return fail(ADOP_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(pending));
+    return ok();
+}
+
+bool uniform_model(int32_t n_views, const adop_camera *cams, int &model) {
+    model = cams[0].model;
+    for (int v = 1; v < n_views; ++v)
+        if (cams[v].model != model) return false;
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t layers) {
+    if (width < 1 || height < 1 || layers < 1 || layers > ADOP_MAX_LAYERS) return 0;
+    int64_t t = 0;
+    for (int l = 0; l < layers; ++l) t += (int64_t)layer_size(width, l) * layer_size(height, l);
+    return t;
+}
+
+adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_params *params,
+                                int64_t record_capacity, size_t *bytes) {
+    if (!points || !params || !bytes) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 1) return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views < 1");
+    if (params->layers < 1 || params->layers > ADOP_MAX_LAYERS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad layers");
+    if (points->n < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "n < 0");
+    int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * params->layers;
+    *bytes = kHeaderBytes + kPartialBytes + (size_t)cap * sizeof(Record);
+    return ok();
+}
+
+adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                               const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                               void *workspace, size_t workspace_bytes, void *stream) {
+    Ws ws;
+    adop_status s = prologue(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, false, ws);
+    if (s) return s;
+    int model;
+    if (!uniform_model(n_views, cameras, model))
+        return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    int e = launch_clear(a, stream);
+    if (e) return cuda_status(e, "clear launch");
+    if (points->n > 0) {
+        e = launch_depth(a, model, vec_path(points), device_sms(), stream);
+        if (e) return cuda_status(e, "depth launch");
+    }
+    return ok();
+}
+
+adop_status adop_forward_blend(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                               const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                               void *workspace, size_t workspace_bytes, void *stream) {
+    Ws ws;
+    adop_status s = prologue(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, true, ws);
+    if (s) return s;
+    int model;
+    if (!uniform_model(n_views, cameras, model))
+        return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
+    if (points->n == 0) return ok();
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    int e = launch_blend(a, model, vec_path(points), device_sms(), stream);
+    if (e) return cuda_status(e, "blend launch");
+    return ok();
+}
+
+adop_status adop_forward_resolve(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                 const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    Ws ws;
+    adop_status s = prologue(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, false, ws);
+    if (s) return s;
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    int e = launch_resolve(a, stream);
+    if (e) return cuda_status(e, "resolve launch");
+    return ok();
+}
+
+adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                   const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                   void *workspace, size_t workspace_bytes, void *stream) {
+    adop_status s;
+    if ((s = check_points(points, true))) return s;
+    if ((s = adop_forward_depth(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream)))
+        return s;
+    if ((s = adop_forward_blend(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream)))
+        return s;
+    return adop_forward_resolve(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream);
+}
+
+adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                    const adop_pose *poses, const adop_params *params,
+                                    const adop_pyramid *fwd_views, const float *const *grad_image, float *d_feat,
+                                    float *d_pos, double *d_pose, void *workspace, size_t workspace_bytes,
+                                    void *stream) {
+    Ws ws;
+    adop_status s = prologue(points, n_views, cameras, poses, params, fwd_views, workspace, workspace_bytes, true, ws);
+    if (s) return s;
+    if (!grad_image) return fail(ADOP_ERR_INVALID_ARGUMENT, "grad_image is NULL");
+    for (int v = 0; v < n_views; ++v)
+        if (!grad_image[v] || !aligned(grad_image[v], 4))
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "grad_image[%d] is NULL or misaligned", v);
+    if (d_feat && !aligned(d_feat, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_feat misaligned");
+    if (d_pos && !aligned(d_pos, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pos misaligned");
+    if (d_pose && !aligned(d_pose, 8)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pose misaligned");
+    int model;
+    if (!uniform_model(n_views, cameras, model))
+        return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, fwd_views, &ws);
+    for (int v = 0; v < n_views; ++v) a.v[v].grad = grad_image[v];
+    a.d_feat = d_feat;
+    a.d_pos = d_pos;
+    if (points->n == 0) {
+        if (d_pose && !params->grad_accumulate) {
+            int e = (int)cudaMemsetAsync(d_pose, 0, sizeof(double) * 6 * n_views, (cudaStream_t)stream);
+            if (e) return cuda_status(e, "memset d_pose");
+        }
+        return ok();
+    }
+    int e = launch_backward(a, model, vec_path(points), device_sms(), kMaxBwdBlocks, d_pose, stream);
+    if (e) return cuda_status(e, "backward launch");
+    return ok();
+}
+
+adop_status adop_point_masks(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                             const adop_pose *poses, const adop_params *params, uint8_t *mask, void *stream) {
+    adop_status s;
+    if ((s = check_params(params))) return s;
+    if ((s = check_points(points, false))) return s;
+    if ((s = check_views(n_views, cameras, poses, params, nullptr, points->channels, false))) return s;
+    if (!mask && points->n > 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "mask is NULL");
+    int model;
+    if (!uniform_model(n_views, cameras, model))
+        return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
+    if (points->n == 0) return ok();
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, nullptr, nullptr);
+    a.mask = mask;
+    int e = launch_masks(a, model, stream);
+    if (e) return cuda_status(e, "mask launch");
+    return ok();
+}
+
+adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream, int64_t *records,
+                                 int32_t *overflowed) {
+    if (!workspace || workspace_bytes < kHeaderBytes) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad workspace");
+    WsHeader h;
+    cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status((int)e, "workspace stats");
+    if (records) *records = (int64_t)h.records;
+    if (overflowed) *overflowed = h.overflow;
+    return ok();
+}
+
+const char *adop_last_error(void) { return g_err; }
+
+const char *adop_version(void) { return "adop-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

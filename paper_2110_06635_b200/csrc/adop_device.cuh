@@ -1,0 +1,166 @@
+// adop_device.cuh -- device-side building blocks of the sm_100a rasterizer.
+//
+// Every operation that decides an integer (pixel index, bounds, depth key,
+// discard / ghost bits, fuzzy and Eq. 11 case choices) uses explicitly
+// rounded fp32 intrinsics (__fmul_rn / __fadd_rn / __frcp_rn / __fdiv_rn) in
+// the operation order fixed by DESIGN.md R1-R14, so nvcc cannot contract it
+// into FMAs; this is what makes keys and masks bit-identical to the CPU oracle.
+// Citations: PAPER.md line numbers (Lnnn) with the equation they belong to.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "adop_internal.h"
+
+namespace adop {
+
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+
+// Round half away from zero (Eq. 3, reading R3).  x - trunc(x) is exact.
+__device__ __forceinline__ float round_away(float x) {
+    float t = truncf(x);
+    float d = __fsub_rn(x, t);
+    return fabsf(d) >= 0.5f ? __fadd_rn(t, copysignf(1.0f, x)) : t;
+}
+
+// 2^-l as an exact float (Eq. 2's 1/2^l).
+__device__ __forceinline__ float pow2_neg(int l) { return __int_as_float((127 - l) << 23); }
+
+// Counter-based hash (R11, R13): integer finalizer with two odd multipliers.
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ uint32_t h24(uint32_t salt, uint32_t gi) { return mix32(gi ^ salt) >> 8; }
+
+// Projection result of one point in one view (Eq. 2 with camera model R6).
+struct Proj {
+    float X, Y, Z;  // camera-space point (R1)
+    float u0, v0;   // layer-0 continuous pixel coordinates
+    float iz;       // 1 / Z (IEEE)
+};
+
+// Xc = R x + t in the pinned order ((r0 x + r1 y) + r2 z) + t (R1).
+__device__ __forceinline__ void to_camera(const ViewDesc &v, float x, float y, float z, float &X, float &Y,
+                                          float &Z) {
+    X = fadd(fadd(fadd(fmul(v.R[0], x), fmul(v.R[1], y)), fmul(v.R[2], z)), v.t[0]);
+    Y = fadd(fadd(fadd(fmul(v.R[3], x), fmul(v.R[4], y)), fmul(v.R[5], z)), v.t[1]);
+    Z = fadd(fadd(fadd(fmul(v.R[6], x), fmul(v.R[7], y)), fmul(v.R[8], z)), v.t[2]);
+}
+
+// Conservative, division-free frustum test (never rejects a point the exact
+// per-layer test would accept).  Z > z_near already holds.
+template <int MODEL>
+__device__ __forceinline__ bool precull_pass(const ViewDesc &v, float X, float Y, float Z) {
+    if (MODEL == 0) {
+        float su = fmaf(v.fx, X, v.cx * Z);
+        float sv = fmaf(v.fy, Y, v.cy * Z);
+        return su >= v.ulo * Z && su <= v.uhi * Z && sv >= v.vlo * Z && sv <= v.vhi * Z;
+    } else {
+        float r2z = fmaf(X, X, Y * Y);
+        return r2z <= v.r2cull * (Z * Z);
+    }
+}
+
+// Exact projection after the pre-cull (R2, R6): returns false if culled.
+template <int MODEL>
+__device__ __forceinline__ bool project_exact(const ViewDesc &v, Proj &p) {
+    p.iz = __frcp_rn(p.Z);
+    float xn = fmul(p.X, p.iz), yn = fmul(p.Y, p.iz);
+    float xd = xn, yd = yn;
+    if (MODEL == 1) {
+        float xx = fmul(xn, xn), yy = fmul(yn, yn), xy = fmul(xn, yn);
+        float r2 = fadd(xx, yy);
+        if (!(r2 <= v.r2_max)) return false;
+        float r4 = fmul(r2, r2), r6 = fmul(r4, r2);
+        float num = fadd(fadd(fadd(1.0f, fmul(v.k[0], r2)), fmul(v.k[1], r4)), fmul(v.k[2], r6));
+        float den = fadd(fadd(fadd(1.0f, fmul(v.k[3], r2)), fmul(v.k[4], r4)), fmul(v.k[5], r6));
+        if (!(den > 0.0f)) return false;
+        float radial = __fdiv_rn(num, den);
+        float a1 = fmul(2.0f, xy);
+        float a2 = fadd(r2, fmul(2.0f, xx));
+        float a3 = fadd(r2, fmul(2.0f, yy));
+        xd = fadd(fadd(fmul(xn, radial), fmul(v.p[0], a1)), fmul(v.p[1], a2));
+        yd = fadd(fadd(fmul(yn, radial), fmul(v.p[0], a3)), fmul(v.p[1], a1));
+    }
+    p.u0 = fadd(fmul(v.fx, xd), v.cx);
+    p.v0 = fadd(fmul(v.fy, yd), v.cy);
+    return true;
+}
+
+// Full projection of a point: validity (R7), pre-cull, exact projection.
+template <int MODEL>
+__device__ __forceinline__ bool project_point(const ViewDesc &v, float z_near, float x, float y, float z, Proj &p) {
+    to_camera(v, x, y, z, p.X, p.Y, p.Z);
+    if (!(p.Z > z_near && p.Z <= 3.402823466e38f)) return false;
+    if (!precull_pass<MODEL>(v, p.X, p.Y, p.Z)) return false;
+    return project_exact<MODEL>(v, p);
+}
+
+// Eq. 12 (L344) as R10/R11: number of leading layers at which the point is kept.
+__device__ __forceinline__ int keep_layers(const RasterArgs &a, const ViewDesc &v, float rw, float iz, uint32_t gi) {
+    if (!a.discard) return a.layers;
+    float rs0 = fmul(fmul(rw, v.feff), iz);
+    uint32_t h = h24(v.discard_salt, gi);
+    float om = fmul((float)(16777216u - h), 5.9604644775390625e-8f);  // 1 - beta, exact
+    int l = 0;
+#pragma unroll
+    for (int k = 0; k < ADOP_MAX_LAYERS; ++k) {
+        if (k < a.layers) {
+            float al = fmul(a.gamma, fmul(rs0, pow2_neg(k)));
+            if (l == k && fmul(al, al) > om) l = k + 1;
+        }
+    }
+    return l;
+}
+
+// Eqs. 3-4: layer-local pixel (u, v) and bounds.  Returns layer-local linear index or -1.
+__device__ __forceinline__ int layer_pixel(const ViewDesc &v, const Proj &p, int l, int &pu, int &pv) {
+    float s = pow2_neg(l);
+    float ru = round_away(fmul(p.u0, s));
+    float rv = round_away(fmul(p.v0, s));
+    if (!(ru >= 0.0f && ru < (float)v.wl[l] && rv >= 0.0f && rv < (float)v.hl[l])) return -1;
+    pu = (int)ru;
+    pv = (int)rv;
+    return pv * v.wl[l] + pu;
+}
+
+__device__ __forceinline__ uint64_t depth_key(float Z, uint32_t gi) {
+    return ((uint64_t)__float_as_uint(Z) << 32) | gi;  // R8
+}
+
+// Fuzzy depth test Eq. 6 (L209) as R9: z <= fl(fl(1+alpha) * m).
+__device__ __forceinline__ bool fuzzy_pass(float z, uint64_t key, float onepa) {
+    return z <= fmul(onepa, __uint_as_float((uint32_t)(key >> 32)));
+}
+
+// Streaming loads for the point arrays (read once: evict-first in L1 and L2).
+__device__ __forceinline__ float4 ld_stream4(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float ld_stream(const float *p) { return __ldcs(p); }
+
+// sm_90+ vector reduction: accum[0..3] += v in one L2 atomic.
+__device__ __forceinline__ void red_add_v4(float *addr, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add(float *addr, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_min_u64(uint64_t *addr, uint64_t v) {
+    asm volatile("red.global.min.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace adop

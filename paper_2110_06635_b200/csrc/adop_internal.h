@@ -1,0 +1,84 @@
+// adop_internal.h -- kernel argument blocks shared by the host API (adop_api.cu)
+// and the kernels (adop_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/adop.h"
+
+#define ADOP_MAX_VIEWS_PER_LAUNCH 16
+
+namespace adop {
+
+// Per-view constants, passed by value in the __grid_constant__ kernel argument block.
+struct ViewDesc {
+    float R[9];
+    float t[3];
+    float fx, fy, cx, cy;
+    float k[6];
+    float p[2];
+    float r2_max;
+    float feff;            // fl(fl(fx + fy) * 0.5): focal length of the discard radius (R10)
+    float ulo, uhi, vlo, vhi;  // conservative pre-cull window (pixels, all layers)
+    float r2cull;          // OpenCV8 pre-cull on X^2+Y^2 <= r2cull Z^2
+    uint32_t discard_salt; // hash salt of (seed, DISCARD, view id) (R11)
+    int32_t wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS], off[ADOP_MAX_LAYERS];
+    int32_t pixels;        // P
+    uint64_t *keys;
+    float *accum, *count, *image;
+    const float *grad;     // backward: dL/dI (image layout)
+};
+
+struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
+    uint32_t pix;   // pixel index within the view's pyramid (off_l + local)
+    uint32_t zbits; // bits of the point's camera-space z
+    uint32_t idx;   // shard-local point index
+    uint32_t view;  // view slot within the launch
+};
+
+struct WsHeader {
+    unsigned long long records;  // survivors emitted by the last depth pass
+    int32_t overflow;            // set when records > capacity
+    int32_t pad;
+};
+
+struct RasterArgs {
+    const float *x, *y, *z;
+    const float *radius;
+    float radius_uniform;
+    const float *feat;
+    int64_t n;
+    uint32_t goff;
+    int32_t channels;
+    int32_t layers;
+    int32_t nviews;
+    int32_t view_slot0;    // view slot of views[0] in the record's view field (multi-launch chunks)
+    float onepa;           // fl(1 + alpha)
+    float gamma;
+    float z_near;
+    int32_t discard;
+    uint32_t ghost_thr;    // floor(rho * 2^24); 0 = no ghosts
+    uint32_t ghost_salt;
+    int32_t grad_accumulate;
+    float bg[ADOP_MAX_CHANNELS];
+    WsHeader *hdr;
+    Record *records;
+    int64_t rec_capacity;
+    double *pose_partials; // [gridDim.x][nviews][6]
+    float *d_feat;
+    float *d_pos;          // [3][n]
+    uint8_t *mask;         // point-mask debug output [V][n]
+    ViewDesc v[ADOP_MAX_VIEWS_PER_LAUNCH];
+};
+
+// Launchers (adop_kernels.cu).  Return cudaError_t as int.
+int launch_clear(const RasterArgs &a, void *stream);
+int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream);
+int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream);
+int launch_resolve(const RasterArgs &a, void *stream);
+int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
+int launch_masks(const RasterArgs &a, int model, void *stream);
+int backward_grid(int sms);
+
+}  // namespace adop

@@ -1,0 +1,575 @@
+// adop_kernels.cu -- sm_100a kernels of the ADOP one-pixel point rasterizer.
+//
+//   k_clear    keys <- sentinel, accum/count <- 0                          (§4.5 setup)
+//   k_stream   <DEPTH>  all points: project (Eq. 2), round (Eq. 3), bounds (Eq. 4),
+//                       ghost split (§4.3), discard (Eq. 12), 64-bit red.min of the packed
+//                       key per layer (§4.5 depth-only pass, min_z of Eq. 6), survivor records
+//              <BLEND>  overflow fallback: same sweep, fuzzy test + accumulate
+//              <MASKS>  debug/parity: per point per view layer mask
+//   k_blend    survivors: fuzzy test (Eq. 6) + vector red.add of tau and the count (§4.5)
+//   k_resolve  per pixel: Eq. 7 mean or background, planar NCHW output
+//   k_backward all points: texture gradient (R24) and ghost gradient Eqs. 9-11 + chain rule
+//              (Eq. 8) into d_pos and per-block tangent pose partials (Eq. 17)
+//   k_pose_reduce  deterministic fp64 sum of the per-block pose partials
+//
+// Streaming kernels are persistent (grid = SMs x resident blocks) and walk the
+// cloud in warp chunks of 128 points (4 consecutive points per lane, float4 loads
+// of the SoA rows), so every warp-collective below is warp-uniform.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "adop_device.cuh"
+
+namespace adop {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kCap = 256;  // records buffered per warp in shared memory before a flush
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxBwdBlocks = 2048;
+
+enum { MODE_DEPTH = 0, MODE_BLEND = 1, MODE_MASKS = 2 };
+
+// --------------------------------------------------------------------------- //
+// clear
+// --------------------------------------------------------------------------- //
+__global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ RasterArgs a) {
+    const ViewDesc &v = a.v[blockIdx.y];
+    const int64_t P = v.pixels;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t sentinel = 0x7FFFFFFFFFFFFFFFull;
+    for (int64_t p = tid; p < P; p += stride) {
+        v.keys[p] = sentinel;
+        v.count[p] = 0.0f;
+    }
+    const int64_t PA = P * a.channels;
+    float *acc = v.accum;
+    if ((reinterpret_cast<uintptr_t>(acc) & 15) == 0) {
+        for (int64_t q = tid; q < PA / 4; q += stride) reinterpret_cast<float4 *>(acc)[q] = make_float4(0, 0, 0, 0);
+        for (int64_t q = (PA / 4) * 4 + tid; q < PA; q += stride) acc[q] = 0.0f;
+    } else {
+        for (int64_t q = tid; q < PA; q += stride) acc[q] = 0.0f;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        a.hdr->records = 0ull;
+        a.hdr->overflow = 0;
+    }
+}
+
+// --------------------------------------------------------------------------- //
+// point loads for one warp chunk: lane owns points i0..i0+3
+// --------------------------------------------------------------------------- //
+template <bool VEC>
+__device__ __forceinline__ void load_points(const RasterArgs &a, int64_t i0, float (&px)[4], float (&py)[4],
+                                            float (&pz)[4], float (&pr)[4]) {
+    if (VEC && i0 + 3 < a.n) {
+        float4 X = ld_stream4(a.x + i0), Y = ld_stream4(a.y + i0), Z = ld_stream4(a.z + i0);
+        px[0] = X.x; px[1] = X.y; px[2] = X.z; px[3] = X.w;
+        py[0] = Y.x; py[1] = Y.y; py[2] = Y.z; py[3] = Y.w;
+        pz[0] = Z.x; pz[1] = Z.y; pz[2] = Z.z; pz[3] = Z.w;
+        if (a.radius) {
+            float4 Rw = ld_stream4(a.radius + i0);
+            pr[0] = Rw.x; pr[1] = Rw.y; pr[2] = Rw.z; pr[3] = Rw.w;
+        } else {
+            pr[0] = pr[1] = pr[2] = pr[3] = a.radius_uniform;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = i0 + j;
+            if (i < a.n) {
+                px[j] = ld_stream(a.x + i);
+                py[j] = ld_stream(a.y + i);
+                pz[j] = ld_stream(a.z + i);
+                pr[j] = a.radius ? ld_stream(a.radius + i) : a.radius_uniform;
+            } else {
+                px[j] = py[j] = pz[j] = __int_as_float(0x7fc00000);  // NaN: culled by the validity test
+                pr[j] = 0.0f;
+            }
+        }
+    }
+}
+
+// Warp-level flush of the shared-memory record buffer into the global survivor list.
+__device__ __forceinline__ void flush_records(const RasterArgs &a, Record *buf, int &wcount, int lane) {
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.hdr->records, (unsigned long long)wcount);
+    base = __shfl_sync(kFull, base, 0);
+    bool of = false;
+    for (int k = lane; k < wcount; k += 32) {
+        const unsigned long long r = base + (unsigned long long)k;
+        if (r < (unsigned long long)a.rec_capacity)
+            reinterpret_cast<uint4 *>(a.records)[r] = reinterpret_cast<const uint4 *>(buf)[k];
+        else
+            of = true;
+    }
+    if (__any_sync(kFull, of) && lane == 0) atomicExch(&a.hdr->overflow, 1);
+    __syncwarp();
+    wcount = 0;
+}
+
+template <bool VEC4>
+__device__ __forceinline__ void accumulate_feature(const RasterArgs &a, const ViewDesc &v, int64_t idx,
+                                                   uint32_t pix) {
+    const int C = a.channels;
+    const float *f = a.feat + idx * C;
+    float *acc = v.accum + (int64_t)pix * C;
+    if (VEC4) {
+        for (int c = 0; c < C; c += 4) red_add_v4(acc + c, __ldg(reinterpret_cast<const float4 *>(f + c)));
+    } else {
+        for (int c = 0; c < C; ++c) red_add(acc + c, __ldg(f + c));
+    }
+    red_add(v.count + pix, 1.0f);
+}
+
+// --------------------------------------------------------------------------- //
+// streaming sweep over all points (depth pass / blend fallback / masks)
+// --------------------------------------------------------------------------- //
+template <int MODEL, bool VEC, int MODE, bool VEC4>
+__global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ RasterArgs a) {
+    __shared__ __align__(16) Record sbuf[MODE == MODE_DEPTH ? kWarps : 1][MODE == MODE_DEPTH ? kCap : 1];
+    if (MODE == MODE_BLEND && !*(volatile int32_t *)&a.hdr->overflow) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    int wcount = 0;
+    const int64_t nchunks = (a.n + 127) / 128;
+    for (int64_t ch = (int64_t)blockIdx.x * kWarps + wid; ch < nchunks; ch += (int64_t)gridDim.x * kWarps) {
+        const int64_t i0 = ch * 128 + lane * 4;
+        float px[4], py[4], pz[4], pr[4];
+        load_points<VEC>(a, i0, px, py, pz, pr);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = i0 + j;
+            const bool in = i < a.n;
+            const uint32_t gi = a.goff + (uint32_t)i;
+            const bool ghost = in && a.ghost_thr != 0u && h24(a.ghost_salt, gi) < a.ghost_thr;
+            const bool live = MODE == MODE_MASKS ? in : (in && !ghost);
+            if (!__any_sync(kFull, live)) continue;
+            for (int vs = 0; vs < a.nviews; ++vs) {
+                const ViewDesc &v = a.v[vs];
+                Proj p;
+                const bool ok = live && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p);
+                if (MODE == MODE_MASKS) {
+                    unsigned m = ghost ? 0x80u : 0u;
+                    if (ok) {
+                        const int nk = keep_layers(a, v, pr[j], p.iz, gi);
+                        for (int l = 0; l < a.layers; ++l) {
+                            int pu, pv;
+                            if (l < nk && layer_pixel(v, p, l, pu, pv) >= 0) m |= 1u << l;
+                        }
+                    }
+                    if (in) a.mask[(int64_t)vs * a.n + i] = (uint8_t)m;
+                    continue;
+                }
+                if (!__any_sync(kFull, ok)) continue;
+                const int nk = ok ? keep_layers(a, v, pr[j], p.iz, gi) : 0;
+                const uint64_t key = depth_key(p.Z, gi);
+#pragma unroll
+                for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {
+                    if (l >= a.layers) break;
+                    int pu, pv;
+                    const int loc = l < nk ? layer_pixel(v, p, l, pu, pv) : -1;
+                    const bool hit = loc >= 0;
+                    const uint32_t pix = (uint32_t)(v.off[l] + loc);
+                    if (MODE == MODE_DEPTH) {
+                        if (hit) red_min_u64(v.keys + pix, key);
+                        const unsigned b = __ballot_sync(kFull, hit);
+                        if (b) {
+                            if (wcount + 32 > kCap) flush_records(a, sbuf[wid], wcount, lane);
+                            if (hit) {
+                                Record r;
+                                r.pix = pix;
+                                r.zbits = __float_as_uint(p.Z);
+                                r.idx = (uint32_t)i;
+                                r.view = (uint32_t)vs;
+                                sbuf[wid][wcount + __popc(b & lt)] = r;
+                            }
+                            wcount += __popc(b);
+                        }
+                    } else {  // MODE_BLEND: re-streamed accumulate (only after a record overflow)
+                        if (hit && fuzzy_pass(p.Z, v.keys[pix], a.onepa)) accumulate_feature<VEC4>(a, v, i, pix);
+                    }
+                }
+            }
+        }
+    }
+    if (MODE == MODE_DEPTH && wcount > 0) flush_records(a, sbuf[wid], wcount, lane);
+}
+
+// --------------------------------------------------------------------------- //
+// blend over survivor records (§4.5 accumulate pass)
+// --------------------------------------------------------------------------- //
+template <bool VEC4>
+__global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ RasterArgs a) {
+    if (*(volatile int32_t *)&a.hdr->overflow) return;
+    const unsigned long long total = *(volatile unsigned long long *)&a.hdr->records;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
+        const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
+        const ViewDesc &v = a.v[rec.w];
+        const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
+        if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
+    }
+}
+
+// --------------------------------------------------------------------------- //
+// resolve: Eq. 7 (mean or background), planar per-layer output
+// --------------------------------------------------------------------------- //
+template <bool VEC4>
+__global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ RasterArgs a) {
+    const ViewDesc &v = a.v[blockIdx.y];
+    const int C = a.channels;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
+        int l = 0;
+#pragma unroll
+        for (int k = 1; k < ADOP_MAX_LAYERS; ++k)
+            if (k < a.layers && p >= v.off[k]) l = k;
+        const int64_t j = p - v.off[l];
+        const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+        const float cnt = __ldcs(v.count + p);
+        float *img = v.image + (int64_t)C * v.off[l] + j;
+        const float *acc = v.accum + p * C;
+        if (VEC4) {
+            for (int c = 0; c < C; c += 4) {
+                const float4 s = __ldcs(reinterpret_cast<const float4 *>(acc + c));
+                const bool hit = cnt > 0.0f;
+                __stcs(img + (c + 0) * hw, hit ? __fdiv_rn(s.x, cnt) : a.bg[c + 0]);
+                __stcs(img + (c + 1) * hw, hit ? __fdiv_rn(s.y, cnt) : a.bg[c + 1]);
+                __stcs(img + (c + 2) * hw, hit ? __fdiv_rn(s.z, cnt) : a.bg[c + 2]);
+                __stcs(img + (c + 3) * hw, hit ? __fdiv_rn(s.w, cnt) : a.bg[c + 3]);
+            }
+        } else {
+            for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fdiv_rn(acc[c], cnt) : a.bg[c]);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------- //
+// backward
+// --------------------------------------------------------------------------- //
+// Image-space gradient contribution of one neighbour q (Eq. 11 as R14, times G as R16).
+template <int CT>
+__device__ __forceinline__ float neighbour_term(const RasterArgs &a, const ViewDesc &v, int l, int qu, int qv,
+                                                float z, const float *tau) {
+    if (qu < 0 || qv < 0 || qu >= v.wl[l] || qv >= v.hl[l]) return 0.0f;  // outside: no term
+    const int j = qv * v.wl[l] + qu;
+    const int q = v.off[l] + j;
+    const float nq = v.count[q];
+    float factor;
+    if (nq == 0.0f) {
+        factor = 1.0f;                                     // case 1: background neighbour
+    } else {
+        const float m = __uint_as_float((uint32_t)(v.keys[q] >> 32));
+        if (z > fmul(a.onepa, m)) return 0.0f;             // case 2: behind
+        factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
+    }
+    const int C = CT > 0 ? CT : a.channels;
+    const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+    const float *G = v.grad + (int64_t)C * v.off[l] + j;
+    const float *I = v.image + (int64_t)C * v.off[l] + j;
+    float d = 0.0f;
+#pragma unroll
+    for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
+        if (CT == 0 && c >= C) break;
+        d = fmaf(__ldg(G + c * hw), tau[c] - __ldg(I + c * hw), d);
+    }
+    return factor * d;
+}
+
+template <int MODEL>
+__device__ __forceinline__ void jacobian(const ViewDesc &v, const Proj &p, float J[6]) {
+    const float iz = p.iz, xn = p.X * iz, yn = p.Y * iz;
+    // dn/dXc = [[iz, 0, -xn iz], [0, iz, -yn iz]]
+    float D00 = 1.f, D01 = 0.f, D10 = 0.f, D11 = 1.f;
+    if (MODEL == 1) {
+        const float r2 = xn * xn + yn * yn;
+        const float num = 1.f + r2 * (v.k[0] + r2 * (v.k[1] + r2 * v.k[2]));
+        const float den = 1.f + r2 * (v.k[3] + r2 * (v.k[4] + r2 * v.k[5]));
+        const float dnum = v.k[0] + r2 * (2.f * v.k[1] + 3.f * r2 * v.k[2]);
+        const float dden = v.k[3] + r2 * (2.f * v.k[4] + 3.f * r2 * v.k[5]);
+        const float rad = num / den;
+        const float drad = (dnum * den - num * dden) / (den * den);
+        const float p1 = v.p[0], p2 = v.p[1];
+        D00 = rad + 2.f * xn * xn * drad + 2.f * p1 * yn + 6.f * p2 * xn;
+        D01 = 2.f * xn * yn * drad + 2.f * p1 * xn + 2.f * p2 * yn;
+        D10 = D01;
+        D11 = rad + 2.f * yn * yn * drad + 6.f * p1 * yn + 2.f * p2 * xn;
+    }
+    const float a0 = v.fx * iz, a1 = v.fy * iz;
+    // J = diag(f) D N, N = [[1, 0, -xn], [0, 1, -yn]] * iz
+    J[0] = a0 * D00; J[1] = a0 * D01; J[2] = -a0 * (D00 * xn + D01 * yn);
+    J[3] = a1 * D10; J[4] = a1 * D11; J[5] = -a1 * (D10 * xn + D11 * yn);
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    return x;
+}
+
+template <int MODEL, bool VEC, int CT>
+__global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ RasterArgs a) {
+    __shared__ double spose[ADOP_MAX_VIEWS_PER_LAUNCH * 6];
+    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x) spose[t] = 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int C = CT > 0 ? CT : a.channels;
+    constexpr int CR = CT > 0 ? CT : 1;  // register accumulators (generic C works in global memory)
+    const int64_t nchunks = (a.n + 127) / 128;
+    for (int64_t ch = (int64_t)blockIdx.x * kWarps + wid; ch < nchunks; ch += (int64_t)gridDim.x * kWarps) {
+        const int64_t i0 = ch * 128 + lane * 4;
+        float px[4], py[4], pz[4], pr[4];
+        load_points<VEC>(a, i0, px, py, pz, pr);
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = i0 + j;
+            const bool in = i < a.n;
+            const uint32_t gi = a.goff + (uint32_t)i;
+            const bool ghost = in && a.ghost_thr != 0u && h24(a.ghost_salt, gi) < a.ghost_thr;
+            float dt[CR];
+#pragma unroll
+            for (int c = 0; c < CR; ++c) dt[c] = 0.0f;
+            if (CT == 0 && in && a.d_feat && !a.grad_accumulate)
+                for (int c = 0; c < C; ++c) a.d_feat[i * C + c] = 0.0f;
+            float dxx = 0.f, dxy = 0.f, dxz = 0.f;
+            float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
+            bool tau_loaded = false;
+            for (int vs = 0; vs < a.nviews; ++vs) {
+                const ViewDesc &v = a.v[vs];
+                Proj p;
+                const bool ok = in && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p);
+                if (!__any_sync(kFull, ok)) continue;
+                const int nk = ok ? keep_layers(a, v, pr[j], p.iz, gi) : 0;
+                float gu = 0.f, gv = 0.f;
+                bool gc = false;
+                for (int l = 0; l < a.layers; ++l) {
+                    if (l >= nk) break;
+                    int pu, pv;
+                    const int loc = layer_pixel(v, p, l, pu, pv);
+                    if (loc < 0) continue;
+                    if (!ghost) {
+                        // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
+                        const int q = v.off[l] + loc;
+                        if (!fuzzy_pass(p.Z, v.keys[q], a.onepa)) continue;
+                        const float cnt = v.count[q];
+                        const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+                        const float *G = v.grad + (int64_t)C * v.off[l] + loc;
+                        if (CT > 0) {
+#pragma unroll
+                            for (int c = 0; c < CR; ++c) dt[c] += __fdiv_rn(__ldg(G + c * hw), cnt);
+                        } else if (a.d_feat) {
+                            for (int c = 0; c < C; ++c) a.d_feat[i * C + c] += __fdiv_rn(__ldg(G + c * hw), cnt);
+                        }
+                    } else {
+                        if (!tau_loaded) {
+                            for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + i * C + c);
+                            tau_loaded = true;
+                        }
+                        // Eqs. 9-11: signed central differences over the 4-neighbourhood (R14, R15)
+                        const float dup = neighbour_term<CT>(a, v, l, pu + 1, pv, p.Z, tau);
+                        const float dum = neighbour_term<CT>(a, v, l, pu - 1, pv, p.Z, tau);
+                        const float dvp = neighbour_term<CT>(a, v, l, pu, pv + 1, p.Z, tau);
+                        const float dvm = neighbour_term<CT>(a, v, l, pu, pv - 1, p.Z, tau);
+                        const float s = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
+                        gu += s * (dup - dum);
+                        gv += s * (dvp - dvm);
+                        gc = true;
+                    }
+                }
+                if (!__any_sync(kFull, gc)) continue;
+                float w0 = 0.f, w1 = 0.f, w2 = 0.f;
+                if (gc) {
+                    float J[6];
+                    jacobian<MODEL>(v, p, J);
+                    w0 = J[0] * gu + J[3] * gv;  // w = J^T g = dL/dXc
+                    w1 = J[1] * gu + J[4] * gv;
+                    w2 = J[2] * gu + J[5] * gv;
+                    dxx += v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2;  // dx = R^T w
+                    dxy += v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2;
+                    dxz += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
+                }
+                // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64
+                double t6[6];
+                t6[0] = w0; t6[1] = w1; t6[2] = w2;
+                t6[3] = gc ? (double)(p.Y * w2 - p.Z * w1) : 0.0;
+                t6[4] = gc ? (double)(p.Z * w0 - p.X * w2) : 0.0;
+                t6[5] = gc ? (double)(p.X * w1 - p.Y * w0) : 0.0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const double s = warp_sum(t6[k]);
+                    if (lane == 0) atomicAdd(&spose[vs * 6 + k], s);
+                }
+            }
+            if (in) {
+                if (CT > 0 && a.d_feat) {
+                    float *df = a.d_feat + i * C;
+#pragma unroll
+                    for (int c = 0; c < CR; ++c) df[c] = a.grad_accumulate ? df[c] + dt[c] : dt[c];
+                }
+                if (a.d_pos) {
+                    float *dp = a.d_pos;
+                    if (a.grad_accumulate) {
+                        if (dxx != 0.f || dxy != 0.f || dxz != 0.f) {
+                            dp[i] += dxx; dp[a.n + i] += dxy; dp[2 * a.n + i] += dxz;
+                        }
+                    } else {
+                        dp[i] = dxx; dp[a.n + i] = dxy; dp[2 * a.n + i] = dxz;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x)
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = spose[t];
+}
+
+// d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_pose_reduce(const double *partials, int nblocks, int nvals, double *d_pose,
+                                                     int accumulate) {
+    __shared__ double s[256];
+    const int t = blockIdx.x;
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * nvals + t];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) d_pose[t] = accumulate ? d_pose[t] + s[0] : s[0];
+}
+
+// --------------------------------------------------------------------------- //
+// launchers
+// --------------------------------------------------------------------------- //
+template <typename K>
+static int resident_grid(K kernel, int sms, int64_t work_items_per_block, int64_t items) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t need = (items + work_items_per_block - 1) / work_items_per_block;
+    int64_t g = (int64_t)sms * per_sm;
+    if (need < g) g = need;
+    return (int)(g < 1 ? 1 : g);
+}
+
+static bool feat_vec4(const RasterArgs &a) {
+    return a.channels % 4 == 0 && (reinterpret_cast<uintptr_t>(a.feat) & 15) == 0;
+}
+
+static bool accum_vec4(const RasterArgs &a) {
+    if (a.channels % 4 != 0) return false;
+    for (int v = 0; v < a.nviews; ++v)
+        if (reinterpret_cast<uintptr_t>(a.v[v].accum) & 15) return false;
+    return true;
+}
+
+int launch_clear(const RasterArgs &a, void *stream) {
+    int64_t maxP = 1;
+    for (int v = 0; v < a.nviews; ++v) maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+    int64_t bx = (maxP + kThreads * 4 - 1) / (kThreads * 4);
+    if (bx > 1024) bx = 1024;
+    dim3 grid((unsigned)bx, (unsigned)a.nviews);
+    k_clear<<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+template <int MODEL, bool VEC>
+static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
+    auto k = k_stream<MODEL, VEC, MODE_DEPTH, false>;
+    int g = resident_grid(k, sms, kWarps * 128, a.n);
+    k<<<g, kThreads, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream) {
+    if (model == 0) return vec ? launch_depth_t<0, true>(a, sms, stream) : launch_depth_t<0, false>(a, sms, stream);
+    return vec ? launch_depth_t<1, true>(a, sms, stream) : launch_depth_t<1, false>(a, sms, stream);
+}
+
+template <int MODEL, bool VEC, bool VEC4>
+static int launch_blend_t(const RasterArgs &a, int sms, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    {
+        auto k = k_blend<VEC4>;
+        int g = resident_grid(k, sms, kThreads, (int64_t)sms * 64 * kThreads);
+        k<<<g, kThreads, 0, s>>>(a);
+    }
+    {   // overflow fallback: returns immediately unless the record list overflowed
+        auto k = k_stream<MODEL, VEC, MODE_BLEND, VEC4>;
+        int g = resident_grid(k, sms, kWarps * 128, a.n);
+        k<<<g, kThreads, 0, s>>>(a);
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream) {
+    const bool v4 = feat_vec4(a) && accum_vec4(a);
+    if (model == 0) {
+        if (vec) return v4 ? launch_blend_t<0, true, true>(a, sms, stream) : launch_blend_t<0, true, false>(a, sms, stream);
+        return v4 ? launch_blend_t<0, false, true>(a, sms, stream) : launch_blend_t<0, false, false>(a, sms, stream);
+    }
+    if (vec) return v4 ? launch_blend_t<1, true, true>(a, sms, stream) : launch_blend_t<1, true, false>(a, sms, stream);
+    return v4 ? launch_blend_t<1, false, true>(a, sms, stream) : launch_blend_t<1, false, false>(a, sms, stream);
+}
+
+int launch_resolve(const RasterArgs &a, void *stream) {
+    int64_t maxP = 1;
+    for (int v = 0; v < a.nviews; ++v) maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+    int64_t bx = (maxP + kThreads - 1) / kThreads;
+    if (bx > 4096) bx = 4096;
+    dim3 grid((unsigned)bx, (unsigned)a.nviews);
+    if (accum_vec4(a))
+        k_resolve<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else
+        k_resolve<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int backward_grid(int sms) {
+    int g = sms * 8;
+    return g > kMaxBwdBlocks ? kMaxBwdBlocks : g;
+}
+
+template <int MODEL, bool VEC, int CT>
+static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    auto k = k_backward<MODEL, VEC, CT>;
+    int g = resident_grid(k, sms, kWarps * 128, a.n);
+    if (g > grid_cap) g = grid_cap;
+    k<<<g, kThreads, 0, s>>>(a);
+    if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, g, a.nviews * 6, d_pose, a.grad_accumulate);
+    return (int)cudaGetLastError();
+}
+
+template <int MODEL, bool VEC>
+static int launch_backward_c(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
+    if (a.channels == 4) return launch_backward_t<MODEL, VEC, 4>(a, sms, grid_cap, d_pose, stream);
+    if (a.channels == 8) return launch_backward_t<MODEL, VEC, 8>(a, sms, grid_cap, d_pose, stream);
+    return launch_backward_t<MODEL, VEC, 0>(a, sms, grid_cap, d_pose, stream);
+}
+
+int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid_cap, double *d_pose, void *stream) {
+    if (model == 0) return vec ? launch_backward_c<0, true>(a, sms, grid_cap, d_pose, stream)
+                               : launch_backward_c<0, false>(a, sms, grid_cap, d_pose, stream);
+    return vec ? launch_backward_c<1, true>(a, sms, grid_cap, d_pose, stream)
+               : launch_backward_c<1, false>(a, sms, grid_cap, d_pose, stream);
+}
+
+int launch_masks(const RasterArgs &a, int model, void *stream) {
+    const int64_t nchunks = (a.n + 127) / 128;
+    int64_t g = (nchunks + kWarps - 1) / kWarps;
+    if (g < 1) g = 1;
+    if (g > 65535) g = 65535;
+    if (model == 0)
+        k_stream<0, false, MODE_MASKS, false><<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else
+        k_stream<1, false, MODE_MASKS, false><<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace adop

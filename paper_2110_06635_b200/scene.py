@@ -321,8 +321,10 @@ class Workload:
 
 
 def workload(idx: int, device="cpu", n: Optional[int] = None, n_views: Optional[int] = None,
-             morton_block: int = 1024) -> Workload:
-    """BASELINE.json configs[idx] with optional reduced n / views (for parity-size cases)."""
+             morton_block: int = 1024, shard: int = 0) -> Workload:
+    """BASELINE.json configs[idx] with optional reduced n / views (for parity-size cases).
+
+    shard > 0 draws a different cloud of the same room (the shard of rank `shard` in a point-sharded run)."""
     if idx == 0:
         n = 10_000 if n is None else n
         cloud = uniform_cube_cloud(n, 4, device=device)
@@ -338,9 +340,9 @@ def workload(idx: int, device="cpu", n: Optional[int] = None, n_views: Optional[
     n = spec["n"] if n is None else n
     V = spec["views"] if n_views is None else n_views
     room = make_room(spec["S"])
-    cloud = room_cloud(n, room, spec["C"], device=device)
+    cloud = room_cloud(n, room, spec["C"], seed=SEED_SCENE + 1000 * shard, device=device)
     if morton_block:
-        cloud = apply_order(cloud, blocked_morton_order(cloud.pos, morton_block))
+        cloud = apply_order(cloud, blocked_morton_order(cloud.pos, morton_block, seed=SEED_SCENE + shard))
     poses = room_poses(V, room)
     if spec["model"] == PINHOLE:
         cams = [pinhole(spec["w"], spec["h"]) for _ in range(V)]

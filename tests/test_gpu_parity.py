@@ -1,0 +1,244 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Marked gpu: run on the B200 box (pytest -m gpu).  Keys, counts and masks must be bit-exact; floating
+outputs within the tolerances documented in tests/parity.py.
+"""
+import dataclasses
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2110_06635_b200 import adop as A
+from paper_2110_06635_b200 import scene as S
+
+from .parity import compare_backward, compare_forward, grads_for, keys_u64, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tiny_config_forward():
+    w = S.workload(0)
+    r = run_gpu(w.cloud, w.cameras, w.poses, w.params)
+    _, fwd, _ = run_oracle(w.cloud, w.cameras, w.poses, w.params)
+    compare_forward(r, fwd, ctx="tiny")
+    assert (fwd.count > 0).sum() > 1000
+
+
+def test_tiny_config_with_discard_ghosts_background_and_backward():
+    w = S.workload(0)
+    prm = dataclasses.replace(w.params, discard=True, ghost_rate=0.3, background=[0.1, 0.2, 0.3, 0.4])
+    cloud = dataclasses.replace(w.cloud, radius=torch.full_like(w.cloud.radius, 0.02))
+    G = grads_for(w.cameras, prm.layers, 4)
+    r = run_gpu(cloud, w.cameras, w.poses, prm, grads=G)
+    _, fwd, bwd = run_oracle(cloud, w.cameras, w.poses, prm, grads=G)
+    compare_forward(r, fwd, ctx="tiny+")
+    compare_backward(r, bwd, ctx="tiny+")
+    assert np.abs(bwd.dx).sum() > 0 and np.abs(bwd.dtau).sum() > 0
+
+
+@pytest.mark.parametrize("idx,n,views", [(1, 200_000, 4), (2, 200_000, 1), (4, 60_000, 16)])
+def test_room_configs_reduced(idx, n, views):
+    """configs[1], [2], [4] at reduced N (full camera, layers, C, views): several tiles + ragged tails."""
+    w = S.workload(idx, n=n + 13, n_views=views)
+    G = grads_for(w.cameras, w.params.layers, w.cloud.channels) if w.backward else None
+    r = run_gpu(w.cloud, w.cameras, w.poses, w.params, grads=G)
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=G)
+    compare_forward(r, fwd, ctx=w.name)
+    if G is not None:
+        compare_backward(r, bwd, ctx=w.name)
+    assert (fwd.count > 0).sum() > 10_000
+
+
+@pytest.mark.parametrize("C,ghost", [(1, 0.0), (3, 0.25), (8, 0.5), (5, 0.1)])
+def test_channels_scalar_path_uniform_radius(C, ghost):
+    """generic C, the unaligned (scalar-load) path via an odd row stride, radius=NULL."""
+    room = S.make_room(6.0)
+    base = S.room_cloud(40_003, room, C, seed=31)
+    stride = base.n + 3
+    pos = torch.zeros(3, stride)
+    pos[:, :base.n] = base.pos
+    cams = [S.opencv_camera(320, 200, seed=7), S.opencv_camera(320, 200, seed=8)]
+    cams = [dataclasses.replace(c, fx=160.0, fy=160.0) for c in cams]
+    cams = [dataclasses.replace(c, r2_max=S.distortion_r2_max(c)) for c in cams]
+    poses = S.room_poses(2, room, seed=2)
+    prm = S.Params(layers=4, discard=True, ghost_rate=ghost, seed=99, view_id_base=3)
+    dev = torch.device("cuda")
+    pts = A.Points(pos.to(dev), None, base.feat.to(dev), global_offset=1234, radius_uniform=0.02, n=base.n)
+    ap = A.Params(prm, C)
+    pyrs = A.alloc_pyramids(cams, prm.layers, C, dev)
+    ws = A.Workspace(pts, 2, ap, dev)
+    A.rasterize_forward(pts, cams, poses, ap, pyrs, ws)
+    G = grads_for(cams, prm.layers, C)
+    d_feat = torch.empty(base.n, C, device=dev)
+    d_pos = torch.empty(3, base.n, device=dev)
+    d_pose = torch.empty(2, 6, dtype=torch.float64, device=dev)
+    A.rasterize_backward(pts, cams, poses, ap, pyrs, [g.to(dev) for g in G], ws, d_feat, d_pos, d_pose)
+    torch.cuda.synchronize()
+    opts = O.Points(pos.numpy(), None, base.feat.numpy(), 1234, radius_uniform=0.02)
+    opts.n = base.n
+    opts.s.n, opts.s.pos_stride = base.n, stride
+    fwd = O.forward(opts, cams, poses, prm)
+    bwd = O.backward(opts, cams, poses, prm, fwd, np.stack([g.numpy() for g in G]))
+
+    class R:
+        pass
+    r = R()
+    r.pyrs, r.d_feat, r.d_pos, r.d_pose = pyrs, d_feat, d_pos, d_pose
+    compare_forward(r, fwd, ctx=f"C={C}")
+    compare_backward(r, bwd, ctx=f"C={C}")
+
+
+def test_point_masks_bitexact():
+    w = S.workload(2, n=150_001)
+    prm = dataclasses.replace(w.params, ghost_rate=0.25)
+    dev = torch.device("cuda")
+    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, prm)
+    m = r.masks().cpu().numpy()
+    mo = O.point_masks(O.Points.from_cloud(w.cloud), w.cameras, w.poses, prm)
+    assert np.array_equal(m, mo), np.nonzero(m != mo)
+    assert (mo & 0x1F).any() and (mo & 0x80).any()
+
+
+def test_empty_cloud():
+    cam = S.pinhole(64, 48)
+    cloud = S.Cloud(torch.zeros(3, 0), torch.zeros(0), torch.zeros(0, 4))
+    prm = S.Params(layers=3, background=[1.0, 2.0, 3.0, 4.0])
+    G = grads_for([cam], 3, 4)
+    r = run_gpu(cloud, [cam], [S.tiny_pose()], prm, grads=G)
+    _, fwd, bwd = run_oracle(cloud, [cam], [S.tiny_pose()], prm, grads=G)
+    compare_forward(r, fwd, ctx="empty")
+    assert (keys_u64(r.pyrs[0].keys) == np.uint64(A.SENTINEL)).all()
+    assert not r.d_pose.cpu().numpy().any()
+
+
+def test_record_overflow_falls_back_to_restreaming():
+    w = S.workload(1, n=100_000, n_views=2)
+    r = run_gpu(w.cloud, w.cameras, w.poses, w.params, record_capacity=1000)
+    rec, of = r.ws.stats()
+    assert of and rec > 1000
+    _, fwd, _ = run_oracle(w.cloud, w.cameras, w.poses, w.params)
+    compare_forward(r, fwd, ctx="overflow")
+    r2 = run_gpu(w.cloud, w.cameras, w.poses, w.params)
+    rec2, of2 = r2.ws.stats()
+    assert not of2 and rec2 == rec
+
+
+def test_grad_accumulate_adds():
+    w = S.workload(2, n=50_000)
+    dev = torch.device("cuda")
+    G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, w.cloud.channels)]
+    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params)
+    r.forward()
+    f1, p1, q1 = [t.clone() for t in r.backward(G)]
+    r.params.s.grad_accumulate = 1
+    r.backward(G)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(r.d_feat, 2 * f1)
+    torch.testing.assert_close(r.d_pos, 2 * p1)
+    torch.testing.assert_close(r.d_pose, 2 * q1)
+
+
+def test_phase_split_point_sharding_on_one_gpu():
+    """The point-sharded forward (§8e): each shard runs phase 1 into its own keys, keys are min-reduced,
+    each shard runs phase 2 against the global keys, accum/count are sum-reduced, then phase 3.  Done here
+    with 3 shards on one GPU and torch.minimum / + in place of the collectives: keys must equal the
+    unsharded run bit for bit."""
+    w = S.workload(1, n=120_000, n_views=2)
+    dev = torch.device("cuda")
+    cloud = w.cloud.to(dev)
+    C = cloud.channels
+    ap = A.Params(w.params, C)
+    full = A.Renderer(cloud, w.cameras, w.poses, w.params)
+    full.forward()
+    bounds = [0, 37_001, 80_000, cloud.n]
+    shards = []
+    for a, b in zip(bounds, bounds[1:]):
+        pts = A.Points.from_cloud(cloud.slice(a, b), global_offset=a)
+        pyrs = A.alloc_pyramids(w.cameras, w.params.layers, C, dev)
+        ws = A.Workspace(pts, 2, ap, dev)
+        A.forward_depth(pts, w.cameras, w.poses, ap, pyrs, ws)
+        shards.append((pts, pyrs, ws))
+    for v in range(2):
+        kmin = torch.stack([s[1][v].keys for s in shards]).amin(0)
+        for s in shards:
+            s[1][v].keys.copy_(kmin)
+    for pts, pyrs, ws in shards:
+        A.forward_blend(pts, w.cameras, w.poses, ap, pyrs, ws)
+    for v in range(2):
+        tot = torch.stack([s[1][v].ac for s in shards]).sum(0)
+        for s in shards:
+            s[1][v].ac.copy_(tot)
+    pts0, pyrs0, ws0 = shards[0]
+    A.forward_resolve(pts0, w.cameras, w.poses, ap, pyrs0, ws0)
+    torch.cuda.synchronize()
+    for v in range(2):
+        assert torch.equal(pyrs0[v].keys, full.pyrs[v].keys)
+        assert torch.equal(pyrs0[v].count, full.pyrs[v].count)
+        torch.testing.assert_close(pyrs0[v].image, full.pyrs[v].image, rtol=1e-5, atol=1e-6)
+
+
+def test_view_id_base_matches_per_view_calls():
+    """beta is keyed by the global view id: rendering views 2..3 of a batch alone (view_id_base=2)
+    gives the same pyramids as the 4-view call (view sharding)."""
+    w = S.workload(1, n=80_000, n_views=4)
+    allv = run_gpu(w.cloud, w.cameras, w.poses, w.params)
+    part = run_gpu(w.cloud, w.cameras[2:], w.poses[2:], dataclasses.replace(w.params, view_id_base=2))
+    for j in range(2):
+        assert torch.equal(part.pyrs[j].keys, allv.pyrs[2 + j].keys)
+        assert torch.equal(part.pyrs[j].image, allv.pyrs[2 + j].image) or torch.allclose(
+            part.pyrs[j].image, allv.pyrs[2 + j].image, rtol=1e-5, atol=1e-6)
+
+
+# --------------------------------------------------------------------------- #
+# full BASELINE sizes, in the launch configuration bench.py times
+# --------------------------------------------------------------------------- #
+def _cloud_on_gpu(idx, **kw):
+    return S.workload(idx, device="cuda", **kw)
+
+
+def test_full_config3_100M_forward_vs_oracle():
+    """configs[3] (the bench workload): 100M points, 5 layers, 1080p, discard on: full oracle compare."""
+    w = _cloud_on_gpu(3)
+    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params)
+    r.forward()
+    torch.cuda.synchronize()
+    rec, of = r.ws.stats()
+    assert not of and rec > 0
+    _, fwd, _ = run_oracle(w.cloud.to("cpu"), w.cameras, w.poses, w.params)
+    compare_forward(r, fwd, ctx="config3-full")
+
+
+def test_full_config2_10M_fwd_bwd_vs_oracle():
+    w = _cloud_on_gpu(2)
+    G = grads_for(w.cameras, w.params.layers, w.cloud.channels)
+    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params)
+    r.forward()
+    r.backward([g.cuda() for g in G])
+    torch.cuda.synchronize()
+    _, fwd, bwd = run_oracle(w.cloud.to("cpu"), w.cameras, w.poses, w.params, grads=G)
+    compare_forward(r, fwd, ctx="config2-full")
+    compare_backward(r, bwd, ctx="config2-full")
+
+
+def test_full_config4_50M_16views_sampled_views():
+    """configs[4]: 50M points x 16 views 1024^2 in ONE fused sweep (as bench times it); the oracle checks
+    views 0 and 11 of that sweep (forward + per-view pose gradient), and the 2-view backward call."""
+    w = _cloud_on_gpu(4)
+    C = w.cloud.channels
+    G = grads_for(w.cameras, w.params.layers, C)
+    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params)
+    r.forward()
+    r.backward([g.cuda() for g in G])
+    torch.cuda.synchronize()
+    sel = [0, 11]
+    cams = [w.cameras[v] for v in sel]
+    poses = [w.poses[v] for v in sel]
+    cpu = w.cloud.to("cpu")
+    for j, v in enumerate(sel):
+        prm = dataclasses.replace(w.params, view_id_base=v)
+        _, fwd, bwd = run_oracle(cpu, [cams[j]], [poses[j]], prm, grads=[G[v]])
+        compare_forward(r, fwd, views=[v], ctx=f"config4 view {v}")
+        compare_backward(r, bwd, check_feat=False, check_pos=False, views=[v], ctx=f"config4 view {v}")
