@@ -536,13 +536,15 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
             }
             const float *R = Pz->R;
             double X[3] = {proj[0], proj[1], proj[2]};
+            /* tolerance scale: rounding errors of w live in camera space and R^T mixes them into every
+             * component, so each component's scale is the 2-norm of the term vectors R^T J^T e. */
+            double nu = sqrt(wu[0] * wu[0] + wu[1] * wu[1] + wu[2] * wu[2]);
+            double nv = sqrt(wv[0] * wv[0] + wv[1] * wv[1] + wv[2] * wv[2]);
             for (int k = 0; k < 3; ++k) {
                 /* dx = R^T w (Xc = R x + t) */
                 double a = R[0 + k] * w[0] + R[3 + k] * w[1] + R[6 + k] * w[2];
-                double au = R[0 + k] * wu[0] + R[3 + k] * wu[1] + R[6 + k] * wu[2];
-                double av = R[0 + k] * wv[0] + R[3 + k] * wv[1] + R[6 + k] * wv[2];
                 if (dx) dx[k * n + i] += a;
-                if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * fabs(au) + (ga[2] + ga[3]) * fabs(av);
+                if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
             }
             if (dpose || dpose_abs) {
                 /* Eq. 17 left perturbation: dXc/dxi = [I | -[Xc]x] -> (w, Xc x w) (R19) */
@@ -555,8 +557,10 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                         dpose[v * 6 + 3 + k] += cr[k];
                     }
                     if (dpose_abs) {
-                        dpose_abs[v * 6 + k] += (ga[0] + ga[1]) * fabs(wu[k]) + (ga[2] + ga[3]) * fabs(wv[k]);
-                        dpose_abs[v * 6 + 3 + k] += (ga[0] + ga[1]) * fabs(cu[k]) + (ga[2] + ga[3]) * fabs(cvv[k]);
+                        double ncu = sqrt(cu[0] * cu[0] + cu[1] * cu[1] + cu[2] * cu[2]);
+                        double ncv = sqrt(cvv[0] * cvv[0] + cvv[1] * cvv[1] + cvv[2] * cvv[2]);
+                        dpose_abs[v * 6 + k] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
+                        dpose_abs[v * 6 + 3 + k] += (ga[0] + ga[1]) * ncu + (ga[2] + ga[3]) * ncv;
                     }
                 }
             }

@@ -3,5 +3,5 @@ mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
 nproc > gpurun_out/nproc.txt
 timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke.log 2>&1; echo smoke=$? >> gpurun_out/status.txt
-timeout 1500 python -m pytest tests -m gpu -q -p pytest_timeout --timeout 600 > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/status.txt
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/status.txt
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; echo bench=$? >> gpurun_out/status.txt
