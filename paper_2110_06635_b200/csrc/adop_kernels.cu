@@ -199,6 +199,174 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 }
 
 // --------------------------------------------------------------------------- //
+// depth pass, TMA-pipelined (the hot kernel of the forward)
+//
+// Persistent CTAs walk tiles of kTile points.  One elected thread streams the
+// x, y, z rows of each tile into a kStages-deep shared-memory ring with 1-D bulk
+// copies (cp.async.bulk, L2 evict-first) completing on an mbarrier, so memory
+// parallelism no longer depends on registers or occupancy; all 8 warps consume.
+// r_world is read from global only for points that pass the frustum pre-cull.
+// --------------------------------------------------------------------------- //
+constexpr int kTile = 1024;                   // points per pipeline stage (4 per thread)
+constexpr int kStages = 4;                    // TMA ring depth
+constexpr int kPer = kTile / kThreads;        // points per thread per tile
+constexpr int kCapT = 128;                    // records buffered per warp (TMA kernel)
+
+struct DepthSmem {
+    float pos[kStages][3][kTile];
+    uint64_t full[kStages];
+    int done[kStages];
+    Record rec[kWarps][kCapT];
+};
+
+__device__ __forceinline__ void flush_records_cap(const RasterArgs &a, Record *buf, int &wcount, int lane) {
+    flush_records(a, buf, wcount, lane);
+}
+
+// Survivor part of the depth pass for one point and view: exact projection (R2/R6), discard
+// (Eq. 12), per-layer round + bounds (Eqs. 3-4), 64-bit red.min (§4.5), record emission.
+template <int MODEL>
+__device__ __forceinline__ void depth_survivor(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, Proj &p,
+                                               float rw, int64_t i, uint32_t gi, Record *buf, int &wcount,
+                                               int lane, unsigned lt) {
+    if (ok) ok = project_exact<MODEL>(v, p);
+    const int nk = ok ? keep_layers(a, v, rw, p.iz, gi) : 0;
+    const uint64_t key = depth_key(p.Z, gi);
+#pragma unroll 1
+    for (int l = 0; l < a.layers; ++l) {
+        int pu, pv;
+        const int loc = l < nk ? layer_pixel(v, p, l, pu, pv) : -1;
+        const bool hit = loc >= 0;
+        const uint32_t pix = (uint32_t)(v.off[l] + loc);
+        if (hit) red_min_u64(v.keys + pix, key);
+        const unsigned b = __ballot_sync(kFull, hit);
+        if (b == 0u) {
+            if (!__any_sync(kFull, l + 1 < nk)) break;
+            continue;
+        }
+        if (wcount + 32 > kCapT) flush_records(a, buf, wcount, lane);
+        if (hit) {
+            Record r;
+            r.pix = pix;
+            r.zbits = __float_as_uint(p.Z);
+            r.idx = (uint32_t)i;
+            r.view = (uint32_t)vs;
+            buf[wcount + __popc(b & lt)] = r;
+        }
+        wcount += __popc(b);
+    }
+}
+
+// One tile slice of a warp: kPer points per lane, views outermost (view constants are loaded once
+// per tile and reused by the kPer points), pre-cull first for all points (ILP kPer; r_world loads
+// of pre-cull survivors all in flight), then the survivors one by one.
+template <int MODEL>
+__device__ __forceinline__ void depth_tile(const RasterArgs &a, const float *sx, const float *sy, const float *sz,
+                                           int64_t base, int tid, int64_t nvalid, Record *buf, int &wcount,
+                                           int lane, unsigned lt) {
+    bool live[kPer];
+    uint32_t gi[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int e = j * kThreads + tid;
+        gi[j] = a.goff + (uint32_t)(base + e);
+        live[j] = e < nvalid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
+    }
+#pragma unroll 1
+    for (int vs = 0; vs < a.nviews; ++vs) {
+        const ViewDesc &v = a.v[vs];
+        Proj p[kPer];
+        bool pass[kPer];
+        float rw[kPer];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int e = j * kThreads + tid;
+            to_camera(v, sx[e], sy[e], sz[e], p[j].X, p[j].Y, p[j].Z);
+            pass[j] = live[j] && p[j].Z > a.z_near && p[j].Z <= 3.402823466e38f &&
+                      precull_pass<MODEL>(v, p[j].X, p[j].Y, p[j].Z);
+            rw[j] = a.radius_uniform;
+            if (pass[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + base + e);
+            any |= pass[j];
+        }
+        if (!__any_sync(kFull, any)) continue;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            if (!__any_sync(kFull, pass[j])) continue;
+            depth_survivor<MODEL>(a, v, vs, pass[j], p[j], rw[j], base + j * kThreads + tid, gi[j], buf, wcount,
+                                  lane, lt);
+        }
+    }
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(kThreads, 3) k_depth_tma(const __grid_constant__ RasterArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    const int64_t nfull = a.n / kTile;
+    const int64_t G = gridDim.x;
+    const int64_t my_full = nfull > (int64_t)blockIdx.x ? (nfull - blockIdx.x + G - 1) / G : 0;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&sm.full[s], 1);
+            sm.done[s] = 0;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t k) {
+        const uint64_t pol = policy_evict_first();
+        const int s = (int)(k % kStages);
+        const int64_t t = blockIdx.x + k * G;
+        mbar_expect_tx(&sm.full[s], 3u * kTile * sizeof(float));
+        bulk_g2s(sm.pos[s][0], a.x + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
+        bulk_g2s(sm.pos[s][1], a.y + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
+        bulk_g2s(sm.pos[s][2], a.z + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
+    };
+    if (tid == 0)
+        for (int64_t k = 0; k < my_full && k < kStages; ++k) issue(k);
+    Record *buf = sm.rec[wid];
+    int wcount = 0;
+    for (int64_t k = 0; k < my_full; ++k) {
+        const int s = (int)(k % kStages);
+        mbar_wait(&sm.full[s], (uint32_t)((k / kStages) & 1));
+        const int64_t base = (blockIdx.x + k * G) * kTile;
+        depth_tile<MODEL>(a, sm.pos[s][0], sm.pos[s][1], sm.pos[s][2], base, tid, kTile, buf, wcount, lane, lt);
+        // the last warp to finish stage s refills it (no block-wide barrier per tile)
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            const int old = atomicAdd(&sm.done[s], 1);
+            if (old == kWarps - 1) {
+                sm.done[s] = 0;
+                if (k + kStages < my_full) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(k + kStages);
+                }
+            }
+        }
+    }
+    // ragged tail (< kTile points): plain guarded loads into stage-0 registers path
+    if (a.n > nfull * kTile && (int64_t)blockIdx.x == nfull % G) {
+        __syncthreads();  // every warp is done with the ring; reuse stage 0 for the tail
+        float *tx = sm.pos[0][0], *ty = sm.pos[0][1], *tz = sm.pos[0][2];
+        const int64_t base = nfull * kTile;
+        const int64_t nv = a.n - base;
+        for (int e = tid; e < kTile; e += kThreads) {
+            const bool in = e < nv;
+            tx[e] = in ? a.x[base + e] : 0.f;
+            ty[e] = in ? a.y[base + e] : 0.f;
+            tz[e] = in ? a.z[base + e] : 0.f;
+        }
+        __syncthreads();
+        depth_tile<MODEL>(a, tx, ty, tz, base, tid, nv, buf, wcount, lane, lt);
+    }
+    if (wcount > 0) flush_records(a, buf, wcount, lane);
+}
+
+// --------------------------------------------------------------------------- //
 // blend over survivor records (§4.5 accumulate pass)
 // --------------------------------------------------------------------------- //
 template <bool VEC4>
@@ -480,6 +648,23 @@ int launch_clear(const RasterArgs &a, void *stream) {
 
 template <int MODEL, bool VEC>
 static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
+    if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
+        auto k = k_depth_tma<MODEL>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
+            attr = true;
+        }
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(DepthSmem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t tiles = (a.n + kTile - 1) / kTile;
+        int64_t g = (int64_t)sms * per_sm;
+        if (tiles < g) g = tiles;
+        if (g < 1) g = 1;
+        k<<<(unsigned)g, kThreads, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
+        return (int)cudaGetLastError();
+    }
     auto k = k_stream<MODEL, VEC, MODE_DEPTH, false>;
     int g = resident_grid(k, sms, kWarps * 128, a.n);
     k<<<g, kThreads, 0, (cudaStream_t)stream>>>(a);

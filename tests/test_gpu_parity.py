@@ -242,3 +242,30 @@ def test_full_config4_50M_16views_sampled_views():
         _, fwd, bwd = run_oracle(cpu, [cams[j]], [poses[j]], prm, grads=[G[v]])
         compare_forward(r, fwd, views=[v], ctx=f"config4 view {v}")
         compare_backward(r, bwd, check_feat=False, check_pos=False, views=[v], ctx=f"config4 view {v}")
+
+
+@pytest.mark.parametrize("model", [S.PINHOLE, S.OPENCV8])
+def test_precull_is_conservative_at_frustum_borders(model):
+    """Adversarial points around every layer's bounds (u0 near -2^(l-1) and w_l*2^l) and at tiny /
+    huge depths: the GPU's division-free pre-cull must never reject a point the exact test keeps."""
+    rng = np.random.default_rng(17)
+    w, h, f = 64, 48, 40.0
+    cam = S.Camera(w, h, S.PINHOLE, f, f, 32.0, 24.0)
+    if model == S.OPENCV8:
+        cam = dataclasses.replace(cam, model=S.OPENCV8, k=(0.01, -0.02, 0.0, 0.005, 0.0, 0.0), p=(0.001, -0.001))
+        cam = dataclasses.replace(cam, r2_max=S.distortion_r2_max(cam))
+    us = np.concatenate([np.arange(-20, w + 20, 0.25), -0.5 * 2.0 ** np.arange(5), w - 0.5 + np.zeros(5)])
+    vs = np.concatenate([np.arange(-20, h + 20, 0.5), -0.5 * 2.0 ** np.arange(5)])
+    zs = np.array([1e-4, 1e-2, 0.5, 3.0, 1e3, 1e6])
+    U, Vv, Z = [a.ravel() for a in np.meshgrid(us, vs[::3], zs)]
+    U = U + rng.choice([-1e-4, 0, 1e-4], U.shape)
+    X = (U - cam.cx) / f * Z
+    Y = (Vv - cam.cy) / f * Z
+    xyz = np.stack([X, Y, Z]).astype(np.float32)
+    n = xyz.shape[1]
+    cloud = S.Cloud(torch.from_numpy(xyz), torch.full((n,), 0.01), torch.rand(n, 4, generator=torch.Generator().manual_seed(1)))
+    prm = S.Params(layers=5, discard=False)
+    r = run_gpu(cloud, [cam], [S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))], prm)
+    _, fwd, _ = run_oracle(cloud, [cam], [S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))], prm)
+    compare_forward(r, fwd, ctx="precull")
+    assert (fwd.count > 0).sum() > 500
