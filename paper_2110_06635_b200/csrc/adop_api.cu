@@ -212,6 +212,23 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         d.uhi = (float)c.width + lmax + 2.0f;
         d.vlo = -lmax - 2.0f;
         d.vhi = (float)c.height + lmax + 2.0f;
+        // Margin of the FMA-evaluated pre-cull: |Xf - Xp| <= 2^-20 (|x|+|y|+|z| + max|t|) for the FMA and
+        // the pinned evaluations of R x + t (|R| <= 1); the pre-cull combinations add at most
+        // (|f| + |c| + |bound|) times that plus their own rounding, so 2^-18 (...) is conservative.
+        {
+            const double T = std::fmax(std::fabs((double)poses[v].t[0]),
+                                       std::fmax(std::fabs((double)poses[v].t[1]), std::fabs((double)poses[v].t[2])));
+            double S = 1.0;
+            if (c.model == ADOP_PINHOLE) {
+                S = std::fmax(std::fabs((double)c.fx), std::fabs((double)c.fy)) +
+                    std::fmax(std::fabs((double)c.cx), std::fabs((double)c.cy)) +
+                    std::fmax(std::fmax(std::fabs((double)d.ulo), std::fabs((double)d.uhi)),
+                              std::fmax(std::fabs((double)d.vlo), std::fabs((double)d.vhi)));
+            }
+            const double K = std::ldexp(1.0, -18) * S * 1.02;
+            d.fk = (float)K;
+            d.fkt = (float)(K * (T + 1e-30) * 1.02);
+        }
         d.discard_salt = salt_of(pr->seed, kStreamDiscard, (uint32_t)(pr->view_id_base + v));
         int32_t off = 0;
         for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {

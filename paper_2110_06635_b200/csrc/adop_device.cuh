@@ -68,10 +68,31 @@ __device__ __forceinline__ bool precull_pass(const ViewDesc &v, float X, float Y
     }
 }
 
-// Exact projection after the pre-cull (R2, R6): returns false if culled.
+// Conservative pre-cull evaluated with FMAs straight from the world point (no pinned ops):
+// never rejects a point whose pinned projection lands in some layer (margin fk*B + fkt covers the
+// difference between the FMA and the pinned evaluation of R x + t).
 template <int MODEL>
-__device__ __forceinline__ bool project_exact(const ViewDesc &v, Proj &p) {
-    p.iz = __frcp_rn(p.Z);
+__device__ __forceinline__ bool precull_fma(const ViewDesc &v, float x, float y, float z) {
+    const float X = fmaf(v.R[0], x, fmaf(v.R[1], y, fmaf(v.R[2], z, v.t[0])));
+    const float Y = fmaf(v.R[3], x, fmaf(v.R[4], y, fmaf(v.R[5], z, v.t[1])));
+    const float Z = fmaf(v.R[6], x, fmaf(v.R[7], y, fmaf(v.R[8], z, v.t[2])));
+    const float m = fmaf(v.fk, fabsf(x) + fabsf(y) + fabsf(z), v.fkt);
+    if (MODEL == 0) {
+        const float su = fmaf(v.fx, X, v.cx * Z);
+        const float sv = fmaf(v.fy, Y, v.cy * Z);
+        const float d0 = fmaf(-v.ulo, Z, su), d1 = fmaf(v.uhi, Z, -su);
+        const float d2 = fmaf(-v.vlo, Z, sv), d3 = fmaf(v.vhi, Z, -sv);
+        return fminf(fminf(d0, d1), fminf(d2, d3)) >= -m;
+    } else {
+        // |Xp| >= |Xf| - m etc.: (|Xf|-m)+^2 + (|Yf|-m)+^2 <= r2cull (|Zf|+m)^2 is implied by the exact test
+        const float ax = fmaxf(fabsf(X) - m, 0.0f), ay = fmaxf(fabsf(Y) - m, 0.0f), az = fabsf(Z) + m;
+        return Z >= -m && fmaf(ax, ax, ay * ay) <= v.r2cull * (az * az);
+    }
+}
+
+// Exact projection to layer-0 pixels given p.X, p.Y, p.Z (pinned) and p.iz = 1/Z (R2, R6).
+template <int MODEL>
+__device__ __forceinline__ bool project_uv(const ViewDesc &v, Proj &p) {
     float xn = fmul(p.X, p.iz), yn = fmul(p.Y, p.iz);
     float xd = xn, yd = yn;
     if (MODEL == 1) {
@@ -92,6 +113,13 @@ __device__ __forceinline__ bool project_exact(const ViewDesc &v, Proj &p) {
     p.u0 = fadd(fmul(v.fx, xd), v.cx);
     p.v0 = fadd(fmul(v.fy, yd), v.cy);
     return true;
+}
+
+// Exact projection after the pre-cull (R2, R6): returns false if culled.
+template <int MODEL>
+__device__ __forceinline__ bool project_exact(const ViewDesc &v, Proj &p) {
+    p.iz = __frcp_rn(p.Z);
+    return project_uv<MODEL>(v, p);
 }
 
 // Full projection of a point: validity (R7), pre-cull, exact projection.

@@ -22,6 +22,7 @@ struct ViewDesc {
     float feff;            // fl(fl(fx + fy) * 0.5): focal length of the discard radius (R10)
     float ulo, uhi, vlo, vhi;  // conservative pre-cull window (pixels, all layers)
     float r2cull;          // OpenCV8 pre-cull on X^2+Y^2 <= r2cull Z^2
+    float fk, fkt;         // FMA pre-cull margin: m = fk * (|x|+|y|+|z|) + fkt
     uint32_t discard_salt; // hash salt of (seed, DISCARD, view id) (R11)
     int32_t wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS], off[ADOP_MAX_LAYERS];
     int32_t pixels;        // P

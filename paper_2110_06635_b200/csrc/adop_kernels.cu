@@ -223,14 +223,25 @@ __device__ __forceinline__ void flush_records_cap(const RasterArgs &a, Record *b
     flush_records(a, buf, wcount, lane);
 }
 
-// Survivor part of the depth pass for one point and view: exact projection (R2/R6), discard
-// (Eq. 12), per-layer round + bounds (Eqs. 3-4), 64-bit red.min (§4.5), record emission.
+// Candidate part of the depth pass for one point and view (after the FMA pre-cull): pinned
+// Xc = R x + t (R1), validity (R7), discard (Eq. 12) BEFORE the projection so discarded points never
+// pay for it, exact projection (R2/R6), per-layer round + bounds (Eqs. 3-4), 64-bit red.min (§4.5)
+// and record emission.  Warp-collective: every lane calls it.
 template <int MODEL>
-__device__ __forceinline__ void depth_survivor(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, Proj &p,
-                                               float rw, int64_t i, uint32_t gi, Record *buf, int &wcount,
-                                               int lane, unsigned lt) {
-    if (ok) ok = project_exact<MODEL>(v, p);
-    const int nk = ok ? keep_layers(a, v, rw, p.iz, gi) : 0;
+__device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
+                                                float y, float z, float rw, int64_t i, uint32_t gi, Record *buf,
+                                                int &wcount, int lane, unsigned lt) {
+    Proj p;
+    int nk = 0;
+    if (ok) {
+        to_camera(v, x, y, z, p.X, p.Y, p.Z);
+        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
+            p.iz = __frcp_rn(p.Z);
+            nk = keep_layers(a, v, rw, p.iz, gi);
+        }
+    }
+    if (!__any_sync(kFull, nk > 0)) return;
+    if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
     const uint64_t key = depth_key(p.Z, gi);
 #pragma unroll 1
     for (int l = 0; l < a.layers; ++l) {
@@ -257,44 +268,47 @@ __device__ __forceinline__ void depth_survivor(const RasterArgs &a, const ViewDe
     }
 }
 
-// One tile slice of a warp: kPer points per lane, views outermost (view constants are loaded once
-// per tile and reused by the kPer points), pre-cull first for all points (ILP kPer; r_world loads
-// of pre-cull survivors all in flight), then the survivors one by one.
+// One tile of a warp: lane owns 4 consecutive points (LDS.128 of each row), views outermost (view
+// constants loaded once per tile and view), FMA pre-cull of the 4 points first (ILP 4; the r_world
+// loads of the candidates all in flight), then the candidates point by point.
 template <int MODEL>
 __device__ __forceinline__ void depth_tile(const RasterArgs &a, const float *sx, const float *sy, const float *sz,
                                            int64_t base, int tid, int64_t nvalid, Record *buf, int &wcount,
                                            int lane, unsigned lt) {
-    bool live[kPer];
-    uint32_t gi[kPer];
+    const int e0 = 4 * tid;
+    const float4 X4 = *reinterpret_cast<const float4 *>(sx + e0);
+    const float4 Y4 = *reinterpret_cast<const float4 *>(sy + e0);
+    const float4 Z4 = *reinterpret_cast<const float4 *>(sz + e0);
+    const float x[4] = {X4.x, X4.y, X4.z, X4.w}, y[4] = {Y4.x, Y4.y, Y4.z, Y4.w}, z[4] = {Z4.x, Z4.y, Z4.z, Z4.w};
+    bool live[4];
+    uint32_t gi[4];
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int e = j * kThreads + tid;
-        gi[j] = a.goff + (uint32_t)(base + e);
-        live[j] = e < nvalid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
+    for (int j = 0; j < 4; ++j) {
+        gi[j] = a.goff + (uint32_t)(base + e0 + j);
+        live[j] = e0 + j < nvalid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
     }
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
-        Proj p[kPer];
-        bool pass[kPer];
-        float rw[kPer];
+        bool cand[4];
         bool any = false;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            const int e = j * kThreads + tid;
-            to_camera(v, sx[e], sy[e], sz[e], p[j].X, p[j].Y, p[j].Z);
-            pass[j] = live[j] && p[j].Z > a.z_near && p[j].Z <= 3.402823466e38f &&
-                      precull_pass<MODEL>(v, p[j].X, p[j].Y, p[j].Z);
-            rw[j] = a.radius_uniform;
-            if (pass[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + base + e);
-            any |= pass[j];
+        for (int j = 0; j < 4; ++j) {
+            cand[j] = live[j] && precull_fma<MODEL>(v, x[j], y[j], z[j]);
+            any |= cand[j];
         }
         if (!__any_sync(kFull, any)) continue;
+        float rw[4];
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            if (!__any_sync(kFull, pass[j])) continue;
-            depth_survivor<MODEL>(a, v, vs, pass[j], p[j], rw[j], base + j * kThreads + tid, gi[j], buf, wcount,
-                                  lane, lt);
+        for (int j = 0; j < 4; ++j) {
+            rw[j] = a.radius_uniform;
+            if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + base + e0 + j);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!__any_sync(kFull, cand[j])) continue;
+            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], base + e0 + j, gi[j], buf, wcount,
+                                   lane, lt);
         }
     }
 }
