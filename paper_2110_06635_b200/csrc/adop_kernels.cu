@@ -199,29 +199,31 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 }
 
 // --------------------------------------------------------------------------- //
-// depth pass, TMA-pipelined (the hot kernel of the forward)
+// depth pass, async-copy pipelined (the hot kernel of the forward)
 //
-// Persistent CTAs walk tiles of kTile points.  One elected thread streams the
-// x, y, z rows of each tile into a kStages-deep shared-memory ring with 1-D bulk
-// copies (cp.async.bulk, L2 evict-first) completing on an mbarrier, so memory
-// parallelism no longer depends on registers or occupancy; all 8 warps consume.
-// r_world is read from global only for points that pass the frustum pre-cull.
+// Work unit = a warp tile of 128 consecutive (blocked-Morton ordered) points; warp w of the grid
+// takes tiles w, w + W, w + 2W, ...  Each lane owns 4 consecutive points and streams its own 16-byte
+// pieces of the x, y, z rows into a private kStages-deep shared-memory ring with cp.async (L2
+// evict-first), so loads of the next kStages-1 tiles are in flight while the current one is
+// processed, without registers, barriers or any coupling between lanes or warps.  r_world is read
+// only for points that pass the pre-cull.
 // --------------------------------------------------------------------------- //
-constexpr int kTile = 1024;                   // points per pipeline stage (4 per thread)
-constexpr int kStages = 4;                    // TMA ring depth
-constexpr int kPer = kTile / kThreads;        // points per thread per tile
-constexpr int kCapT = 128;                    // records buffered per warp (TMA kernel)
+constexpr int kStages = 4;
+constexpr int kCapT = 128;  // records buffered per warp
 
 struct DepthSmem {
-    float pos[kStages][3][kTile];
-    uint64_t full[kStages];
-    int done[kStages];
+    float4 pos[kStages][3][kThreads];
     Record rec[kWarps][kCapT];
 };
 
-__device__ __forceinline__ void flush_records_cap(const RasterArgs &a, Record *buf, int &wcount, int lane) {
-    flush_records(a, buf, wcount, lane);
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol)
+                 : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Candidate part of the depth pass for one point and view (after the FMA pre-cull): pinned
 // Xc = R x + t (R1), validity (R7), discard (Eq. 12) BEFORE the projection so discarded points never
@@ -268,24 +270,19 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     }
 }
 
-// One tile of a warp: lane owns 4 consecutive points (LDS.128 of each row), views outermost (view
-// constants loaded once per tile and view), FMA pre-cull of the 4 points first (ILP 4; the r_world
-// loads of the candidates all in flight), then the candidates point by point.
+// The 4 points of one lane (indices i0..i0+3, `valid` of them real), all views.  Views outermost;
+// the FMA pre-cull of the 4 points is branch-free (ILP 4, view constants stay in registers), the
+// r_world loads of all candidates are issued together, then the candidates one by one.
 template <int MODEL>
-__device__ __forceinline__ void depth_tile(const RasterArgs &a, const float *sx, const float *sy, const float *sz,
-                                           int64_t base, int tid, int64_t nvalid, Record *buf, int &wcount,
-                                           int lane, unsigned lt) {
-    const int e0 = 4 * tid;
-    const float4 X4 = *reinterpret_cast<const float4 *>(sx + e0);
-    const float4 Y4 = *reinterpret_cast<const float4 *>(sy + e0);
-    const float4 Z4 = *reinterpret_cast<const float4 *>(sz + e0);
+__device__ __forceinline__ void depth_quad(const RasterArgs &a, float4 X4, float4 Y4, float4 Z4, int64_t i0,
+                                           int valid, Record *buf, int &wcount, int lane, unsigned lt) {
     const float x[4] = {X4.x, X4.y, X4.z, X4.w}, y[4] = {Y4.x, Y4.y, Y4.z, Y4.w}, z[4] = {Z4.x, Z4.y, Z4.z, Z4.w};
     bool live[4];
     uint32_t gi[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        gi[j] = a.goff + (uint32_t)(base + e0 + j);
-        live[j] = e0 + j < nvalid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
+        gi[j] = a.goff + (uint32_t)(i0 + j);
+        live[j] = j < valid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
     }
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
@@ -294,7 +291,7 @@ __device__ __forceinline__ void depth_tile(const RasterArgs &a, const float *sx,
         bool any = false;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            cand[j] = live[j] && precull_fma<MODEL>(v, x[j], y[j], z[j]);
+            cand[j] = precull_fma<MODEL>(v, x[j], y[j], z[j]) & live[j];
             any |= cand[j];
         }
         if (!__any_sync(kFull, any)) continue;
@@ -302,81 +299,70 @@ __device__ __forceinline__ void depth_tile(const RasterArgs &a, const float *sx,
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             rw[j] = a.radius_uniform;
-            if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + base + e0 + j);
+            if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + i0 + j);
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (!__any_sync(kFull, cand[j])) continue;
-            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], base + e0 + j, gi[j], buf, wcount,
-                                   lane, lt);
+            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], i0 + j, gi[j], buf, wcount, lane, lt);
         }
     }
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(kThreads, 3) k_depth_tma(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t nfull = a.n / kTile;
-    const int64_t G = gridDim.x;
-    const int64_t my_full = nfull > (int64_t)blockIdx.x ? (nfull - blockIdx.x + G - 1) / G : 0;
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&sm.full[s], 1);
-            sm.done[s] = 0;
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
+    const int64_t ntiles = (a.n + 127) / 128;
+    const int64_t W = (int64_t)gridDim.x * kWarps;
+    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
+    const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
+    const uint64_t pol = policy_evict_first();
+    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * 128 <= a.n; };
     auto issue = [&](int64_t k) {
-        const uint64_t pol = policy_evict_first();
-        const int s = (int)(k % kStages);
-        const int64_t t = blockIdx.x + k * G;
-        mbar_expect_tx(&sm.full[s], 3u * kTile * sizeof(float));
-        bulk_g2s(sm.pos[s][0], a.x + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
-        bulk_g2s(sm.pos[s][1], a.y + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
-        bulk_g2s(sm.pos[s][2], a.z + t * kTile, kTile * sizeof(float), &sm.full[s], pol);
+        if (k < my && full_tile(k)) {
+            const int s = (int)(k % kStages);
+            const int64_t i0 = (w0 + k * W) * 128 + 4 * lane;
+            cp_async16(&sm.pos[s][0][tid], a.x + i0, pol);
+            cp_async16(&sm.pos[s][1][tid], a.y + i0, pol);
+            cp_async16(&sm.pos[s][2][tid], a.z + i0, pol);
+        }
+        cp_async_commit();  // one (possibly empty) group per tile keeps the group count uniform
     };
-    if (tid == 0)
-        for (int64_t k = 0; k < my_full && k < kStages; ++k) issue(k);
+#pragma unroll
+    for (int k = 0; k < kStages - 1; ++k) issue(k);
     Record *buf = sm.rec[wid];
     int wcount = 0;
-    for (int64_t k = 0; k < my_full; ++k) {
-        const int s = (int)(k % kStages);
-        mbar_wait(&sm.full[s], (uint32_t)((k / kStages) & 1));
-        const int64_t base = (blockIdx.x + k * G) * kTile;
-        depth_tile<MODEL>(a, sm.pos[s][0], sm.pos[s][1], sm.pos[s][2], base, tid, kTile, buf, wcount, lane, lt);
-        // the last warp to finish stage s refills it (no block-wide barrier per tile)
-        __syncwarp();
-        if (lane == 0) {
-            __threadfence_block();
-            const int old = atomicAdd(&sm.done[s], 1);
-            if (old == kWarps - 1) {
-                sm.done[s] = 0;
-                if (k + kStages < my_full) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    issue(k + kStages);
-                }
+    for (int64_t k = 0; k < my; ++k) {
+        issue(k + kStages - 1);
+        cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
+        const int64_t i0 = (w0 + k * W) * 128 + 4 * lane;
+        float4 X4, Y4, Z4;
+        int valid = 4;
+        if (full_tile(k)) {
+            const int s = (int)(k % kStages);
+            X4 = sm.pos[s][0][tid];
+            Y4 = sm.pos[s][1][tid];
+            Z4 = sm.pos[s][2][tid];
+        } else {  // ragged last tile: guarded scalar loads
+            float t[3][4];
+            for (int j = 0; j < 4; ++j) {
+                const bool in = i0 + j < a.n;
+                t[0][j] = in ? a.x[i0 + j] : 0.f;
+                t[1][j] = in ? a.y[i0 + j] : 0.f;
+                t[2][j] = in ? a.z[i0 + j] : 0.f;
             }
+            X4 = make_float4(t[0][0], t[0][1], t[0][2], t[0][3]);
+            Y4 = make_float4(t[1][0], t[1][1], t[1][2], t[1][3]);
+            Z4 = make_float4(t[2][0], t[2][1], t[2][2], t[2][3]);
+            const int64_t rem = a.n - i0;
+            valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
         }
+        depth_quad<MODEL>(a, X4, Y4, Z4, i0, valid, buf, wcount, lane, lt);
     }
-    // ragged tail (< kTile points): plain guarded loads into stage-0 registers path
-    if (a.n > nfull * kTile && (int64_t)blockIdx.x == nfull % G) {
-        __syncthreads();  // every warp is done with the ring; reuse stage 0 for the tail
-        float *tx = sm.pos[0][0], *ty = sm.pos[0][1], *tz = sm.pos[0][2];
-        const int64_t base = nfull * kTile;
-        const int64_t nv = a.n - base;
-        for (int e = tid; e < kTile; e += kThreads) {
-            const bool in = e < nv;
-            tx[e] = in ? a.x[base + e] : 0.f;
-            ty[e] = in ? a.y[base + e] : 0.f;
-            tz[e] = in ? a.z[base + e] : 0.f;
-        }
-        __syncthreads();
-        depth_tile<MODEL>(a, tx, ty, tz, base, tid, nv, buf, wcount, lane, lt);
-    }
+    cp_async_wait<0>();
     if (wcount > 0) flush_records(a, buf, wcount, lane);
 }
 
@@ -663,7 +649,7 @@ int launch_clear(const RasterArgs &a, void *stream) {
 template <int MODEL, bool VEC>
 static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
     if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
-        auto k = k_depth_tma<MODEL>;
+        auto k = k_depth_async<MODEL>;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
@@ -672,9 +658,9 @@ static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(DepthSmem));
         if (per_sm < 1) per_sm = 1;
-        int64_t tiles = (a.n + kTile - 1) / kTile;
+        int64_t tiles = (a.n + 127) / 128;
         int64_t g = (int64_t)sms * per_sm;
-        if (tiles < g) g = tiles;
+        if ((tiles + kWarps - 1) / kWarps < g) g = (tiles + kWarps - 1) / kWarps;
         if (g < 1) g = 1;
         k<<<(unsigned)g, kThreads, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
         return (int)cudaGetLastError();
