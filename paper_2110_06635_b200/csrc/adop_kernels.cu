@@ -209,12 +209,9 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 // only for points that pass the pre-cull.
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 4;
-constexpr int kCapT = 128;  // records buffered per warp
+constexpr int kCapT = 96;  // records buffered per warp
 
-struct DepthSmem {
-    float4 pos[kStages][3][kThreads];
-    Record rec[kWarps][kCapT];
-};
+
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -225,28 +222,26 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Candidate part of the depth pass for one point and view (after the FMA pre-cull): pinned
-// Xc = R x + t (R1), validity (R7), discard (Eq. 12) BEFORE the projection so discarded points never
-// pay for it, exact projection (R2/R6), per-layer round + bounds (Eqs. 3-4), 64-bit red.min (§4.5)
-// and record emission.  Warp-collective: every lane calls it.
-template <int MODEL>
-__device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
-                                                float y, float z, float rw, int64_t i, uint32_t gi, Record *buf,
-                                                int &wcount, int lane, unsigned lt) {
+// Warp queue of kept points (compaction): the layer loop then runs with full warps instead of the
+// ~25% of lanes whose point survives stochastic discarding.
+constexpr int kQCap = 64;
+struct WarpQueue {
+    float4 e[kQCap];           // u0, v0, bits(z), shard-local index
+    uint8_t meta[kQCap];       // kept layers (low 4 bits) | view slot << 4
+};
+
+// Layers of one kept point per lane (nk = 0: idle lane): round + bounds per layer (Eqs. 3-4),
+// 64-bit red.min of the packed key (§4.5, R8), record emission.  Warp-collective.
+__device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc &v, int vs, int nk, float u0,
+                                             float v0, uint32_t zbits, uint32_t idx, Record *buf, int &wcount,
+                                             int lane, unsigned lt) {
+    const uint64_t key = ((uint64_t)zbits << 32) | (a.goff + idx);
     Proj p;
-    int nk = 0;
-    if (ok) {
-        to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
-            p.iz = __frcp_rn(p.Z);
-            nk = keep_layers(a, v, rw, p.iz, gi);
-        }
-    }
-    if (!__any_sync(kFull, nk > 0)) return;
-    if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
-    const uint64_t key = depth_key(p.Z, gi);
-#pragma unroll 1
-    for (int l = 0; l < a.layers; ++l) {
+    p.u0 = u0;
+    p.v0 = v0;
+#pragma unroll
+    for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {
+        if (l >= a.layers) break;
         int pu, pv;
         const int loc = l < nk ? layer_pixel(v, p, l, pu, pv) : -1;
         const bool hit = loc >= 0;
@@ -261,8 +256,8 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
         if (hit) {
             Record r;
             r.pix = pix;
-            r.zbits = __float_as_uint(p.Z);
-            r.idx = (uint32_t)i;
+            r.zbits = zbits;
+            r.idx = idx;
             r.view = (uint32_t)vs;
             buf[wcount + __popc(b & lt)] = r;
         }
@@ -270,12 +265,62 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     }
 }
 
+// Process `cnt` (<= 32) entries from the top of the queue, one per lane.
+__device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, int qview, Record *buf,
+                                      int &wcount, int lane, unsigned lt) {
+    __syncwarp();
+    int nk = 0;
+    float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < cnt) {
+        e = q.e[qn - cnt + lane];
+        nk = q.meta[qn - cnt + lane] & 15;
+    }
+    __syncwarp();
+    qn -= cnt;
+    depth_layers(a, a.v[qview], qview, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), buf, wcount, lane,
+                 lt);
+}
+
+// Candidate part for one point and view (after the FMA pre-cull): pinned Xc = R x + t (R1), validity
+// (R7), discard (Eq. 12) BEFORE the projection, exact projection (R2/R6); kept points are appended to
+// the warp queue, which is drained 32 at a time.  Warp-collective.
+template <int MODEL>
+__device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
+                                                float y, float z, float rw, int64_t i, uint32_t gi, WarpQueue &q,
+                                                int &qn, int &qview, Record *buf, int &wcount, int lane,
+                                                unsigned lt) {
+    Proj p;
+    int nk = 0;
+    if (ok) {
+        to_camera(v, x, y, z, p.X, p.Y, p.Z);
+        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
+            p.iz = __frcp_rn(p.Z);
+            nk = keep_layers(a, v, rw, p.iz, gi);
+        }
+    }
+    const unsigned kb = __ballot_sync(kFull, nk > 0);
+    if (kb == 0u) return;
+    if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
+    const unsigned b = __ballot_sync(kFull, nk > 0);
+    if (b == 0u) return;
+    if (qview != vs && qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);  // queue holds one view only
+    qview = vs;
+    if (nk > 0) {
+        const int slot = qn + __popc(b & lt);
+        q.e[slot] = make_float4(p.u0, p.v0, p.Z, __uint_as_float((uint32_t)i));
+        q.meta[slot] = (uint8_t)(nk | (vs << 4));
+    }
+    qn += __popc(b);
+    if (qn >= 32) drain(a, q, qn, 32, qview, buf, wcount, lane, lt);
+}
+
 // The 4 points of one lane (indices i0..i0+3, `valid` of them real), all views.  Views outermost;
 // the FMA pre-cull of the 4 points is branch-free (ILP 4, view constants stay in registers), the
 // r_world loads of all candidates are issued together, then the candidates one by one.
 template <int MODEL>
 __device__ __forceinline__ void depth_quad(const RasterArgs &a, float4 X4, float4 Y4, float4 Z4, int64_t i0,
-                                           int valid, Record *buf, int &wcount, int lane, unsigned lt) {
+                                           int valid, WarpQueue &q, int &qn, int &qview, Record *buf, int &wcount,
+                                           int lane, unsigned lt) {
     const float x[4] = {X4.x, X4.y, X4.z, X4.w}, y[4] = {Y4.x, Y4.y, Y4.z, Y4.w}, z[4] = {Z4.x, Z4.y, Z4.z, Z4.w};
     bool live[4];
     uint32_t gi[4];
@@ -304,10 +349,17 @@ __device__ __forceinline__ void depth_quad(const RasterArgs &a, float4 X4, float
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (!__any_sync(kFull, cand[j])) continue;
-            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], i0 + j, gi[j], buf, wcount, lane, lt);
+            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], i0 + j, gi[j], q, qn, qview, buf,
+                                   wcount, lane, lt);
         }
     }
 }
+
+struct DepthSmem {
+    float4 pos[kStages][3][kThreads];
+    Record rec[kWarps][kCapT];
+    WarpQueue q[kWarps];
+};
 
 template <int MODEL>
 __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
@@ -334,7 +386,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
 #pragma unroll
     for (int k = 0; k < kStages - 1; ++k) issue(k);
     Record *buf = sm.rec[wid];
-    int wcount = 0;
+    WarpQueue &q = sm.q[wid];
+    int wcount = 0, qn = 0, qview = 0;
     for (int64_t k = 0; k < my; ++k) {
         issue(k + kStages - 1);
         cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
@@ -360,9 +413,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
             const int64_t rem = a.n - i0;
             valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
         }
-        depth_quad<MODEL>(a, X4, Y4, Z4, i0, valid, buf, wcount, lane, lt);
+        depth_quad<MODEL>(a, X4, Y4, Z4, i0, valid, q, qn, qview, buf, wcount, lane, lt);
     }
     cp_async_wait<0>();
+    if (qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);
     if (wcount > 0) flush_records(a, buf, wcount, lane);
 }
 
