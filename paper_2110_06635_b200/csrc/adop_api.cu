@@ -229,6 +229,42 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
             d.fk = (float)K;
             d.fkt = (float)(K * (T + 1e-30) * 1.02);
         }
+        // World-space planes for the per-warp bounding-box cull: camera-space
+        // half-spaces ncam . Xc + dc >= 0 that every point passing the exact test satisfies with slack,
+        // mapped to world space n = R^T ncam, d = ncam . t + dc.
+        {
+            double nc[5][3] = {{0}}, dc[5] = {0, 0, 0, 0, -(double)pr->z_near};
+            if (c.model == ADOP_PINHOLE) {
+                const double fx = c.fx, fy = c.fy, cx = c.cx, cy = c.cy;
+                const double ncam[4][3] = {{fx, 0, cx - d.ulo}, {-fx, 0, d.uhi - cx},
+                                           {0, fy, cy - d.vlo}, {0, -fy, d.vhi - cy}};
+                std::memcpy(nc, ncam, sizeof(ncam));
+            } else if (!std::isinf(d.r2cull)) {
+                const double sr = std::sqrt((double)d.r2cull) * (1.0 + 1.0 / 1024.0);
+                const double ncam[4][3] = {{-1, 0, sr}, {1, 0, sr}, {0, -1, sr}, {0, 1, sr}};
+                std::memcpy(nc, ncam, sizeof(ncam));
+            } else {
+                for (int k = 0; k < 4; ++k) dc[k] = 1.0;  // no lateral bound
+            }
+            nc[4][2] = 1.0;
+            const double T = std::fabs((double)poses[v].t[0]) + std::fabs((double)poses[v].t[1]) +
+                             std::fabs((double)poses[v].t[2]);
+            const float *R = poses[v].R;
+            for (int k = 0; k < 5; ++k) {
+                double n[3], dd = dc[k], l1 = 0.0;
+                for (int ax = 0; ax < 3; ++ax)
+                    n[ax] = (double)R[0 + ax] * nc[k][0] + (double)R[3 + ax] * nc[k][1] + (double)R[6 + ax] * nc[k][2];
+                for (int r = 0; r < 3; ++r) {
+                    dd += nc[k][r] * (double)poses[v].t[r];
+                    l1 += std::fabs(nc[k][r]);
+                }
+                for (int ax = 0; ax < 3; ++ax) d.pl[k][ax] = (float)n[ax];
+                d.pl[k][3] = (float)dd;
+                const double ck = std::ldexp(1.0, -18) * l1 * 1.02;  // pinned-vs-real deviation of Xc, x4
+                d.pm[k][0] = (float)ck;
+                d.pm[k][1] = (float)(ck * T * 1.02);
+            }
+        }
         d.discard_salt = salt_of(pr->seed, kStreamDiscard, (uint32_t)(pr->view_id_base + v));
         int32_t off = 0;
         for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {

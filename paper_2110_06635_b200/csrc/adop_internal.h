@@ -23,6 +23,8 @@ struct ViewDesc {
     float ulo, uhi, vlo, vhi;  // conservative pre-cull window (pixels, all layers)
     float r2cull;          // OpenCV8 pre-cull on X^2+Y^2 <= r2cull Z^2
     float fk, fkt;         // FMA pre-cull margin: m = fk * (|x|+|y|+|z|) + fkt
+    float pl[5][4];        // conservative world-space frustum planes n.p + d >= 0 (warp-box cull)
+    float pm[5][2];        // their margins: m = pm0 * sum_a max|p_a| + pm1 (+ 2^-16 |terms|)
     uint32_t discard_salt; // hash salt of (seed, DISCARD, view id) (R11)
     int32_t wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS], off[ADOP_MAX_LAYERS];
     int32_t pixels;        // P

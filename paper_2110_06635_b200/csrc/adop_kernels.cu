@@ -314,6 +314,57 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     if (qn >= 32) drain(a, q, qn, 32, qview, buf, wcount, lane, lt);
 }
 
+// Warp bounding box of the tile's points (NaN coordinates ignored; empty box if no valid point).
+struct Box {
+    float lo[3], hi[3];
+};
+__device__ __forceinline__ int f2ord(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+__device__ __forceinline__ Box warp_box(const float (&x)[4], const float (&y)[4], const float (&z)[4], int valid) {
+    Box b;
+    const float *c[3] = {x, y, z};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < valid) {
+                lo = fminf(lo, c[ax][j]);
+                hi = fmaxf(hi, c[ax][j]);
+            }
+        b.lo[ax] = ord2f(__reduce_min_sync(kFull, f2ord(lo)));
+        b.hi[ax] = ord2f(__reduce_max_sync(kFull, f2ord(hi)));
+    }
+    return b;
+}
+
+// true if no point of the box can pass the exact projection test of view v (conservative).
+__device__ __forceinline__ bool box_culled(const ViewDesc &v, const Box &b) {
+    if (!(b.lo[0] <= b.hi[0])) return true;  // no valid point in the tile
+    float ext[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) ext[ax] = fmaxf(fabsf(b.lo[ax]), fabsf(b.hi[ax]));
+    const float B = ext[0] + ext[1] + ext[2];
+    bool out = false;
+#pragma unroll
+    for (int k = 4; k >= 0; --k) {  // near plane first
+        float val = v.pl[k][3], mag = fabsf(v.pl[k][3]);
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const float n = v.pl[k][ax];
+            val += fmaxf(n * b.lo[ax], n * b.hi[ax]);
+            mag = fmaf(fabsf(n), ext[ax], mag);
+        }
+        const float m = fmaf(v.pm[k][0], B, v.pm[k][1]) + mag * 1.52587890625e-05f;  // + 2^-16 |terms|
+        out |= val < -m;
+    }
+    return out;
+}
+
 // The 4 points of one lane (indices i0..i0+3, `valid` of them real), all views.  Views outermost;
 // the FMA pre-cull of the 4 points is branch-free (ILP 4, view constants stay in registers), the
 // r_world loads of all candidates are issued together, then the candidates one by one.
@@ -329,9 +380,11 @@ __device__ __forceinline__ void depth_quad(const RasterArgs &a, float4 X4, float
         gi[j] = a.goff + (uint32_t)(i0 + j);
         live[j] = j < valid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
     }
+    const Box box = warp_box(x, y, z, valid);
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
+        if (box_culled(v, box)) continue;  // whole warp tile outside the frustum (warp-uniform)
         bool cand[4];
         bool any = false;
 #pragma unroll
