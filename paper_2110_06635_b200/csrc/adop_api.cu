@@ -260,9 +260,13 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
                 }
                 for (int ax = 0; ax < 3; ++ax) d.pl[k][ax] = (float)n[ax];
                 d.pl[k][3] = (float)dd;
-                const double ck = std::ldexp(1.0, -18) * l1 * 1.02;  // pinned-vs-real deviation of Xc, x4
-                d.pm[k][0] = (float)ck;
-                d.pm[k][1] = (float)(ck * T * 1.02);
+                // margin m = kb0 * B + kb1, B = sum_a max|p_a| over the box: the pinned-vs-real deviation
+                // of Xc (2^-18 |ncam|_1 (B + T), x4 slack) plus the fp32 evaluation of the plane (2^-16 |n|_1 B
+                // + 2^-16 |d|, ~10x the rounding bound)
+                const double n1 = std::fabs(n[0]) + std::fabs(n[1]) + std::fabs(n[2]);
+                const double ck = std::ldexp(1.0, -18) * l1 * 1.02;
+                d.pm[k][0] = (float)((ck + std::ldexp(1.0, -16) * n1) * 1.02);
+                d.pm[k][1] = (float)((ck * T + std::ldexp(1.0, -16) * std::fabs(dd)) * 1.02 + 1e-30);
             }
         }
         d.discard_salt = salt_of(pr->seed, kStreamDiscard, (uint32_t)(pr->view_id_base + v));

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 // processed, without registers, barriers or any coupling between lanes or warps.  r_world is read
 // only for points that pass the pre-cull.
 // --------------------------------------------------------------------------- //
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kCapT = 96;  // records buffered per warp
 
 
@@ -314,125 +314,128 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     if (qn >= 32) drain(a, q, qn, 32, qview, buf, wcount, lane, lt);
 }
 
-// Warp bounding box of the tile's points (NaN coordinates ignored; empty box if no valid point).
+// Bounding box of a lane's points; a lane whose box lies outside one of the view's five conservative
+// half-spaces (4 side planes + near plane, world space) cannot have a point that passes the exact
+// projection test, so its per-point tests are skipped when every lane of the warp agrees.
 struct Box {
-    float lo[3], hi[3];
+    float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
 };
-__device__ __forceinline__ int f2ord(float f) {
-    const int i = __float_as_int(f);
-    return i >= 0 ? i : i ^ 0x7FFFFFFF;
-}
-__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
-__device__ __forceinline__ Box warp_box(const float (&x)[4], const float (&y)[4], const float (&z)[4], int valid) {
+__device__ __forceinline__ Box lane_box(const float (&x)[8], const float (&y)[8], const float (&z)[8], int valid) {
     Box b;
-    const float *c[3] = {x, y, z};
+    const float *co[3] = {x, y, z};
+    float ext = 0.0f;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 8; ++j)
             if (j < valid) {
-                lo = fminf(lo, c[ax][j]);
-                hi = fmaxf(hi, c[ax][j]);
+                lo = fminf(lo, co[ax][j]);
+                hi = fmaxf(hi, co[ax][j]);
             }
-        b.lo[ax] = ord2f(__reduce_min_sync(kFull, f2ord(lo)));
-        b.hi[ax] = ord2f(__reduce_max_sync(kFull, f2ord(hi)));
+        b.c[ax] = 0.5f * (lo + hi);
+        b.e[ax] = 0.5f * (hi - lo);
+        ext += fmaxf(fabsf(lo), fabsf(hi));
     }
+    b.B = ext;  // NaN if the lane has no valid point (lo > hi): then the box never culls
+    if (!(b.e[0] >= 0.0f)) b.B = -1.0f;
     return b;
 }
 
-// true if no point of the box can pass the exact projection test of view v (conservative).
+// true if no point of the lane's box can pass the exact projection test of view v (conservative).
 __device__ __forceinline__ bool box_culled(const ViewDesc &v, const Box &b) {
-    if (!(b.lo[0] <= b.hi[0])) return true;  // no valid point in the tile
-    float ext[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) ext[ax] = fmaxf(fabsf(b.lo[ax]), fabsf(b.hi[ax]));
-    const float B = ext[0] + ext[1] + ext[2];
+    if (b.B < 0.0f) return true;  // no valid point
     bool out = false;
 #pragma unroll
-    for (int k = 4; k >= 0; --k) {  // near plane first
-        float val = v.pl[k][3], mag = fabsf(v.pl[k][3]);
+    for (int k = 4; k >= 0; --k) {
+        float val = v.pl[k][3];
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-            const float n = v.pl[k][ax];
-            val += fmaxf(n * b.lo[ax], n * b.hi[ax]);
-            mag = fmaf(fabsf(n), ext[ax], mag);
+            val = fmaf(v.pl[k][ax], b.c[ax], val);
+            val = fmaf(fabsf(v.pl[k][ax]), b.e[ax], val);
         }
-        const float m = fmaf(v.pm[k][0], B, v.pm[k][1]) + mag * 1.52587890625e-05f;  // + 2^-16 |terms|
-        out |= val < -m;
+        out |= val < -fmaf(v.pm[k][0], b.B, v.pm[k][1]);
     }
     return out;
 }
 
-// The 4 points of one lane (indices i0..i0+3, `valid` of them real), all views.  Views outermost;
-// the FMA pre-cull of the 4 points is branch-free (ILP 4, view constants stay in registers), the
-// r_world loads of all candidates are issued together, then the candidates one by one.
+// The 8 points of one lane (indices i0..i0+7, `valid` of them real), all views.  Views outermost;
+// the lane-box test first, then for two groups of 4 points the branch-free FMA pre-cull (ILP 4, view
+// constants in registers), the r_world loads of all candidates together, then the candidates.
 template <int MODEL>
-__device__ __forceinline__ void depth_quad(const RasterArgs &a, float4 X4, float4 Y4, float4 Z4, int64_t i0,
-                                           int valid, WarpQueue &q, int &qn, int &qview, Record *buf, int &wcount,
-                                           int lane, unsigned lt) {
-    const float x[4] = {X4.x, X4.y, X4.z, X4.w}, y[4] = {Y4.x, Y4.y, Y4.z, Y4.w}, z[4] = {Z4.x, Z4.y, Z4.z, Z4.w};
-    bool live[4];
-    uint32_t gi[4];
+__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float (&x)[8], const float (&y)[8],
+                                            const float (&z)[8], int64_t i0, int valid, WarpQueue &q, int &qn,
+                                            int &qview, Record *buf, int &wcount, int lane, unsigned lt) {
+    uint32_t ghostmask = 0u;
+    if (a.ghost_thr != 0u) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        gi[j] = a.goff + (uint32_t)(i0 + j);
-        live[j] = j < valid && !(a.ghost_thr != 0u && h24(a.ghost_salt, gi[j]) < a.ghost_thr);
+        for (int j = 0; j < 8; ++j)
+            if (h24(a.ghost_salt, a.goff + (uint32_t)(i0 + j)) < a.ghost_thr) ghostmask |= 1u << j;
     }
-    const Box box = warp_box(x, y, z, valid);
+    const Box box = lane_box(x, y, z, valid);
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
-        if (box_culled(v, box)) continue;  // whole warp tile outside the frustum (warp-uniform)
-        bool cand[4];
-        bool any = false;
+        if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            cand[j] = precull_fma<MODEL>(v, x[j], y[j], z[j]) & live[j];
-            any |= cand[j];
-        }
-        if (!__any_sync(kFull, any)) continue;
-        float rw[4];
+        for (int g = 0; g < 2; ++g) {
+            bool cand[4];
+            bool any = false;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            rw[j] = a.radius_uniform;
-            if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + i0 + j);
-        }
+            for (int j = 0; j < 4; ++j) {
+                const int jj = 4 * g + j;
+                cand[j] = precull_fma<MODEL>(v, x[jj], y[jj], z[jj]) & (jj < valid) & !((ghostmask >> jj) & 1u);
+                any |= cand[j];
+            }
+            if (!__any_sync(kFull, any)) continue;
+            float rw[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!__any_sync(kFull, cand[j])) continue;
-            depth_candidate<MODEL>(a, v, vs, cand[j], x[j], y[j], z[j], rw[j], i0 + j, gi[j], q, qn, qview, buf,
-                                   wcount, lane, lt);
+            for (int j = 0; j < 4; ++j) {
+                rw[j] = a.radius_uniform;
+                if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + i0 + 4 * g + j);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!__any_sync(kFull, cand[j])) continue;
+                const int jj = 4 * g + j;
+                depth_candidate<MODEL>(a, v, vs, cand[j], x[jj], y[jj], z[jj], rw[j], i0 + jj,
+                                       a.goff + (uint32_t)(i0 + jj), q, qn, qview, buf, wcount, lane, lt);
+            }
         }
     }
 }
 
+constexpr int kWTile = 256;  // points per warp tile (8 per lane)
+
 struct DepthSmem {
-    float4 pos[kStages][3][kThreads];
+    float4 pos[kStages][3][2][kThreads];  // stage, row, half, thread: the lane's 8 points per row
     Record rec[kWarps][kCapT];
     WarpQueue q[kWarps];
 };
 
 template <int MODEL>
-__global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t ntiles = (a.n + 127) / 128;
+    const int64_t ntiles = (a.n + kWTile - 1) / kWTile;
     const int64_t W = (int64_t)gridDim.x * kWarps;
     const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
     const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
     const uint64_t pol = policy_evict_first();
-    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * 128 <= a.n; };
+    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
     auto issue = [&](int64_t k) {
         if (k < my && full_tile(k)) {
             const int s = (int)(k % kStages);
-            const int64_t i0 = (w0 + k * W) * 128 + 4 * lane;
-            cp_async16(&sm.pos[s][0][tid], a.x + i0, pol);
-            cp_async16(&sm.pos[s][1][tid], a.y + i0, pol);
-            cp_async16(&sm.pos[s][2][tid], a.z + i0, pol);
+            const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
+            const float *src[3] = {a.x + i0, a.y + i0, a.z + i0};
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                cp_async16(&sm.pos[s][r][0][tid], src[r], pol);
+                cp_async16(&sm.pos[s][r][1][tid], src[r] + 4, pol);
+            }
         }
         cp_async_commit();  // one (possibly empty) group per tile keeps the group count uniform
     };
@@ -444,29 +447,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     for (int64_t k = 0; k < my; ++k) {
         issue(k + kStages - 1);
         cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
-        const int64_t i0 = (w0 + k * W) * 128 + 4 * lane;
-        float4 X4, Y4, Z4;
-        int valid = 4;
+        const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
+        float x[8], y[8], z[8];
+        int valid = 8;
         if (full_tile(k)) {
             const int s = (int)(k % kStages);
-            X4 = sm.pos[s][0][tid];
-            Y4 = sm.pos[s][1][tid];
-            Z4 = sm.pos[s][2][tid];
+            float *dst[3] = {x, y, z};
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float4 t = sm.pos[s][r][h][tid];
+                    dst[r][4 * h + 0] = t.x;
+                    dst[r][4 * h + 1] = t.y;
+                    dst[r][4 * h + 2] = t.z;
+                    dst[r][4 * h + 3] = t.w;
+                }
         } else {  // ragged last tile: guarded scalar loads
-            float t[3][4];
-            for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
                 const bool in = i0 + j < a.n;
-                t[0][j] = in ? a.x[i0 + j] : 0.f;
-                t[1][j] = in ? a.y[i0 + j] : 0.f;
-                t[2][j] = in ? a.z[i0 + j] : 0.f;
+                x[j] = in ? a.x[i0 + j] : 0.f;
+                y[j] = in ? a.y[i0 + j] : 0.f;
+                z[j] = in ? a.z[i0 + j] : 0.f;
             }
-            X4 = make_float4(t[0][0], t[0][1], t[0][2], t[0][3]);
-            Y4 = make_float4(t[1][0], t[1][1], t[1][2], t[1][3]);
-            Z4 = make_float4(t[2][0], t[2][1], t[2][2], t[2][3]);
             const int64_t rem = a.n - i0;
-            valid = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
+            valid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
         }
-        depth_quad<MODEL>(a, X4, Y4, Z4, i0, valid, q, qn, qview, buf, wcount, lane, lt);
+        depth_lane8<MODEL>(a, x, y, z, i0, valid, q, qn, qview, buf, wcount, lane, lt);
     }
     cp_async_wait<0>();
     if (qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);
@@ -765,7 +773,7 @@ static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(DepthSmem));
         if (per_sm < 1) per_sm = 1;
-        int64_t tiles = (a.n + 127) / 128;
+        int64_t tiles = (a.n + kWTile - 1) / kWTile;
         int64_t g = (int64_t)sms * per_sm;
         if ((tiles + kWarps - 1) / kWarps < g) g = (tiles + kWarps - 1) / kWarps;
         if (g < 1) g = 1;
