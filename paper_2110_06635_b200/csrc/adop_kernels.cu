@@ -360,48 +360,53 @@ __device__ __forceinline__ bool box_culled(const ViewDesc &v, const Box &b) {
     return out;
 }
 
-// The 8 points of one lane (indices i0..i0+7, `valid` of them real), all views.  Views outermost;
-// the lane-box test first, then for two groups of 4 points the branch-free FMA pre-cull (ILP 4, view
-// constants in registers), the r_world loads of all candidates together, then the candidates.
+// The 8 points of one lane (indices i0..i0+7, `valid` of them real), all views, read from the lane's
+// shared-memory slots st[row][half][tid].  Views outermost: the lane-box test, the branch-free FMA
+// pre-cull of the 8 points into a candidate bit mask, r_world prefetches of the candidates, then one
+// candidate per lane per iteration until no lane has any left (compacts across the lane's points).
 template <int MODEL>
-__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float (&x)[8], const float (&y)[8],
-                                            const float (&z)[8], int64_t i0, int valid, WarpQueue &q, int &qn,
-                                            int &qview, Record *buf, int &wcount, int lane, unsigned lt) {
-    uint32_t ghostmask = 0u;
+__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*st)[2][kThreads], int tid,
+                                            int64_t i0, int valid, WarpQueue &q, int &qn, int &qview,
+                                            Record *buf, int &wcount, int lane, unsigned lt) {
+    float x[8], y[8], z[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float4 X = st[0][h][tid], Y = st[1][h][tid], Z = st[2][h][tid];
+        x[4 * h] = X.x; x[4 * h + 1] = X.y; x[4 * h + 2] = X.z; x[4 * h + 3] = X.w;
+        y[4 * h] = Y.x; y[4 * h + 1] = Y.y; y[4 * h + 2] = Y.z; y[4 * h + 3] = Y.w;
+        z[4 * h] = Z.x; z[4 * h + 1] = Z.y; z[4 * h + 2] = Z.z; z[4 * h + 3] = Z.w;
+    }
+    uint32_t live = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
     if (a.ghost_thr != 0u) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (h24(a.ghost_salt, a.goff + (uint32_t)(i0 + j)) < a.ghost_thr) ghostmask |= 1u << j;
+            if (h24(a.ghost_salt, a.goff + (uint32_t)(i0 + j)) < a.ghost_thr) live &= ~(1u << j);
     }
     const Box box = lane_box(x, y, z, valid);
+    const float *sx = reinterpret_cast<const float *>(&st[0][0][tid]);
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
         if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
+        uint32_t m = 0u;
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-            bool cand[4];
-            bool any = false;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int jj = 4 * g + j;
-                cand[j] = precull_fma<MODEL>(v, x[jj], y[jj], z[jj]) & (jj < valid) & !((ghostmask >> jj) & 1u);
-                any |= cand[j];
-            }
-            if (!__any_sync(kFull, any)) continue;
-            float rw[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                rw[j] = a.radius_uniform;
-                if (cand[j] && a.discard && a.radius) rw[j] = __ldg(a.radius + i0 + 4 * g + j);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (!__any_sync(kFull, cand[j])) continue;
-                const int jj = 4 * g + j;
-                depth_candidate<MODEL>(a, v, vs, cand[j], x[jj], y[jj], z[jj], rw[j], i0 + jj,
-                                       a.goff + (uint32_t)(i0 + jj), q, qn, qview, buf, wcount, lane, lt);
-            }
+        for (int j = 0; j < 8; ++j) m |= (precull_fma<MODEL>(v, x[j], y[j], z[j]) ? 1u : 0u) << j;
+        m &= live;
+        if (!__any_sync(kFull, m != 0u)) continue;
+        if (a.discard && a.radius && m != 0u) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.radius + i0));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.radius + i0 + 7));
+        }
+        while (__any_sync(kFull, m != 0u)) {
+            const bool ok = m != 0u;
+            const int j = ok ? __ffs(m) - 1 : 0;
+            m &= m - 1u;
+            // the lane's point j: row r at float index (r * 2 * kThreads + (j >> 2) * kThreads) * 4 + (j & 3)
+            const int o = (j >> 2) * kThreads * 4 + (j & 3);
+            const float px = sx[o], py = sx[o + 2 * kThreads * 4], pz = sx[o + 4 * kThreads * 4];
+            const float rw = (ok && a.discard && a.radius) ? __ldg(a.radius + i0 + j) : a.radius_uniform;
+            depth_candidate<MODEL>(a, v, vs, ok, px, py, pz, rw, i0 + j, a.goff + (uint32_t)(i0 + j), q, qn, qview,
+                                   buf, wcount, lane, lt);
         }
     }
 }
@@ -448,33 +453,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_depth_async(const __grid_consta
         issue(k + kStages - 1);
         cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
         const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
-        float x[8], y[8], z[8];
+        const int s = (int)(k % kStages);
         int valid = 8;
-        if (full_tile(k)) {
-            const int s = (int)(k % kStages);
-            float *dst[3] = {x, y, z};
-#pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const float4 t = sm.pos[s][r][h][tid];
-                    dst[r][4 * h + 0] = t.x;
-                    dst[r][4 * h + 1] = t.y;
-                    dst[r][4 * h + 2] = t.z;
-                    dst[r][4 * h + 3] = t.w;
-                }
-        } else {  // ragged last tile: guarded scalar loads
+        if (!full_tile(k)) {  // ragged last tile: guarded loads into this stage's (unused) slots
+            float t[3][8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const bool in = i0 + j < a.n;
-                x[j] = in ? a.x[i0 + j] : 0.f;
-                y[j] = in ? a.y[i0 + j] : 0.f;
-                z[j] = in ? a.z[i0 + j] : 0.f;
+                t[0][j] = in ? a.x[i0 + j] : 0.f;
+                t[1][j] = in ? a.y[i0 + j] : 0.f;
+                t[2][j] = in ? a.z[i0 + j] : 0.f;
+            }
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                sm.pos[s][r][0][tid] = make_float4(t[r][0], t[r][1], t[r][2], t[r][3]);
+                sm.pos[s][r][1][tid] = make_float4(t[r][4], t[r][5], t[r][6], t[r][7]);
             }
             const int64_t rem = a.n - i0;
             valid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
         }
-        depth_lane8<MODEL>(a, x, y, z, i0, valid, q, qn, qview, buf, wcount, lane, lt);
+        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, q, qn, qview, buf, wcount, lane, lt);
     }
     cp_async_wait<0>();
     if (qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);
