@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 // processed, without registers, barriers or any coupling between lanes or warps.  r_world is read
 // only for points that pass the pre-cull.
 // --------------------------------------------------------------------------- //
-constexpr int kStages = 3;
+constexpr int kStages = 2;
 constexpr int kCapT = 96;  // records buffered per warp
 
 
@@ -321,25 +321,26 @@ struct Box {
     float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
 };
 
-__device__ __forceinline__ Box lane_box(const float (&x)[8], const float (&y)[8], const float (&z)[8], int valid) {
+__device__ __forceinline__ Box lane_box(const float4 (*st)[2][kThreads], int tid, int valid) {
     Box b;
-    const float *co[3] = {x, y, z};
     float ext = 0.0f;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
+        const float4 A = st[ax][0][tid], Bv = st[ax][1][tid];
+        const float c[8] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w};
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (j < valid) {
-                lo = fminf(lo, co[ax][j]);
-                hi = fmaxf(hi, co[ax][j]);
+                lo = fminf(lo, c[j]);
+                hi = fmaxf(hi, c[j]);
             }
         b.c[ax] = 0.5f * (lo + hi);
         b.e[ax] = 0.5f * (hi - lo);
         ext += fmaxf(fabsf(lo), fabsf(hi));
     }
-    b.B = ext;  // NaN if the lane has no valid point (lo > hi): then the box never culls
-    if (!(b.e[0] >= 0.0f)) b.B = -1.0f;
+    b.B = ext;
+    if (!(b.e[0] >= 0.0f)) b.B = -1.0f;  // no valid point in the lane
     return b;
 }
 
@@ -368,21 +369,13 @@ template <int MODEL>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*st)[2][kThreads], int tid,
                                             int64_t i0, int valid, WarpQueue &q, int &qn, int &qview,
                                             Record *buf, int &wcount, int lane, unsigned lt) {
-    float x[8], y[8], z[8];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const float4 X = st[0][h][tid], Y = st[1][h][tid], Z = st[2][h][tid];
-        x[4 * h] = X.x; x[4 * h + 1] = X.y; x[4 * h + 2] = X.z; x[4 * h + 3] = X.w;
-        y[4 * h] = Y.x; y[4 * h + 1] = Y.y; y[4 * h + 2] = Y.z; y[4 * h + 3] = Y.w;
-        z[4 * h] = Z.x; z[4 * h + 1] = Z.y; z[4 * h + 2] = Z.z; z[4 * h + 3] = Z.w;
-    }
     uint32_t live = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
     if (a.ghost_thr != 0u) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (h24(a.ghost_salt, a.goff + (uint32_t)(i0 + j)) < a.ghost_thr) live &= ~(1u << j);
     }
-    const Box box = lane_box(x, y, z, valid);
+    const Box box = lane_box(st, tid, valid);
     const float *sx = reinterpret_cast<const float *>(&st[0][0][tid]);
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
@@ -390,7 +383,13 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
         if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
         uint32_t m = 0u;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m |= (precull_fma<MODEL>(v, x[j], y[j], z[j]) ? 1u : 0u) << j;
+        for (int h = 0; h < 2; ++h) {
+            const float4 X = st[0][h][tid], Y = st[1][h][tid], Z = st[2][h][tid];
+            m |= (precull_fma<MODEL>(v, X.x, Y.x, Z.x) ? 1u : 0u) << (4 * h);
+            m |= (precull_fma<MODEL>(v, X.y, Y.y, Z.y) ? 2u : 0u) << (4 * h);
+            m |= (precull_fma<MODEL>(v, X.z, Y.z, Z.z) ? 4u : 0u) << (4 * h);
+            m |= (precull_fma<MODEL>(v, X.w, Y.w, Z.w) ? 8u : 0u) << (4 * h);
+        }
         m &= live;
         if (!__any_sync(kFull, m != 0u)) continue;
         if (a.discard && a.radius && m != 0u) {
@@ -420,7 +419,7 @@ struct DepthSmem {
 };
 
 template <int MODEL>
-__global__ void __launch_bounds__(kThreads, 2) k_depth_async(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
