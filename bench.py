@@ -228,7 +228,7 @@ def run_ours(args, rank, world, local_rank):
                        "gamma": prm.gamma, "alpha": prm.alpha,
                        "parallelism": f"point-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "inputs (1.6 GB/GPU positions+radii) exceed the 126 MB L2; no flush needed",
-                       "records_per_frame": records, "record_overflow": overflow},
+                       "record_slots_per_frame": records, "record_overflow": overflow},
             "phases_ms": {"depth": depth_ms, "key_allreduce": statistics.mean(ph[1]),
                           "blend": statistics.mean(ph[2]), "accum_allreduce": statistics.mean(ph[3]),
                           "resolve": statistics.mean(ph[4])},

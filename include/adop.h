@@ -129,10 +129,11 @@ typedef struct {
 ADOP_API int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t layers);
 
 /* Workspace bytes for calls over `n_views` views of `points`.
- * record_capacity: number of 16-byte survivor records the depth pass may emit
- * ((point, view, layer) hits of the render set); < 0 selects the worst case
- * n * n_views * layers.  If a call's survivors exceed the capacity, the blend
- * pass falls back to re-streaming all points (correct, slower).
+ * record_capacity: number of 16-byte survivor record slots the depth pass may use
+ * (one per (point, view, layer) hit of the render set, reserved per warp in chunks
+ * of 256 whose unused slots are marked dead); < 0 selects the worst case
+ * n * n_views * layers plus chunk slack.  If a call's survivors exceed the capacity,
+ * the blend pass falls back to re-streaming all points (correct, slower).
  * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, n_views < 1, bad layers). */
 ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_params *params,
                                 int64_t record_capacity, size_t *bytes);
@@ -188,7 +189,7 @@ ADOP_API adop_status adop_point_masks(const adop_points *points, int32_t n_views
                              const adop_pose *poses, const adop_params *params, uint8_t *mask, void *stream);
 
 /* Survivor statistics of the last depth pass in `workspace` (synchronizes `stream`):
- * records emitted and whether they overflowed the capacity. */
+ * record slots used (including dead chunk tails) and whether they overflowed the capacity. */
 ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream,
                                  int64_t *records, int32_t *overflowed);
 

@@ -226,13 +226,14 @@ class Workspace:
 
 
 def default_record_capacity(n: int, n_views: int, layers: int, discard: bool) -> int:
-    """Worst case n*V*L when affordable (< 4 GiB), else a generous bound: with stochastic discarding
+    """Worst case n*V*L (+ chunk slack) when affordable (< 4 GiB), else a generous bound: with stochastic discarding
     the kept points per pixel are bounded (Eq. 12), so the records are far below the worst case;
     exceeding the capacity is still correct (the blend pass re-streams the points)."""
+    slack = 1 << 20  # partially filled per-warp record chunks (dead slots)
     worst = n * n_views * layers
     if worst * 16 <= (4 << 30) or not discard:
-        return worst
-    return max(1 << 22, worst // 4)
+        return worst + slack
+    return max(1 << 22, worst // 4) + slack
 
 
 def _stream(stream):

@@ -46,6 +46,7 @@ uint32_t salt_of(uint64_t seed, uint32_t stream, uint32_t view) {
 constexpr uint32_t kStreamGhost = 1, kStreamDiscard = 2;
 
 constexpr size_t kHeaderBytes = 256;
+constexpr int64_t kRecordSlack = 1 << 20;  // >= resident warps x 256-slot record chunks
 constexpr int kMaxBwdBlocks = 2048;
 constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 6 * sizeof(double);
 
@@ -338,7 +339,8 @@ adop_status adop_workspace_size(const adop_points *points, int32_t n_views, cons
     if (n_views < 1) return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views < 1");
     if (params->layers < 1 || params->layers > ADOP_MAX_LAYERS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad layers");
     if (points->n < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "n < 0");
-    int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * params->layers;
+    // worst case n*V*L plus slack for partially filled per-warp record chunks (dead slots)
+    int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * params->layers + kRecordSlack;
     *bytes = kHeaderBytes + kPartialBytes + (size_t)cap * sizeof(Record);
     return ok();
 }

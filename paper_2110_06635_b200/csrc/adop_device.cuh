@@ -90,6 +90,27 @@ __device__ __forceinline__ bool precull_fma(const ViewDesc &v, float x, float y,
     }
 }
 
+// Same test, also returning the FMA depth and the margin (for the early discard test).
+template <int MODEL>
+__device__ __forceinline__ bool precull_fma_z(const ViewDesc &v, float x, float y, float z, float &Zo, float &mo) {
+    const float X = fmaf(v.R[0], x, fmaf(v.R[1], y, fmaf(v.R[2], z, v.t[0])));
+    const float Y = fmaf(v.R[3], x, fmaf(v.R[4], y, fmaf(v.R[5], z, v.t[1])));
+    const float Z = fmaf(v.R[6], x, fmaf(v.R[7], y, fmaf(v.R[8], z, v.t[2])));
+    const float m = fmaf(v.fk, fabsf(x) + fabsf(y) + fabsf(z), v.fkt);
+    Zo = Z;
+    mo = m;
+    if (MODEL == 0) {
+        const float su = fmaf(v.fx, X, v.cx * Z);
+        const float sv = fmaf(v.fy, Y, v.cy * Z);
+        const float d0 = fmaf(-v.ulo, Z, su), d1 = fmaf(v.uhi, Z, -su);
+        const float d2 = fmaf(-v.vlo, Z, sv), d3 = fmaf(v.vhi, Z, -sv);
+        return fminf(fminf(d0, d1), fminf(d2, d3)) >= -m;
+    } else {
+        const float ax = fmaxf(fabsf(X) - m, 0.0f), ay = fmaxf(fabsf(Y) - m, 0.0f), az = fabsf(Z) + m;
+        return Z >= -m && fmaf(ax, ax, ay * ay) <= v.r2cull * (az * az);
+    }
+}
+
 // Exact projection to layer-0 pixels given p.X, p.Y, p.Z (pinned) and p.iz = 1/Z (R2, R6).
 template <int MODEL>
 __device__ __forceinline__ bool project_uv(const ViewDesc &v, Proj &p) {

@@ -201,17 +201,26 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 // --------------------------------------------------------------------------- //
 // depth pass, async-copy pipelined (the hot kernel of the forward)
 //
-// Work unit = a warp tile of 128 consecutive (blocked-Morton ordered) points; warp w of the grid
-// takes tiles w, w + W, w + 2W, ...  Each lane owns 4 consecutive points and streams its own 16-byte
-// pieces of the x, y, z rows into a private kStages-deep shared-memory ring with cp.async (L2
-// evict-first), so loads of the next kStages-1 tiles are in flight while the current one is
-// processed, without registers, barriers or any coupling between lanes or warps.  r_world is read
-// only for points that pass the pre-cull.
+// Work unit = a warp tile of 256 consecutive (blocked-Morton ordered) points; warp w of the grid
+// takes tiles w, w + W, w + 2W, ...  Each lane owns 8 consecutive points and streams its own 16-byte
+// pieces of the x, y, z (and r_world) rows into a private 2-deep shared-memory ring with cp.async
+// (L2 evict-first): the next tile is in flight while the current one is processed, with no registers,
+// barriers or coupling between lanes or warps.  Per tile and view:
+//   1. lane-box cull: a lane whose 8-point bounding box lies outside one of 5 conservative world-space
+//      half-spaces skips its points; a warp whose lanes all agree skips the tile;
+//   2. per point, branch-free: FMA pre-cull + a conservative early discard test (Eq. 12 evaluated on
+//      a lower bound of z) -> candidate bit mask;
+//   3. candidates, one per lane per iteration: pinned transform (R1), validity (R7), exact discard
+//      (R10), exact projection (R2/R6); kept points go to a warp queue;
+//   4. the queue is drained 32 at a time: per layer round + bounds (Eqs. 3-4), 64-bit red.min of the
+//      packed key (§4.5, R8) and survivor records, written straight to global memory into per-warp
+//      chunks of kChunk slots reserved with one atomic (unused slots are marked dead).
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 2;
-constexpr int kCapT = 96;  // records buffered per warp
-
-
+constexpr int kWTile = 256;  // points per warp tile (8 per lane)
+constexpr int kQCap = 64;
+constexpr int kChunk = 256;  // record slots reserved per warp at a time
+constexpr uint32_t kDeadView = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -222,19 +231,42 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Warp queue of kept points (compaction): the layer loop then runs with full warps instead of the
-// ~25% of lanes whose point survives stochastic discarding.
-constexpr int kQCap = 64;
 struct WarpQueue {
-    float4 e[kQCap];           // u0, v0, bits(z), shard-local index
-    uint8_t meta[kQCap];       // kept layers (low 4 bits) | view slot << 4
+    float4 e[kQCap];      // u0, v0, bits(z), shard-local index
+    uint8_t meta[kQCap];  // kept layers (low 4 bits) | view slot << 4
 };
 
-// Layers of one kept point per lane (nk = 0: idle lane): round + bounds per layer (Eqs. 3-4),
-// 64-bit red.min of the packed key (§4.5, R8), record emission.  Warp-collective.
+struct DepthSmem {
+    float4 pos[kStages][4][2][kThreads];  // stage, row (x, y, z, r_world), half, thread
+    WarpQueue q[kWarps];
+};
+
+struct RecChunk {  // warp-uniform
+    unsigned long long base;
+    int left;
+};
+
+__device__ __forceinline__ void put_record(const RasterArgs &a, unsigned long long slot, uint4 r) {
+    if (slot < (unsigned long long)a.rec_capacity)
+        reinterpret_cast<uint4 *>(a.records)[slot] = r;
+    else
+        atomicExch(&a.hdr->overflow, 1);
+}
+
+// mark the chunk's unused slots dead, then reserve a fresh chunk (one atomic per kChunk slots)
+__device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, int lane, bool fresh) {
+    for (int k = lane; k < c.left; k += 32) put_record(a, c.base + k, make_uint4(0u, 0u, 0u, kDeadView));
+    if (!fresh) return;
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(&a.hdr->records, (unsigned long long)kChunk);
+    c.base = __shfl_sync(kFull, b, 0);
+    c.left = kChunk;
+}
+
+// Layers of one kept point per lane (nk = 0: idle lane).  Warp-collective.
 __device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc &v, int vs, int nk, float u0,
-                                             float v0, uint32_t zbits, uint32_t idx, Record *buf, int &wcount,
-                                             int lane, unsigned lt) {
+                                             float v0, uint32_t zbits, uint32_t idx, RecChunk &c, int lane,
+                                             unsigned lt) {
     const uint64_t key = ((uint64_t)zbits << 32) | (a.goff + idx);
     Proj p;
     p.u0 = u0;
@@ -252,22 +284,17 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc
             if (!__any_sync(kFull, l + 1 < nk)) break;
             continue;
         }
-        if (wcount + 32 > kCapT) flush_records(a, buf, wcount, lane);
-        if (hit) {
-            Record r;
-            r.pix = pix;
-            r.zbits = zbits;
-            r.idx = idx;
-            r.view = (uint32_t)vs;
-            buf[wcount + __popc(b & lt)] = r;
-        }
-        wcount += __popc(b);
+        const int nb = __popc(b);
+        if (nb > c.left) rec_reserve(a, c, lane, true);
+        if (hit) put_record(a, c.base + __popc(b & lt), make_uint4(pix, zbits, idx, (uint32_t)vs));
+        c.base += nb;
+        c.left -= nb;
     }
 }
 
 // Process `cnt` (<= 32) entries from the top of the queue, one per lane.
-__device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, int qview, Record *buf,
-                                      int &wcount, int lane, unsigned lt) {
+__device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, int qview, RecChunk &c,
+                                   int lane, unsigned lt) {
     __syncwarp();
     int nk = 0;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -277,18 +304,16 @@ __device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, i
     }
     __syncwarp();
     qn -= cnt;
-    depth_layers(a, a.v[qview], qview, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), buf, wcount, lane,
-                 lt);
+    depth_layers(a, a.v[qview], qview, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
 }
 
-// Candidate part for one point and view (after the FMA pre-cull): pinned Xc = R x + t (R1), validity
-// (R7), discard (Eq. 12) BEFORE the projection, exact projection (R2/R6); kept points are appended to
-// the warp queue, which is drained 32 at a time.  Warp-collective.
+// Candidate part for one point and view: pinned Xc = R x + t (R1), validity (R7), exact discard (Eq. 12,
+// R10) BEFORE the projection, exact projection (R2/R6); kept points are appended to the warp queue,
+// which is drained 32 at a time.  Warp-collective.
 template <int MODEL>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
                                                 float y, float z, float rw, int64_t i, uint32_t gi, WarpQueue &q,
-                                                int &qn, int &qview, Record *buf, int &wcount, int lane,
-                                                unsigned lt) {
+                                                int &qn, int &qview, RecChunk &c, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
     if (ok) {
@@ -298,12 +323,10 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
             nk = keep_layers(a, v, rw, p.iz, gi);
         }
     }
-    const unsigned kb = __ballot_sync(kFull, nk > 0);
-    if (kb == 0u) return;
     if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
     const unsigned b = __ballot_sync(kFull, nk > 0);
     if (b == 0u) return;
-    if (qview != vs && qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);  // queue holds one view only
+    if (qview != vs && qn > 0) drain(a, q, qn, qn, qview, c, lane, lt);  // the queue holds one view only
     qview = vs;
     if (nk > 0) {
         const int slot = qn + __popc(b & lt);
@@ -311,12 +334,10 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
     qn += __popc(b);
-    if (qn >= 32) drain(a, q, qn, 32, qview, buf, wcount, lane, lt);
+    if (qn >= 32) drain(a, q, qn, 32, qview, c, lane, lt);
 }
 
-// Bounding box of a lane's points; a lane whose box lies outside one of the view's five conservative
-// half-spaces (4 side planes + near plane, world space) cannot have a point that passes the exact
-// projection test, so its per-point tests are skipped when every lane of the warp agrees.
+// Bounding box of a lane's points (see box_culled).
 struct Box {
     float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
 };
@@ -344,9 +365,10 @@ __device__ __forceinline__ Box lane_box(const float4 (*st)[2][kThreads], int tid
     return b;
 }
 
-// true if no point of the lane's box can pass the exact projection test of view v (conservative).
+// true if no point of the lane's box can pass the exact projection test of view v (conservative:
+// the planes hold with slack for every passing point; margins in adop_api.cu fill_args).
 __device__ __forceinline__ bool box_culled(const ViewDesc &v, const Box &b) {
-    if (b.B < 0.0f) return true;  // no valid point
+    if (b.B < 0.0f) return true;
     bool out = false;
 #pragma unroll
     for (int k = 4; k >= 0; --k) {
@@ -361,14 +383,24 @@ __device__ __forceinline__ bool box_culled(const ViewDesc &v, const Box &b) {
     return out;
 }
 
+// Early discard test (Eq. 12 at layer 0) on an upper bound of the projected radius: z >= Zf - m (the
+// pre-cull's margin bounds |Zf - Zp|), r_screen <= gamma r_w f_eff / (Zf - m).  Returns false only if
+// the exact test (R10) cannot keep the point at layer 0 -- and so at no layer (nested keep sets).
+__device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &v, float rw, float Zf, float m,
+                                           uint32_t gi) {
+    const float zl = Zf - m;
+    const float r = a.gamma * rw * v.feff * __fdividef(1.0f, zl);
+    const uint32_t h = h24(v.discard_salt, gi);
+    const float om = (float)(16777216u - h) * 5.9604644775390625e-8f;
+    return !(zl > 0.0f) || r * r * 1.002f > om;
+}
+
 // The 8 points of one lane (indices i0..i0+7, `valid` of them real), all views, read from the lane's
-// shared-memory slots st[row][half][tid].  Views outermost: the lane-box test, the branch-free FMA
-// pre-cull of the 8 points into a candidate bit mask, r_world prefetches of the candidates, then one
-// candidate per lane per iteration until no lane has any left (compacts across the lane's points).
+// shared-memory slots st[row][half][tid].
 template <int MODEL>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*st)[2][kThreads], int tid,
-                                            int64_t i0, int valid, WarpQueue &q, int &qn, int &qview,
-                                            Record *buf, int &wcount, int lane, unsigned lt) {
+                                            int64_t i0, int valid, bool staged_r, WarpQueue &q, int &qn,
+                                            int &qview, RecChunk &c, int lane, unsigned lt) {
     uint32_t live = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
     if (a.ghost_thr != 0u) {
 #pragma unroll
@@ -377,6 +409,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
     }
     const Box box = lane_box(st, tid, valid);
     const float *sx = reinterpret_cast<const float *>(&st[0][0][tid]);
+    constexpr int kRow = 2 * kThreads * 4;  // floats between rows of the lane's slots
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
@@ -385,38 +418,31 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float4 X = st[0][h][tid], Y = st[1][h][tid], Z = st[2][h][tid];
-            m |= (precull_fma<MODEL>(v, X.x, Y.x, Z.x) ? 1u : 0u) << (4 * h);
-            m |= (precull_fma<MODEL>(v, X.y, Y.y, Z.y) ? 2u : 0u) << (4 * h);
-            m |= (precull_fma<MODEL>(v, X.z, Y.z, Z.z) ? 4u : 0u) << (4 * h);
-            m |= (precull_fma<MODEL>(v, X.w, Y.w, Z.w) ? 8u : 0u) << (4 * h);
+            const float4 Rw = staged_r ? st[3][h][tid] : make_float4(a.radius_uniform, a.radius_uniform,
+                                                                     a.radius_uniform, a.radius_uniform);
+            const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w}, zs[4] = {Z.x, Z.y, Z.z, Z.w};
+            const float rs[4] = {Rw.x, Rw.y, Rw.z, Rw.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float Zf, mz;
+                bool cand = precull_fma_z<MODEL>(v, xs[j], ys[j], zs[j], Zf, mz);
+                if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)(i0 + 4 * h + j));
+                m |= (cand ? 1u : 0u) << (4 * h + j);
+            }
         }
         m &= live;
-        if (!__any_sync(kFull, m != 0u)) continue;
-        if (a.discard && a.radius && m != 0u) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.radius + i0));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.radius + i0 + 7));
-        }
         while (__any_sync(kFull, m != 0u)) {
             const bool ok = m != 0u;
             const int j = ok ? __ffs(m) - 1 : 0;
             m &= m - 1u;
-            // the lane's point j: row r at float index (r * 2 * kThreads + (j >> 2) * kThreads) * 4 + (j & 3)
             const int o = (j >> 2) * kThreads * 4 + (j & 3);
-            const float px = sx[o], py = sx[o + 2 * kThreads * 4], pz = sx[o + 4 * kThreads * 4];
-            const float rw = (ok && a.discard && a.radius) ? __ldg(a.radius + i0 + j) : a.radius_uniform;
+            const float px = sx[o], py = sx[o + kRow], pz = sx[o + 2 * kRow];
+            const float rw = staged_r ? sx[o + 3 * kRow] : a.radius_uniform;
             depth_candidate<MODEL>(a, v, vs, ok, px, py, pz, rw, i0 + j, a.goff + (uint32_t)(i0 + j), q, qn, qview,
-                                   buf, wcount, lane, lt);
+                                   c, lane, lt);
         }
     }
 }
-
-constexpr int kWTile = 256;  // points per warp tile (8 per lane)
-
-struct DepthSmem {
-    float4 pos[kStages][3][2][kThreads];  // stage, row, half, thread: the lane's 8 points per row
-    Record rec[kWarps][kCapT];
-    WarpQueue q[kWarps];
-};
 
 template <int MODEL>
 __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
@@ -428,26 +454,31 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     const int64_t W = (int64_t)gridDim.x * kWarps;
     const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
     const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
+    const bool staged_r = a.discard && a.radius != nullptr;
+    const int rows = staged_r ? 4 : 3;
     const uint64_t pol = policy_evict_first();
     auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
     auto issue = [&](int64_t k) {
         if (k < my && full_tile(k)) {
             const int s = (int)(k % kStages);
             const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
-            const float *src[3] = {a.x + i0, a.y + i0, a.z + i0};
+            const float *src[4] = {a.x + i0, a.y + i0, a.z + i0, a.radius + i0};
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                cp_async16(&sm.pos[s][r][0][tid], src[r], pol);
-                cp_async16(&sm.pos[s][r][1][tid], src[r] + 4, pol);
-            }
+            for (int r = 0; r < 4; ++r)
+                if (r < rows) {
+                    cp_async16(&sm.pos[s][r][0][tid], src[r], pol);
+                    cp_async16(&sm.pos[s][r][1][tid], src[r] + 4, pol);
+                }
         }
         cp_async_commit();  // one (possibly empty) group per tile keeps the group count uniform
     };
 #pragma unroll
     for (int k = 0; k < kStages - 1; ++k) issue(k);
-    Record *buf = sm.rec[wid];
     WarpQueue &q = sm.q[wid];
-    int wcount = 0, qn = 0, qview = 0;
+    int qn = 0, qview = 0;
+    RecChunk c;
+    c.base = 0;
+    c.left = 0;
     for (int64_t k = 0; k < my; ++k) {
         issue(k + kStages - 1);
         cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
@@ -455,27 +486,28 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
         const int s = (int)(k % kStages);
         int valid = 8;
         if (!full_tile(k)) {  // ragged last tile: guarded loads into this stage's (unused) slots
-            float t[3][8];
+            float t[4][8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const bool in = i0 + j < a.n;
                 t[0][j] = in ? a.x[i0 + j] : 0.f;
                 t[1][j] = in ? a.y[i0 + j] : 0.f;
                 t[2][j] = in ? a.z[i0 + j] : 0.f;
+                t[3][j] = (in && staged_r) ? a.radius[i0 + j] : 0.f;
             }
 #pragma unroll
-            for (int r = 0; r < 3; ++r) {
+            for (int r = 0; r < 4; ++r) {
                 sm.pos[s][r][0][tid] = make_float4(t[r][0], t[r][1], t[r][2], t[r][3]);
                 sm.pos[s][r][1][tid] = make_float4(t[r][4], t[r][5], t[r][6], t[r][7]);
             }
             const int64_t rem = a.n - i0;
             valid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
         }
-        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, q, qn, qview, buf, wcount, lane, lt);
+        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, staged_r, q, qn, qview, c, lane, lt);
     }
     cp_async_wait<0>();
-    if (qn > 0) drain(a, q, qn, qn, qview, buf, wcount, lane, lt);
-    if (wcount > 0) flush_records(a, buf, wcount, lane);
+    if (qn > 0) drain(a, q, qn, qn, qview, c, lane, lt);
+    rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
 
 // --------------------------------------------------------------------------- //
@@ -488,6 +520,7 @@ __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ Rast
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
         const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
+        if (rec.w == kDeadView) continue;
         const ViewDesc &v = a.v[rec.w];
         const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
         if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
