@@ -292,19 +292,21 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc
     }
 }
 
-// Process `cnt` (<= 32) entries from the top of the queue, one per lane.
-__device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, int qview, RecChunk &c,
-                                   int lane, unsigned lt) {
+// Process `cnt` (<= 32) entries from the top of the queue, one per lane (each with its own view slot).
+__device__ __forceinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, RecChunk &c, int lane,
+                                      unsigned lt) {
     __syncwarp();
-    int nk = 0;
+    int nk = 0, vs = 0;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
     if (lane < cnt) {
         e = q.e[qn - cnt + lane];
-        nk = q.meta[qn - cnt + lane] & 15;
+        const int meta = q.meta[qn - cnt + lane];
+        nk = meta & 15;
+        vs = meta >> 4;
     }
     __syncwarp();
     qn -= cnt;
-    depth_layers(a, a.v[qview], qview, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
+    depth_layers(a, a.v[vs], vs, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
 }
 
 // Candidate part for one point and view: pinned Xc = R x + t (R1), validity (R7), exact discard (Eq. 12,
@@ -313,7 +315,7 @@ __device__ __noinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, i
 template <int MODEL>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
                                                 float y, float z, float rw, int64_t i, uint32_t gi, WarpQueue &q,
-                                                int &qn, int &qview, RecChunk &c, int lane, unsigned lt) {
+                                                int &qn, RecChunk &c, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
     if (ok) {
@@ -326,15 +328,13 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
     const unsigned b = __ballot_sync(kFull, nk > 0);
     if (b == 0u) return;
-    if (qview != vs && qn > 0) drain(a, q, qn, qn, qview, c, lane, lt);  // the queue holds one view only
-    qview = vs;
     if (nk > 0) {
         const int slot = qn + __popc(b & lt);
         q.e[slot] = make_float4(p.u0, p.v0, p.Z, __uint_as_float((uint32_t)i));
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
     qn += __popc(b);
-    if (qn >= 32) drain(a, q, qn, 32, qview, c, lane, lt);
+    if (qn >= 32) drain(a, q, qn, 32, c, lane, lt);
 }
 
 // Bounding box of a lane's points (see box_culled).
@@ -400,7 +400,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 template <int MODEL>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*st)[2][kThreads], int tid,
                                             int64_t i0, int valid, bool staged_r, WarpQueue &q, int &qn,
-                                            int &qview, RecChunk &c, int lane, unsigned lt) {
+                                            RecChunk &c, int lane, unsigned lt) {
     uint32_t live = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
     if (a.ghost_thr != 0u) {
 #pragma unroll
@@ -438,8 +438,8 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
             const int o = (j >> 2) * kThreads * 4 + (j & 3);
             const float px = sx[o], py = sx[o + kRow], pz = sx[o + 2 * kRow];
             const float rw = staged_r ? sx[o + 3 * kRow] : a.radius_uniform;
-            depth_candidate<MODEL>(a, v, vs, ok, px, py, pz, rw, i0 + j, a.goff + (uint32_t)(i0 + j), q, qn, qview,
-                                   c, lane, lt);
+            depth_candidate<MODEL>(a, v, vs, ok, px, py, pz, rw, i0 + j, a.goff + (uint32_t)(i0 + j), q, qn, c,
+                                   lane, lt);
         }
     }
 }
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
 #pragma unroll
     for (int k = 0; k < kStages - 1; ++k) issue(k);
     WarpQueue &q = sm.q[wid];
-    int qn = 0, qview = 0;
+    int qn = 0;
     RecChunk c;
     c.base = 0;
     c.left = 0;
@@ -503,10 +503,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
             const int64_t rem = a.n - i0;
             valid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
         }
-        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, staged_r, q, qn, qview, c, lane, lt);
+        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, staged_r, q, qn, c, lane, lt);
     }
     cp_async_wait<0>();
-    if (qn > 0) drain(a, q, qn, qn, qview, c, lane, lt);
+    if (qn > 0) drain(a, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
 
