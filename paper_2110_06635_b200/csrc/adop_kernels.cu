@@ -237,7 +237,8 @@ struct WarpQueue {
 };
 
 struct DepthSmem {
-    float4 pos[kStages][4][2][kThreads];  // stage, row (x, y, z, r_world), half, thread
+    float pos[kStages][4][kWarps][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
+    uint64_t bar[kWarps][kStages];          // per-warp TMA completion barriers
     WarpQueue q[kWarps];
 };
 
@@ -342,17 +343,23 @@ struct Box {
     float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
 };
 
-__device__ __forceinline__ Box lane_box(const float4 (*st)[2][kThreads], int tid, int valid) {
+// The lane owns points e = h*128 + 4*lane + j (h = 0, 1; j = 0..3) of the warp tile: every LDS.128
+// of a row is then one contiguous 512-byte warp access.
+__device__ __forceinline__ float4 lane_row(const float *row, int lane, int h) {
+    return *reinterpret_cast<const float4 *>(row + h * 128 + 4 * lane);
+}
+
+__device__ __forceinline__ Box lane_box(const float *const *rows, int lane, int valid) {
     Box b;
     float ext = 0.0f;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-        const float4 A = st[ax][0][tid], Bv = st[ax][1][tid];
+        const float4 A = lane_row(rows[ax], lane, 0), Bv = lane_row(rows[ax], lane, 1);
         const float c[8] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w};
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (j < valid) {
+            if ((valid >> j) & 1) {
                 lo = fminf(lo, c[j]);
                 hi = fmaxf(hi, c[j]);
             }
@@ -395,21 +402,20 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
     return !(zl > 0.0f) || r * r * 1.002f > om;
 }
 
-// The 8 points of one lane (indices i0..i0+7, `valid` of them real), all views, read from the lane's
-// shared-memory slots st[row][half][tid].
+// The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
+// read from the warp tile's shared-memory rows.
 template <int MODEL>
-__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*st)[2][kThreads], int tid,
-                                            int64_t i0, int valid, bool staged_r, WarpQueue &q, int &qn,
-                                            RecChunk &c, int lane, unsigned lt) {
-    uint32_t live = valid >= 8 ? 0xFFu : ((1u << valid) - 1u);
+__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
+                                            bool staged_r, WarpQueue &q, int &qn, RecChunk &c, int lane,
+                                            unsigned lt) {
+    auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
+    uint32_t live = (uint32_t)vmask;
     if (a.ghost_thr != 0u) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (h24(a.ghost_salt, a.goff + (uint32_t)(i0 + j)) < a.ghost_thr) live &= ~(1u << j);
+            if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
     }
-    const Box box = lane_box(st, tid, valid);
-    const float *sx = reinterpret_cast<const float *>(&st[0][0][tid]);
-    constexpr int kRow = 2 * kThreads * 4;  // floats between rows of the lane's slots
+    const Box box = lane_box(rows, lane, vmask);
 #pragma unroll 1
     for (int vs = 0; vs < a.nviews; ++vs) {
         const ViewDesc &v = a.v[vs];
@@ -417,16 +423,17 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
         uint32_t m = 0u;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const float4 X = st[0][h][tid], Y = st[1][h][tid], Z = st[2][h][tid];
-            const float4 Rw = staged_r ? st[3][h][tid] : make_float4(a.radius_uniform, a.radius_uniform,
-                                                                     a.radius_uniform, a.radius_uniform);
+            const float4 X = lane_row(rows[0], lane, h), Y = lane_row(rows[1], lane, h), Z = lane_row(rows[2], lane, h);
+            const float4 Rw = staged_r ? lane_row(rows[3], lane, h)
+                                       : make_float4(a.radius_uniform, a.radius_uniform, a.radius_uniform,
+                                                     a.radius_uniform);
             const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w}, zs[4] = {Z.x, Z.y, Z.z, Z.w};
             const float rs[4] = {Rw.x, Rw.y, Rw.z, Rw.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 float Zf, mz;
                 bool cand = precull_fma_z<MODEL>(v, xs[j], ys[j], zs[j], Zf, mz);
-                if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)(i0 + 4 * h + j));
+                if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)pidx(4 * h + j));
                 m |= (cand ? 1u : 0u) << (4 * h + j);
             }
         }
@@ -435,11 +442,10 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float4 (*
             const bool ok = m != 0u;
             const int j = ok ? __ffs(m) - 1 : 0;
             m &= m - 1u;
-            const int o = (j >> 2) * kThreads * 4 + (j & 3);
-            const float px = sx[o], py = sx[o + kRow], pz = sx[o + 2 * kRow];
-            const float rw = staged_r ? sx[o + 3 * kRow] : a.radius_uniform;
-            depth_candidate<MODEL>(a, v, vs, ok, px, py, pz, rw, i0 + j, a.goff + (uint32_t)(i0 + j), q, qn, c,
-                                   lane, lt);
+            const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+            const float rw = staged_r ? rows[3][e] : a.radius_uniform;
+            depth_candidate<MODEL>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
+                                   a.goff + (uint32_t)(base + e), q, qn, c, lane, lt);
         }
     }
 }
@@ -456,56 +462,53 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
-    const uint64_t pol = policy_evict_first();
+    const float *src[4] = {a.x, a.y, a.z, a.radius};
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
     auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
+    // lane 0 of each warp streams its own tiles: `rows` 1-KB bulk copies (TMA engine, L2 evict-first)
     auto issue = [&](int64_t k) {
-        if (k < my && full_tile(k)) {
-            const int s = (int)(k % kStages);
-            const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
-            const float *src[4] = {a.x + i0, a.y + i0, a.z + i0, a.radius + i0};
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                if (r < rows) {
-                    cp_async16(&sm.pos[s][r][0][tid], src[r], pol);
-                    cp_async16(&sm.pos[s][r][1][tid], src[r] + 4, pol);
-                }
+        if (lane == 0 && k < my && full_tile(k)) {
+            const uint64_t pol = policy_evict_first();
+            const int st = (int)(k % kStages);
+            const int64_t base = (w0 + k * W) * kWTile;
+            mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
+            for (int r = 0; r < rows; ++r)
+                bulk_g2s(sm.pos[st][r][wid], src[r] + base, kWTile * sizeof(float), &sm.bar[wid][st], pol);
         }
-        cp_async_commit();  // one (possibly empty) group per tile keeps the group count uniform
     };
-#pragma unroll
-    for (int k = 0; k < kStages - 1; ++k) issue(k);
+    for (int k = 0; k < kStages; ++k) issue(k);
     WarpQueue &q = sm.q[wid];
     int qn = 0;
     RecChunk c;
     c.base = 0;
     c.left = 0;
     for (int64_t k = 0; k < my; ++k) {
-        issue(k + kStages - 1);
-        cp_async_wait<kStages - 1>();  // this lane's pieces of tile k have landed
-        const int64_t i0 = (w0 + k * W) * kWTile + 8 * lane;
-        const int s = (int)(k % kStages);
-        int valid = 8;
-        if (!full_tile(k)) {  // ragged last tile: guarded loads into this stage's (unused) slots
-            float t[4][8];
+        const int st = (int)(k % kStages);
+        const int64_t base = (w0 + k * W) * kWTile;
+        const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
+        int vmask = 0xFF;
+        if (full_tile(k)) {
+            mbar_wait(&sm.bar[wid][st], (uint32_t)((k / kStages) & 1));
+        } else {  // ragged last tile: guarded loads into this stage (no copy was issued for it)
+            vmask = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const bool in = i0 + j < a.n;
-                t[0][j] = in ? a.x[i0 + j] : 0.f;
-                t[1][j] = in ? a.y[i0 + j] : 0.f;
-                t[2][j] = in ? a.z[i0 + j] : 0.f;
-                t[3][j] = (in && staged_r) ? a.radius[i0 + j] : 0.f;
+                const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+                const bool in = base + e < a.n;
+                for (int r = 0; r < 4; ++r)
+                    sm.pos[st][r][wid][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                vmask |= (in ? 1 : 0) << j;
             }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                sm.pos[s][r][0][tid] = make_float4(t[r][0], t[r][1], t[r][2], t[r][3]);
-                sm.pos[s][r][1][tid] = make_float4(t[r][4], t[r][5], t[r][6], t[r][7]);
-            }
-            const int64_t rem = a.n - i0;
-            valid = rem <= 0 ? 0 : (rem >= 8 ? 8 : (int)rem);
+            __syncwarp();
         }
-        depth_lane8<MODEL>(a, sm.pos[s], tid, i0, valid, staged_r, q, qn, c, lane, lt);
+        depth_lane8<MODEL>(a, rp, base, vmask, staged_r, q, qn, c, lane, lt);
+        __syncwarp();  // every lane is done with stage st
+        issue(k + kStages);
     }
-    cp_async_wait<0>();
     if (qn > 0) drain(a, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
