@@ -139,7 +139,7 @@ ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_vi
                                 int64_t record_capacity, size_t *bytes);
 
 /* Phase 1, depth-only render pass (§4.5; Eqs. 2-4, 12, min_z of Eq. 6):
- * sets keys to the sentinel and accum/count to zero for every view, then
+ * sets keys to the sentinel for every view, then
  * atomically min-reduces the packed key of every render-set point into every
  * layer it lands on, and records the survivors in the workspace.
  * Caller-run collectives (point sharding) may min-reduce keys (as int64 or
@@ -150,8 +150,10 @@ ADOP_API adop_status adop_forward_depth(const adop_points *points, int32_t n_vie
                                void *workspace, size_t workspace_bytes, void *stream);
 
 /* Phase 2, accumulate (§4.5; fuzzy test Eq. 6, sums of Eq. 7):
- * for every survivor of phase 1 that passes z <= (1+alpha) * min_z against the
- * (possibly globally reduced) keys, adds tau to accum and 1 to count.
+ * sets accum and count to zero, then for every survivor of phase 1 that passes
+ * z <= (1+alpha) * min_z against the (possibly globally reduced) keys, adds tau
+ * to accum and 1 to count.  Caller-run collectives (point sharding) may
+ * sum-reduce accum and count before phase 3.
  * Must follow adop_forward_depth with the same arguments and workspace. */
 ADOP_API adop_status adop_forward_blend(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                const adop_pose *poses, const adop_params *params, const adop_pyramid *views,

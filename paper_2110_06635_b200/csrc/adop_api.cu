@@ -356,7 +356,7 @@ adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const
         return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, views, &ws);
-    int e = launch_clear(a, stream);
+    int e = launch_clear(a, 0, stream);
     if (e) return cuda_status(e, "clear launch");
     if (points->n > 0) {
         e = launch_depth(a, model, vec_path(points), device_sms(), stream);

@@ -76,7 +76,7 @@ struct RasterArgs {
 };
 
 // Launchers (adop_kernels.cu).  Return cudaError_t as int.
-int launch_clear(const RasterArgs &a, void *stream);
+int launch_clear(const RasterArgs &a, int what, void *stream);  // 0 keys+header, 1 accum+count
 int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream);
 int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream);
 int launch_resolve(const RasterArgs &a, void *stream);

@@ -33,27 +33,43 @@ enum { MODE_DEPTH = 0, MODE_BLEND = 1, MODE_MASKS = 2 };
 // --------------------------------------------------------------------------- //
 // clear
 // --------------------------------------------------------------------------- //
+// CLEAR_KEYS (phase 1): keys <- sentinel, workspace header reset.
+// CLEAR_ACC  (phase 2): accum, count <- 0 right before the blend, so the blend's reductions and the
+//                        resolve find these 55 MB (configs[3]) still in L2.
+enum { CLEAR_KEYS = 0, CLEAR_ACC = 1 };
+template <int WHAT>
 __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     const int64_t P = v.pixels;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const uint64_t sentinel = 0x7FFFFFFFFFFFFFFFull;
-    for (int64_t p = tid; p < P; p += stride) {
-        v.keys[p] = sentinel;
-        v.count[p] = 0.0f;
+    if (WHAT == CLEAR_KEYS) {
+        const unsigned long long sentinel = 0x7FFFFFFFFFFFFFFFull;
+        unsigned long long *k = reinterpret_cast<unsigned long long *>(v.keys);
+        if ((reinterpret_cast<uintptr_t>(k) & 15) == 0) {
+            for (int64_t q = tid; q < P / 2; q += stride)
+                reinterpret_cast<ulonglong2 *>(k)[q] = make_ulonglong2(sentinel, sentinel);
+            for (int64_t q = (P / 2) * 2 + tid; q < P; q += stride) k[q] = sentinel;
+        } else {
+            for (int64_t q = tid; q < P; q += stride) k[q] = sentinel;
+        }
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+            a.hdr->records = 0ull;
+            a.hdr->overflow = 0;
+        }
+        return;
     }
-    const int64_t PA = P * a.channels;
-    float *acc = v.accum;
-    if ((reinterpret_cast<uintptr_t>(acc) & 15) == 0) {
-        for (int64_t q = tid; q < PA / 4; q += stride) reinterpret_cast<float4 *>(acc)[q] = make_float4(0, 0, 0, 0);
-        for (int64_t q = (PA / 4) * 4 + tid; q < PA; q += stride) acc[q] = 0.0f;
-    } else {
-        for (int64_t q = tid; q < PA; q += stride) acc[q] = 0.0f;
-    }
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-        a.hdr->records = 0ull;
-        a.hdr->overflow = 0;
+    float *bufs[2] = {v.accum, v.count};
+    const int64_t lens[2] = {P * a.channels, P};
+    for (int b = 0; b < 2; ++b) {
+        float *acc = bufs[b];
+        const int64_t n = lens[b];
+        if ((reinterpret_cast<uintptr_t>(acc) & 15) == 0) {
+            for (int64_t q = tid; q < n / 4; q += stride) reinterpret_cast<float4 *>(acc)[q] = make_float4(0, 0, 0, 0);
+            for (int64_t q = (n / 4) * 4 + tid; q < n; q += stride) acc[q] = 0.0f;
+        } else {
+            for (int64_t q = tid; q < n; q += stride) acc[q] = 0.0f;
+        }
     }
 }
 
@@ -128,9 +144,8 @@ __device__ __forceinline__ void accumulate_feature(const RasterArgs &a, const Vi
 // streaming sweep over all points (depth pass / blend fallback / masks)
 // --------------------------------------------------------------------------- //
 template <int MODEL, bool VEC, int MODE, bool VEC4>
-__global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ RasterArgs a) {
+__device__ __forceinline__ void stream_sweep(const RasterArgs &a) {
     __shared__ __align__(16) Record sbuf[MODE == MODE_DEPTH ? kWarps : 1][MODE == MODE_DEPTH ? kCap : 1];
-    if (MODE == MODE_BLEND && !*(volatile int32_t *)&a.hdr->overflow) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     int wcount = 0;
@@ -196,6 +211,11 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
         }
     }
     if (MODE == MODE_DEPTH && wcount > 0) flush_records(a, sbuf[wid], wcount, lane);
+}
+
+template <int MODEL, bool VEC, int MODE, bool VEC4>
+__global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ RasterArgs a) {
+    stream_sweep<MODEL, VEC, MODE, VEC4>(a);
 }
 
 // --------------------------------------------------------------------------- //
@@ -516,9 +536,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
 // --------------------------------------------------------------------------- //
 // blend over survivor records (§4.5 accumulate pass)
 // --------------------------------------------------------------------------- //
-template <bool VEC4>
+template <int MODEL, bool VEC, bool VEC4>
 __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ RasterArgs a) {
-    if (*(volatile int32_t *)&a.hdr->overflow) return;
+    if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
+        stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
+        return;
+    }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->records;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
@@ -533,11 +556,43 @@ __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ Rast
 // --------------------------------------------------------------------------- //
 // resolve: Eq. 7 (mean or background), planar per-layer output
 // --------------------------------------------------------------------------- //
+// Groups of 4 consecutive pixels of one layer (host guarantees off_l and h_l*w_l are multiples of 4
+// when VEC4): one 16-B count load, accum read only for covered pixels, one 16-B store per channel plane.
 template <bool VEC4>
 __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     const int C = a.channels;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (VEC4) {
+        for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < v.pixels / 4; g += stride) {
+            const int64_t p = 4 * g;
+            int l = 0;
+#pragma unroll
+            for (int k = 1; k < ADOP_MAX_LAYERS; ++k)
+                if (k < a.layers && p >= v.off[k]) l = k;
+            const int64_t j = p - v.off[l];
+            const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+            const float4 cnt = __ldcs(reinterpret_cast<const float4 *>(v.count + p));
+            const float cn[4] = {cnt.x, cnt.y, cnt.z, cnt.w};
+            float *img = v.image + (int64_t)C * v.off[l] + j;
+            for (int c0 = 0; c0 < C; c0 += 4) {
+                float o[4][4];  // [channel][pixel]
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (cn[q] > 0.0f) acc = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
+                    const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc)
+                        o[cc][q] = cn[q] > 0.0f ? __fdiv_rn(av[cc], cn[q]) : a.bg[c0 + cc];
+                }
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc)
+                    __stcs(reinterpret_cast<float4 *>(img + (c0 + cc) * hw), make_float4(o[cc][0], o[cc][1], o[cc][2], o[cc][3]));
+            }
+        }
+        return;
+    }
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
         int l = 0;
 #pragma unroll
@@ -548,18 +603,7 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
         const float cnt = __ldcs(v.count + p);
         float *img = v.image + (int64_t)C * v.off[l] + j;
         const float *acc = v.accum + p * C;
-        if (VEC4) {
-            for (int c = 0; c < C; c += 4) {
-                const float4 s = __ldcs(reinterpret_cast<const float4 *>(acc + c));
-                const bool hit = cnt > 0.0f;
-                __stcs(img + (c + 0) * hw, hit ? __fdiv_rn(s.x, cnt) : a.bg[c + 0]);
-                __stcs(img + (c + 1) * hw, hit ? __fdiv_rn(s.y, cnt) : a.bg[c + 1]);
-                __stcs(img + (c + 2) * hw, hit ? __fdiv_rn(s.z, cnt) : a.bg[c + 2]);
-                __stcs(img + (c + 3) * hw, hit ? __fdiv_rn(s.w, cnt) : a.bg[c + 3]);
-            }
-        } else {
-            for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fdiv_rn(acc[c], cnt) : a.bg[c]);
-        }
+        for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fdiv_rn(acc[c], cnt) : a.bg[c]);
     }
 }
 
@@ -784,13 +828,16 @@ static bool accum_vec4(const RasterArgs &a) {
     return true;
 }
 
-int launch_clear(const RasterArgs &a, void *stream) {
+int launch_clear(const RasterArgs &a, int what, void *stream) {
     int64_t maxP = 1;
     for (int v = 0; v < a.nviews; ++v) maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
     int64_t bx = (maxP + kThreads * 4 - 1) / (kThreads * 4);
-    if (bx > 1024) bx = 1024;
+    if (bx > 1184) bx = 1184;
     dim3 grid((unsigned)bx, (unsigned)a.nviews);
-    k_clear<<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    if (what == CLEAR_KEYS)
+        k_clear<CLEAR_KEYS><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else
+        k_clear<CLEAR_ACC><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
 }
 
@@ -827,16 +874,11 @@ int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream
 template <int MODEL, bool VEC, bool VEC4>
 static int launch_blend_t(const RasterArgs &a, int sms, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    {
-        auto k = k_blend<VEC4>;
-        int g = resident_grid(k, sms, kThreads, (int64_t)sms * 64 * kThreads);
-        k<<<g, kThreads, 0, s>>>(a);
-    }
-    {   // overflow fallback: returns immediately unless the record list overflowed
-        auto k = k_stream<MODEL, VEC, MODE_BLEND, VEC4>;
-        int g = resident_grid(k, sms, kWarps * 128, a.n);
-        k<<<g, kThreads, 0, s>>>(a);
-    }
+    int e = launch_clear(a, CLEAR_ACC, stream);
+    if (e) return e;
+    auto k = k_blend<MODEL, VEC, VEC4>;
+    int g = resident_grid(k, sms, kWarps * 128, a.n > 0 ? a.n : 1);
+    k<<<g, kThreads, 0, s>>>(a);
     return (int)cudaGetLastError();
 }
 
@@ -856,7 +898,15 @@ int launch_resolve(const RasterArgs &a, void *stream) {
     int64_t bx = (maxP + kThreads - 1) / kThreads;
     if (bx > 4096) bx = 4096;
     dim3 grid((unsigned)bx, (unsigned)a.nviews);
-    if (accum_vec4(a))
+    bool v4 = accum_vec4(a);
+    for (int v = 0; v < a.nviews && v4; ++v) {
+        if (reinterpret_cast<uintptr_t>(a.v[v].count) & 15) v4 = false;
+        if (reinterpret_cast<uintptr_t>(a.v[v].image) & 15) v4 = false;
+        for (int l = 0; l < a.layers; ++l)
+            if ((a.v[v].off[l] & 3) || (((int64_t)a.v[v].wl[l] * a.v[v].hl[l]) & 3)) v4 = false;
+        if (a.v[v].pixels & 3) v4 = false;
+    }
+    if (v4)
         k_resolve<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
     else
         k_resolve<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
