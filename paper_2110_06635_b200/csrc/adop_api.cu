@@ -374,10 +374,9 @@ adop_status adop_forward_blend(const adop_points *points, int32_t n_views, const
     int model;
     if (!uniform_model(n_views, cameras, model))
         return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
-    if (points->n == 0) return ok();
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, views, &ws);
-    int e = launch_blend(a, model, vec_path(points), device_sms(), stream);
+    int e = launch_blend(a, model, vec_path(points), device_sms(), stream);  // also clears accum/count
     if (e) return cuda_status(e, "blend launch");
     return ok();
 }
