@@ -787,6 +787,221 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
         a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = spose[t];
 }
 
+// --------------------------------------------------------------------------- //
+// backward, TMA-pipelined (same tiling as k_depth_async)
+//
+// Overwrite mode first zero-fills d_feat / d_pos (k_fill, write bandwidth); the sweep then only
+// touches points that are rendered or ghosts at some layer of some view: per tile and view the
+// lane-box cull, the branch-free FMA pre-cull + early discard mask, then one candidate per lane per
+// iteration: exact projection and discard (bit-identical to the forward), the texture gradient of
+// rendered points (fuzzy membership against the forward's keys, G / |Lambda|, R24) and, for ghosts,
+// the 4-neighbour Eq. 11 terms (R14-R16) -> g (R17) -> w = J^T g (R21) -> dx = R^T w and the tangent
+// pose terms (w, Xc x w) (R19), warp-reduced in fp64.  Each point belongs to one lane, so its gradient
+// rows are updated with plain read-modify-writes (no atomics).
+// --------------------------------------------------------------------------- //
+__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float *bufs[2] = {p, q};
+    const int64_t lens[2] = {n, m};
+    for (int b = 0; b < 2; ++b) {
+        float *x = bufs[b];
+        const int64_t len = lens[b];
+        if (!x) continue;
+        const int64_t head = (int64_t)(((16 - (reinterpret_cast<uintptr_t>(x) & 15)) & 15) / 4);
+        const int64_t h = head < len ? head : len;
+        for (int64_t k = tid; k < h; k += stride) x[k] = 0.0f;
+        float4 *x4 = reinterpret_cast<float4 *>(x + h);
+        const int64_t n4 = (len - h) / 4;
+        for (int64_t k = tid; k < n4; k += stride) x4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t k = h + 4 * n4 + tid; k < len; k += stride) x[k] = 0.0f;
+    }
+}
+
+template <int MODEL, int CT>
+__device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost,
+                                              float x, float y, float z, float rw, int64_t i, uint32_t gi,
+                                              double *spose, int lane) {
+    const int C = CT > 0 ? CT : a.channels;
+    Proj p;
+    int nk = 0;
+    if (ok) {
+        to_camera(v, x, y, z, p.X, p.Y, p.Z);
+        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
+            p.iz = __frcp_rn(p.Z);
+            nk = keep_layers(a, v, rw, p.iz, gi);
+            if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
+        }
+    }
+    if (nk > 0 && !ghost && a.d_feat) {
+        // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
+        float *df = a.d_feat + i * C;
+        for (int l = 0; l < nk; ++l) {
+            int pu, pv;
+            const int loc = layer_pixel(v, p, l, pu, pv);
+            if (loc < 0) continue;
+            const int q = v.off[l] + loc;
+            if (!fuzzy_pass(p.Z, __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + q), a.onepa)) continue;
+            const float cnt = __ldcg(v.count + q);
+            const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+            const float *G = v.grad + (int64_t)C * v.off[l] + loc;
+#pragma unroll
+            for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
+                if (CT == 0 && c >= C) break;
+                df[c] += __fdiv_rn(__ldg(G + c * hw), cnt);
+            }
+        }
+    }
+    float gu = 0.f, gv = 0.f;
+    bool gc = false;
+    if (nk > 0 && ghost) {
+        float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
+        for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + i * C + c);
+        for (int l = 0; l < nk; ++l) {
+            int pu, pv;
+            const int loc = layer_pixel(v, p, l, pu, pv);
+            if (loc < 0) continue;
+            // Eqs. 9-11: signed central differences over the 4-neighbourhood (R14, R15)
+            const float dup = neighbour_term<CT>(a, v, l, pu + 1, pv, p.Z, tau);
+            const float dum = neighbour_term<CT>(a, v, l, pu - 1, pv, p.Z, tau);
+            const float dvp = neighbour_term<CT>(a, v, l, pu, pv + 1, p.Z, tau);
+            const float dvm = neighbour_term<CT>(a, v, l, pu, pv - 1, p.Z, tau);
+            const float sc = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
+            gu += sc * (dup - dum);
+            gv += sc * (dvp - dvm);
+            gc = true;
+        }
+    }
+    if (!__any_sync(kFull, gc)) return;
+    float w0 = 0.f, w1 = 0.f, w2 = 0.f;
+    if (gc) {
+        float J[6];
+        jacobian<MODEL>(v, p, J);
+        w0 = J[0] * gu + J[3] * gv;  // w = J^T g = dL/dXc
+        w1 = J[1] * gu + J[4] * gv;
+        w2 = J[2] * gu + J[5] * gv;
+        if (a.d_pos) {
+            float *dp = a.d_pos;
+            dp[i] += v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2;  // dx = R^T w
+            dp[a.n + i] += v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2;
+            dp[2 * a.n + i] += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
+        }
+    }
+    // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64
+    double t6[6];
+    t6[0] = w0; t6[1] = w1; t6[2] = w2;
+    t6[3] = gc ? (double)(p.Y * w2 - p.Z * w1) : 0.0;
+    t6[4] = gc ? (double)(p.Z * w0 - p.X * w2) : 0.0;
+    t6[5] = gc ? (double)(p.X * w1 - p.Y * w0) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const double sum = warp_sum(t6[k]);
+        if (lane == 0) atomicAdd(&spose[vs * 6 + k], sum);
+    }
+}
+
+struct BwdSmem {
+    float pos[kStages][4][kWarps][kWTile];
+    uint64_t bar[kWarps][kStages];
+    double spose[ADOP_MAX_VIEWS_PER_LAUNCH * 6];
+};
+
+template <int MODEL, int CT>
+__global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_constant__ RasterArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int t = tid; t < a.nviews * 6; t += kThreads) sm.spose[t] = 0.0;
+    const int64_t ntiles = (a.n + kWTile - 1) / kWTile;
+    const int64_t W = (int64_t)gridDim.x * kWarps;
+    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
+    const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
+    const bool staged_r = a.discard && a.radius != nullptr;
+    const int rows = staged_r ? 4 : 3;
+    const float *src[4] = {a.x, a.y, a.z, a.radius};
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
+    auto issue = [&](int64_t k) {
+        if (lane == 0 && k < my && full_tile(k)) {
+            const uint64_t pol = policy_evict_first();
+            const int st = (int)(k % kStages);
+            const int64_t base = (w0 + k * W) * kWTile;
+            mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
+            for (int r = 0; r < rows; ++r)
+                bulk_g2s(sm.pos[st][r][wid], src[r] + base, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+        }
+    };
+    for (int k = 0; k < kStages; ++k) issue(k);
+    for (int64_t k = 0; k < my; ++k) {
+        const int st = (int)(k % kStages);
+        const int64_t base = (w0 + k * W) * kWTile;
+        const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
+        int vmask = 0xFF;
+        if (full_tile(k)) {
+            mbar_wait(&sm.bar[wid][st], (uint32_t)((k / kStages) & 1));
+        } else {
+            vmask = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+                const bool in = base + e < a.n;
+                for (int r = 0; r < 4; ++r) sm.pos[st][r][wid][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                vmask |= (in ? 1 : 0) << j;
+            }
+            __syncwarp();
+        }
+        auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
+        uint32_t ghosts = 0u;
+        if (a.ghost_thr != 0u) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
+        }
+        const Box box = lane_box(rp, lane, vmask);
+#pragma unroll 1
+        for (int vs = 0; vs < a.nviews; ++vs) {
+            const ViewDesc &v = a.v[vs];
+            if (__all_sync(kFull, box_culled(v, box))) continue;
+            uint32_t m = 0u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float4 X = lane_row(rp[0], lane, h), Y = lane_row(rp[1], lane, h), Z = lane_row(rp[2], lane, h);
+                const float4 Rw = staged_r ? lane_row(rp[3], lane, h)
+                                           : make_float4(a.radius_uniform, a.radius_uniform, a.radius_uniform,
+                                                         a.radius_uniform);
+                const float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w}, zs[4] = {Z.x, Z.y, Z.z, Z.w};
+                const float rs[4] = {Rw.x, Rw.y, Rw.z, Rw.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float Zf, mz;
+                    bool cand = precull_fma_z<MODEL>(v, xs[j], ys[j], zs[j], Zf, mz);
+                    if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)pidx(4 * h + j));
+                    m |= (cand ? 1u : 0u) << (4 * h + j);
+                }
+            }
+            m &= (uint32_t)vmask;
+            while (__any_sync(kFull, m != 0u)) {
+                const bool ok = m != 0u;
+                const int j = ok ? __ffs(m) - 1 : 0;
+                m &= m - 1u;
+                const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+                const float rw = staged_r ? rp[3][e] : a.radius_uniform;
+                bwd_candidate<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
+                                         a.goff + (uint32_t)(base + e), sm.spose, lane);
+            }
+        }
+        __syncwarp();
+        issue(k + kStages);
+    }
+    __syncthreads();
+    for (int t = tid; t < a.nviews * 6; t += kThreads)
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = sm.spose[t];
+}
+
 // d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
 __global__ void __launch_bounds__(256) k_pose_reduce(const double *partials, int nblocks, int nvals, double *d_pose,
                                                      int accumulate) {
@@ -921,10 +1136,40 @@ int backward_grid(int sms) {
 template <int MODEL, bool VEC, int CT>
 static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    auto k = k_backward<MODEL, VEC, CT>;
-    int g = resident_grid(k, sms, kWarps * 128, a.n);
-    if (g > grid_cap) g = grid_cap;
-    k<<<g, kThreads, 0, s>>>(a);
+    int g = 1;
+    if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0)) {
+        if (!a.grad_accumulate && (a.d_feat || a.d_pos)) {
+            int64_t nf = a.d_feat ? a.n * a.channels : 0, np = a.d_pos ? 3 * a.n : 0;
+            int64_t mx = nf > np ? nf : np;
+            int64_t bx = (mx / 4 + kThreads - 1) / kThreads;
+            if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
+            if (bx < 1) bx = 1;
+            k_fill<<<(unsigned)bx, kThreads, 0, s>>>(a.d_feat, nf, a.d_pos, np);
+        }
+        RasterArgs b = a;
+        b.grad_accumulate = 1;  // the sweep adds into the (zeroed or caller's) gradients
+        auto k = k_backward_async<MODEL, CT>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
+            attr = true;
+        }
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(BwdSmem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t tiles = (a.n + kWTile - 1) / kWTile;
+        int64_t gg = (int64_t)sms * per_sm;
+        if ((tiles + kWarps - 1) / kWarps < gg) gg = (tiles + kWarps - 1) / kWarps;
+        if (gg > grid_cap) gg = grid_cap;
+        if (gg < 1) gg = 1;
+        g = (int)gg;
+        k<<<g, kThreads, sizeof(BwdSmem), s>>>(b);
+    } else {
+        auto k = k_backward<MODEL, VEC, CT>;
+        g = resident_grid(k, sms, kWarps * 128, a.n);
+        if (g > grid_cap) g = grid_cap;
+        k<<<g, kThreads, 0, s>>>(a);
+    }
     if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, g, a.nviews * 6, d_pose, a.grad_accumulate);
     return (int)cudaGetLastError();
 }
