@@ -171,7 +171,7 @@ ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n
                                    void *workspace, size_t workspace_bytes, void *stream);
 
 /* Backward (§4.2-4.5): re-renders every point (L361) against the forward's
- * keys/count/image (which must be unmodified) and the upstream gradient
+ * keys/count/accum/image (which must be unmodified) and the upstream gradient
  * grad_image[v] (device, image layout) and produces
  *   d_feat [n][C]: sum over views/layers of G/|Lambda| for rendered points (ghosts 0),
  *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17),

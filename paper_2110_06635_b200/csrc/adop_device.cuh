@@ -170,7 +170,8 @@ __device__ __forceinline__ int keep_layers(const RasterArgs &a, const ViewDesc &
 }
 
 // Eqs. 3-4: layer-local pixel (u, v) and bounds.  Returns layer-local linear index or -1.
-__device__ __forceinline__ int layer_pixel(const ViewDesc &v, const Proj &p, int l, int &pu, int &pv) {
+template <typename VD>
+__device__ __forceinline__ int layer_pixel(const VD &v, const Proj &p, int l, int &pu, int &pv) {
     float s = pow2_neg(l);
     float ru = round_away(fmul(p.u0, s));
     float rv = round_away(fmul(p.v0, s));

@@ -31,6 +31,7 @@ struct ViewDesc {
     uint64_t *keys;
     float *accum, *count, *image;
     const float *grad;     // backward: dL/dI (image layout)
+    const float *gradT;    // backward: dL/dI transposed to [P][C] in the workspace (or NULL)
 };
 
 struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
@@ -41,9 +42,11 @@ struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
 };
 
 struct WsHeader {
-    unsigned long long records;  // survivors emitted by the last depth pass
-    int32_t overflow;            // set when records > capacity
+    unsigned long long records;    // record slots used by the last depth pass
+    int32_t overflow;              // set when records > capacity
     int32_t pad;
+    unsigned long long tiles_fwd;  // dynamic tile counters of the depth and backward sweeps
+    unsigned long long tiles_bwd;
 };
 
 struct RasterArgs {

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
             a.hdr->records = 0ull;
             a.hdr->overflow = 0;
+            a.hdr->tiles_fwd = 0ull;
         }
         return;
     }
@@ -256,11 +257,30 @@ struct WarpQueue {
     uint8_t meta[kQCap];  // kept layers (low 4 bits) | view slot << 4
 };
 
+// Per-view layer table in shared memory: the drain indexes it with a per-lane view slot (divergent
+// constant-bank loads would serialise).
+struct LayerDesc {
+    int32_t off[ADOP_MAX_LAYERS], wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS];
+    uint64_t *keys;
+};
+
 struct DepthSmem {
     float pos[kStages][4][kWarps][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
     uint64_t bar[kWarps][kStages];          // per-warp TMA completion barriers
+    long long tile[kWarps][kStages];        // tile claimed into each stage
     WarpQueue q[kWarps];
+    LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
 };
+
+__device__ __forceinline__ void init_layer_descs(const RasterArgs &a, LayerDesc *ld) {
+    for (int t = threadIdx.x; t < a.nviews * (3 * ADOP_MAX_LAYERS + 1); t += blockDim.x) {
+        const int v = t / (3 * ADOP_MAX_LAYERS + 1), f = t % (3 * ADOP_MAX_LAYERS + 1);
+        if (f < ADOP_MAX_LAYERS) ld[v].off[f] = a.v[v].off[f];
+        else if (f < 2 * ADOP_MAX_LAYERS) ld[v].wl[f - ADOP_MAX_LAYERS] = a.v[v].wl[f - ADOP_MAX_LAYERS];
+        else if (f < 3 * ADOP_MAX_LAYERS) ld[v].hl[f - 2 * ADOP_MAX_LAYERS] = a.v[v].hl[f - 2 * ADOP_MAX_LAYERS];
+        else ld[v].keys = a.v[v].keys;
+    }
+}
 
 struct RecChunk {  // warp-uniform
     unsigned long long base;
@@ -285,7 +305,7 @@ __device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, in
 }
 
 // Layers of one kept point per lane (nk = 0: idle lane).  Warp-collective.
-__device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc &v, int vs, int nk, float u0,
+__device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDesc &v, int vs, int nk, float u0,
                                              float v0, uint32_t zbits, uint32_t idx, RecChunk &c, int lane,
                                              unsigned lt) {
     const uint64_t key = ((uint64_t)zbits << 32) | (a.goff + idx);
@@ -314,8 +334,8 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const ViewDesc
 }
 
 // Process `cnt` (<= 32) entries from the top of the queue, one per lane (each with its own view slot).
-__device__ __forceinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn, int cnt, RecChunk &c, int lane,
-                                      unsigned lt) {
+__device__ __forceinline__ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int cnt,
+                                      RecChunk &c, int lane, unsigned lt) {
     __syncwarp();
     int nk = 0, vs = 0;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -327,7 +347,7 @@ __device__ __forceinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn
     }
     __syncwarp();
     qn -= cnt;
-    depth_layers(a, a.v[vs], vs, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
+    depth_layers(a, ld[vs], vs, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
 }
 
 // Candidate part for one point and view: pinned Xc = R x + t (R1), validity (R7), exact discard (Eq. 12,
@@ -335,8 +355,8 @@ __device__ __forceinline__ void drain(const RasterArgs &a, WarpQueue &q, int &qn
 // which is drained 32 at a time.  Warp-collective.
 template <int MODEL>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
-                                                float y, float z, float rw, int64_t i, uint32_t gi, WarpQueue &q,
-                                                int &qn, RecChunk &c, int lane, unsigned lt) {
+                                                float y, float z, float rw, int64_t i, uint32_t gi, const LayerDesc *ld,
+                                                WarpQueue &q, int &qn, RecChunk &c, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
     if (ok) {
@@ -355,7 +375,7 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
     qn += __popc(b);
-    if (qn >= 32) drain(a, q, qn, 32, c, lane, lt);
+    if (qn >= 32) drain(a, ld, q, qn, 32, c, lane, lt);
 }
 
 // Bounding box of a lane's points (see box_culled).
@@ -426,8 +446,8 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 // read from the warp tile's shared-memory rows.
 template <int MODEL>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
-                                            bool staged_r, WarpQueue &q, int &qn, RecChunk &c, int lane,
-                                            unsigned lt) {
+                                            bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
+                                            int lane, unsigned lt) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     uint32_t live = (uint32_t)vmask;
     if (a.ghost_thr != 0u) {
@@ -465,7 +485,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
             const float rw = staged_r ? rows[3][e] : a.radius_uniform;
             depth_candidate<MODEL>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
-                                   a.goff + (uint32_t)(base + e), q, qn, c, lane, lt);
+                                   a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
         }
     }
 }
@@ -476,43 +496,49 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t ntiles = (a.n + kWTile - 1) / kWTile;
-    const int64_t W = (int64_t)gridDim.x * kWarps;
-    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
-    const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
+    const long long ntiles = (a.n + kWTile - 1) / kWTile;
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
     const float *src[4] = {a.x, a.y, a.z, a.radius};
+    init_layer_descs(a, sm.ld);
     if (lane == 0) {
         for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
         fence_mbar_init();
     }
-    __syncwarp();
-    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
-    // lane 0 of each warp streams its own tiles: `rows` 1-KB bulk copies (TMA engine, L2 evict-first)
-    auto issue = [&](int64_t k) {
-        if (lane == 0 && k < my && full_tile(k)) {
-            const uint64_t pol = policy_evict_first();
-            const int st = (int)(k % kStages);
-            const int64_t base = (w0 + k * W) * kWTile;
-            mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-            for (int r = 0; r < rows; ++r)
-                bulk_g2s(sm.pos[st][r][wid], src[r] + base, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+    __syncthreads();
+    auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
+    // lane 0 of each warp claims the next tile of the whole grid (dynamic load balance) and streams it
+    // with `rows` 1-KB bulk copies (TMA engine, L2 evict-first) into stage st
+    auto issue = [&](int st) {
+        if (lane == 0) {
+            const long long t = (long long)atomicAdd(&a.hdr->tiles_fwd, 1ull);
+            sm.tile[wid][st] = t;
+            if (t < ntiles && full_tile(t)) {
+                const uint64_t pol = policy_evict_first();
+                mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
+                for (int r = 0; r < rows; ++r)
+                    bulk_g2s(sm.pos[st][r][wid], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+            }
         }
     };
-    for (int k = 0; k < kStages; ++k) issue(k);
+    for (int st = 0; st < kStages; ++st) issue(st);
+    __syncwarp();
     WarpQueue &q = sm.q[wid];
     int qn = 0;
     RecChunk c;
     c.base = 0;
     c.left = 0;
-    for (int64_t k = 0; k < my; ++k) {
+    uint32_t phase = 0u;
+    for (int64_t k = 0;; ++k) {
         const int st = (int)(k % kStages);
-        const int64_t base = (w0 + k * W) * kWTile;
+        const long long t = *(volatile long long *)&sm.tile[wid][st];
+        if (t >= ntiles) break;
+        const int64_t base = t * kWTile;
         const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
         int vmask = 0xFF;
-        if (full_tile(k)) {
-            mbar_wait(&sm.bar[wid][st], (uint32_t)((k / kStages) & 1));
+        if (full_tile(t)) {
+            mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
+            phase ^= 1u << st;
         } else {  // ragged last tile: guarded loads into this stage (no copy was issued for it)
             vmask = 0;
 #pragma unroll
@@ -525,11 +551,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
             }
             __syncwarp();
         }
-        depth_lane8<MODEL>(a, rp, base, vmask, staged_r, q, qn, c, lane, lt);
+        depth_lane8<MODEL>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
         __syncwarp();  // every lane is done with stage st
-        issue(k + kStages);
+        issue(st);
+        __syncwarp();
     }
-    if (qn > 0) drain(a, q, qn, qn, c, lane, lt);
+    if (qn > 0) drain(a, sm.ld, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
 
@@ -610,33 +637,66 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
 // --------------------------------------------------------------------------- //
 // backward
 // --------------------------------------------------------------------------- //
-// Image-space gradient contribution of one neighbour q (Eq. 11 as R14, times G as R16).
+// Image-space gradient contribution of one neighbour q (Eq. 11 as R14, times G as R16).  I_q is
+// recomputed from the forward's interleaved accum/count exactly as k_resolve computed it
+// (bit-identical), and G is read from the transposed copy when available: one or two sectors per
+// neighbour instead of 2C scattered planar reads.
 template <int CT>
 __device__ __forceinline__ float neighbour_term(const RasterArgs &a, const ViewDesc &v, int l, int qu, int qv,
                                                 float z, const float *tau) {
     if (qu < 0 || qv < 0 || qu >= v.wl[l] || qv >= v.hl[l]) return 0.0f;  // outside: no term
     const int j = qv * v.wl[l] + qu;
     const int q = v.off[l] + j;
-    const float nq = v.count[q];
+    const float nq = __ldcg(v.count + q);
     float factor;
     if (nq == 0.0f) {
         factor = 1.0f;                                     // case 1: background neighbour
     } else {
-        const float m = __uint_as_float((uint32_t)(v.keys[q] >> 32));
+        const float m = __uint_as_float((uint32_t)(__ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + q) >> 32));
         if (z > fmul(a.onepa, m)) return 0.0f;             // case 2: behind
         factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
     }
     const int C = CT > 0 ? CT : a.channels;
-    const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
-    const float *G = v.grad + (int64_t)C * v.off[l] + j;
-    const float *I = v.image + (int64_t)C * v.off[l] + j;
     float d = 0.0f;
+    if (v.gradT) {
+        const float *G = v.gradT + (int64_t)q * C;
+        const float *A = v.accum + (int64_t)q * C;
 #pragma unroll
-    for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
-        if (CT == 0 && c >= C) break;
-        d = fmaf(__ldg(G + c * hw), tau[c] - __ldg(I + c * hw), d);
+        for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
+            if (CT == 0 && c >= C) break;
+            const float Iq = nq > 0.0f ? __fdiv_rn(__ldcg(A + c), nq) : a.bg[c];
+            d = fmaf(__ldcg(G + c), tau[c] - Iq, d);
+        }
+    } else {
+        const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+        const float *G = v.grad + (int64_t)C * v.off[l] + j;
+        const float *I = v.image + (int64_t)C * v.off[l] + j;
+#pragma unroll
+        for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
+            if (CT == 0 && c >= C) break;
+            d = fmaf(__ldg(G + c * hw), tau[c] - __ldg(I + c * hw), d);
+        }
     }
     return factor * d;
+}
+
+// dL/dI of one view transposed from the planar layout [C][h_l][w_l] to [P][C] (workspace scratch),
+// so the backward's gathers read one contiguous row per pixel.
+__global__ void __launch_bounds__(kThreads) k_transpose_grad(const __grid_constant__ RasterArgs a) {
+    const ViewDesc &v = a.v[blockIdx.y];
+    const int C = a.channels;
+    float *out = const_cast<float *>(v.gradT);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
+        int l = 0;
+#pragma unroll
+        for (int k = 1; k < ADOP_MAX_LAYERS; ++k)
+            if (k < a.layers && p >= v.off[k]) l = k;
+        const int64_t j = p - v.off[l];
+        const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+        const float *G = v.grad + (int64_t)C * v.off[l] + j;
+        for (int c = 0; c < C; ++c) out[p * C + c] = __ldcs(G + c * hw);
+    }
 }
 
 template <int MODEL>
@@ -799,8 +859,10 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
 // pose terms (w, Xc x w) (R19), warp-reduced in fp64.  Each point belongs to one lane, so its gradient
 // rows are updated with plain read-modify-writes (no atomics).
 // --------------------------------------------------------------------------- //
-__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m) {
+__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m,
+                                                   unsigned long long *counter) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid == 0 && counter) *counter = 0ull;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     float *bufs[2] = {p, q};
     const int64_t lens[2] = {n, m};
@@ -843,8 +905,8 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
             const int q = v.off[l] + loc;
             if (!fuzzy_pass(p.Z, __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + q), a.onepa)) continue;
             const float cnt = __ldcg(v.count + q);
-            const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
-            const float *G = v.grad + (int64_t)C * v.off[l] + loc;
+            const int64_t hw = v.gradT ? 1 : (int64_t)v.wl[l] * v.hl[l];
+            const float *G = v.gradT ? v.gradT + (int64_t)q * C : v.grad + (int64_t)C * v.off[l] + loc;
 #pragma unroll
             for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
                 if (CT == 0 && c >= C) break;
@@ -903,6 +965,7 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
 struct BwdSmem {
     float pos[kStages][4][kWarps][kWTile];
     uint64_t bar[kWarps][kStages];
+    long long tile[kWarps][kStages];
     double spose[ADOP_MAX_VIEWS_PER_LAUNCH * 6];
 };
 
@@ -912,10 +975,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int t = tid; t < a.nviews * 6; t += kThreads) sm.spose[t] = 0.0;
-    const int64_t ntiles = (a.n + kWTile - 1) / kWTile;
-    const int64_t W = (int64_t)gridDim.x * kWarps;
-    const int64_t w0 = (int64_t)blockIdx.x * kWarps + wid;
-    const int64_t my = ntiles > w0 ? (ntiles - w0 + W - 1) / W : 0;
+    const long long ntiles = (a.n + kWTile - 1) / kWTile;
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
     const float *src[4] = {a.x, a.y, a.z, a.radius};
@@ -924,25 +984,32 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
         fence_mbar_init();
     }
     __syncthreads();
-    auto full_tile = [&](int64_t k) { return (w0 + k * W + 1) * kWTile <= a.n; };
-    auto issue = [&](int64_t k) {
-        if (lane == 0 && k < my && full_tile(k)) {
-            const uint64_t pol = policy_evict_first();
-            const int st = (int)(k % kStages);
-            const int64_t base = (w0 + k * W) * kWTile;
-            mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-            for (int r = 0; r < rows; ++r)
-                bulk_g2s(sm.pos[st][r][wid], src[r] + base, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+    auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
+    auto issue = [&](int st) {
+        if (lane == 0) {
+            const long long t = (long long)atomicAdd(&a.hdr->tiles_bwd, 1ull);
+            sm.tile[wid][st] = t;
+            if (t < ntiles && full_tile(t)) {
+                const uint64_t pol = policy_evict_first();
+                mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
+                for (int r = 0; r < rows; ++r)
+                    bulk_g2s(sm.pos[st][r][wid], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+            }
         }
     };
-    for (int k = 0; k < kStages; ++k) issue(k);
-    for (int64_t k = 0; k < my; ++k) {
+    for (int st = 0; st < kStages; ++st) issue(st);
+    __syncwarp();
+    uint32_t phase = 0u;
+    for (int64_t k = 0;; ++k) {
         const int st = (int)(k % kStages);
-        const int64_t base = (w0 + k * W) * kWTile;
+        const long long t = *(volatile long long *)&sm.tile[wid][st];
+        if (t >= ntiles) break;
+        const int64_t base = t * kWTile;
         const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
         int vmask = 0xFF;
-        if (full_tile(k)) {
-            mbar_wait(&sm.bar[wid][st], (uint32_t)((k / kStages) & 1));
+        if (full_tile(t)) {
+            mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
+            phase ^= 1u << st;
         } else {
             vmask = 0;
 #pragma unroll
@@ -995,7 +1062,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
             }
         }
         __syncwarp();
-        issue(k + kStages);
+        issue(st);
+        __syncwarp();
     }
     __syncthreads();
     for (int t = tid; t < a.nviews * 6; t += kThreads)
@@ -1138,16 +1206,36 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     cudaStream_t s = (cudaStream_t)stream;
     int g = 1;
     if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0)) {
-        if (!a.grad_accumulate && (a.d_feat || a.d_pos)) {
-            int64_t nf = a.d_feat ? a.n * a.channels : 0, np = a.d_pos ? 3 * a.n : 0;
+        {   // zero-fill (overwrite mode) and reset the dynamic tile counter
+            const bool fill = !a.grad_accumulate;
+            int64_t nf = (fill && a.d_feat) ? a.n * a.channels : 0, np = (fill && a.d_pos) ? 3 * a.n : 0;
             int64_t mx = nf > np ? nf : np;
             int64_t bx = (mx / 4 + kThreads - 1) / kThreads;
             if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
             if (bx < 1) bx = 1;
-            k_fill<<<(unsigned)bx, kThreads, 0, s>>>(a.d_feat, nf, a.d_pos, np);
+            k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np,
+                                                    &a.hdr->tiles_bwd);
         }
         RasterArgs b = a;
         b.grad_accumulate = 1;  // the sweep adds into the (zeroed or caller's) gradients
+        {   // transpose dL/dI to [P][C] in the record region of the workspace (records are dead after the blend)
+            int64_t need = 0, maxP = 1;
+            for (int v = 0; v < a.nviews; ++v) {
+                need += (int64_t)a.v[v].pixels * a.channels;
+                maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+            }
+            if (need * (int64_t)sizeof(float) <= a.rec_capacity * (int64_t)sizeof(Record)) {
+                float *gt = reinterpret_cast<float *>(a.records);
+                int64_t off = 0;
+                for (int v = 0; v < a.nviews; ++v) {
+                    b.v[v].gradT = gt + off;
+                    off += (int64_t)a.v[v].pixels * a.channels;
+                }
+                int64_t bx = (maxP + kThreads - 1) / kThreads;
+                if (bx > 2048) bx = 2048;
+                k_transpose_grad<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
+            }
+        }
         auto k = k_backward_async<MODEL, CT>;
         static bool attr = false;
         if (!attr) {
