@@ -257,6 +257,29 @@ struct WarpQueue {
     uint8_t meta[kQCap];  // kept layers (low 4 bits) | view slot << 4
 };
 
+// Dynamic tile scheduling: lane 0 of a warp claims batches of `kc` consecutive tiles from a global
+// counter, one batch ahead (the atomic's latency overlaps the current batch); kc is sized so every warp
+// gets several batches (load balance) while keeping the single-address atomics few.
+struct TileClaim {
+    long long cur, end, next;
+    int kc;
+    __device__ __forceinline__ void init(unsigned long long *ctr, long long ntiles, long long warps) {
+        long long k = ntiles / (warps * 4);
+        kc = (int)(k < 1 ? 1 : (k > 16 ? 16 : k));
+        cur = (long long)atomicAdd(ctr, (unsigned long long)kc);
+        end = cur + kc;
+        next = (long long)atomicAdd(ctr, (unsigned long long)kc);
+    }
+    __device__ __forceinline__ long long take(unsigned long long *ctr) {
+        if (cur >= end) {
+            cur = next;
+            end = cur + kc;
+            next = (long long)atomicAdd(ctr, (unsigned long long)kc);
+        }
+        return cur++;
+    }
+};
+
 // Per-view layer table in shared memory: the drain indexes it with a per-lane view slot (divergent
 // constant-bank loads would serialise).
 struct LayerDesc {
@@ -509,9 +532,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
     // lane 0 of each warp claims the next tile of the whole grid (dynamic load balance) and streams it
     // with `rows` 1-KB bulk copies (TMA engine, L2 evict-first) into stage st
+    TileClaim tc;
+    if (lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kWarps);
     auto issue = [&](int st) {
         if (lane == 0) {
-            const long long t = (long long)atomicAdd(&a.hdr->tiles_fwd, 1ull);
+            const long long t = tc.take(&a.hdr->tiles_fwd);
             sm.tile[wid][st] = t;
             if (t < ntiles && full_tile(t)) {
                 const uint64_t pol = policy_evict_first();
@@ -985,9 +1010,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
     }
     __syncthreads();
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
+    TileClaim tc;
+    if (lane == 0) tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kWarps);
     auto issue = [&](int st) {
         if (lane == 0) {
-            const long long t = (long long)atomicAdd(&a.hdr->tiles_bwd, 1ull);
+            const long long t = tc.take(&a.hdr->tiles_bwd);
             sm.tile[wid][st] = t;
             if (t < ntiles && full_tile(t)) {
                 const uint64_t pol = policy_evict_first();
