@@ -32,6 +32,7 @@ struct ViewDesc {
     float *accum, *count, *image;
     const float *grad;     // backward: dL/dI (image layout)
     const float *gradT;    // backward: dL/dI transposed to [P][C] in the workspace (or NULL)
+    const uint4 *ptab;     // backward: per-pixel {key lo, key hi, bits(count), bits(sum_c G I)} (or NULL)
 };
 
 struct Record {  // one (point, view, layer) hit of the render set, 16 bytes

@@ -662,55 +662,46 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
 // --------------------------------------------------------------------------- //
 // backward
 // --------------------------------------------------------------------------- //
-// Image-space gradient contribution of one neighbour q (Eq. 11 as R14, times G as R16).  I_q is
-// recomputed from the forward's interleaved accum/count exactly as k_resolve computed it
-// (bit-identical), and G is read from the transposed copy when available: one or two sectors per
-// neighbour instead of 2C scattered planar reads.
+// Image-space gradient contribution of one neighbour q (Eq. 11 as R14, times G as R16), planar reads
+// (fallback sweep for unaligned inputs).
 template <int CT>
 __device__ __forceinline__ float neighbour_term(const RasterArgs &a, const ViewDesc &v, int l, int qu, int qv,
                                                 float z, const float *tau) {
     if (qu < 0 || qv < 0 || qu >= v.wl[l] || qv >= v.hl[l]) return 0.0f;  // outside: no term
     const int j = qv * v.wl[l] + qu;
     const int q = v.off[l] + j;
-    const float nq = __ldcg(v.count + q);
+    const float nq = v.count[q];
     float factor;
     if (nq == 0.0f) {
         factor = 1.0f;                                     // case 1: background neighbour
     } else {
-        const float m = __uint_as_float((uint32_t)(__ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + q) >> 32));
+        const float m = __uint_as_float((uint32_t)(v.keys[q] >> 32));
         if (z > fmul(a.onepa, m)) return 0.0f;             // case 2: behind
         factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
     }
     const int C = CT > 0 ? CT : a.channels;
+    const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
+    const float *G = v.grad + (int64_t)C * v.off[l] + j;
+    const float *I = v.image + (int64_t)C * v.off[l] + j;
     float d = 0.0f;
-    if (v.gradT) {
-        const float *G = v.gradT + (int64_t)q * C;
-        const float *A = v.accum + (int64_t)q * C;
 #pragma unroll
-        for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
-            if (CT == 0 && c >= C) break;
-            const float Iq = nq > 0.0f ? __fdiv_rn(__ldcg(A + c), nq) : a.bg[c];
-            d = fmaf(__ldcg(G + c), tau[c] - Iq, d);
-        }
-    } else {
-        const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
-        const float *G = v.grad + (int64_t)C * v.off[l] + j;
-        const float *I = v.image + (int64_t)C * v.off[l] + j;
-#pragma unroll
-        for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
-            if (CT == 0 && c >= C) break;
-            d = fmaf(__ldg(G + c * hw), tau[c] - __ldg(I + c * hw), d);
-        }
+    for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
+        if (CT == 0 && c >= C) break;
+        d = fmaf(__ldg(G + c * hw), tau[c] - __ldg(I + c * hw), d);
     }
     return factor * d;
 }
 
-// dL/dI of one view transposed from the planar layout [C][h_l][w_l] to [P][C] (workspace scratch),
-// so the backward's gathers read one contiguous row per pixel.
-__global__ void __launch_bounds__(kThreads) k_transpose_grad(const __grid_constant__ RasterArgs a) {
+// Backward pixel tables of one view (workspace scratch), built once per call:
+//   ptab[p]  = {key lo, key hi, bits(count), bits(S_p)}, S_p = sum_c G_c(p) I_c(p) with I exactly as
+//              k_resolve computes it (accum/count, or the background when empty);
+//   gradT[p] = dL/dI(p) as a contiguous [C] row.
+// With them each Eq. 11 neighbour costs one 16-B load + one G row: Delta . G = factor (tau . G - S).
+__global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     const int C = a.channels;
-    float *out = const_cast<float *>(v.gradT);
+    float *gt = const_cast<float *>(v.gradT);
+    uint4 *pt = const_cast<uint4 *>(v.ptab);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
         int l = 0;
@@ -720,7 +711,16 @@ __global__ void __launch_bounds__(kThreads) k_transpose_grad(const __grid_consta
         const int64_t j = p - v.off[l];
         const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
         const float *G = v.grad + (int64_t)C * v.off[l] + j;
-        for (int c = 0; c < C; ++c) out[p * C + c] = __ldcs(G + c * hw);
+        const float cnt = __ldcs(v.count + p);
+        const unsigned long long key = __ldcs(reinterpret_cast<const unsigned long long *>(v.keys) + p);
+        float S = 0.0f;
+        for (int c = 0; c < C; ++c) {
+            const float g = __ldcs(G + c * hw);
+            const float I = cnt > 0.0f ? __fdiv_rn(__ldcs(v.accum + p * C + c), cnt) : a.bg[c];
+            S = fmaf(g, I, S);
+            gt[p * C + c] = g;
+        }
+        pt[p] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), __float_as_uint(cnt), __float_as_uint(S));
     }
 }
 
@@ -905,10 +905,65 @@ __global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q
     }
 }
 
+template <int CT>
+__device__ __forceinline__ float row_dot(const float *row, const float *tau, int C) {
+    float d = 0.0f;
+    if (CT > 0 && CT % 4 == 0) {
+#pragma unroll
+        for (int c = 0; c < CT; c += 4) {
+            const float4 g = __ldcg(reinterpret_cast<const float4 *>(row + c));
+            d = fmaf(g.x, tau[c], d);
+            d = fmaf(g.y, tau[c + 1], d);
+            d = fmaf(g.z, tau[c + 2], d);
+            d = fmaf(g.w, tau[c + 3], d);
+        }
+    } else {
+        for (int c = 0; c < C; ++c) d = fmaf(__ldcg(row + c), tau[c], d);
+    }
+    return d;
+}
+
+// Ghost image-space gradient at one layer (Eqs. 9-11, R14-R16) from the pixel tables: the four
+// neighbours' table entries are loaded together, then their G rows.
+template <int CT>
+__device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc &v, int l, int pu, int pv, float z,
+                                           const float *tau, float &gu, float &gv) {
+    const int C = CT > 0 ? CT : a.channels;
+    const int du[4] = {1, -1, 0, 0}, dv[4] = {0, 0, 1, -1};
+    int q[4];
+    uint4 e[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int qu = pu + du[k], qv = pv + dv[k];
+        const bool in = qu >= 0 && qv >= 0 && qu < v.wl[l] && qv < v.hl[l];
+        q[k] = in ? v.off[l] + qv * v.wl[l] + qu : -1;
+        e[k] = in ? __ldcg(v.ptab + q[k]) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    float d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        d[k] = 0.0f;
+        if (q[k] < 0) continue;  // outside: no term
+        const float nq = __uint_as_float(e[k].z);
+        float factor;
+        if (nq == 0.0f) {
+            factor = 1.0f;                                            // case 1: background
+        } else {
+            const float m = __uint_as_float(e[k].y);
+            if (z > fmul(a.onepa, m)) continue;                       // case 2: behind
+            factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
+        }
+        d[k] = factor * (row_dot<CT>(v.gradT + (int64_t)q[k] * C, tau, C) - __uint_as_float(e[k].w));
+    }
+    const float sc = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
+    gu += sc * (d[0] - d[1]);
+    gv += sc * (d[2] - d[3]);
+}
+
 template <int MODEL, int CT>
 __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost,
                                               float x, float y, float z, float rw, int64_t i, uint32_t gi,
-                                              double *spose, int lane) {
+                                              double *wpose, int lane) {
     const int C = CT > 0 ? CT : a.channels;
     Proj p;
     int nk = 0;
@@ -922,21 +977,24 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
     }
     if (nk > 0 && !ghost && a.d_feat) {
         // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
-        float *df = a.d_feat + i * C;
+        float acc[CT > 0 ? CT : ADOP_MAX_CHANNELS];
+        for (int c = 0; c < C; ++c) acc[c] = 0.0f;
+        bool any = false;
         for (int l = 0; l < nk; ++l) {
             int pu, pv;
             const int loc = layer_pixel(v, p, l, pu, pv);
             if (loc < 0) continue;
             const int q = v.off[l] + loc;
-            if (!fuzzy_pass(p.Z, __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + q), a.onepa)) continue;
-            const float cnt = __ldcg(v.count + q);
-            const int64_t hw = v.gradT ? 1 : (int64_t)v.wl[l] * v.hl[l];
-            const float *G = v.gradT ? v.gradT + (int64_t)q * C : v.grad + (int64_t)C * v.off[l] + loc;
-#pragma unroll
-            for (int c = 0; c < (CT > 0 ? CT : ADOP_MAX_CHANNELS); ++c) {
-                if (CT == 0 && c >= C) break;
-                df[c] += __fdiv_rn(__ldg(G + c * hw), cnt);
-            }
+            const uint4 e = __ldcg(v.ptab + q);
+            if (!(p.Z <= fmul(a.onepa, __uint_as_float(e.y)))) continue;  // fuzzy test (Eq. 6, R9)
+            const float cnt = __uint_as_float(e.z);
+            const float *G = v.gradT + (int64_t)q * C;
+            for (int c = 0; c < C; ++c) acc[c] += __fdiv_rn(__ldcg(G + c), cnt);
+            any = true;
+        }
+        if (any) {
+            float *df = a.d_feat + i * C;
+            for (int c = 0; c < C; ++c) df[c] += acc[c];
         }
     }
     float gu = 0.f, gv = 0.f;
@@ -946,16 +1004,8 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
         for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + i * C + c);
         for (int l = 0; l < nk; ++l) {
             int pu, pv;
-            const int loc = layer_pixel(v, p, l, pu, pv);
-            if (loc < 0) continue;
-            // Eqs. 9-11: signed central differences over the 4-neighbourhood (R14, R15)
-            const float dup = neighbour_term<CT>(a, v, l, pu + 1, pv, p.Z, tau);
-            const float dum = neighbour_term<CT>(a, v, l, pu - 1, pv, p.Z, tau);
-            const float dvp = neighbour_term<CT>(a, v, l, pu, pv + 1, p.Z, tau);
-            const float dvm = neighbour_term<CT>(a, v, l, pu, pv - 1, p.Z, tau);
-            const float sc = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
-            gu += sc * (dup - dum);
-            gv += sc * (dvp - dvm);
+            if (layer_pixel(v, p, l, pu, pv) < 0) continue;
+            ghost_layer<CT>(a, v, l, pu, pv, p.Z, tau, gu, gv);
             gc = true;
         }
     }
@@ -974,7 +1024,8 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
             dp[2 * a.n + i] += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
         }
     }
-    // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64
+    // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64 into this warp's
+    // private shared-memory slots (no atomics)
     double t6[6];
     t6[0] = w0; t6[1] = w1; t6[2] = w2;
     t6[3] = gc ? (double)(p.Y * w2 - p.Z * w1) : 0.0;
@@ -983,7 +1034,7 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         const double sum = warp_sum(t6[k]);
-        if (lane == 0) atomicAdd(&spose[vs * 6 + k], sum);
+        if (lane == 0) wpose[vs * 6 + k] += sum;
     }
 }
 
@@ -991,7 +1042,7 @@ struct BwdSmem {
     float pos[kStages][4][kWarps][kWTile];
     uint64_t bar[kWarps][kStages];
     long long tile[kWarps][kStages];
-    double spose[ADOP_MAX_VIEWS_PER_LAUNCH * 6];
+    double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * 6];  // per-warp pose sums
 };
 
 template <int MODEL, int CT>
@@ -999,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int t = tid; t < a.nviews * 6; t += kThreads) sm.spose[t] = 0.0;
+    for (int t = tid; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += kThreads) (&sm.wpose[0][0])[t] = 0.0;
     const long long ntiles = (a.n + kWTile - 1) / kWTile;
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
@@ -1085,7 +1136,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const float rw = staged_r ? rp[3][e] : a.radius_uniform;
                 bwd_candidate<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
-                                         a.goff + (uint32_t)(base + e), sm.spose, lane);
+                                         a.goff + (uint32_t)(base + e), sm.wpose[wid], lane);
             }
         }
         __syncwarp();
@@ -1093,8 +1144,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
         __syncwarp();
     }
     __syncthreads();
-    for (int t = tid; t < a.nviews * 6; t += kThreads)
-        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = sm.spose[t];
+    for (int t = tid; t < a.nviews * 6; t += kThreads) {
+        double acc = 0.0;
+        for (int w = 0; w < kWarps; ++w) acc += sm.wpose[w][t];  // fixed order
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = acc;
+    }
 }
 
 // d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
@@ -1232,7 +1286,12 @@ template <int MODEL, bool VEC, int CT>
 static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int g = 1;
-    if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0)) {
+    int64_t table_bytes = 0;
+    for (int v = 0; v < a.nviews; ++v)
+        table_bytes += (int64_t)a.v[v].pixels * (int64_t)(sizeof(uint4) + sizeof(float) * a.channels);
+    const bool tables_fit = table_bytes <= a.rec_capacity * (int64_t)sizeof(Record);
+    if (VEC && tables_fit && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
+        (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0)) {
         {   // zero-fill (overwrite mode) and reset the dynamic tile counter
             const bool fill = !a.grad_accumulate;
             int64_t nf = (fill && a.d_feat) ? a.n * a.channels : 0, np = (fill && a.d_pos) ? 3 * a.n : 0;
@@ -1245,23 +1304,25 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         }
         RasterArgs b = a;
         b.grad_accumulate = 1;  // the sweep adds into the (zeroed or caller's) gradients
-        {   // transpose dL/dI to [P][C] in the record region of the workspace (records are dead after the blend)
-            int64_t need = 0, maxP = 1;
+        {   // per-pixel tables (ptab, gradT) in the record region of the workspace (records are dead after the blend)
+            int64_t px = 0, maxP = 1;
             for (int v = 0; v < a.nviews; ++v) {
-                need += (int64_t)a.v[v].pixels * a.channels;
+                px += a.v[v].pixels;
                 maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
             }
-            if (need * (int64_t)sizeof(float) <= a.rec_capacity * (int64_t)sizeof(Record)) {
-                float *gt = reinterpret_cast<float *>(a.records);
-                int64_t off = 0;
-                for (int v = 0; v < a.nviews; ++v) {
-                    b.v[v].gradT = gt + off;
-                    off += (int64_t)a.v[v].pixels * a.channels;
-                }
-                int64_t bx = (maxP + kThreads - 1) / kThreads;
-                if (bx > 2048) bx = 2048;
-                k_transpose_grad<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
+            char *base = reinterpret_cast<char *>(a.records);
+            int64_t off = 0;
+            for (int v = 0; v < a.nviews; ++v) {
+                b.v[v].ptab = reinterpret_cast<const uint4 *>(base + off);
+                off += (int64_t)a.v[v].pixels * sizeof(uint4);
             }
+            for (int v = 0; v < a.nviews; ++v) {
+                b.v[v].gradT = reinterpret_cast<const float *>(base + off);
+                off += (int64_t)a.v[v].pixels * a.channels * sizeof(float);
+            }
+            int64_t bx = (maxP + kThreads - 1) / kThreads;
+            if (bx > 2048) bx = 2048;
+            k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
         }
         auto k = k_backward_async<MODEL, CT>;
         static bool attr = false;
