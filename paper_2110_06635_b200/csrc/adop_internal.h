@@ -48,6 +48,8 @@ struct WsHeader {
     int32_t pad;
     unsigned long long tiles_fwd;  // dynamic tile counters of the depth and backward sweeps
     unsigned long long tiles_bwd;
+    unsigned long long btex_n;     // backward work lists: texture-gradient hits, ghost entries
+    unsigned long long bgh_n;
 };
 
 struct RasterArgs {
@@ -73,6 +75,11 @@ struct RasterArgs {
     Record *records;
     int64_t rec_capacity;
     double *pose_partials; // [gridDim.x][nviews][6]
+    uint4 *btex;           // backward texture-gradient work list (16-B slots)
+    int64_t btex_cap;
+    uint4 *bgh;            // backward ghost work list (32-B slots, 2 x uint4)
+    int64_t bgh_cap;
+    int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     float *d_feat;
     float *d_pos;          // [3][n]
     uint8_t *mask;         // point-mask debug output [V][n]

@@ -884,10 +884,15 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
 // pose terms (w, Xc x w) (R19), warp-reduced in fp64.  Each point belongs to one lane, so its gradient
 // rows are updated with plain read-modify-writes (no atomics).
 // --------------------------------------------------------------------------- //
-__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m,
-                                                   unsigned long long *counter) {
+__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m, WsHeader *hdr,
+                                                   double *inline_row, int inline_len) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid == 0 && counter) *counter = 0ull;
+    if (tid == 0 && hdr) {
+        hdr->tiles_bwd = 0ull;
+        hdr->btex_n = 0ull;
+        hdr->bgh_n = 0ull;
+    }
+    if (inline_row && tid < inline_len) inline_row[tid] = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     float *bufs[2] = {p, q};
     const int64_t lens[2] = {n, m};
@@ -960,11 +965,106 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
     gv += sc * (d[2] - d[3]);
 }
 
+// ---- record-driven backward: the sweep emits work lists, two balanced kernels consume them ----
+constexpr uint32_t kDead = 0xFFFFFFFFu;
+constexpr int kBChunk = 128;
+
+struct ListChunk {  // warp-uniform per-warp chunk of a work list
+    long long base;
+    int left;  // -1: the list is full (process inline)
+};
+
+// Reserve `nb` slots for the lanes in ballot b of a list of `cap` slots of `words` uint4 each; returns the
+// lane's slot or -1 (no space: the caller processes its item inline).  Unused tail slots are marked dead.
+__device__ __forceinline__ long long list_slot(unsigned long long *counter, uint4 *list, int64_t cap, int words,
+                                               ListChunk &c, unsigned b, bool mine, int lane, unsigned lt) {
+    const int nb = __popc(b);
+    if (c.left >= 0 && nb > c.left) {
+        for (int k = lane; k < c.left; k += 32)
+            if (c.base + k < cap) list[(c.base + k) * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
+        unsigned long long nbase = 0;
+        if (lane == 0) nbase = atomicAdd(counter, (unsigned long long)kBChunk);
+        nbase = __shfl_sync(kFull, nbase, 0);
+        if ((long long)nbase + kBChunk <= cap) {
+            c.base = (long long)nbase;
+            c.left = kBChunk;
+        } else {
+            // the chunk straddles the end: mark its in-range part dead, stop emitting
+            for (long long k = (long long)nbase + lane; k < cap; k += 32)
+                list[k * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
+            c.left = -1;
+        }
+    }
+    if (c.left < 0) return -1;
+    const long long slot = mine ? c.base + __popc(b & lt) : -1;
+    c.base += nb;
+    c.left -= nb;
+    return slot;
+}
+
+__device__ __forceinline__ void list_close(uint4 *list, int64_t cap, int words, ListChunk &c, int lane) {
+    for (int k = lane; k < c.left; k += 32)
+        if (c.base + k < cap) list[(c.base + k) * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
+}
+
+__device__ __forceinline__ void red_add_row(float *dst, const float *src, int C, float scale) {
+    if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        for (int c = 0; c < C; c += 4) {
+            const float4 g = __ldcg(reinterpret_cast<const float4 *>(src + c));
+            red_add_v4(dst + c, make_float4(__fdiv_rn(g.x, scale), __fdiv_rn(g.y, scale), __fdiv_rn(g.z, scale),
+                                            __fdiv_rn(g.w, scale)));
+        }
+    } else {
+        for (int c = 0; c < C; ++c) red_add(dst + c, __fdiv_rn(__ldcg(src + c), scale));
+    }
+}
+
+// texture gradient of one rendered hit (R24): fuzzy membership against the forward's key, G / |Lambda|
+__device__ __forceinline__ void tex_hit(const RasterArgs &a, const ViewDesc &v, uint32_t q, float z, int64_t idx) {
+    const uint4 e = __ldcg(v.ptab + q);
+    if (!(z <= fmul(a.onepa, __uint_as_float(e.y)))) return;  // fuzzy test (Eq. 6, R9)
+    const int C = a.channels;
+    red_add_row(a.d_feat + idx * C, v.gradT + (int64_t)q * C, C, __uint_as_float(e.z));
+}
+
+// ghost: image gradient over its kept layers (Eqs. 9-11), chain rule (Eq. 8) -> dx (atomics), and the
+// pose terms (w, Xc x w) returned for the caller's reduction.
 template <int MODEL, int CT>
-__device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost,
-                                              float x, float y, float z, float rw, int64_t i, uint32_t gi,
-                                              double *wpose, int lane) {
+__device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc &v, const Proj &p, int nk,
+                                            int64_t idx, double *t6) {
     const int C = CT > 0 ? CT : a.channels;
+    float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
+    for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + idx * C + c);
+    float gu = 0.f, gv = 0.f;
+    bool gc = false;
+    for (int l = 0; l < nk; ++l) {
+        int pu, pv;
+        if (layer_pixel(v, p, l, pu, pv) < 0) continue;
+        ghost_layer<CT>(a, v, l, pu, pv, p.Z, tau, gu, gv);
+        gc = true;
+    }
+    if (!gc) return false;
+    float J[6];
+    jacobian<MODEL>(v, p, J);
+    const float w0 = J[0] * gu + J[3] * gv, w1 = J[1] * gu + J[4] * gv, w2 = J[2] * gu + J[5] * gv;
+    if (a.d_pos) {
+        red_add(a.d_pos + idx, v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2);  // dx = R^T w
+        red_add(a.d_pos + a.n + idx, v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2);
+        red_add(a.d_pos + 2 * a.n + idx, v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2);
+    }
+    t6[0] = w0; t6[1] = w1; t6[2] = w2;
+    t6[3] = (double)(p.Y * w2 - p.Z * w1);
+    t6[4] = (double)(p.Z * w0 - p.X * w2);
+    t6[5] = (double)(p.X * w1 - p.Y * w0);
+    return true;
+}
+
+// Sweep candidate: exact projection and discard, then emit the rendered hits to the texture list and
+// the ghost to the ghost list (inline processing when a list is full).  Warp-collective.
+template <int MODEL, int CT>
+__device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost, float x,
+                                         float y, float z, float rw, int64_t i, uint32_t gi, ListChunk &ct,
+                                         ListChunk &cg, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
     if (ok) {
@@ -975,66 +1075,107 @@ __device__ __forceinline__ void bwd_candidate(const RasterArgs &a, const ViewDes
             if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
         }
     }
-    if (nk > 0 && !ghost && a.d_feat) {
-        // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
-        float acc[CT > 0 ? CT : ADOP_MAX_CHANNELS];
-        for (int c = 0; c < C; ++c) acc[c] = 0.0f;
-        bool any = false;
-        for (int l = 0; l < nk; ++l) {
+    const bool rend = nk > 0 && !ghost && a.d_feat;
+    if (__any_sync(kFull, rend)) {
+#pragma unroll 1
+        for (int l = 0; l < a.layers; ++l) {
             int pu, pv;
-            const int loc = layer_pixel(v, p, l, pu, pv);
-            if (loc < 0) continue;
-            const int q = v.off[l] + loc;
-            const uint4 e = __ldcg(v.ptab + q);
-            if (!(p.Z <= fmul(a.onepa, __uint_as_float(e.y)))) continue;  // fuzzy test (Eq. 6, R9)
-            const float cnt = __uint_as_float(e.z);
-            const float *G = v.gradT + (int64_t)q * C;
-            for (int c = 0; c < C; ++c) acc[c] += __fdiv_rn(__ldcg(G + c), cnt);
-            any = true;
-        }
-        if (any) {
-            float *df = a.d_feat + i * C;
-            for (int c = 0; c < C; ++c) df[c] += acc[c];
-        }
-    }
-    float gu = 0.f, gv = 0.f;
-    bool gc = false;
-    if (nk > 0 && ghost) {
-        float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
-        for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + i * C + c);
-        for (int l = 0; l < nk; ++l) {
-            int pu, pv;
-            if (layer_pixel(v, p, l, pu, pv) < 0) continue;
-            ghost_layer<CT>(a, v, l, pu, pv, p.Z, tau, gu, gv);
-            gc = true;
+            const int loc = (rend && l < nk) ? layer_pixel(v, p, l, pu, pv) : -1;
+            const bool hit = loc >= 0;
+            const unsigned b = __ballot_sync(kFull, hit);
+            if (b == 0u) {
+                if (!__any_sync(kFull, rend && l + 1 < nk)) break;
+                continue;
+            }
+            const uint32_t q = (uint32_t)(v.off[l] + loc);
+            const long long slot = list_slot(&a.hdr->btex_n, a.btex, a.btex_cap, 1, ct, b, hit, lane, lt);
+            if (hit) {
+                if (slot >= 0)
+                    a.btex[slot] = make_uint4(q, (uint32_t)i, __float_as_uint(p.Z), (uint32_t)vs);
+                else
+                    tex_hit(a, v, q, p.Z, i);
+            }
         }
     }
-    if (!__any_sync(kFull, gc)) return;
-    float w0 = 0.f, w1 = 0.f, w2 = 0.f;
-    if (gc) {
-        float J[6];
-        jacobian<MODEL>(v, p, J);
-        w0 = J[0] * gu + J[3] * gv;  // w = J^T g = dL/dXc
-        w1 = J[1] * gu + J[4] * gv;
-        w2 = J[2] * gu + J[5] * gv;
-        if (a.d_pos) {
-            float *dp = a.d_pos;
-            dp[i] += v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2;  // dx = R^T w
-            dp[a.n + i] += v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2;
-            dp[2 * a.n + i] += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
-        }
+    const bool gh = nk > 0 && ghost;
+    const unsigned bg = __ballot_sync(kFull, gh);
+    if (bg == 0u) return;
+    const long long slot = list_slot(&a.hdr->bgh_n, a.bgh, a.bgh_cap, 2, cg, bg, gh, lane, lt);
+    if (!gh) return;
+    if (slot >= 0) {
+        a.bgh[2 * slot] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X),
+                                     __float_as_uint(p.Y));
+        a.bgh[2 * slot + 1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), 0u);
+    } else {
+        double t6[6];
+        if (ghost_point<MODEL, CT>(a, v, p, nk, i, t6))
+            for (int k = 0; k < 6; ++k) atomicAdd(&a.pose_partials[((int64_t)a.inline_row * a.nviews + vs) * 6 + k], t6[k]);
     }
-    // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64 into this warp's
-    // private shared-memory slots (no atomics)
-    double t6[6];
-    t6[0] = w0; t6[1] = w1; t6[2] = w2;
-    t6[3] = gc ? (double)(p.Y * w2 - p.Z * w1) : 0.0;
-    t6[4] = gc ? (double)(p.Z * w0 - p.X * w2) : 0.0;
-    t6[5] = gc ? (double)(p.X * w1 - p.Y * w0) : 0.0;
+}
+
+// texture list consumer: one thread per hit (balanced), vector reductions into d_feat
+__global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
+    unsigned long long total = *(volatile unsigned long long *)&a.hdr->btex_n;
+    if (total > (unsigned long long)a.btex_cap) total = (unsigned long long)a.btex_cap;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
+        const uint4 e = __ldcs(a.btex + r);
+        if (e.w == kDead) continue;
+        tex_hit(a, a.v[e.w], e.x, __uint_as_float(e.z), (int64_t)e.y);
+    }
+}
+
+// ghost list consumer: one thread per (ghost, view) (balanced); pose terms warp-reduced in fp64 into
+// per-warp shared slots, per-block partials reduced by k_pose_reduce in a fixed order.
+template <int MODEL, int CT>
+__global__ void __launch_bounds__(kThreads) k_bwd_ghost(const __grid_constant__ RasterArgs a) {
+    __shared__ double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * 6];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
+    __syncthreads();
+    unsigned long long total = *(volatile unsigned long long *)&a.hdr->bgh_n;
+    if (total > (unsigned long long)a.bgh_cap) total = (unsigned long long)a.bgh_cap;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x; r0 < total; r0 += stride) {
+        const unsigned long long r = r0 + threadIdx.x;
+        double t6[6] = {0, 0, 0, 0, 0, 0};
+        int vs = -1;
+        if (r < total) {
+            const uint4 e1 = __ldcs(a.bgh + 2 * r + 1);
+            if (e1.z != kDead) {
+                const uint4 e0 = __ldcs(a.bgh + 2 * r);
+                vs = (int)(e1.z & 0xFF);
+                const int nk = (int)(e1.z >> 8);
+                const ViewDesc &v = a.v[vs];
+                Proj p;
+                p.u0 = __uint_as_float(e0.x);
+                p.v0 = __uint_as_float(e0.y);
+                p.X = __uint_as_float(e0.z);
+                p.Y = __uint_as_float(e0.w);
+                p.Z = __uint_as_float(e1.x);
+                p.iz = __frcp_rn(p.Z);
+                if (!ghost_point<MODEL, CT>(a, v, p, nk, (int64_t)e1.y, t6)) vs = -1;
+            }
+        }
+        // warp reduction per distinct view present in the warp (usually one)
+        unsigned pending = __ballot_sync(kFull, vs >= 0);
+        while (pending) {
+            const int leader = __ffs(pending) - 1;
+            const int vv = __shfl_sync(kFull, vs, leader);
+            const bool mine = vs == vv;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        const double sum = warp_sum(t6[k]);
-        if (lane == 0) wpose[vs * 6 + k] += sum;
+            for (int k = 0; k < 6; ++k) {
+                const double sum = warp_sum(mine ? t6[k] : 0.0);
+                if (lane == 0) wpose[wid][vv * 6 + k] += sum;
+            }
+            pending &= ~__ballot_sync(kFull, mine);
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x) {
+        double acc = 0.0;
+        for (int w = 0; w < kWarps; ++w) acc += wpose[w][t];
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = acc;
     }
 }
 
@@ -1042,15 +1183,17 @@ struct BwdSmem {
     float pos[kStages][4][kWarps][kWTile];
     uint64_t bar[kWarps][kStages];
     long long tile[kWarps][kStages];
-    double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * 6];  // per-warp pose sums
 };
 
 template <int MODEL, int CT>
-__global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 3) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (int t = tid; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += kThreads) (&sm.wpose[0][0])[t] = 0.0;
+    const unsigned lt = lanemask_lt();
+    ListChunk ct, cg;
+    ct.base = cg.base = 0;
+    ct.left = cg.left = 0;
     const long long ntiles = (a.n + kWTile - 1) / kWTile;
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
@@ -1135,20 +1278,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_backward_async(const __grid_con
                 m &= m - 1u;
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const float rw = staged_r ? rp[3][e] : a.radius_uniform;
-                bwd_candidate<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
-                                         a.goff + (uint32_t)(base + e), sm.wpose[wid], lane);
+                bwd_emit<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
+                                    a.goff + (uint32_t)(base + e), ct, cg, lane, lt);
             }
         }
         __syncwarp();
         issue(st);
         __syncwarp();
     }
-    __syncthreads();
-    for (int t = tid; t < a.nviews * 6; t += kThreads) {
-        double acc = 0.0;
-        for (int w = 0; w < kWarps; ++w) acc += sm.wpose[w][t];  // fixed order
-        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = acc;
-    }
+    list_close(a.btex, a.btex_cap, 1, ct, lane);
+    list_close(a.bgh, a.bgh_cap, 2, cg, lane);
 }
 
 // d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
@@ -1285,46 +1424,63 @@ int backward_grid(int sms) {
 template <int MODEL, bool VEC, int CT>
 static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    int g = 1;
-    int64_t table_bytes = 0;
-    for (int v = 0; v < a.nviews; ++v)
+    const int64_t cap_bytes = a.rec_capacity * (int64_t)sizeof(Record);
+    int64_t table_bytes = 0, maxP = 1;
+    for (int v = 0; v < a.nviews; ++v) {
         table_bytes += (int64_t)a.v[v].pixels * (int64_t)(sizeof(uint4) + sizeof(float) * a.channels);
-    const bool tables_fit = table_bytes <= a.rec_capacity * (int64_t)sizeof(Record);
-    if (VEC && tables_fit && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
-        (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0)) {
-        {   // zero-fill (overwrite mode) and reset the dynamic tile counter
-            const bool fill = !a.grad_accumulate;
-            int64_t nf = (fill && a.d_feat) ? a.n * a.channels : 0, np = (fill && a.d_pos) ? 3 * a.n : 0;
-            int64_t mx = nf > np ? nf : np;
-            int64_t bx = (mx / 4 + kThreads - 1) / kThreads;
-            if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
-            if (bx < 1) bx = 1;
-            k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np,
-                                                    &a.hdr->tiles_bwd);
-        }
-        RasterArgs b = a;
-        b.grad_accumulate = 1;  // the sweep adds into the (zeroed or caller's) gradients
-        {   // per-pixel tables (ptab, gradT) in the record region of the workspace (records are dead after the blend)
-            int64_t px = 0, maxP = 1;
-            for (int v = 0; v < a.nviews; ++v) {
-                px += a.v[v].pixels;
-                maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
-            }
-            char *base = reinterpret_cast<char *>(a.records);
-            int64_t off = 0;
-            for (int v = 0; v < a.nviews; ++v) {
-                b.v[v].ptab = reinterpret_cast<const uint4 *>(base + off);
-                off += (int64_t)a.v[v].pixels * sizeof(uint4);
-            }
-            for (int v = 0; v < a.nviews; ++v) {
-                b.v[v].gradT = reinterpret_cast<const float *>(base + off);
-                off += (int64_t)a.v[v].pixels * a.channels * sizeof(float);
-            }
-            int64_t bx = (maxP + kThreads - 1) / kThreads;
-            if (bx > 2048) bx = 2048;
-            k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
-        }
-        auto k = k_backward_async<MODEL, CT>;
+        maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+    }
+    table_bytes = (table_bytes + 255) / 256 * 256;
+    const bool fast = VEC && table_bytes + (int64_t)(1 << 16) <= cap_bytes &&
+                      (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
+                      (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0);
+    if (!fast) {  // planar fused sweep (unaligned inputs or a small workspace)
+        auto k = k_backward<MODEL, VEC, CT>;
+        int g = resident_grid(k, sms, kWarps * 128, a.n);
+        if (g > grid_cap) g = grid_cap;
+        k<<<g, kThreads, 0, s>>>(a);
+        if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, g, a.nviews * 6, d_pose, a.grad_accumulate);
+        return (int)cudaGetLastError();
+    }
+    RasterArgs b = a;
+    b.grad_accumulate = 1;  // every kernel below adds into the (zeroed or caller's) gradients
+    // workspace record region: [pixel tables | texture list (16-B slots) | ghost list (32-B slots)]
+    char *base = reinterpret_cast<char *>(a.records);
+    int64_t off = 0;
+    for (int v = 0; v < a.nviews; ++v) {
+        b.v[v].ptab = reinterpret_cast<const uint4 *>(base + off);
+        off += (int64_t)a.v[v].pixels * sizeof(uint4);
+    }
+    for (int v = 0; v < a.nviews; ++v) {
+        b.v[v].gradT = reinterpret_cast<const float *>(base + off);
+        off += (int64_t)a.v[v].pixels * a.channels * sizeof(float);
+    }
+    const int64_t rest = cap_bytes - table_bytes;
+    b.btex = reinterpret_cast<uint4 *>(base + table_bytes);
+    b.btex_cap = (rest / 2) / 16;
+    b.bgh = reinterpret_cast<uint4 *>(base + table_bytes + b.btex_cap * 16);
+    b.bgh_cap = (rest - b.btex_cap * 16) / 32;
+    // ghost-list kernel grid (its per-block pose partials) and the inline-overflow row after them
+    int gg = sms * 4;
+    if (gg > grid_cap - 1) gg = grid_cap - 1;
+    b.inline_row = gg;
+    {   // zero-fill (overwrite mode), reset the work-list counters and the inline pose row
+        const bool fill = !a.grad_accumulate;
+        int64_t nf = (fill && a.d_feat) ? a.n * a.channels : 0, np = (fill && a.d_pos) ? 3 * a.n : 0;
+        int64_t mx = nf > np ? nf : np;
+        int64_t bx = (mx / 4 + kThreads - 1) / kThreads;
+        if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
+        if (bx < 1) bx = 1;
+        k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np, a.hdr,
+                                                a.pose_partials + (int64_t)gg * a.nviews * 6, a.nviews * 6);
+    }
+    {   // per-pixel tables
+        int64_t bx = (maxP + kThreads - 1) / kThreads;
+        if (bx > 2048) bx = 2048;
+        k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
+    }
+    {   // sweep: emit work lists
+        auto k = k_bwd_sweep<MODEL, CT>;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
@@ -1334,19 +1490,14 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(BwdSmem));
         if (per_sm < 1) per_sm = 1;
         int64_t tiles = (a.n + kWTile - 1) / kWTile;
-        int64_t gg = (int64_t)sms * per_sm;
-        if ((tiles + kWarps - 1) / kWarps < gg) gg = (tiles + kWarps - 1) / kWarps;
-        if (gg > grid_cap) gg = grid_cap;
-        if (gg < 1) gg = 1;
-        g = (int)gg;
-        k<<<g, kThreads, sizeof(BwdSmem), s>>>(b);
-    } else {
-        auto k = k_backward<MODEL, VEC, CT>;
-        g = resident_grid(k, sms, kWarps * 128, a.n);
-        if (g > grid_cap) g = grid_cap;
-        k<<<g, kThreads, 0, s>>>(a);
+        int64_t g = (int64_t)sms * per_sm;
+        if ((tiles + kWarps - 1) / kWarps < g) g = (tiles + kWarps - 1) / kWarps;
+        if (g < 1) g = 1;
+        k<<<(unsigned)g, kThreads, sizeof(BwdSmem), s>>>(b);
     }
-    if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, g, a.nviews * 6, d_pose, a.grad_accumulate);
+    k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
+    k_bwd_ghost<MODEL, CT><<<gg, kThreads, 0, s>>>(b);
+    if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, gg + 1, a.nviews * 6, d_pose, a.grad_accumulate);
     return (int)cudaGetLastError();
 }
 

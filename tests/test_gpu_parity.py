@@ -277,3 +277,21 @@ def test_precull_is_conservative_at_frustum_borders(model, tight):
     _, fwd, _ = run_oracle(cloud, [cam], [S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))], prm)
     compare_forward(r, fwd, ctx="precull")
     assert (fwd.count > 0).sum() > (50 if tight else 500)
+
+
+def test_backward_work_lists_overflow_to_inline():
+    """A workspace whose record region barely holds the backward pixel tables: the texture/ghost work
+    lists overflow almost at once and the sweep processes the rest inline -- same results."""
+    w = S.workload(2, n=120_000)
+    C = w.cloud.channels
+    P = A.pyramid_pixels(w.cameras[0].width, w.cameras[0].height, w.params.layers)
+    table = -(-P * (16 + 4 * C) // 256) * 256
+    cap = table // 16 + (1 << 16) // 16 + 300
+    G = grads_for(w.cameras, w.params.layers, C)
+    r = run_gpu(w.cloud, w.cameras, w.poses, w.params, grads=G, record_capacity=max(cap, 300_000))
+    small = run_gpu(w.cloud, w.cameras, w.poses, w.params, record_capacity=cap)
+    small.backward([g.cuda() for g in G])
+    torch.cuda.synchronize()
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=G)
+    compare_backward(r, bwd, ctx="lists")
+    compare_backward(small, bwd, ctx="inline")
