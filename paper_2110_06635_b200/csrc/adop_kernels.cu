@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 2;
 constexpr int kWTile = 256;  // points per warp tile (8 per lane)
-constexpr int kQCap = 64;
+constexpr int kQCap = 48;
 constexpr int kChunk = 256;  // record slots reserved per warp at a time
 constexpr uint32_t kDeadView = 0xFFFFFFFFu;
 
@@ -280,11 +280,25 @@ struct TileClaim {
     }
 };
 
+// Bounding box of a lane's points (see box_culled).
+struct Box {
+    float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
+};
+
+// float <-> int with the same order (for REDUX min/max of floats)
+__device__ __forceinline__ int f2ord(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
 // Per-view layer table in shared memory: the drain indexes it with a per-lane view slot (divergent
 // constant-bank loads would serialise).
 struct LayerDesc {
     int32_t off[ADOP_MAX_LAYERS], wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS];
     uint64_t *keys;
+    float4 pl[5];  // frustum half-spaces (n, d) and their margins (see box_culled)
+    float2 pm[5];
 };
 
 struct DepthSmem {
@@ -296,13 +310,64 @@ struct DepthSmem {
 };
 
 __device__ __forceinline__ void init_layer_descs(const RasterArgs &a, LayerDesc *ld) {
-    for (int t = threadIdx.x; t < a.nviews * (3 * ADOP_MAX_LAYERS + 1); t += blockDim.x) {
-        const int v = t / (3 * ADOP_MAX_LAYERS + 1), f = t % (3 * ADOP_MAX_LAYERS + 1);
+    constexpr int F = 3 * ADOP_MAX_LAYERS + 1 + 5;
+    for (int t = threadIdx.x; t < a.nviews * F; t += blockDim.x) {
+        const int v = t / F, f = t % F;
         if (f < ADOP_MAX_LAYERS) ld[v].off[f] = a.v[v].off[f];
         else if (f < 2 * ADOP_MAX_LAYERS) ld[v].wl[f - ADOP_MAX_LAYERS] = a.v[v].wl[f - ADOP_MAX_LAYERS];
         else if (f < 3 * ADOP_MAX_LAYERS) ld[v].hl[f - 2 * ADOP_MAX_LAYERS] = a.v[v].hl[f - 2 * ADOP_MAX_LAYERS];
-        else ld[v].keys = a.v[v].keys;
+        else if (f == 3 * ADOP_MAX_LAYERS) ld[v].keys = a.v[v].keys;
+        else {
+            const int k = f - 3 * ADOP_MAX_LAYERS - 1;
+            ld[v].pl[k] = make_float4(a.v[v].pl[k][0], a.v[v].pl[k][1], a.v[v].pl[k][2], a.v[v].pl[k][3]);
+            ld[v].pm[k] = make_float2(a.v[v].pm[k][0], a.v[v].pm[k][1]);
+        }
     }
+}
+
+// Views whose (widened) frustum may contain a point of the warp's tile, as a warp-uniform bit mask.
+// With more than 2 views the warp's union box is tested against all views at once (lane v tests
+// view v from the shared-memory table); otherwise every view is returned.
+__device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const LayerDesc *ld, const Box &b, int lane) {
+    if (a.nviews <= 2) return (1u << a.nviews) - 1u;
+    float lo[3], hi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        const bool valid = b.B >= 0.0f;
+        const float l0 = valid ? b.c[ax] - b.e[ax] : __int_as_float(0x7f800000);
+        const float h0 = valid ? b.c[ax] + b.e[ax] : -__int_as_float(0x7f800000);
+        lo[ax] = ord2f(__reduce_min_sync(kFull, f2ord(l0)));
+        hi[ax] = ord2f(__reduce_max_sync(kFull, f2ord(h0)));
+    }
+    if (!(lo[0] <= hi[0])) return 0u;  // no valid point in the tile
+    Box w;
+    float ext = 0.0f;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        w.c[ax] = 0.5f * (lo[ax] + hi[ax]);
+        w.e[ax] = 0.5f * (hi[ax] - lo[ax]) * 1.0000002f;  // covers the rounding of c -+ e
+        ext += fmaxf(fabsf(lo[ax]), fabsf(hi[ax]));
+    }
+    w.B = ext;
+    bool in = false;
+    if (lane < a.nviews) {
+        const LayerDesc &v = ld[lane];
+        bool out = false;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const float4 P = v.pl[k];
+            float val = P.w;
+            val = fmaf(P.x, w.c[0], val);
+            val = fmaf(fabsf(P.x), w.e[0], val);
+            val = fmaf(P.y, w.c[1], val);
+            val = fmaf(fabsf(P.y), w.e[1], val);
+            val = fmaf(P.z, w.c[2], val);
+            val = fmaf(fabsf(P.z), w.e[2], val);
+            out |= val < -fmaf(v.pm[k].x, w.B, v.pm[k].y);
+        }
+        in = !out;
+    }
+    return __ballot_sync(kFull, in);
 }
 
 struct RecChunk {  // warp-uniform
@@ -401,10 +466,6 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     if (qn >= 32) drain(a, ld, q, qn, 32, c, lane, lt);
 }
 
-// Bounding box of a lane's points (see box_culled).
-struct Box {
-    float c[3], e[3], B;  // centre, half extent, sum_a max|p_a|
-};
 
 // The lane owns points e = h*128 + 4*lane + j (h = 0, 1; j = 0..3) of the warp tile: every LDS.128
 // of a row is then one contiguous 512-byte warp access.
@@ -479,8 +540,11 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
     }
     const Box box = lane_box(rows, lane, vmask);
+    uint32_t views = tile_views(a, ld, box, lane);
 #pragma unroll 1
-    for (int vs = 0; vs < a.nviews; ++vs) {
+    while (views) {
+        const int vs = __ffs(views) - 1;
+        views &= views - 1u;
         const ViewDesc &v = a.v[vs];
         if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
         uint32_t m = 0u;
@@ -1183,6 +1247,7 @@ struct BwdSmem {
     float pos[kStages][4][kWarps][kWTile];
     uint64_t bar[kWarps][kStages];
     long long tile[kWarps][kStages];
+    LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
 };
 
 template <int MODEL, int CT>
@@ -1198,6 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bwd_sweep(const __grid_constant
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
     const float *src[4] = {a.x, a.y, a.z, a.radius};
+    init_layer_descs(a, sm.ld);
     if (lane == 0) {
         for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
         fence_mbar_init();
@@ -1250,8 +1316,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_bwd_sweep(const __grid_constant
                 if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
         }
         const Box box = lane_box(rp, lane, vmask);
+        uint32_t views = tile_views(a, sm.ld, box, lane);
 #pragma unroll 1
-        for (int vs = 0; vs < a.nviews; ++vs) {
+        while (views) {
+            const int vs = __ffs(views) - 1;
+            views &= views - 1u;
             const ViewDesc &v = a.v[vs];
             if (__all_sync(kFull, box_culled(v, box))) continue;
             uint32_t m = 0u;
