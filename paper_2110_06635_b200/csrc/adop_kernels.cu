@@ -238,8 +238,10 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 //      chunks of kChunk slots reserved with one atomic (unused slots are marked dead).
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 2;
+constexpr int kSW = 12;              // warps per CTA of the TMA sweeps (2 CTAs x 12 warps per SM)
+constexpr int kST = kSW * 32;
 constexpr int kWTile = 256;  // points per warp tile (8 per lane)
-constexpr int kQCap = 48;
+constexpr int kQCap = 64;
 constexpr int kChunk = 256;  // record slots reserved per warp at a time
 constexpr uint32_t kDeadView = 0xFFFFFFFFu;
 
@@ -302,10 +304,10 @@ struct LayerDesc {
 };
 
 struct DepthSmem {
-    float pos[kStages][4][kWarps][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
-    uint64_t bar[kWarps][kStages];          // per-warp TMA completion barriers
-    long long tile[kWarps][kStages];        // tile claimed into each stage
-    WarpQueue q[kWarps];
+    float pos[kStages][4][kSW][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
+    uint64_t bar[kSW][kStages];          // per-warp TMA completion barriers
+    long long tile[kSW][kStages];        // tile claimed into each stage
+    WarpQueue q[kSW];
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
 };
 
@@ -577,8 +579,10 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
     }
 }
 
+static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / 2, "depth sweep: 2 CTAs per SM must fit in shared memory");
+
 template <int MODEL>
-__global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kST, 2) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -597,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_depth_async(const __grid_consta
     // lane 0 of each warp claims the next tile of the whole grid (dynamic load balance) and streams it
     // with `rows` 1-KB bulk copies (TMA engine, L2 evict-first) into stage st
     TileClaim tc;
-    if (lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kWarps);
+    if (lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kSW);
     auto issue = [&](int st) {
         if (lane == 0) {
             const long long t = tc.take(&a.hdr->tiles_fwd);
@@ -1244,14 +1248,16 @@ __global__ void __launch_bounds__(kThreads) k_bwd_ghost(const __grid_constant__ 
 }
 
 struct BwdSmem {
-    float pos[kStages][4][kWarps][kWTile];
-    uint64_t bar[kWarps][kStages];
-    long long tile[kWarps][kStages];
+    float pos[kStages][4][kSW][kWTile];
+    uint64_t bar[kSW][kStages];
+    long long tile[kSW][kStages];
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
 };
 
+static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 2, "backward sweep: 2 CTAs per SM must fit in shared memory");
+
 template <int MODEL, int CT>
-__global__ void __launch_bounds__(kThreads, 3) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kST, 2) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1271,7 +1277,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_bwd_sweep(const __grid_constant
     __syncthreads();
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
     TileClaim tc;
-    if (lane == 0) tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kWarps);
+    if (lane == 0) tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kSW);
     auto issue = [&](int st) {
         if (lane == 0) {
             const long long t = tc.take(&a.hdr->tiles_bwd);
@@ -1423,13 +1429,13 @@ static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
             attr = true;
         }
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(DepthSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(DepthSmem));
         if (per_sm < 1) per_sm = 1;
         int64_t tiles = (a.n + kWTile - 1) / kWTile;
         int64_t g = (int64_t)sms * per_sm;
-        if ((tiles + kWarps - 1) / kWarps < g) g = (tiles + kWarps - 1) / kWarps;
+        if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
         if (g < 1) g = 1;
-        k<<<(unsigned)g, kThreads, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
+        k<<<(unsigned)g, kST, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
         return (int)cudaGetLastError();
     }
     auto k = k_stream<MODEL, VEC, MODE_DEPTH, false>;
@@ -1556,13 +1562,13 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
             attr = true;
         }
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, sizeof(BwdSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(BwdSmem));
         if (per_sm < 1) per_sm = 1;
         int64_t tiles = (a.n + kWTile - 1) / kWTile;
         int64_t g = (int64_t)sms * per_sm;
-        if ((tiles + kWarps - 1) / kWarps < g) g = (tiles + kWarps - 1) / kWarps;
+        if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
         if (g < 1) g = 1;
-        k<<<(unsigned)g, kThreads, sizeof(BwdSmem), s>>>(b);
+        k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
     }
     k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
     k_bwd_ghost<MODEL, CT><<<gg, kThreads, 0, s>>>(b);
