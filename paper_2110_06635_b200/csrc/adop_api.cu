@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 
@@ -184,6 +185,15 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     a.ghost_thr = (uint32_t)std::floor((double)pr->ghost_rate * 16777216.0);
     a.ghost_salt = salt_of(pr->seed, kStreamGhost, 0u);
     a.grad_accumulate = pr->grad_accumulate ? 1 : 0;
+    {   // tile scheduling of the sweeps (bit 0 depth, bit 1 backward): static round-robin streams the cloud
+        // as one contiguous front; dynamic claiming balances irregular (backward) work.  ADOP_TILES overrides.
+        static int mode = -1;
+        if (mode < 0) {
+            const char *e = std::getenv("ADOP_TILES");
+            mode = e ? std::atoi(e) : 2;
+        }
+        a.dyn_tiles = mode;
+    }
     for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
     if (ws) {
         a.hdr = ws->hdr;

@@ -80,6 +80,7 @@ struct RasterArgs {
     uint4 *bgh;            // backward ghost work list (32-B slots, 2 x uint4)
     int64_t bgh_cap;
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
+    int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
     float *d_feat;
     float *d_pos;          // [3][n]
     uint8_t *mask;         // point-mask debug output [V][n]

@@ -263,9 +263,17 @@ struct WarpQueue {
 // counter, one batch ahead (the atomic's latency overlaps the current batch); kc is sized so every warp
 // gets several batches (load balance) while keeping the single-address atomics few.
 struct TileClaim {
-    long long cur, end, next;
+    long long cur, end, next, stride;
     int kc;
-    __device__ __forceinline__ void init(unsigned long long *ctr, long long ntiles, long long warps) {
+    bool dyn;
+    __device__ __forceinline__ void init(unsigned long long *ctr, long long ntiles, long long warps, long long wglobal,
+                                         bool dynamic) {
+        dyn = dynamic;
+        if (!dyn) {  // static round-robin: warp w takes tiles w, w + W, ... (contiguous front through memory)
+            cur = wglobal;
+            stride = warps;
+            return;
+        }
         long long k = ntiles / (warps * 4);
         kc = (int)(k < 1 ? 1 : (k > 16 ? 16 : k));
         cur = (long long)atomicAdd(ctr, (unsigned long long)kc);
@@ -273,6 +281,11 @@ struct TileClaim {
         next = (long long)atomicAdd(ctr, (unsigned long long)kc);
     }
     __device__ __forceinline__ long long take(unsigned long long *ctr) {
+        if (!dyn) {
+            const long long t = cur;
+            cur += stride;
+            return t;
+        }
         if (cur >= end) {
             cur = next;
             end = cur + kc;
@@ -601,7 +614,9 @@ __global__ void __launch_bounds__(kST, 2) k_depth_async(const __grid_constant__ 
     // lane 0 of each warp claims the next tile of the whole grid (dynamic load balance) and streams it
     // with `rows` 1-KB bulk copies (TMA engine, L2 evict-first) into stage st
     TileClaim tc;
-    if (lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kSW);
+    if (lane == 0)
+        tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kSW, (long long)blockIdx.x * kSW + wid,
+                a.dyn_tiles & 1);
     auto issue = [&](int st) {
         if (lane == 0) {
             const long long t = tc.take(&a.hdr->tiles_fwd);
@@ -1277,7 +1292,9 @@ __global__ void __launch_bounds__(kST, 2) k_bwd_sweep(const __grid_constant__ Ra
     __syncthreads();
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
     TileClaim tc;
-    if (lane == 0) tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kSW);
+    if (lane == 0)
+        tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kSW, (long long)blockIdx.x * kSW + wid,
+                (a.dyn_tiles >> 1) & 1);
     auto issue = [&](int st) {
         if (lane == 0) {
             const long long t = tc.take(&a.hdr->tiles_bwd);
