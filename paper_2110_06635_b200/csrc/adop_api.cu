@@ -46,7 +46,7 @@ uint32_t salt_of(uint64_t seed, uint32_t stream, uint32_t view) {
 }
 constexpr uint32_t kStreamGhost = 1, kStreamDiscard = 2;
 
-constexpr size_t kHeaderBytes = 256;
+constexpr size_t kHeaderBytes = 4096;  // WsHeader at 0, PlaneTab[16] at 256
 constexpr int64_t kRecordSlack = 1 << 20;  // >= resident warps x 256-slot record chunks
 constexpr int kMaxBwdBlocks = 2048;
 constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 6 * sizeof(double);
@@ -190,13 +190,14 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         static int mode = -1;
         if (mode < 0) {
             const char *e = std::getenv("ADOP_TILES");
-            mode = e ? std::atoi(e) : 2;
+            mode = e ? std::atoi(e) : 0;
         }
         a.dyn_tiles = mode;
     }
     for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
     if (ws) {
         a.hdr = ws->hdr;
+        a.planes = reinterpret_cast<PlaneTab *>(reinterpret_cast<char *>(ws->hdr) + 256);
         a.records = ws->records;
         a.rec_capacity = ws->capacity;
         a.pose_partials = ws->partials;

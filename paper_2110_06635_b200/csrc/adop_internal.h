@@ -52,6 +52,13 @@ struct WsHeader {
     unsigned long long bgh_n;
 };
 
+// Frustum half-spaces of every view in the workspace (written by k_clear<KEYS> of the depth phase;
+// the backward sweep writes its own copy): tile_views reads them with a per-lane view index through L1.
+struct PlaneTab {
+    float4 pl[5];  // (n, d)
+    float2 pm[5];  // margins (see box_culled)
+};
+
 struct RasterArgs {
     const float *x, *y, *z;
     const float *radius;
@@ -81,6 +88,7 @@ struct RasterArgs {
     int64_t bgh_cap;
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
+    PlaneTab *planes;      // [nviews] in the workspace header area
     float *d_feat;
     float *d_pos;          // [3][n]
     uint8_t *mask;         // point-mask debug output [V][n]

@@ -58,6 +58,11 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
             a.hdr->overflow = 0;
             a.hdr->tiles_fwd = 0ull;
         }
+        if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for tile_views
+            const int k = threadIdx.x;
+            a.planes[blockIdx.y].pl[k] = make_float4(v.pl[k][0], v.pl[k][1], v.pl[k][2], v.pl[k][3]);
+            a.planes[blockIdx.y].pm[k] = make_float2(v.pm[k][0], v.pm[k][1]);
+        }
         return;
     }
     float *bufs[2] = {v.accum, v.count};
@@ -238,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 //      chunks of kChunk slots reserved with one atomic (unused slots are marked dead).
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 2;
-constexpr int kSW = 12;              // warps per CTA of the TMA sweeps (2 CTAs x 12 warps per SM)
+constexpr int kSW = 8;               // warps per CTA of the TMA sweeps (3 CTAs x 8 warps per SM)
 constexpr int kST = kSW * 32;
 constexpr int kWTile = 256;  // points per warp tile (8 per lane)
 constexpr int kQCap = 64;
@@ -312,9 +317,9 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 struct LayerDesc {
     int32_t off[ADOP_MAX_LAYERS], wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS];
     uint64_t *keys;
-    float4 pl[5];  // frustum half-spaces (n, d) and their margins (see box_culled)
-    float2 pm[5];
 };
+
+
 
 struct DepthSmem {
     float pos[kStages][4][kSW][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
@@ -325,25 +330,20 @@ struct DepthSmem {
 };
 
 __device__ __forceinline__ void init_layer_descs(const RasterArgs &a, LayerDesc *ld) {
-    constexpr int F = 3 * ADOP_MAX_LAYERS + 1 + 5;
+    constexpr int F = 3 * ADOP_MAX_LAYERS + 1;
     for (int t = threadIdx.x; t < a.nviews * F; t += blockDim.x) {
         const int v = t / F, f = t % F;
         if (f < ADOP_MAX_LAYERS) ld[v].off[f] = a.v[v].off[f];
         else if (f < 2 * ADOP_MAX_LAYERS) ld[v].wl[f - ADOP_MAX_LAYERS] = a.v[v].wl[f - ADOP_MAX_LAYERS];
         else if (f < 3 * ADOP_MAX_LAYERS) ld[v].hl[f - 2 * ADOP_MAX_LAYERS] = a.v[v].hl[f - 2 * ADOP_MAX_LAYERS];
-        else if (f == 3 * ADOP_MAX_LAYERS) ld[v].keys = a.v[v].keys;
-        else {
-            const int k = f - 3 * ADOP_MAX_LAYERS - 1;
-            ld[v].pl[k] = make_float4(a.v[v].pl[k][0], a.v[v].pl[k][1], a.v[v].pl[k][2], a.v[v].pl[k][3]);
-            ld[v].pm[k] = make_float2(a.v[v].pm[k][0], a.v[v].pm[k][1]);
-        }
+        else ld[v].keys = a.v[v].keys;
     }
 }
 
 // Views whose (widened) frustum may contain a point of the warp's tile, as a warp-uniform bit mask.
 // With more than 2 views the warp's union box is tested against all views at once (lane v tests
 // view v from the shared-memory table); otherwise every view is returned.
-__device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const LayerDesc *ld, const Box &b, int lane) {
+__device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const Box &b, int lane) {
     if (a.nviews <= 2) return (1u << a.nviews) - 1u;
     float lo[3], hi[3];
 #pragma unroll
@@ -366,11 +366,12 @@ __device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const LayerD
     w.B = ext;
     bool in = false;
     if (lane < a.nviews) {
-        const LayerDesc &v = ld[lane];
+        const PlaneTab &v = a.planes[lane];
         bool out = false;
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            const float4 P = v.pl[k];
+            const float4 P = __ldg(&v.pl[k]);
+            const float2 M = __ldg(&v.pm[k]);
             float val = P.w;
             val = fmaf(P.x, w.c[0], val);
             val = fmaf(fabsf(P.x), w.e[0], val);
@@ -378,7 +379,7 @@ __device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const LayerD
             val = fmaf(fabsf(P.y), w.e[1], val);
             val = fmaf(P.z, w.c[2], val);
             val = fmaf(fabsf(P.z), w.e[2], val);
-            out |= val < -fmaf(v.pm[k].x, w.B, v.pm[k].y);
+            out |= val < -fmaf(M.x, w.B, M.y);
         }
         in = !out;
     }
@@ -543,7 +544,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
-template <int MODEL>
+template <int MODEL, bool MV>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
                                             int lane, unsigned lt) {
@@ -555,7 +556,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
     }
     const Box box = lane_box(rows, lane, vmask);
-    uint32_t views = tile_views(a, ld, box, lane);
+    uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
 #pragma unroll 1
     while (views) {
         const int vs = __ffs(views) - 1;
@@ -592,10 +593,10 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
     }
 }
 
-static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / 2, "depth sweep: 2 CTAs per SM must fit in shared memory");
+static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / 3, "depth sweep: 3 CTAs per SM must fit in shared memory");
 
-template <int MODEL>
-__global__ void __launch_bounds__(kST, 2) k_depth_async(const __grid_constant__ RasterArgs a) {
+template <int MODEL, bool MV>
+__global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -659,7 +660,7 @@ __global__ void __launch_bounds__(kST, 2) k_depth_async(const __grid_constant__ 
             }
             __syncwarp();
         }
-        depth_lane8<MODEL>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
+        depth_lane8<MODEL, MV>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
@@ -782,6 +783,11 @@ __device__ __forceinline__ float neighbour_term(const RasterArgs &a, const ViewD
 // With them each Eq. 11 neighbour costs one 16-B load + one G row: Delta . G = factor (tau . G - S).
 __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
+    if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for the sweep's tile_views
+        const int k = threadIdx.x;
+        a.planes[blockIdx.y].pl[k] = make_float4(v.pl[k][0], v.pl[k][1], v.pl[k][2], v.pl[k][3]);
+        a.planes[blockIdx.y].pm[k] = make_float2(v.pm[k][0], v.pm[k][1]);
+    }
     const int C = a.channels;
     float *gt = const_cast<float *>(v.gradT);
     uint4 *pt = const_cast<uint4 *>(v.ptab);
@@ -1269,10 +1275,10 @@ struct BwdSmem {
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
 };
 
-static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 2, "backward sweep: 2 CTAs per SM must fit in shared memory");
+static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 3, "backward sweep: 3 CTAs per SM must fit in shared memory");
 
-template <int MODEL, int CT>
-__global__ void __launch_bounds__(kST, 2) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
+template <int MODEL, int CT, bool MV>
+__global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1339,7 +1345,7 @@ __global__ void __launch_bounds__(kST, 2) k_bwd_sweep(const __grid_constant__ Ra
                 if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
         }
         const Box box = lane_box(rp, lane, vmask);
-        uint32_t views = tile_views(a, sm.ld, box, lane);
+        uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
 #pragma unroll 1
         while (views) {
             const int vs = __ffs(views) - 1;
@@ -1436,25 +1442,29 @@ int launch_clear(const RasterArgs &a, int what, void *stream) {
     return (int)cudaGetLastError();
 }
 
+template <int MODEL, bool MV>
+static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
+    auto k = k_depth_async<MODEL, MV>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(DepthSmem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t tiles = (a.n + kWTile - 1) / kWTile;
+    int64_t g = (int64_t)sms * per_sm;
+    if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
+    if (g < 1) g = 1;
+    k<<<(unsigned)g, kST, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
 template <int MODEL, bool VEC>
 static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
-    if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0) {
-        auto k = k_depth_async<MODEL>;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
-            attr = true;
-        }
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(DepthSmem));
-        if (per_sm < 1) per_sm = 1;
-        int64_t tiles = (a.n + kWTile - 1) / kWTile;
-        int64_t g = (int64_t)sms * per_sm;
-        if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
-        if (g < 1) g = 1;
-        k<<<(unsigned)g, kST, sizeof(DepthSmem), (cudaStream_t)stream>>>(a);
-        return (int)cudaGetLastError();
-    }
+    if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0)
+        return a.nviews > 2 ? launch_depth_async<MODEL, true>(a, sms, stream) : launch_depth_async<MODEL, false>(a, sms, stream);
     auto k = k_stream<MODEL, VEC, MODE_DEPTH, false>;
     int g = resident_grid(k, sms, kWarps * 128, a.n);
     k<<<g, kThreads, 0, (cudaStream_t)stream>>>(a);
@@ -1572,12 +1582,8 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
     }
     {   // sweep: emit work lists
-        auto k = k_bwd_sweep<MODEL, CT>;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
-            attr = true;
-        }
+        auto k = a.nviews > 2 ? k_bwd_sweep<MODEL, CT, true> : k_bwd_sweep<MODEL, CT, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(BwdSmem));
         if (per_sm < 1) per_sm = 1;
