@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "adop_internal.h"
 
@@ -304,6 +305,34 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     }
 }
 
+// 2-D TMA descriptor over the x/y/z rows (dims {n, 3}, row stride pos_stride * 4 bytes, box 256 x 3).
+// Resolved through the runtime's driver entry point (no libcuda link); on any failure the kernels fall
+// back to one 1-D bulk copy per row.
+void encode_pos_tmap(RasterArgs &a, const adop_points *pts) {
+    a.use_tmap = 0;
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+        else
+            cudaGetLastError();
+    }
+    if (!encode || pts->n < 256 || pts->n >= ((int64_t)1 << 31)) return;
+    const cuuint64_t dims[2] = {(cuuint64_t)pts->n, 3};
+    const cuuint64_t strides[1] = {(cuuint64_t)pts->pos_stride * sizeof(float)};
+    const cuuint32_t box[2] = {256, 3};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&a.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(pts->pos), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    a.use_tmap = r == CUDA_SUCCESS ? 1 : 0;
+}
+
 bool vec_path(const adop_points *pts) {
     return pts->n > 0 && aligned(pts->pos, 16) && pts->pos_stride % 4 == 0 && (!pts->radius || aligned(pts->radius, 16));
 }
@@ -367,6 +396,7 @@ adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const
         return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    if (vec_path(points)) encode_pos_tmap(a, points);
     int e = launch_clear(a, 0, stream);
     if (e) return cuda_status(e, "clear launch");
     if (points->n > 0) {
@@ -438,6 +468,7 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, fwd_views, &ws);
     for (int v = 0; v < n_views; ++v) a.v[v].grad = grad_image[v];
+    if (vec_path(points)) encode_pos_tmap(a, points);
     a.d_feat = d_feat;
     a.d_pos = d_pos;
     if (points->n == 0) {

@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 
 #include "../../include/adop.h"
 
@@ -60,6 +61,8 @@ struct PlaneTab {
 };
 
 struct RasterArgs {
+    CUtensorMap tmap;      // 2-D TMA descriptor of the x/y/z rows ([3][pos_stride] fp32), box 256 x 3
+    int32_t use_tmap;
     const float *x, *y, *z;
     const float *radius;
     float radius_uniform;

@@ -322,7 +322,7 @@ struct LayerDesc {
 
 
 struct DepthSmem {
-    float pos[kStages][4][kSW][kWTile];  // stage, row (x, y, z, r_world), warp, point of the warp tile
+    float pos[kStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
     uint64_t bar[kSW][kStages];          // per-warp TMA completion barriers
     long long tile[kSW][kStages];        // tile claimed into each stage
     WarpQueue q[kSW];
@@ -497,12 +497,17 @@ __device__ __forceinline__ Box lane_box(const float *const *rows, int lane, int 
         const float4 A = lane_row(rows[ax], lane, 0), Bv = lane_row(rows[ax], lane, 1);
         const float c[8] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w};
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+        if (valid == 0xFF) {  // full tile: branch-free 3-input min/max trees
+            lo = fminf(fminf(fminf(c[0], c[1]), fminf(c[2], c[3])), fminf(fminf(c[4], c[5]), fminf(c[6], c[7])));
+            hi = fmaxf(fmaxf(fmaxf(c[0], c[1]), fmaxf(c[2], c[3])), fmaxf(fmaxf(c[4], c[5]), fmaxf(c[6], c[7])));
+        } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if ((valid >> j) & 1) {
-                lo = fminf(lo, c[j]);
-                hi = fmaxf(hi, c[j]);
-            }
+            for (int j = 0; j < 8; ++j)
+                if ((valid >> j) & 1) {
+                    lo = fminf(lo, c[j]);
+                    hi = fmaxf(hi, c[j]);
+                }
+        }
         b.c[ax] = 0.5f * (lo + hi);
         b.e[ax] = 0.5f * (hi - lo);
         ext += fmaxf(fabsf(lo), fabsf(hi));
@@ -544,7 +549,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
-template <int MODEL, bool MV>
+template <int MODEL, int VM>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
                                             int lane, unsigned lt) {
@@ -556,10 +561,10 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
     }
     const Box box = lane_box(rows, lane, vmask);
-    uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
+    uint32_t views = VM == 2 ? tile_views(a, box, lane) : (VM == 0 ? 1u : (1u << a.nviews) - 1u);
 #pragma unroll 1
     while (views) {
-        const int vs = __ffs(views) - 1;
+        const int vs = VM == 0 ? 0 : __ffs(views) - 1;  // VM 0: compile-time view 0 (constant-bank operands)
         views &= views - 1u;
         const ViewDesc &v = a.v[vs];
         if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
@@ -595,7 +600,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
 
 static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / 3, "depth sweep: 3 CTAs per SM must fit in shared memory");
 
-template <int MODEL, bool MV>
+template <int MODEL, int VM>
 __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
@@ -625,8 +630,14 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
             if (t < ntiles && full_tile(t)) {
                 const uint64_t pol = policy_evict_first();
                 mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-                for (int r = 0; r < rows; ++r)
-                    bulk_g2s(sm.pos[st][r][wid], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                if (a.use_tmap) {  // x, y, z rows in one 2-D tensor copy, r_world in a 1-D bulk copy
+                    tensor_g2s_2d(sm.pos[st][wid][0], &a.tmap, (int)(t * kWTile), 0, &sm.bar[wid][st], pol);
+                    if (rows == 4)
+                        bulk_g2s(sm.pos[st][wid][3], src[3] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                } else {
+                    for (int r = 0; r < rows; ++r)
+                        bulk_g2s(sm.pos[st][wid][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                }
             }
         }
     };
@@ -643,7 +654,7 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
         const long long t = *(volatile long long *)&sm.tile[wid][st];
         if (t >= ntiles) break;
         const int64_t base = t * kWTile;
-        const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
+        const float *rp[4] = {sm.pos[st][wid][0], sm.pos[st][wid][1], sm.pos[st][wid][2], sm.pos[st][wid][3]};
         int vmask = 0xFF;
         if (full_tile(t)) {
             mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
@@ -655,12 +666,12 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const bool in = base + e < a.n;
                 for (int r = 0; r < 4; ++r)
-                    sm.pos[st][r][wid][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                    sm.pos[st][wid][r][e] = (in && r < rows) ? src[r][base + e] : 0.f;
                 vmask |= (in ? 1 : 0) << j;
             }
             __syncwarp();
         }
-        depth_lane8<MODEL, MV>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
+        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
@@ -1269,7 +1280,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_ghost(const __grid_constant__ 
 }
 
 struct BwdSmem {
-    float pos[kStages][4][kSW][kWTile];
+    float pos[kStages][kSW][4][kWTile];
     uint64_t bar[kSW][kStages];
     long long tile[kSW][kStages];
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
@@ -1308,8 +1319,14 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             if (t < ntiles && full_tile(t)) {
                 const uint64_t pol = policy_evict_first();
                 mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-                for (int r = 0; r < rows; ++r)
-                    bulk_g2s(sm.pos[st][r][wid], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                if (a.use_tmap) {  // x, y, z rows in one 2-D tensor copy, r_world in a 1-D bulk copy
+                    tensor_g2s_2d(sm.pos[st][wid][0], &a.tmap, (int)(t * kWTile), 0, &sm.bar[wid][st], pol);
+                    if (rows == 4)
+                        bulk_g2s(sm.pos[st][wid][3], src[3] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                } else {
+                    for (int r = 0; r < rows; ++r)
+                        bulk_g2s(sm.pos[st][wid][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+                }
             }
         }
     };
@@ -1321,7 +1338,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         const long long t = *(volatile long long *)&sm.tile[wid][st];
         if (t >= ntiles) break;
         const int64_t base = t * kWTile;
-        const float *rp[4] = {sm.pos[st][0][wid], sm.pos[st][1][wid], sm.pos[st][2][wid], sm.pos[st][3][wid]};
+        const float *rp[4] = {sm.pos[st][wid][0], sm.pos[st][wid][1], sm.pos[st][wid][2], sm.pos[st][wid][3]};
         int vmask = 0xFF;
         if (full_tile(t)) {
             mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
@@ -1332,7 +1349,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             for (int j = 0; j < 8; ++j) {
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const bool in = base + e < a.n;
-                for (int r = 0; r < 4; ++r) sm.pos[st][r][wid][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                for (int r = 0; r < 4; ++r) sm.pos[st][wid][r][e] = (in && r < rows) ? src[r][base + e] : 0.f;
                 vmask |= (in ? 1 : 0) << j;
             }
             __syncwarp();
@@ -1442,9 +1459,9 @@ int launch_clear(const RasterArgs &a, int what, void *stream) {
     return (int)cudaGetLastError();
 }
 
-template <int MODEL, bool MV>
+template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
-    auto k = k_depth_async<MODEL, MV>;
+    auto k = k_depth_async<MODEL, VM>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
@@ -1464,7 +1481,8 @@ static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
 template <int MODEL, bool VEC>
 static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
     if (VEC && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0)
-        return a.nviews > 2 ? launch_depth_async<MODEL, true>(a, sms, stream) : launch_depth_async<MODEL, false>(a, sms, stream);
+        return a.nviews > 2 ? launch_depth_async<MODEL, 2>(a, sms, stream)
+               : (a.nviews == 1 ? launch_depth_async<MODEL, 0>(a, sms, stream) : launch_depth_async<MODEL, 1>(a, sms, stream));
     auto k = k_stream<MODEL, VEC, MODE_DEPTH, false>;
     int g = resident_grid(k, sms, kWarps * 128, a.n);
     k<<<g, kThreads, 0, (cudaStream_t)stream>>>(a);
