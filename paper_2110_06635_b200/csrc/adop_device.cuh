@@ -203,6 +203,23 @@ __device__ __forceinline__ void red_add_v4(float *addr, float4 v) {
 __device__ __forceinline__ void red_add(float *addr, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
 }
+// Keys are re-read by the blend and the backward: keep their lines in L2 while the cloud streams past.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void red_min_u64_keep(uint64_t *addr, uint64_t v, uint64_t pol) {
+    asm volatile("red.global.min.u64.L2::cache_hint [%0], %1, %2;" ::"l"(addr), "l"(v), "l"(pol) : "memory");
+}
+// Features of blended points are read once: do not let them evict the accumulators.
+__device__ __forceinline__ float4 ld_once4(const float *p, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
 __device__ __forceinline__ void red_min_u64(uint64_t *addr, uint64_t v) {
     asm volatile("red.global.min.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
 }

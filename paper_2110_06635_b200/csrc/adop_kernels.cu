@@ -139,7 +139,8 @@ __device__ __forceinline__ void accumulate_feature(const RasterArgs &a, const Vi
     const float *f = a.feat + idx * C;
     float *acc = v.accum + (int64_t)pix * C;
     if (VEC4) {
-        for (int c = 0; c < C; c += 4) red_add_v4(acc + c, __ldg(reinterpret_cast<const float4 *>(f + c)));
+        const uint64_t pol = policy_evict_first();
+        for (int c = 0; c < C; c += 4) red_add_v4(acc + c, ld_once4(f + c, pol));
     } else {
         for (int c = 0; c < C; ++c) red_add(acc + c, __ldg(f + c));
     }
@@ -423,7 +424,7 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
         const int loc = l < nk ? layer_pixel(v, p, l, pu, pv) : -1;
         const bool hit = loc >= 0;
         const uint32_t pix = (uint32_t)(v.off[l] + loc);
-        if (hit) red_min_u64(v.keys + pix, key);
+        if (hit) red_min_u64_keep(v.keys + pix, key, policy_evict_last());
         const unsigned b = __ballot_sync(kFull, hit);
         if (b == 0u) {
             if (!__any_sync(kFull, l + 1 < nk)) break;
