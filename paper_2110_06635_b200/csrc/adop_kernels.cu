@@ -414,8 +414,6 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
                                              float v0, uint32_t zbits, uint32_t idx, RecChunk &c, int lane,
                                              unsigned lt) {
     const uint64_t key = ((uint64_t)zbits << 32) | (a.goff + idx);
-    if (nk > 0 && a.feat)  // the blend will gather this point's features: start pulling them into L2 now
-        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a.feat + (int64_t)idx * a.channels));
     Proj p;
     p.u0 = u0;
     p.v0 = v0;
