@@ -690,46 +690,14 @@ __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ Rast
         stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
         return;
     }
-    unsigned long long total = *(volatile unsigned long long *)&a.hdr->records;
-    if (total > (unsigned long long)a.rec_capacity) total = (unsigned long long)a.rec_capacity;
+    const unsigned long long total = *(volatile unsigned long long *)&a.hdr->records;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    const int C = a.channels;
-    const uint64_t pol = policy_evict_first();
-    // 4 records per thread per iteration, all loads (records, keys, features) issued before any use:
-    // the pass is latency-bound, so memory-level parallelism is what sets its speed
-    constexpr int U = 4;
-    for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r0 < total;
-         r0 += stride * U) {
-        uint4 rec[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const unsigned long long r = r0 + u * stride;
-            rec[u] = r < total ? __ldcs(reinterpret_cast<const uint4 *>(a.records) + r)
-                               : make_uint4(0u, 0u, 0u, kDeadView);
-        }
-        unsigned long long key[U];
-        float4 f[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            key[u] = 0ull;
-            f[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (rec[u].w != kDeadView) {
-                key[u] = __ldcg(reinterpret_cast<const unsigned long long *>(a.v[rec[u].w].keys) + rec[u].x);
-                if (VEC4 && C == 4) f[u] = ld_once4(a.feat + (int64_t)rec[u].z * 4, pol);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (rec[u].w == kDeadView) continue;
-            const ViewDesc &v = a.v[rec[u].w];
-            if (!fuzzy_pass(__uint_as_float(rec[u].y), key[u], a.onepa)) continue;
-            if (VEC4 && C == 4) {
-                red_add_v4(v.accum + (int64_t)rec[u].x * 4, f[u]);
-                red_add(v.count + rec[u].x, 1.0f);
-            } else {
-                accumulate_feature<VEC4>(a, v, rec[u].z, rec[u].x);
-            }
-        }
+    for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
+        const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
+        if (rec.w == kDeadView) continue;
+        const ViewDesc &v = a.v[rec.w];
+        const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
+        if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
     }
 }
 
