@@ -47,7 +47,7 @@ uint32_t salt_of(uint64_t seed, uint32_t stream, uint32_t view) {
 }
 constexpr uint32_t kStreamGhost = 1, kStreamDiscard = 2;
 
-constexpr size_t kHeaderBytes = 4096;  // WsHeader at 0, PlaneTab[16] at 256
+constexpr size_t kHeaderBytes = 4096;  // WsHeader at 0, PlaneTab[16] at 256, LayerDesc[16] at 2304
 constexpr int64_t kRecordSlack = 1 << 20;  // >= resident warps x 256-slot record chunks
 constexpr int kMaxBwdBlocks = 2048;
 constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 6 * sizeof(double);
@@ -199,6 +199,9 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     if (ws) {
         a.hdr = ws->hdr;
         a.planes = reinterpret_cast<PlaneTab *>(reinterpret_cast<char *>(ws->hdr) + 256);
+        a.ldesc = reinterpret_cast<LayerDesc *>(reinterpret_cast<char *>(ws->hdr) + 2304);
+        static_assert(256 + ADOP_MAX_VIEWS_PER_LAUNCH * sizeof(PlaneTab) <= 2304, "header layout");
+        static_assert(2304 + ADOP_MAX_VIEWS_PER_LAUNCH * sizeof(LayerDesc) <= kHeaderBytes, "header layout");
         a.records = ws->records;
         a.rec_capacity = ws->capacity;
         a.pose_partials = ws->partials;

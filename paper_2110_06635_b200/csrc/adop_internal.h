@@ -60,6 +60,13 @@ struct PlaneTab {
     float2 pm[5];  // margins (see box_culled)
 };
 
+// Layer table of one view (read with a per-lane view slot by the depth drain; in the workspace header,
+// written by k_clear<KEYS>, and in shared memory for the backward sweep).
+struct LayerDesc {
+    int32_t off[ADOP_MAX_LAYERS], wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS];
+    uint64_t *keys;
+};
+
 struct RasterArgs {
     CUtensorMap tmap;      // 2-D TMA descriptor of the x/y/z rows ([3][pos_stride] fp32), box 256 x 3
     int32_t use_tmap;
@@ -92,6 +99,7 @@ struct RasterArgs {
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
     PlaneTab *planes;      // [nviews] in the workspace header area
+    LayerDesc *ldesc;      // [nviews] in the workspace header area
     float *d_feat;
     float *d_pos;          // [3][n]
     uint8_t *mask;         // point-mask debug output [V][n]

@@ -63,6 +63,14 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
             a.planes[blockIdx.y].pl[k] = make_float4(v.pl[k][0], v.pl[k][1], v.pl[k][2], v.pl[k][3]);
             a.planes[blockIdx.y].pm[k] = make_float2(v.pm[k][0], v.pm[k][1]);
         }
+        if (blockIdx.x == 0 && threadIdx.x < ADOP_MAX_LAYERS) {  // this view's layer table for the drain
+            LayerDesc &d = a.ldesc[blockIdx.y];
+            const int l = threadIdx.x;
+            d.off[l] = v.off[l];
+            d.wl[l] = v.wl[l];
+            d.hl[l] = v.hl[l];
+            if (l == 0) d.keys = v.keys;
+        }
         return;
     }
     float *bufs[2] = {v.accum, v.count};
@@ -313,21 +321,17 @@ __device__ __forceinline__ int f2ord(float f) {
 }
 __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
-// Per-view layer table in shared memory: the drain indexes it with a per-lane view slot (divergent
-// constant-bank loads would serialise).
-struct LayerDesc {
-    int32_t off[ADOP_MAX_LAYERS], wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS];
-    uint64_t *keys;
-};
+// The drain indexes the per-view layer table (LayerDesc, adop_internal.h) with a per-lane view slot:
+// divergent constant-bank loads would serialise, so it reads the workspace copy through L1.
 
 
 
 struct DepthSmem {
     float pos[kStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
     uint64_t bar[kSW][kStages];          // per-warp TMA completion barriers
-    long long tile[kSW][kStages];        // tile claimed into each stage
+    int tile[kSW][kStages];              // tile claimed into each stage (dynamic claiming)
     WarpQueue q[kSW];
-    LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
+    uint8_t cand[kSW][kWTile];           // compacted candidate list of the warp tile (tile offsets)
 };
 
 __device__ __forceinline__ void init_layer_descs(const RasterArgs &a, LayerDesc *ld) {
@@ -553,7 +557,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 template <int MODEL, int VM>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
-                                            int lane, unsigned lt) {
+                                            uint8_t *cl, int lane, unsigned lt) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     uint32_t live = (uint32_t)vmask;
     if (a.ghost_thr != 0u) {
@@ -587,15 +591,26 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             }
         }
         m &= live;
-        while (__any_sync(kFull, m != 0u)) {
-            const bool ok = m != 0u;
-            const int j = ok ? __ffs(m) - 1 : 0;
-            m &= m - 1u;
-            const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+        if (!__any_sync(kFull, m != 0u)) continue;
+        // compact the warp's candidates into a list of tile offsets, then run the exact path 32 at a time
+        // with every lane busy (a per-lane loop would idle the lanes whose points are all rejected)
+        int cn = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const bool bit = (m >> j) & 1u;
+            const unsigned b = __ballot_sync(kFull, bit);
+            if (bit) cl[cn + __popc(b & lt)] = (uint8_t)((j >> 2) * 128 + 4 * lane + (j & 3));
+            cn += __popc(b);
+        }
+        __syncwarp();
+        for (int i0 = 0; i0 < cn; i0 += 32) {
+            const bool ok = i0 + lane < cn;
+            const int e = ok ? cl[i0 + lane] : 0;
             const float rw = staged_r ? rows[3][e] : a.radius_uniform;
             depth_candidate<MODEL>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
                                    a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
         }
+        __syncwarp();  // the list is rewritten by the next view / tile
     }
 }
 
@@ -607,39 +622,50 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const long long ntiles = (a.n + kWTile - 1) / kWTile;
+    const int ntiles = (int)((a.n + kWTile - 1) / kWTile);  // n < 2^32 (32-bit point indices)
+    const int nfull = (int)(a.n / kWTile);                  // tiles [0, nfull) are full: TMA-streamed
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
-    const float *src[4] = {a.x, a.y, a.z, a.radius};
-    init_layer_descs(a, sm.ld);
+    const bool dyn = a.dyn_tiles & 1;
     if (lane == 0) {
         for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
         fence_mbar_init();
     }
-    __syncthreads();
-    auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
-    // lane 0 of each warp claims the next tile of the whole grid (dynamic load balance) and streams it
-    // with `rows` 1-KB bulk copies (TMA engine, L2 evict-first) into stage st
+    __syncwarp();
+    // per-warp constants of the issue path: shared-window addresses, L2 policy, tile sequence
+    constexpr uint32_t kStageBytes = sizeof(sm.pos[0]), kRowBytes = kWTile * sizeof(float);
+    const uint32_t bar_s = smem_addr(&sm.bar[wid][0]);
+    const uint32_t pos_s = smem_addr(&sm.pos[0][wid][0][0]);
+    const uint32_t txb = (uint32_t)rows * kRowBytes;
+    const uint64_t pol = policy_evict_first();
+    const int stride = (int)gridDim.x * kSW;
+    int t_next = (int)blockIdx.x * kSW + wid;  // static order: warp w takes tiles w, w + W, ...
     TileClaim tc;
-    if (lane == 0)
-        tc.init(&a.hdr->tiles_fwd, ntiles, (long long)gridDim.x * kSW, (long long)blockIdx.x * kSW + wid,
-                a.dyn_tiles & 1);
+    if (dyn && lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, stride, t_next, true);
+    // lane 0 claims the stage's next tile and streams its rows with the TMA engine (L2 evict-first):
+    // x, y, z in one 2-D tensor copy (or three 1-D bulk copies), r_world in a 1-D bulk copy
     auto issue = [&](int st) {
-        if (lane == 0) {
-            const long long t = tc.take(&a.hdr->tiles_fwd);
+        if (lane != 0) return;
+        int t;
+        if (dyn) {
+            t = (int)tc.take(&a.hdr->tiles_fwd);
             sm.tile[wid][st] = t;
-            if (t < ntiles && full_tile(t)) {
-                const uint64_t pol = policy_evict_first();
-                mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-                if (a.use_tmap) {  // x, y, z rows in one 2-D tensor copy, r_world in a 1-D bulk copy
-                    tensor_g2s_2d(sm.pos[st][wid][0], &a.tmap, (int)(t * kWTile), 0, &sm.bar[wid][st], pol);
-                    if (rows == 4)
-                        bulk_g2s(sm.pos[st][wid][3], src[3] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
-                } else {
-                    for (int r = 0; r < rows; ++r)
-                        bulk_g2s(sm.pos[st][wid][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
+        } else {
+            t = t_next;
+            t_next += stride;
+        }
+        if (t < nfull) {
+            const uint32_t bar = bar_s + 8u * st, dst = pos_s + kStageBytes * st;
+            mbar_expect_tx_a(bar, txb);
+            if (a.use_tmap) {
+                tensor_g2s_2d_a(dst, &a.tmap, t * kWTile, 0, bar, pol);
+            } else {
+                for (int r = 0; r < 3; ++r) {
+                    const float *src = r == 0 ? a.x : (r == 1 ? a.y : a.z);
+                    bulk_g2s_a(dst + r * kRowBytes, src + (int64_t)t * kWTile, kRowBytes, bar, pol);
                 }
             }
+            if (rows == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
         }
     };
     for (int st = 0; st < kStages; ++st) issue(st);
@@ -650,17 +676,24 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
     c.base = 0;
     c.left = 0;
     uint32_t phase = 0u;
-    for (int64_t k = 0;; ++k) {
-        const int st = (int)(k % kStages);
-        const long long t = *(volatile long long *)&sm.tile[wid][st];
+    int t_cons = (int)blockIdx.x * kSW + wid;
+    for (int st = 0;; st = (st + 1) & (kStages - 1)) {
+        int t;
+        if (dyn) {
+            t = *(volatile int *)&sm.tile[wid][st];
+        } else {
+            t = t_cons;
+            t_cons += stride;
+        }
         if (t >= ntiles) break;
-        const int64_t base = t * kWTile;
+        const int64_t base = (int64_t)t * kWTile;
         const float *rp[4] = {sm.pos[st][wid][0], sm.pos[st][wid][1], sm.pos[st][wid][2], sm.pos[st][wid][3]};
         int vmask = 0xFF;
-        if (full_tile(t)) {
-            mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
+        if (t < nfull) {
+            mbar_wait_a(bar_s + 8u * st, (phase >> st) & 1u);
             phase ^= 1u << st;
         } else {  // ragged last tile: guarded loads into this stage (no copy was issued for it)
+            const float *src[4] = {a.x, a.y, a.z, a.radius};
             vmask = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -672,12 +705,12 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
             }
             __syncwarp();
         }
-        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, sm.ld, q, qn, c, lane, lt);
+        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt);
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
     }
-    if (qn > 0) drain(a, sm.ld, q, qn, qn, c, lane, lt);
+    if (qn > 0) drain(a, a.ldesc, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
 
