@@ -175,6 +175,8 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     a.radius_uniform = pts->radius_uniform;
     a.feat = pts->feat;
     a.n = pts->n;
+    a.ntiles = (int32_t)((pts->n + 255) / 256);
+    a.nfull = (int32_t)(pts->n / 256);
     a.goff = (uint32_t)pts->global_offset;
     a.channels = pts->channels;
     a.layers = pr->layers;

@@ -75,6 +75,7 @@ struct RasterArgs {
     float radius_uniform;
     const float *feat;
     int64_t n;
+    int32_t ntiles, nfull; // depth sweep: ceil(n / 256) tiles, of which the first n / 256 are full
     uint32_t goff;
     int32_t channels;
     int32_t layers;

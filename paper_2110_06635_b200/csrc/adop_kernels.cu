@@ -503,8 +503,9 @@ __device__ __forceinline__ Box lane_box(const float *const *rows, int lane, int 
         const float c[8] = {A.x, A.y, A.z, A.w, Bv.x, Bv.y, Bv.z, Bv.w};
         float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
         if (valid == 0xFF) {  // full tile: branch-free 3-input min/max trees
-            lo = fminf(fminf(fminf(c[0], c[1]), fminf(c[2], c[3])), fminf(fminf(c[4], c[5]), fminf(c[6], c[7])));
-            hi = fmaxf(fmaxf(fmaxf(c[0], c[1]), fmaxf(c[2], c[3])), fmaxf(fmaxf(c[4], c[5]), fmaxf(c[6], c[7])));
+            // 3-input FMNMX3 chains: 8 values in 4 ops
+            lo = fminf(fminf(fminf(fminf(fminf(fminf(c[0], c[1]), c[2]), c[3]), c[4]), fminf(c[5], c[6])), c[7]);
+            hi = fmaxf(fmaxf(fmaxf(fmaxf(fmaxf(fmaxf(c[0], c[1]), c[2]), c[3]), c[4]), fmaxf(c[5], c[6])), c[7]);
         } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -622,8 +623,8 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int ntiles = (int)((a.n + kWTile - 1) / kWTile);  // n < 2^32 (32-bit point indices)
-    const int nfull = (int)(a.n / kWTile);                  // tiles [0, nfull) are full: TMA-streamed
+    static_assert(kWTile == 256, "RasterArgs::ntiles / nfull are counted in 256-point tiles");
+    const int ntiles = a.ntiles, nfull = a.nfull;  // tiles [0, nfull) are full: TMA-streamed
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
     const bool dyn = a.dyn_tiles & 1;
