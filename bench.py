@@ -149,7 +149,7 @@ def run_ours(args, rank, world, local_rank):
     ap = A.Params(prm, C)
     pyrs = A.alloc_pyramids(cams, prm.layers, C, dev)
     cap = A.default_record_capacity(N, len(cams), prm.layers, prm.discard)
-    ws = A.Workspace(pts, len(cams), ap, dev, cap)
+    ws = A.Workspace(pts, cams, ap, dev, cap)
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):

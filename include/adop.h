@@ -128,15 +128,20 @@ typedef struct {
 /* Pixels of one pyramid: sum_l ceil(w/2^l) * ceil(h/2^l).  Returns 0 on invalid sizes. */
 ADOP_API int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t layers);
 
-/* Workspace bytes for calls over `n_views` views of `points`.
- * record_capacity: number of 16-byte survivor record slots the depth pass may use
- * (one per (point, view, layer) hit of the render set, reserved per warp in chunks
- * of 256 whose unused slots are marked dead); < 0 selects the worst case
- * n * n_views * layers plus chunk slack.  If a call's survivors exceed the capacity,
- * the blend pass falls back to re-streaming all points (correct, slower).
- * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, n_views < 1, bad layers). */
-ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_params *params,
-                                int64_t record_capacity, size_t *bytes);
+/* Workspace bytes for calls over `n_views` views (cameras: host [n_views]) of `points`.
+ * Layout: 4 KiB header | pose partials | backward pixel tables (per view and pixel one
+ * 16-byte {key, count, sum_c G I} entry and one [C] gradient row) | record region.
+ * record_capacity: 16-byte slots of the record region.  The depth pass fills it from
+ * the front with survivor records (one per (point, view, layer) hit of the render set)
+ * and, when params->ghost_rate > 0, from the back with ghost entries (2 slots per kept
+ * (ghost, view)); both are reserved per warp in chunks of 256 slots whose unused slots
+ * are marked dead.  < 0 selects the worst case n * n_views * max(layers, 2) plus chunk
+ * slack.  If the lists do not fit, the blend pass re-streams all points and the
+ * backward re-renders them (correct, slower).
+ * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, n_views not in [1, 16], bad layers,
+ * channels or camera sizes). */
+ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                const adop_params *params, int64_t record_capacity, size_t *bytes);
 
 /* Phase 1, depth-only render pass (§4.5; Eqs. 2-4, 12, min_z of Eq. 6):
  * sets keys to the sentinel for every view, then
@@ -172,7 +177,13 @@ ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n
 
 /* Backward (§4.2-4.5): re-renders every point (L361) against the forward's
  * keys/count/accum/image (which must be unmodified) and the upstream gradient
- * grad_image[v] (device, image layout) and produces
+ * grad_image[v] (device, image layout).  The re-render's work lists (rendered hits,
+ * kept ghosts) are exactly the survivor records and ghost list the depth pass left in
+ * the workspace: when the workspace still holds them for the same inputs (a
+ * fingerprint of points, cameras, poses, params and pyramids), they are consumed
+ * directly; otherwise (different inputs, an overflowed record region, or a forward on
+ * the unaligned path) every point is re-projected.  Results are the same either way.
+ * It produces
  *   d_feat [n][C]: sum over views/layers of G/|Lambda| for rendered points (ghosts 0),
  *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17),
  *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment).

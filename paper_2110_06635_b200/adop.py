@@ -89,7 +89,8 @@ def lib():
         L.adop_pyramid_pixels.restype = C.c_int64
         L.adop_pyramid_pixels.argtypes = [C.c_int32, C.c_int32, C.c_int32]
         L.adop_workspace_size.restype = C.c_int
-        L.adop_workspace_size.argtypes = [P(adop_points), C.c_int32, P(adop_params), C.c_int64, P(C.c_size_t)]
+        L.adop_workspace_size.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_params), C.c_int64,
+                                          P(C.c_size_t)]
         L.adop_workspace_stats.restype = C.c_int
         L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int32)]
         L.adop_last_error.restype = C.c_char_p
@@ -210,9 +211,15 @@ def alloc_pyramids(cams, layers: int, channels: int, device) -> List[Pyramid]:
 
 
 class Workspace:
-    def __init__(self, points: Points, n_views: int, params: Params, device, record_capacity: int = -1):
+    """Caller-owned scratch of adop_workspace_size bytes (256-B aligned): header, pose partials, the
+    backward's pixel tables and the record region (survivor records + ghost list).  The backward consumes
+    the depth pass's lists when it is given the same workspace and the same inputs."""
+
+    def __init__(self, points: Points, cams, params: Params, device, record_capacity: int = -1):
+        V = len(cams)
+        ca = (adop_camera * V)(*[camera_struct(c) for c in cams])
         size = C.c_size_t(0)
-        _check(lib().adop_workspace_size(C.byref(points.s), n_views, C.byref(params.s), int(record_capacity),
+        _check(lib().adop_workspace_size(C.byref(points.s), V, ca, C.byref(params.s), int(record_capacity),
                                          C.byref(size)))
         self.nbytes = int(size.value)
         self.buf = torch.empty((self.nbytes + 255) // 256 * 256 + 256, dtype=torch.uint8, device=device)
@@ -230,7 +237,7 @@ def default_record_capacity(n: int, n_views: int, layers: int, discard: bool) ->
     the kept points per pixel are bounded (Eq. 12), so the records are far below the worst case;
     exceeding the capacity is still correct (the blend pass re-streams the points)."""
     slack = 1 << 20  # partially filled per-warp record chunks (dead slots)
-    worst = n * n_views * layers
+    worst = n * n_views * max(layers, 2)  # a ghost entry takes 2 slots
     if worst * 16 <= (4 << 30) or not discard:
         return worst + slack
     return max(1 << 22, worst // 4) + slack
@@ -316,7 +323,7 @@ class Renderer:
         self.pyrs = alloc_pyramids(self.cams, params.layers, self.C, device)
         if record_capacity is None:
             record_capacity = default_record_capacity(self.points.n, len(self.cams), params.layers, params.discard)
-        self.ws = Workspace(self.points, len(self.cams), self.params, device, record_capacity)
+        self.ws = Workspace(self.points, self.cams, self.params, device, record_capacity)
         self.device = device
         self.d_feat = self.d_pos = self.d_pose = None
 

@@ -147,22 +147,57 @@ adop_status check_views(int32_t n_views, const adop_camera *cams, const adop_pos
 struct Ws {
     WsHeader *hdr;
     double *partials;
+    void *tables;
     Record *records;
     int64_t capacity;
 };
 
-adop_status carve_workspace(void *ws, size_t bytes, Ws &out) {
+// Backward pixel tables (one ptab uint4 + one [C] gradient row per pixel per view), 256-B rounded.
+size_t table_bytes(int32_t n_views, const adop_camera *cams, int32_t layers, int32_t channels) {
+    size_t t = 0;
+    for (int v = 0; v < n_views; ++v)
+        t += (size_t)adop_pyramid_pixels(cams[v].width, cams[v].height, layers) * (16u + 4u * (size_t)channels);
+    return (t + 255) / 256 * 256;
+}
+
+// Workspace layout: [header 4 KiB | pose partials | backward pixel tables | record region (16-B slots)].
+adop_status carve_workspace(void *ws, size_t bytes, size_t tbytes, Ws &out) {
     if (!ws) return fail(ADOP_ERR_INVALID_ARGUMENT, "workspace is NULL");
     if (!aligned(ws, 256)) return fail(ADOP_ERR_INVALID_ARGUMENT, "workspace must be 256-byte aligned");
-    if (bytes < kHeaderBytes + kPartialBytes)
-        return fail(ADOP_ERR_WORKSPACE_TOO_SMALL, "workspace of %zu bytes < minimum %zu", bytes,
-                    kHeaderBytes + kPartialBytes);
+    const size_t fixed = kHeaderBytes + kPartialBytes + tbytes;
+    if (bytes < fixed)
+        return fail(ADOP_ERR_WORKSPACE_TOO_SMALL, "workspace of %zu bytes < minimum %zu for these views", bytes, fixed);
     char *b = static_cast<char *>(ws);
     out.hdr = reinterpret_cast<WsHeader *>(b);
     out.partials = reinterpret_cast<double *>(b + kHeaderBytes);
-    out.records = reinterpret_cast<Record *>(b + kHeaderBytes + kPartialBytes);
-    out.capacity = (int64_t)((bytes - kHeaderBytes - kPartialBytes) / sizeof(Record));
+    out.tables = b + kHeaderBytes + kPartialBytes;
+    out.records = reinterpret_cast<Record *>(b + fixed);
+    out.capacity = (int64_t)((bytes - fixed) / sizeof(Record));
     return ok();
+}
+
+// Fingerprint of a call's inputs: the backward consumes the depth pass's lists only if its own
+// fingerprint equals the one the depth pass stored in the workspace header (FNV-1a, never 0).
+struct Fnv {
+    uint64_t h = 1469598103934665603ull;
+    void add(const void *p, size_t n) {
+        const unsigned char *c = static_cast<const unsigned char *>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    }
+    template <typename T>
+    void put(const T &v) { add(&v, sizeof(v)); }
+};
+uint64_t call_tag(const adop_points *pts, int32_t n_views, const adop_camera *cams, const adop_pose *poses,
+                  const adop_params *pr, const adop_pyramid *views, size_t ws_bytes) {
+    Fnv f;
+    f.put(pts->n); f.put(pts->global_offset); f.put(pts->pos_stride); f.put(pts->pos); f.put(pts->radius);
+    f.put(pts->radius_uniform); f.put(pts->channels); f.put(n_views); f.put(ws_bytes);
+    f.add(cams, sizeof(adop_camera) * (size_t)n_views);
+    f.add(poses, sizeof(adop_pose) * (size_t)n_views);
+    f.put(pr->layers); f.put(pr->alpha); f.put(pr->discard); f.put(pr->gamma); f.put(pr->ghost_rate);
+    f.put(pr->z_near); f.put(pr->seed); f.put(pr->view_id_base);
+    for (int v = 0; views && v < n_views; ++v) f.put(views[v].keys);
+    return f.h | 1ull;
 }
 
 void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const adop_camera *cams,
@@ -206,6 +241,7 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         static_assert(2304 + ADOP_MAX_VIEWS_PER_LAUNCH * sizeof(LayerDesc) <= kHeaderBytes, "header layout");
         a.records = ws->records;
         a.rec_capacity = ws->capacity;
+        a.tables = ws->tables;
         a.pose_partials = ws->partials;
     }
     const float lmax = (float)(1 << (pr->layers - 1));
@@ -354,7 +390,9 @@ adop_status prologue(const adop_points *points, int32_t n_views, const adop_came
     if ((s = check_params(params))) return s;
     if ((s = check_points(points, need_feat))) return s;
     if ((s = check_views(n_views, cameras, poses, params, views, points->channels, true))) return s;
-    if ((s = carve_workspace(workspace, workspace_bytes, ws))) return s;
+    if ((s = carve_workspace(workspace, workspace_bytes,
+                             table_bytes(n_views, cameras, params->layers, points->channels), ws)))
+        return s;
     cudaError_t pending = cudaGetLastError();
     if (pending != cudaSuccess) return fail(ADOP_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(pending));
     return ok();
@@ -378,15 +416,23 @@ int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t layers) {
     return t;
 }
 
-adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_params *params,
-                                int64_t record_capacity, size_t *bytes) {
-    if (!points || !params || !bytes) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (n_views < 1) return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views < 1");
+adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                const adop_params *params, int64_t record_capacity, size_t *bytes) {
+    if (!points || !params || !bytes || !cameras) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 1 || n_views > ADOP_MAX_VIEWS_PER_LAUNCH)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views = %d not in [1, %d]", n_views, ADOP_MAX_VIEWS_PER_LAUNCH);
     if (params->layers < 1 || params->layers > ADOP_MAX_LAYERS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad layers");
     if (points->n < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "n < 0");
-    // worst case n*V*L plus slack for partially filled per-warp record chunks (dead slots)
-    int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * params->layers + kRecordSlack;
-    *bytes = kHeaderBytes + kPartialBytes + (size_t)cap * sizeof(Record);
+    if (points->channels < 1 || points->channels > ADOP_MAX_CHANNELS)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "channels = %d not in [1, %d]", points->channels, ADOP_MAX_CHANNELS);
+    for (int v = 0; v < n_views; ++v)
+        if (adop_pyramid_pixels(cameras[v].width, cameras[v].height, params->layers) <= 0)
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: bad width/height", v);
+    // worst case n*V*max(L, 2) (a ghost entry takes 2 slots) plus slack for partially filled per-warp chunks
+    const int64_t per = params->layers > 2 ? params->layers : 2;
+    int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * per + kRecordSlack;
+    *bytes = kHeaderBytes + kPartialBytes + table_bytes(n_views, cameras, params->layers, points->channels) +
+             (size_t)cap * sizeof(Record);
     return ok();
 }
 
@@ -402,6 +448,8 @@ adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, views, &ws);
     if (vec_path(points)) encode_pos_tmap(a, points);
+    // only the pipelined depth kernel (vector path) writes the ghost list the backward can consume
+    a.tag = vec_path(points) ? call_tag(points, n_views, cameras, poses, params, views, workspace_bytes) : 0ull;
     int e = launch_clear(a, 0, stream);
     if (e) return cuda_status(e, "clear launch");
     if (points->n > 0) {
@@ -474,6 +522,7 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     fill_args(a, points, n_views, cameras, poses, params, fwd_views, &ws);
     for (int v = 0; v < n_views; ++v) a.v[v].grad = grad_image[v];
     if (vec_path(points)) encode_pos_tmap(a, points);
+    a.tag = call_tag(points, n_views, cameras, poses, params, fwd_views, workspace_bytes);
     a.d_feat = d_feat;
     a.d_pos = d_pos;
     if (points->n == 0) {
@@ -514,7 +563,7 @@ adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, 
     cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_status((int)e, "workspace stats");
-    if (records) *records = (int64_t)h.records;
+    if (records) *records = (int64_t)(h.front_ok + h.back_ok);  // survivor slots + ghost-list slots
     if (overflowed) *overflowed = h.overflow;
     return ok();
 }

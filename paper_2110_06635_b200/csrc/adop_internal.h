@@ -40,17 +40,35 @@ struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
     uint32_t pix;   // pixel index within the view's pyramid (off_l + local)
     uint32_t zbits; // bits of the point's camera-space z
     uint32_t idx;   // shard-local point index
-    uint32_t view;  // view slot within the launch
+    uint32_t view;  // view slot within the launch (0xFFFFFFFF: dead slot)
 };
 
+struct GhostEntry {  // one (ghost point, view) kept at >= 1 layer (§4.3), 32 bytes = 2 record slots
+    float u0, v0;    // layer-0 continuous pixel coordinates (R2/R6)
+    float X, Y;      // camera-space point (R1)
+    float Z;
+    uint32_t idx;    // shard-local point index
+    uint32_t vsnk;   // view slot | kept layers << 8 (0xFFFFFFFF: dead entry)
+    uint32_t pad;
+};
+constexpr int kResvBackShift = 40;
+
+// The record region of the workspace holds two lists: survivor records (16-B Record slots) growing
+// from the front -- written by the depth pass, read by the blend and by the backward's texture gradient
+// -- and ghost entries (GhostEntry, two slots each) growing from the back, written by the backward
+// sweep.  (When the backward cannot reuse the survivor records it re-renders them into the front list.)
+// Both are reserved per warp in chunks through ONE 64-bit counter `resv` (front slots in the low 40
+// bits, back chunks of 256 slots in the high 24); the successful reservations form the prefixes
+// [0, front_ok) and [capacity - back_ok, capacity) (see resv_take in adop_kernels.cu).
 struct WsHeader {
-    unsigned long long records;    // record slots used by the last depth pass
-    int32_t overflow;              // set when records > capacity
-    int32_t pad;
+    unsigned long long resv;       // front slots | back chunks << 40 (see above)
+    int32_t overflow;              // set when a reservation did not fit (the lists are incomplete)
+    int32_t mode;                  // backward: 1 = texture list = the depth pass's records, 0 = full re-render
+    unsigned long long tag;        // fingerprint of the call that wrote the lists (0: not reusable)
+    unsigned long long front_ok;   // slots of the front list (survivor / texture records)
+    unsigned long long back_ok;    // slots of the back list (ghost entries, 2 slots each)
     unsigned long long tiles_fwd;  // dynamic tile counters of the depth and backward sweeps
     unsigned long long tiles_bwd;
-    unsigned long long btex_n;     // backward work lists: texture-gradient hits, ghost entries
-    unsigned long long bgh_n;
 };
 
 // Frustum half-spaces of every view in the workspace (written by k_clear<KEYS> of the depth phase;
@@ -90,15 +108,13 @@ struct RasterArgs {
     int32_t grad_accumulate;
     float bg[ADOP_MAX_CHANNELS];
     WsHeader *hdr;
-    Record *records;
-    int64_t rec_capacity;
+    Record *records;       // record region: survivor records (front) + ghost list (back), see WsHeader
+    int64_t rec_capacity;  // in 16-B slots
+    void *tables;          // backward pixel tables: per view ptab [P] uint4, then per view gradT [P][C]
     double *pose_partials; // [gridDim.x][nviews][6]
-    uint4 *btex;           // backward texture-gradient work list (16-B slots)
-    int64_t btex_cap;
-    uint4 *bgh;            // backward ghost work list (32-B slots, 2 x uint4)
-    int64_t bgh_cap;
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
+    unsigned long long tag;// fingerprint of this call's inputs (host); 0 = records not reusable by the backward
     PlaneTab *planes;      // [nviews] in the workspace header area
     LayerDesc *ldesc;      // [nviews] in the workspace header area
     float *d_feat;

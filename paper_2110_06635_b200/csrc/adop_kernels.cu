@@ -54,8 +54,11 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
             for (int64_t q = tid; q < P; q += stride) k[q] = sentinel;
         }
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-            a.hdr->records = 0ull;
+            a.hdr->resv = 0ull;
+            a.hdr->front_ok = 0ull;
+            a.hdr->back_ok = 0ull;
             a.hdr->overflow = 0;
+            a.hdr->tag = a.tag;
             a.hdr->tiles_fwd = 0ull;
         }
         if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for tile_views
@@ -121,21 +124,47 @@ __device__ __forceinline__ void load_points(const RasterArgs &a, int64_t i0, flo
     }
 }
 
+// ---- record-region reservations (WsHeader::resv: front slots | back chunks << 40) ----
+constexpr int kChunk = 256;  // record slots reserved per warp at a time (back list: kChunk / 2 ghost entries)
+constexpr unsigned long long kFrontMask = (1ull << kResvBackShift) - 1ull;
+constexpr unsigned long long kNoSlot = ~0ull;
+
+__device__ __forceinline__ unsigned long long resv_front_used(unsigned long long r) { return r & kFrontMask; }
+__device__ __forceinline__ unsigned long long resv_back_slots(unsigned long long r) {
+    return (r >> kResvBackShift) * (unsigned long long)kChunk;
+}
+// Reserve k front slots (BACK = false) or one back chunk of kChunk slots (BACK = true).  One atomicAdd on
+// `resv` orders every reservation of both lists; a reservation succeeds if, counting everything reserved
+// before it on either side, the two lists do not collide.  Failures are monotone (both counts only grow),
+// so the successful ones form a prefix of each list: [0, front_ok) and [capacity - back_ok, capacity).
+// Returns the first slot, or kNoSlot (then `overflow` is set when `flag`: the depth pass's list is
+// incomplete).
+template <bool BACK>
+__device__ __forceinline__ unsigned long long resv_take(const RasterArgs &a, unsigned long long k, bool flag) {
+    const unsigned long long cap = (unsigned long long)a.rec_capacity;
+    const unsigned long long o = atomicAdd(&a.hdr->resv, BACK ? (1ull << kResvBackShift) : k);
+    const unsigned long long f = resv_front_used(o), b = resv_back_slots(o);
+    if ((BACK ? f + b + kChunk : f + k + b) > cap) {
+        if (flag) atomicExch(&a.hdr->overflow, 1);
+        return kNoSlot;
+    }
+    if (BACK) {
+        atomicMax(&a.hdr->back_ok, b + kChunk);
+        return cap - b - kChunk;
+    }
+    atomicMax(&a.hdr->front_ok, f + k);
+    return f;
+}
+
 // Warp-level flush of the shared-memory record buffer into the global survivor list.
 __device__ __forceinline__ void flush_records(const RasterArgs &a, Record *buf, int &wcount, int lane) {
     __syncwarp();
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.hdr->records, (unsigned long long)wcount);
+    if (lane == 0) base = resv_take<false>(a, (unsigned long long)wcount, true);
     base = __shfl_sync(kFull, base, 0);
-    bool of = false;
-    for (int k = lane; k < wcount; k += 32) {
-        const unsigned long long r = base + (unsigned long long)k;
-        if (r < (unsigned long long)a.rec_capacity)
-            reinterpret_cast<uint4 *>(a.records)[r] = reinterpret_cast<const uint4 *>(buf)[k];
-        else
-            of = true;
-    }
-    if (__any_sync(kFull, of) && lane == 0) atomicExch(&a.hdr->overflow, 1);
+    if (base != kNoSlot)
+        for (int k = lane; k < wcount; k += 32)
+            reinterpret_cast<uint4 *>(a.records)[base + k] = reinterpret_cast<const uint4 *>(buf)[k];
     __syncwarp();
     wcount = 0;
 }
@@ -256,7 +285,6 @@ constexpr int kSW = 8;               // warps per CTA of the TMA sweeps (3 CTAs 
 constexpr int kST = kSW * 32;
 constexpr int kWTile = 256;  // points per warp tile (8 per lane)
 constexpr int kQCap = 64;
-constexpr int kChunk = 256;  // record slots reserved per warp at a time
 constexpr uint32_t kDeadView = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint64_t pol) {
@@ -396,11 +424,9 @@ struct RecChunk {  // warp-uniform
     int left;
 };
 
+// A chunk that could not be reserved has base = capacity: its records are dropped (overflow is set).
 __device__ __forceinline__ void put_record(const RasterArgs &a, unsigned long long slot, uint4 r) {
-    if (slot < (unsigned long long)a.rec_capacity)
-        reinterpret_cast<uint4 *>(a.records)[slot] = r;
-    else
-        atomicExch(&a.hdr->overflow, 1);
+    if (slot < (unsigned long long)a.rec_capacity) reinterpret_cast<uint4 *>(a.records)[slot] = r;
 }
 
 // mark the chunk's unused slots dead, then reserve a fresh chunk (one atomic per kChunk slots)
@@ -408,8 +434,9 @@ __device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, in
     for (int k = lane; k < c.left; k += 32) put_record(a, c.base + k, make_uint4(0u, 0u, 0u, kDeadView));
     if (!fresh) return;
     unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(&a.hdr->records, (unsigned long long)kChunk);
-    c.base = __shfl_sync(kFull, b, 0);
+    if (lane == 0) b = resv_take<false>(a, kChunk, true);
+    b = __shfl_sync(kFull, b, 0);
+    c.base = b == kNoSlot ? (unsigned long long)a.rec_capacity : b;
     c.left = kChunk;
 }
 
@@ -561,7 +588,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
                                             uint8_t *cl, int lane, unsigned lt) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     uint32_t live = (uint32_t)vmask;
-    if (a.ghost_thr != 0u) {
+    if (a.ghost_thr != 0u) {  // ghosts take no part in the depth test (§4.3)
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
@@ -724,7 +751,7 @@ __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ Rast
         stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
         return;
     }
-    const unsigned long long total = *(volatile unsigned long long *)&a.hdr->records;
+    const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
         const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
@@ -837,6 +864,8 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
     const int C = a.channels;
     float *gt = const_cast<float *>(v.gradT);
     uint4 *pt = const_cast<uint4 *>(v.ptab);
+    const bool v4 = (C & 3) == 0 && (reinterpret_cast<uintptr_t>(v.accum) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(gt) & 15) == 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
         int l = 0;
@@ -849,11 +878,30 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
         const float cnt = __ldcs(v.count + p);
         const unsigned long long key = __ldcs(reinterpret_cast<const unsigned long long *>(v.keys) + p);
         float S = 0.0f;
-        for (int c = 0; c < C; ++c) {
-            const float g = __ldcs(G + c * hw);
-            const float I = cnt > 0.0f ? __fdiv_rn(__ldcs(v.accum + p * C + c), cnt) : a.bg[c];
-            S = fmaf(g, I, S);
-            gt[p * C + c] = g;
+        if (v4) {  // 16-B accum reads and gradT writes (C % 4 == 0, aligned rows)
+            for (int c = 0; c < C; c += 4) {
+                const float4 g = make_float4(__ldcs(G + c * hw), __ldcs(G + (c + 1) * hw), __ldcs(G + (c + 2) * hw),
+                                             __ldcs(G + (c + 3) * hw));
+                float4 I;
+                if (cnt > 0.0f) {
+                    const float4 s = __ldcs(reinterpret_cast<const float4 *>(v.accum + p * C + c));
+                    I = make_float4(__fdiv_rn(s.x, cnt), __fdiv_rn(s.y, cnt), __fdiv_rn(s.z, cnt), __fdiv_rn(s.w, cnt));
+                } else {
+                    I = make_float4(a.bg[c], a.bg[c + 1], a.bg[c + 2], a.bg[c + 3]);
+                }
+                S = fmaf(g.x, I.x, S);
+                S = fmaf(g.y, I.y, S);
+                S = fmaf(g.z, I.z, S);
+                S = fmaf(g.w, I.w, S);
+                __stcg(reinterpret_cast<float4 *>(gt + p * C + c), g);
+            }
+        } else {
+            for (int c = 0; c < C; ++c) {
+                const float g = __ldcs(G + c * hw);
+                const float I = cnt > 0.0f ? __fdiv_rn(__ldcs(v.accum + p * C + c), cnt) : a.bg[c];
+                S = fmaf(g, I, S);
+                gt[p * C + c] = g;
+            }
         }
         pt[p] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), __float_as_uint(cnt), __float_as_uint(S));
     }
@@ -1019,13 +1067,26 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
 // pose terms (w, Xc x w) (R19), warp-reduced in fp64.  Each point belongs to one lane, so its gradient
 // rows are updated with plain read-modify-writes (no atomics).
 // --------------------------------------------------------------------------- //
+// Thread 0 also picks the backward's mode: the depth pass's survivor records are exactly the re-render's
+// rendered hits when they were written by a call with the same inputs (tag) and did not
+// overflow -> the texture gradient consumes them and the sweep only collects ghosts (mode 1); otherwise
+// the sweep re-renders every point into fresh lists (mode 0).  Either way the ghost list starts empty.
 __global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m, WsHeader *hdr,
-                                                   double *inline_row, int inline_len) {
+                                                   double *inline_row, int inline_len, unsigned long long tag) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0 && hdr) {
+        const bool reuse = tag != 0ull && hdr->tag == tag && hdr->overflow == 0;
+        hdr->mode = reuse ? 1 : 0;
+        if (reuse) {  // keep the survivor records, drop an earlier backward's ghost list
+            hdr->resv = hdr->front_ok;
+        } else {      // the sweep's lists overwrite the record region
+            hdr->tag = 0ull;
+            hdr->resv = 0ull;
+            hdr->front_ok = 0ull;
+            hdr->overflow = 0;
+        }
+        hdr->back_ok = 0ull;
         hdr->tiles_bwd = 0ull;
-        hdr->btex_n = 0ull;
-        hdr->bgh_n = 0ull;
     }
     if (inline_row && tid < inline_len) inline_row[tid] = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1100,46 +1161,52 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
     gv += sc * (d[2] - d[3]);
 }
 
-// ---- record-driven backward: the sweep emits work lists, two balanced kernels consume them ----
+// ---- record-driven backward: work lists in the record region, two balanced kernels consume them ----
+// Texture list = the front list (Record layout): the depth pass's survivor records (mode 1) or the
+// sweep's rendered hits (mode 0).  Ghost list = the back list (GhostEntry layout), written by the sweep.
 constexpr uint32_t kDead = 0xFFFFFFFFu;
-constexpr int kBChunk = 128;
 
 struct ListChunk {  // warp-uniform per-warp chunk of a work list
-    long long base;
-    int left;  // -1: the list is full (process inline)
+    unsigned long long base;  // slot of the next free item
+    int left;                 // items left in the chunk; -1: the list is full (process inline)
 };
 
-// Reserve `nb` slots for the lanes in ballot b of a list of `cap` slots of `words` uint4 each; returns the
-// lane's slot or -1 (no space: the caller processes its item inline).  Unused tail slots are marked dead.
-__device__ __forceinline__ long long list_slot(unsigned long long *counter, uint4 *list, int64_t cap, int words,
-                                               ListChunk &c, unsigned b, bool mine, int lane, unsigned lt) {
-    const int nb = __popc(b);
-    if (c.left >= 0 && nb > c.left) {
-        for (int k = lane; k < c.left; k += 32)
-            if (c.base + k < cap) list[(c.base + k) * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
-        unsigned long long nbase = 0;
-        if (lane == 0) nbase = atomicAdd(counter, (unsigned long long)kBChunk);
-        nbase = __shfl_sync(kFull, nbase, 0);
-        if ((long long)nbase + kBChunk <= cap) {
-            c.base = (long long)nbase;
-            c.left = kBChunk;
-        } else {
-            // the chunk straddles the end: mark its in-range part dead, stop emitting
-            for (long long k = (long long)nbase + lane; k < cap; k += 32)
-                list[k * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
-            c.left = -1;
-        }
+// Mark the chunk's unused items dead (front: Record.view, back: GhostEntry.vsnk).
+template <bool BACK>
+__device__ __forceinline__ void list_close(const RasterArgs &a, const ListChunk &c, int lane) {
+    uint4 *r = reinterpret_cast<uint4 *>(a.records);
+    for (int k = lane; k < c.left; k += 32) {
+        if (BACK)
+            r[c.base + 2ull * k + 1] = make_uint4(0u, 0u, kDead, kDead);
+        else
+            r[c.base + k] = make_uint4(0u, 0u, 0u, kDead);
     }
-    if (c.left < 0) return -1;
-    const long long slot = mine ? c.base + __popc(b & lt) : -1;
-    c.base += nb;
-    c.left -= nb;
-    return slot;
 }
 
-__device__ __forceinline__ void list_close(uint4 *list, int64_t cap, int words, ListChunk &c, int lane) {
-    for (int k = lane; k < c.left; k += 32)
-        if (c.base + k < cap) list[(c.base + k) * words + words - 1] = make_uint4(kDead, kDead, kDead, kDead);
+// Slots for the lanes in ballot b (front: 1 slot per item, back: 2); returns the lane's slot, or kNoSlot
+// when the record region is full (the caller processes its item inline).  Warp-collective.
+template <bool BACK>
+__device__ __forceinline__ unsigned long long list_take(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
+                                                        int lane, unsigned lt) {
+    constexpr int W = BACK ? 2 : 1;
+    const int nb = __popc(b);
+    if (c.left >= 0 && nb > c.left) {
+        list_close<BACK>(a, c, lane);
+        unsigned long long s = 0;
+        if (lane == 0) s = resv_take<BACK>(a, kChunk, false);
+        s = __shfl_sync(kFull, s, 0);
+        if (s == kNoSlot) {
+            c.left = -1;
+        } else {
+            c.base = s;
+            c.left = kChunk / W;
+        }
+    }
+    if (c.left < 0) return kNoSlot;
+    const unsigned long long slot = c.base + (unsigned long long)W * __popc(b & lt);
+    c.base += (unsigned long long)W * nb;
+    c.left -= nb;
+    return mine ? slot : kNoSlot;
 }
 
 __device__ __forceinline__ void red_add_row(float *dst, const float *src, int C, float scale) {
@@ -1194,12 +1261,12 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
     return true;
 }
 
-// Sweep candidate: exact projection and discard, then emit the rendered hits to the texture list and
-// the ghost to the ghost list (inline processing when a list is full).  Warp-collective.
+// Sweep candidate: exact projection and discard, then emit the rendered hits to the texture list (mode 0
+// only) and the ghost to the ghost list (inline processing when the region is full).  Warp-collective.
 template <int MODEL, int CT>
 __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost, float x,
                                          float y, float z, float rw, int64_t i, uint32_t gi, ListChunk &ct,
-                                         ListChunk &cg, int lane, unsigned lt) {
+                                         ListChunk &cg, bool tex_on, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
     if (ok) {
@@ -1210,7 +1277,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
             if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
         }
     }
-    const bool rend = nk > 0 && !ghost && a.d_feat;
+    const bool rend = tex_on && nk > 0 && !ghost && a.d_feat;
     if (__any_sync(kFull, rend)) {
 #pragma unroll 1
         for (int l = 0; l < a.layers; ++l) {
@@ -1223,10 +1290,11 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
                 continue;
             }
             const uint32_t q = (uint32_t)(v.off[l] + loc);
-            const long long slot = list_slot(&a.hdr->btex_n, a.btex, a.btex_cap, 1, ct, b, hit, lane, lt);
+            const unsigned long long slot = list_take<false>(a, ct, b, hit, lane, lt);
             if (hit) {
-                if (slot >= 0)
-                    a.btex[slot] = make_uint4(q, (uint32_t)i, __float_as_uint(p.Z), (uint32_t)vs);
+                if (slot != kNoSlot)
+                    reinterpret_cast<uint4 *>(a.records)[slot] =
+                        make_uint4(q, __float_as_uint(p.Z), (uint32_t)i, (uint32_t)vs);  // Record
                 else
                     tex_hit(a, v, q, p.Z, i);
             }
@@ -1235,12 +1303,12 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     const bool gh = nk > 0 && ghost;
     const unsigned bg = __ballot_sync(kFull, gh);
     if (bg == 0u) return;
-    const long long slot = list_slot(&a.hdr->bgh_n, a.bgh, a.bgh_cap, 2, cg, bg, gh, lane, lt);
+    const unsigned long long slot = list_take<true>(a, cg, bg, gh, lane, lt);
     if (!gh) return;
-    if (slot >= 0) {
-        a.bgh[2 * slot] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X),
-                                     __float_as_uint(p.Y));
-        a.bgh[2 * slot + 1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), 0u);
+    if (slot != kNoSlot) {  // GhostEntry
+        uint4 *r = reinterpret_cast<uint4 *>(a.records) + slot;
+        r[0] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X), __float_as_uint(p.Y));
+        r[1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), 0u);
     } else {
         double t6[6];
         if (ghost_point<MODEL, CT>(a, v, p, nk, i, t6))
@@ -1248,15 +1316,15 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     }
 }
 
-// texture list consumer: one thread per hit (balanced), vector reductions into d_feat
+// texture list consumer: one thread per hit (balanced), vector reductions into d_feat.
 __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
-    unsigned long long total = *(volatile unsigned long long *)&a.hdr->btex_n;
-    if (total > (unsigned long long)a.btex_cap) total = (unsigned long long)a.btex_cap;
+    const uint4 *list = reinterpret_cast<const uint4 *>(a.records);
+    const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
-        const uint4 e = __ldcs(a.btex + r);
+        const uint4 e = __ldcs(list + r);
         if (e.w == kDead) continue;
-        tex_hit(a, a.v[e.w], e.x, __uint_as_float(e.z), (int64_t)e.y);
+        tex_hit(a, a.v[e.w], e.x, __uint_as_float(e.y), (int64_t)e.z);
     }
 }
 
@@ -1268,17 +1336,19 @@ __global__ void __launch_bounds__(kThreads) k_bwd_ghost(const __grid_constant__ 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
     __syncthreads();
-    unsigned long long total = *(volatile unsigned long long *)&a.hdr->bgh_n;
-    if (total > (unsigned long long)a.bgh_cap) total = (unsigned long long)a.bgh_cap;
+    // the sweep's ghost list: the back of the record region
+    const unsigned long long back = *(volatile unsigned long long *)&a.hdr->back_ok;
+    const uint4 *list = reinterpret_cast<const uint4 *>(a.records) + ((unsigned long long)a.rec_capacity - back);
+    const unsigned long long total = back / 2;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x; r0 < total; r0 += stride) {
         const unsigned long long r = r0 + threadIdx.x;
         double t6[6] = {0, 0, 0, 0, 0, 0};
         int vs = -1;
         if (r < total) {
-            const uint4 e1 = __ldcs(a.bgh + 2 * r + 1);
+            const uint4 e1 = __ldcs(list + 2 * r + 1);
             if (e1.z != kDead) {
-                const uint4 e0 = __ldcs(a.bgh + 2 * r);
+                const uint4 e0 = __ldcs(list + 2 * r);
                 vs = (int)(e1.z & 0xFF);
                 const int nk = (int)(e1.z >> 8);
                 const ViewDesc &v = a.v[vs];
@@ -1319,14 +1389,18 @@ struct BwdSmem {
     uint64_t bar[kSW][kStages];
     long long tile[kSW][kStages];
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
+    uint8_t gl[kSW][kWTile];  // mode 1: compacted ghost points of the warp tile (tile offsets)
 };
 
 static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 3, "backward sweep: 3 CTAs per SM must fit in shared memory");
 
-template <int MODEL, int CT, bool MV>
+// GO (ghosts only) is launched for mode 1, !GO for mode 0; the instance not matching the mode exits.
+template <int MODEL, int CT, bool MV, bool GO>
 __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
+    if ((*(volatile int32_t *)&a.hdr->mode == 1) != GO) return;
+    constexpr bool tex_on = !GO;  // mode 1: the survivor records are the texture list
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
     ListChunk ct, cg;
@@ -1396,6 +1470,48 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             for (int j = 0; j < 8; ++j)
                 if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
         }
+        if (GO) {
+            // mode 1: only ghosts (~rho of the points) are left to find -- compact them, then pre-cull and
+            // project only those, 32 per warp iteration (every lane busy)
+            const uint32_t gm = ghosts & (uint32_t)vmask;
+            int gn = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const bool bit = (gm >> j) & 1u;
+                const unsigned b = __ballot_sync(kFull, bit);
+                if (bit) sm.gl[wid][gn + __popc(b & lt)] = (uint8_t)((j >> 2) * 128 + 4 * lane + (j & 3));
+                gn += __popc(b);
+            }
+            __syncwarp();
+            if (gn > 0) {
+                const Box box = lane_box(rp, lane, vmask);
+                uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
+#pragma unroll 1
+                while (views) {
+                    const int vs = __ffs(views) - 1;
+                    views &= views - 1u;
+                    const ViewDesc &v = a.v[vs];
+                    if (__all_sync(kFull, box_culled(v, box))) continue;
+                    for (int i0 = 0; i0 < gn; i0 += 32) {
+                        const bool in = i0 + lane < gn;
+                        const int e = in ? sm.gl[wid][i0 + lane] : 0;
+                        const float x = rp[0][e], y = rp[1][e], z = rp[2][e];
+                        const float rw = staged_r ? rp[3][e] : a.radius_uniform;
+                        const uint32_t gi = a.goff + (uint32_t)(base + e);
+                        float Zf, mz;
+                        bool cand = in && precull_fma_z<MODEL>(v, x, y, z, Zf, mz);
+                        if (a.discard) cand = cand && maybe_kept(a, v, rw, Zf, mz, gi);
+                        if (__any_sync(kFull, cand))
+                            bwd_emit<MODEL, CT>(a, v, vs, cand, true, x, y, z, rw, base + e, gi, ct, cg, false, lane, lt);
+                    }
+                }
+            }
+            __syncwarp();  // the ghost list is rewritten by the next tile
+            __syncwarp();
+            issue(st);
+            __syncwarp();
+            continue;
+        }
         const Box box = lane_box(rp, lane, vmask);
         uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
 #pragma unroll 1
@@ -1429,15 +1545,15 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const float rw = staged_r ? rp[3][e] : a.radius_uniform;
                 bwd_emit<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
-                                    a.goff + (uint32_t)(base + e), ct, cg, lane, lt);
+                                    a.goff + (uint32_t)(base + e), ct, cg, tex_on, lane, lt);
             }
         }
         __syncwarp();
         issue(st);
         __syncwarp();
     }
-    list_close(a.btex, a.btex_cap, 1, ct, lane);
-    list_close(a.bgh, a.bgh_cap, 2, cg, lane);
+    list_close<false>(a, ct, lane);
+    list_close<true>(a, cg, lane);
 }
 
 // d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
@@ -1579,14 +1695,9 @@ int backward_grid(int sms) {
 template <int MODEL, bool VEC, int CT>
 static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t cap_bytes = a.rec_capacity * (int64_t)sizeof(Record);
-    int64_t table_bytes = 0, maxP = 1;
-    for (int v = 0; v < a.nviews; ++v) {
-        table_bytes += (int64_t)a.v[v].pixels * (int64_t)(sizeof(uint4) + sizeof(float) * a.channels);
-        maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
-    }
-    table_bytes = (table_bytes + 255) / 256 * 256;
-    const bool fast = VEC && table_bytes + (int64_t)(1 << 16) <= cap_bytes &&
+    int64_t maxP = 1;
+    for (int v = 0; v < a.nviews; ++v) maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+    const bool fast = VEC && a.tables != nullptr && a.rec_capacity >= 4 * kChunk &&
                       (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
                       (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0);
     if (!fast) {  // planar fused sweep (unaligned inputs or a small workspace)
@@ -1599,8 +1710,8 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     }
     RasterArgs b = a;
     b.grad_accumulate = 1;  // every kernel below adds into the (zeroed or caller's) gradients
-    // workspace record region: [pixel tables | texture list (16-B slots) | ghost list (32-B slots)]
-    char *base = reinterpret_cast<char *>(a.records);
+    // pixel tables in their own workspace region
+    char *base = reinterpret_cast<char *>(a.tables);
     int64_t off = 0;
     for (int v = 0; v < a.nviews; ++v) {
         b.v[v].ptab = reinterpret_cast<const uint4 *>(base + off);
@@ -1610,11 +1721,6 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         b.v[v].gradT = reinterpret_cast<const float *>(base + off);
         off += (int64_t)a.v[v].pixels * a.channels * sizeof(float);
     }
-    const int64_t rest = cap_bytes - table_bytes;
-    b.btex = reinterpret_cast<uint4 *>(base + table_bytes);
-    b.btex_cap = (rest / 2) / 16;
-    b.bgh = reinterpret_cast<uint4 *>(base + table_bytes + b.btex_cap * 16);
-    b.bgh_cap = (rest - b.btex_cap * 16) / 32;
     // ghost-list kernel grid (its per-block pose partials) and the inline-overflow row after them
     int gg = sms * 4;
     if (gg > grid_cap - 1) gg = grid_cap - 1;
@@ -1627,7 +1733,7 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
         if (bx < 1) bx = 1;
         k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np, a.hdr,
-                                                a.pose_partials + (int64_t)gg * a.nviews * 6, a.nviews * 6);
+                                                a.pose_partials + (int64_t)gg * a.nviews * 6, a.nviews * 6, a.tag);
     }
     {   // per-pixel tables
         int64_t bx = (maxP + kThreads - 1) / kThreads;
@@ -1635,16 +1741,19 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(b);
     }
     {   // sweep: emit work lists
-        auto k = a.nviews > 2 ? k_bwd_sweep<MODEL, CT, true> : k_bwd_sweep<MODEL, CT, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(BwdSmem));
-        if (per_sm < 1) per_sm = 1;
-        int64_t tiles = (a.n + kWTile - 1) / kWTile;
-        int64_t g = (int64_t)sms * per_sm;
-        if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
-        if (g < 1) g = 1;
-        k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
+        for (int go = 0; go < 2; ++go) {  // the instance not matching the device-side mode exits at once
+            auto k = a.nviews > 2 ? (go ? k_bwd_sweep<MODEL, CT, true, true> : k_bwd_sweep<MODEL, CT, true, false>)
+                                  : (go ? k_bwd_sweep<MODEL, CT, false, true> : k_bwd_sweep<MODEL, CT, false, false>);
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem));
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(BwdSmem));
+            if (per_sm < 1) per_sm = 1;
+            int64_t tiles = (a.n + kWTile - 1) / kWTile;
+            int64_t g = (int64_t)sms * per_sm;
+            if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
+            if (g < 1) g = 1;
+            k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
+        }
     }
     k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
     k_bwd_ghost<MODEL, CT><<<gg, kThreads, 0, s>>>(b);
