@@ -130,7 +130,7 @@ ADOP_API int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t laye
 
 /* Workspace bytes for calls over `n_views` views (cameras: host [n_views]) of `points`.
  * Layout: 4 KiB header | pose partials | backward pixel tables (per view and pixel one
- * 16-byte {key, count, sum_c G I} entry and one [C] gradient row) | record region.
+ * row {min depth, count, sum_c G I, 0, G[C]} of 16 + 4 * roundup4(C) bytes) | record region.
  * record_capacity: 16-byte slots of the record region.  The depth pass fills it from
  * the front with survivor records (one per (point, view, layer) hit of the render set)
  * and, when params->ghost_rate > 0, from the back with ghost entries (2 slots per kept

@@ -152,11 +152,12 @@ struct Ws {
     int64_t capacity;
 };
 
-// Backward pixel tables (one ptab uint4 + one [C] gradient row per pixel per view), 256-B rounded.
+// Backward pixel tables: per view and pixel one row {m, count, S, 0, G[C]} of 16 + 4 * roundup4(C)
+// bytes (k_bwd_prep), 256-B rounded.
 size_t table_bytes(int32_t n_views, const adop_camera *cams, int32_t layers, int32_t channels) {
     size_t t = 0;
-    for (int v = 0; v < n_views; ++v)
-        t += (size_t)adop_pyramid_pixels(cams[v].width, cams[v].height, layers) * (16u + 4u * (size_t)channels);
+    const size_t row = 16u + 4u * (size_t)((channels + 3) & ~3);
+    for (int v = 0; v < n_views; ++v) t += (size_t)adop_pyramid_pixels(cams[v].width, cams[v].height, layers) * row;
     return (t + 255) / 256 * 256;
 }
 

@@ -32,8 +32,7 @@ struct ViewDesc {
     uint64_t *keys;
     float *accum, *count, *image;
     const float *grad;     // backward: dL/dI (image layout)
-    const float *gradT;    // backward: dL/dI transposed to [P][C] in the workspace (or NULL)
-    const uint4 *ptab;     // backward: per-pixel {key lo, key hi, bits(count), bits(sum_c G I)} (or NULL)
+    const float *prow;     // backward pixel table: [P] rows of RasterArgs::prow floats (k_bwd_prep)
 };
 
 struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
@@ -110,7 +109,8 @@ struct RasterArgs {
     WsHeader *hdr;
     Record *records;       // record region: survivor records (front) + ghost list (back), see WsHeader
     int64_t rec_capacity;  // in 16-B slots
-    void *tables;          // backward pixel tables: per view ptab [P] uint4, then per view gradT [P][C]
+    void *tables;          // backward pixel tables, per view [P][prow] floats
+    int32_t prow;          // pixel-table row stride in floats: 4 + C rounded up to a multiple of 4
     double *pose_partials; // [gridDim.x][nviews][6]
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming

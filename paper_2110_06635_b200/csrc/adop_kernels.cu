@@ -849,11 +849,11 @@ __device__ __forceinline__ float neighbour_term(const RasterArgs &a, const ViewD
     return factor * d;
 }
 
-// Backward pixel tables of one view (workspace scratch), built once per call:
-//   ptab[p]  = {key lo, key hi, bits(count), bits(S_p)}, S_p = sum_c G_c(p) I_c(p) with I exactly as
-//              k_resolve computes it (accum/count, or the background when empty);
-//   gradT[p] = dL/dI(p) as a contiguous [C] row.
-// With them each Eq. 11 neighbour costs one 16-B load + one G row: Delta . G = factor (tau . G - S).
+// Backward pixel table of one view (workspace scratch), built once per call: one row of a.prow floats per
+// pixel, {bits(m_p), count_p, S_p, 0, G_0(p) .. G_{C-1}(p)}, m_p = the pixel's min depth (key >> 32),
+// S_p = sum_c G_c(p) I_c(p) with I exactly as k_resolve computes it (accum/count, or the background).
+// A gather of one neighbour (Eq. 11) or texture hit then touches ONE row -- one 32-B sector at C = 4 --
+// and Delta . G = factor (tau . G - S).
 __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for the sweep's tile_views
@@ -861,11 +861,9 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
         a.planes[blockIdx.y].pl[k] = make_float4(v.pl[k][0], v.pl[k][1], v.pl[k][2], v.pl[k][3]);
         a.planes[blockIdx.y].pm[k] = make_float2(v.pm[k][0], v.pm[k][1]);
     }
-    const int C = a.channels;
-    float *gt = const_cast<float *>(v.gradT);
-    uint4 *pt = const_cast<uint4 *>(v.ptab);
-    const bool v4 = (C & 3) == 0 && (reinterpret_cast<uintptr_t>(v.accum) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(gt) & 15) == 0;
+    const int C = a.channels, RS = a.prow;
+    float *rows = const_cast<float *>(v.prow);
+    const bool v4 = (C & 3) == 0 && (reinterpret_cast<uintptr_t>(v.accum) & 15) == 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
         int l = 0;
@@ -875,17 +873,19 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
         const int64_t j = p - v.off[l];
         const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
         const float *G = v.grad + (int64_t)C * v.off[l] + j;
+        float *row = rows + p * RS;
         const float cnt = __ldcs(v.count + p);
         const unsigned long long key = __ldcs(reinterpret_cast<const unsigned long long *>(v.keys) + p);
         float S = 0.0f;
-        if (v4) {  // 16-B accum reads and gradT writes (C % 4 == 0, aligned rows)
+        if (v4) {  // 16-B accum reads and row writes (C % 4 == 0)
             for (int c = 0; c < C; c += 4) {
                 const float4 g = make_float4(__ldcs(G + c * hw), __ldcs(G + (c + 1) * hw), __ldcs(G + (c + 2) * hw),
                                              __ldcs(G + (c + 3) * hw));
                 float4 I;
                 if (cnt > 0.0f) {
-                    const float4 s = __ldcs(reinterpret_cast<const float4 *>(v.accum + p * C + c));
-                    I = make_float4(__fdiv_rn(s.x, cnt), __fdiv_rn(s.y, cnt), __fdiv_rn(s.z, cnt), __fdiv_rn(s.w, cnt));
+                    const float4 sa = __ldcs(reinterpret_cast<const float4 *>(v.accum + p * C + c));
+                    I = make_float4(__fdiv_rn(sa.x, cnt), __fdiv_rn(sa.y, cnt), __fdiv_rn(sa.z, cnt),
+                                    __fdiv_rn(sa.w, cnt));
                 } else {
                     I = make_float4(a.bg[c], a.bg[c + 1], a.bg[c + 2], a.bg[c + 3]);
                 }
@@ -893,17 +893,18 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
                 S = fmaf(g.y, I.y, S);
                 S = fmaf(g.z, I.z, S);
                 S = fmaf(g.w, I.w, S);
-                __stcg(reinterpret_cast<float4 *>(gt + p * C + c), g);
+                __stcg(reinterpret_cast<float4 *>(row + 4 + c), g);
             }
         } else {
             for (int c = 0; c < C; ++c) {
                 const float g = __ldcs(G + c * hw);
                 const float I = cnt > 0.0f ? __fdiv_rn(__ldcs(v.accum + p * C + c), cnt) : a.bg[c];
                 S = fmaf(g, I, S);
-                gt[p * C + c] = g;
+                row[4 + c] = g;
             }
         }
-        pt[p] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), __float_as_uint(cnt), __float_as_uint(S));
+        __stcg(reinterpret_cast<uint4 *>(row),
+               make_uint4((uint32_t)(key >> 32), __float_as_uint(cnt), __float_as_uint(S), 0u));
     }
 }
 
@@ -1138,23 +1139,23 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
         const int qu = pu + du[k], qv = pv + dv[k];
         const bool in = qu >= 0 && qv >= 0 && qu < v.wl[l] && qv < v.hl[l];
         q[k] = in ? v.off[l] + qv * v.wl[l] + qu : -1;
-        e[k] = in ? __ldcg(v.ptab + q[k]) : make_uint4(0u, 0u, 0u, 0u);
+        e[k] = in ? __ldcg(reinterpret_cast<const uint4 *>(v.prow + (int64_t)q[k] * a.prow)) : make_uint4(0u, 0u, 0u, 0u);
     }
     float d[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         d[k] = 0.0f;
         if (q[k] < 0) continue;  // outside: no term
-        const float nq = __uint_as_float(e[k].z);
+        const float nq = __uint_as_float(e[k].y);
         float factor;
         if (nq == 0.0f) {
             factor = 1.0f;                                            // case 1: background
         } else {
-            const float m = __uint_as_float(e[k].y);
+            const float m = __uint_as_float(e[k].x);
             if (z > fmul(a.onepa, m)) continue;                       // case 2: behind
             factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
         }
-        d[k] = factor * (row_dot<CT>(v.gradT + (int64_t)q[k] * C, tau, C) - __uint_as_float(e[k].w));
+        d[k] = factor * (row_dot<CT>(v.prow + (int64_t)q[k] * a.prow + 4, tau, C) - __uint_as_float(e[k].z));
     }
     const float sc = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
     gu += sc * (d[0] - d[1]);
@@ -1223,10 +1224,11 @@ __device__ __forceinline__ void red_add_row(float *dst, const float *src, int C,
 
 // texture gradient of one rendered hit (R24): fuzzy membership against the forward's key, G / |Lambda|
 __device__ __forceinline__ void tex_hit(const RasterArgs &a, const ViewDesc &v, uint32_t q, float z, int64_t idx) {
-    const uint4 e = __ldcg(v.ptab + q);
-    if (!(z <= fmul(a.onepa, __uint_as_float(e.y)))) return;  // fuzzy test (Eq. 6, R9)
+    const float *row = v.prow + (int64_t)q * a.prow;
+    const uint4 e = __ldcg(reinterpret_cast<const uint4 *>(row));
+    if (!(z <= fmul(a.onepa, __uint_as_float(e.x)))) return;  // fuzzy test (Eq. 6, R9)
     const int C = a.channels;
-    red_add_row(a.d_feat + idx * C, v.gradT + (int64_t)q * C, C, __uint_as_float(e.z));
+    red_add_row(a.d_feat + idx * C, row + 4, C, __uint_as_float(e.y));
 }
 
 // ghost: image gradient over its kept layers (Eqs. 9-11), chain rule (Eq. 8) -> dx (atomics), and the
@@ -1713,13 +1715,10 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     // pixel tables in their own workspace region
     char *base = reinterpret_cast<char *>(a.tables);
     int64_t off = 0;
+    b.prow = 4 + ((a.channels + 3) & ~3);  // row stride in floats (16-B multiple)
     for (int v = 0; v < a.nviews; ++v) {
-        b.v[v].ptab = reinterpret_cast<const uint4 *>(base + off);
-        off += (int64_t)a.v[v].pixels * sizeof(uint4);
-    }
-    for (int v = 0; v < a.nviews; ++v) {
-        b.v[v].gradT = reinterpret_cast<const float *>(base + off);
-        off += (int64_t)a.v[v].pixels * a.channels * sizeof(float);
+        b.v[v].prow = reinterpret_cast<const float *>(base + off);
+        off += (int64_t)a.v[v].pixels * b.prow * (int64_t)sizeof(float);
     }
     // ghost-list kernel grid (its per-block pose partials) and the inline-overflow row after them
     int gg = sms * 4;
@@ -1755,7 +1754,7 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
             k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
         }
     }
-    k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
+    if (a.d_feat) k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
     k_bwd_ghost<MODEL, CT><<<gg, kThreads, 0, s>>>(b);
     if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, gg + 1, a.nviews * 6, d_pose, a.grad_accumulate);
     return (int)cudaGetLastError();

@@ -42,7 +42,7 @@ def test_pyramid_pixels_and_workspace_size():
     cams = (A.adop_camera * 2)(cam, cam)
     assert A.lib().adop_workspace_size(C.byref(pts), 2, cams, C.byref(prm), -1, C.byref(sz)) == 0
     P = A.pyramid_pixels(64, 32, 5)
-    tables = -(-2 * P * (16 + 4 * 4) // 256) * 256
+    tables = -(-2 * P * (16 + 4 * 4) // 256) * 256  # rows of 16 + 4 roundup4(C) bytes
     assert sz.value == 4096 + 2048 * 16 * 6 * 8 + tables + (1000 * 2 * 5 + (1 << 20)) * 16
     assert A.lib().adop_workspace_size(C.byref(pts), 2, cams, C.byref(prm), 100, C.byref(sz)) == 0
     assert sz.value == 4096 + 2048 * 16 * 6 * 8 + tables + 100 * 16

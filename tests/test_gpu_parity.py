@@ -126,6 +126,26 @@ def test_record_overflow_falls_back_to_restreaming():
     assert not of2 and rec2 > 1000  # slot counts vary with the dynamic tile schedule (dead chunk tails)
 
 
+def test_backward_null_outputs():
+    """Any of d_feat / d_pos / d_pose may be NULL (include/adop.h); the others are unchanged."""
+    w = S.workload(2, n=60_000)
+    dev = torch.device("cuda")
+    G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, w.cloud.channels)]
+    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params)
+    r.forward()
+    f1, p1, q1 = [t.clone() for t in r.backward(G)]
+    for drop in range(3):
+        outs = [torch.full_like(f1, 7.0), torch.full_like(p1, 7.0), torch.full_like(q1, 7.0)]
+        args = [None if k == drop else outs[k] for k in range(3)]
+        A.rasterize_backward(r.points, r.cams, r.poses, r.params, r.pyrs, G, r.ws, *args)
+        torch.cuda.synchronize()
+        for k, ref in enumerate((f1, p1, q1)):
+            if k == drop:
+                assert (outs[k] == 7.0).all()
+            else:
+                torch.testing.assert_close(outs[k], ref, rtol=1e-5, atol=1e-6)
+
+
 def test_grad_accumulate_adds():
     w = S.workload(2, n=50_000)
     dev = torch.device("cuda")
