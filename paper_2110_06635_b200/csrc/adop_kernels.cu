@@ -745,6 +745,8 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
 // --------------------------------------------------------------------------- //
 // blend over survivor records (§4.5 accumulate pass)
 // --------------------------------------------------------------------------- //
+// (Measured: a separate low-register record kernel at higher occupancy moved more DRAM bytes and ran
+// slower on configs[4]; the L2 reductions, not latency, bound this pass.)
 template <int MODEL, bool VEC, bool VEC4>
 __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ RasterArgs a) {
     if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
@@ -1333,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ Ra
 // ghost list consumer: one thread per (ghost, view) (balanced); pose terms warp-reduced in fp64 into
 // per-warp shared slots, per-block partials reduced by k_pose_reduce in a fixed order.
 template <int MODEL, int CT>
-__global__ void __launch_bounds__(kThreads) k_bwd_ghost(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant__ RasterArgs a) {
     __shared__ double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * 6];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
