@@ -212,10 +212,13 @@ def run_ours(args, rank, world, local_rank):
     out = {}
     if rank == 0:
         P = A.pyramid_pixels(cams[0].width, cams[0].height, prm.layers)
-        # algorithmic bytes of the depth pass (k_clear + k_stream<DEPTH>):
-        #   points: pos 12 B + radius 4 B per point; pyramid init: keys 8 + accum 4C + count 4 B per pixel;
-        #   survivor records 16 B each.
-        alg = N * 16 + P * (8 + 4 * C + 4) + 16 * records
+        # algorithmic bytes:
+        #   depth phase (k_clear<KEYS> + k_depth_async): position 12 B + radius 4 B per point read once,
+        #   keys 8 B per pixel written once (survivor records are this design's intermediate, not counted);
+        #   frame: B_fwd = N (12 + 4) + N_blend 4C + P (8 + 4C + 4), N_blend = sum of the counts.
+        alg = N * 16 + P * 8
+        n_blend = int(sum(float(p.count.sum()) for p in pyrs))
+        alg_frame = N * 16 + n_blend * 4 * C + P * (8 + 4 * C + 4)
         peak, peak_src = peaks()
         achieved = alg / (depth_ms * 1e-3) / 1e9
         tr = traffic_from_profiles().get("depth_phase_bytes")
@@ -232,10 +235,14 @@ def run_ours(args, rank, world, local_rank):
             "phases_ms": {"depth": depth_ms, "key_allreduce": statistics.mean(ph[1]),
                           "blend": statistics.mean(ph[2]), "accum_allreduce": statistics.mean(ph[3]),
                           "resolve": statistics.mean(ph[4])},
-            "roofline": {"kernel": "depth pass (k_clear + k_stream<DEPTH>)", "bound": "hbm",
+            "roofline": {"kernel": "depth phase (k_clear<KEYS> + k_depth_async<PINHOLE, 1 view>)", "bound": "hbm",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": achieved / peak, "frac_of_nominal_8TBs": achieved / 8000.0,
-                         "algorithmic_bytes": alg, "traffic": tr},
+                         "algorithmic_bytes": alg, "traffic": tr,
+                         "timing": "CUDA events on the launch stream around the depth phase, mean over the timed steps"},
+            "frame_roofline": {"bound": "hbm", "algorithmic_bytes": alg_frame, "n_blend": n_blend,
+                               "achieved": alg_frame / (ms_per_step * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                               "frac": alg_frame / (ms_per_step * 1e-3) / 1e9 / peak},
             "gpu_launches": 5 * args.steps,
             "clocks": clk,
         }
@@ -335,6 +342,23 @@ def run_secondary(args, dev):
         res[w.name] = {"config": f"BASELINE.json configs[{idx}]", "points": w.cloud.n, "views": V,
                        "fwd_ms": fms, "bwd_ms": bms if G is not None else None,
                        "point_views_per_s": w.cloud.n * V / ((fms + (bms if G is not None else 0)) * 1e-3)}
+        # rooflines of the whole forward / backward call (SURVEY.md §8(d) B_fwd, B_bwd; HBM-bound)
+        peak, _ = peaks()
+        N, C = w.cloud.n, w.cloud.channels
+        P = A.pyramid_pixels(w.cameras[0].width, w.cameras[0].height, w.params.layers)
+        n_blend = int(sum(float(p.count.sum()) for p in r.pyrs))
+        b_fwd = N * 16 + n_blend * 4 * C + V * P * (8 + 4 * C + 4)
+        res[w.name]["fwd_roofline"] = {"bound": "hbm", "algorithmic_bytes": b_fwd, "n_blend": n_blend,
+                                       "achieved": b_fwd / (fms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                                       "frac": b_fwd / (fms * 1e-3) / 1e9 / peak}
+        if G is not None:
+            _, n_ghost, _ = r.ws.stats3()
+            # positions + radii re-read, features of kept ghost entries, d_tau and d_x written once,
+            # per pixel G, I, count and key read
+            b_bwd = N * 16 + n_ghost * 4 * C + N * (4 * C + 12) + V * P * (4 * C + 4 * C + 4 + 8)
+            res[w.name]["bwd_roofline"] = {"bound": "hbm", "algorithmic_bytes": b_bwd, "ghost_entries": n_ghost,
+                                           "achieved": b_bwd / (bms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                                           "frac": b_bwd / (bms * 1e-3) / 1e9 / peak}
         del r, w, G
         torch.cuda.empty_cache()
     return res

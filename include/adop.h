@@ -201,10 +201,12 @@ ADOP_API adop_status adop_rasterize_backward(const adop_points *points, int32_t 
 ADOP_API adop_status adop_point_masks(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                              const adop_pose *poses, const adop_params *params, uint8_t *mask, void *stream);
 
-/* Survivor statistics of the last depth pass in `workspace` (synchronizes `stream`):
- * record slots used (including dead chunk tails) and whether they overflowed the capacity. */
+/* List statistics of `workspace` (synchronizes `stream`); any output may be NULL:
+ * records: survivor-record slots of the last depth pass (including dead chunk tails),
+ * ghost_entries: ghost-list entries of the last backward (including dead chunk tails),
+ * overflowed: whether the depth pass's records did not fit the record region. */
 ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream,
-                                 int64_t *records, int32_t *overflowed);
+                                 int64_t *records, int64_t *ghost_entries, int32_t *overflowed);
 
 /* Thread-local description of the last non-OK status ("" if none). */
 ADOP_API const char *adop_last_error(void);

@@ -92,7 +92,8 @@ def lib():
         L.adop_workspace_size.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_params), C.c_int64,
                                           P(C.c_size_t)]
         L.adop_workspace_stats.restype = C.c_int
-        L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int32)]
+        L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int64),
+                                           P(C.c_int32)]
         L.adop_last_error.restype = C.c_char_p
         L.adop_version.restype = C.c_char_p
         _lib = L
@@ -227,9 +228,16 @@ class Workspace:
         self.ptr = (base + 255) // 256 * 256
 
     def stats(self, stream=None):
-        rec, of = C.c_int64(0), C.c_int32(0)
-        _check(lib().adop_workspace_stats(self.ptr, self.nbytes, _stream(stream), C.byref(rec), C.byref(of)))
-        return int(rec.value), bool(of.value)
+        """(survivor record slots, overflowed) of the last depth pass (synchronizes the stream)."""
+        rec, _, of = self.stats3(stream)
+        return rec, of
+
+    def stats3(self, stream=None):
+        """(survivor record slots, ghost-list entries of the last backward, overflowed)."""
+        rec, gh, of = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+        _check(lib().adop_workspace_stats(self.ptr, self.nbytes, _stream(stream), C.byref(rec), C.byref(gh),
+                                          C.byref(of)))
+        return int(rec.value), int(gh.value), bool(of.value)
 
 
 def default_record_capacity(n: int, n_views: int, layers: int, discard: bool) -> int:

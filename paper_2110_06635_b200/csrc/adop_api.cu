@@ -558,13 +558,14 @@ adop_status adop_point_masks(const adop_points *points, int32_t n_views, const a
 }
 
 adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream, int64_t *records,
-                                 int32_t *overflowed) {
+                                 int64_t *ghost_entries, int32_t *overflowed) {
     if (!workspace || workspace_bytes < kHeaderBytes) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad workspace");
     WsHeader h;
     cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_status((int)e, "workspace stats");
-    if (records) *records = (int64_t)(h.front_ok + h.back_ok);  // survivor slots + ghost-list slots
+    if (records) *records = (int64_t)h.front_ok;
+    if (ghost_entries) *ghost_entries = (int64_t)(h.back_ok / 2);
     if (overflowed) *overflowed = h.overflow;
     return ok();
 }
