@@ -426,6 +426,45 @@ void orc_project_f64(const orc_camera *c, const double *Xc, double *uv)
     uv[1] = c->fy * yd + c->cy;
 }
 
+/* Intrinsics Jacobian d(u0,v0)/d theta (NEXT-1; Eq. 8's chain rule continued into the camera model C
+ * of Eq. 2, which the paper optimizes: Fig. 4), fp64 at the fp32 camera point.
+ * theta = (fx, fy, cx, cy, k1..k6, p1, p2); Jt row-major [2][12].  Camera model R6:
+ *   u0 = fx xd + cx, v0 = fy yd + cy;
+ *   xd = xn rad + 2 p1 xn yn + p2 (r2 + 2 xn^2),  yd = yn rad + p1 (r2 + 2 yn^2) + 2 p2 xn yn,
+ *   rad = num / den, num = 1 + k1 r2 + k2 r2^2 + k3 r2^3, den = 1 + k4 r2 + k5 r2^2 + k6 r2^3.
+ * Pinhole: xd = xn, yd = yn and the distortion columns are 0 (the model has no such parameters). */
+void orc_intrinsics_jacobian(const orc_camera *c, const float *Xc, double *Jt)
+{
+    double xn = (double)Xc[0] / (double)Xc[2], yn = (double)Xc[1] / (double)Xc[2];
+    for (int k = 0; k < 24; ++k) Jt[k] = 0.0;
+    double xd = xn, yd = yn;
+    if (c->model == 1) {
+        double r2 = xn * xn + yn * yn;
+        double r[3] = {r2, r2 * r2, r2 * r2 * r2};
+        double num = 1.0 + c->k[0] * r[0] + c->k[1] * r[1] + c->k[2] * r[2];
+        double den = 1.0 + c->k[3] * r[0] + c->k[4] * r[1] + c->k[5] * r[2];
+        double rad = num / den;
+        xd = xn * rad + 2.0 * c->p[0] * xn * yn + c->p[1] * (r2 + 2.0 * xn * xn);
+        yd = yn * rad + c->p[0] * (r2 + 2.0 * yn * yn) + 2.0 * c->p[1] * xn * yn;
+        for (int i = 0; i < 3; ++i) {
+            double drad_num = r[i] / den;                 /* d rad / d k_{i+1} */
+            double drad_den = -num * r[i] / (den * den);  /* d rad / d k_{i+4} */
+            Jt[0 * 12 + 4 + i] = c->fx * xn * drad_num;
+            Jt[1 * 12 + 4 + i] = c->fy * yn * drad_num;
+            Jt[0 * 12 + 7 + i] = c->fx * xn * drad_den;
+            Jt[1 * 12 + 7 + i] = c->fy * yn * drad_den;
+        }
+        Jt[0 * 12 + 10] = c->fx * 2.0 * xn * yn;          /* p1 */
+        Jt[1 * 12 + 10] = c->fy * (r2 + 2.0 * yn * yn);
+        Jt[0 * 12 + 11] = c->fx * (r2 + 2.0 * xn * xn);   /* p2 */
+        Jt[1 * 12 + 11] = c->fy * 2.0 * xn * yn;
+    }
+    Jt[0 * 12 + 0] = xd;   /* fx */
+    Jt[1 * 12 + 1] = yd;   /* fy */
+    Jt[0 * 12 + 2] = 1.0;  /* cx */
+    Jt[1 * 12 + 3] = 1.0;  /* cy */
+}
+
 /* Ghost image-space gradient at layer l, pixel (u,v) (Eqs. 9-11, R14-R16):
  * g = (g_u, g_v) in layer-l pixels; gabs = per-direction sums of |G.Delta|/2. */
 static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, int64_t local, int32_t C,
@@ -467,13 +506,16 @@ static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, i
 /*   dtau [n][C]   texture gradient of rendered points (R24; ghosts 0)       */
 /*   dx   [3][n]   position gradient of ghost points (R17, R22; others 0)    */
 /*   dpose [V][6]  tangent-space pose gradient (w, Xc x w) (R19)             */
+/*   dintr [V][12] intrinsics gradient (NEXT-1): sum over ghosts of          */
+/*                 (d(u0,v0)/d theta)^T (g_u, g_v), theta as in              */
+/*                 orc_intrinsics_jacobian                                   */
 /* and the per-element sums of |terms| used to scale tolerances (R20).       */
 /* Any output pointer may be NULL.                                           */
 /* ------------------------------------------------------------------------- */
 void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
                   const orc_params *pr, const uint64_t *keys, const double *count, const double *image,
-                  const float *G, double *dtau, double *dx, double *dpose,
-                  double *dtau_abs, double *dx_abs, double *dpose_abs)
+                  const float *G, double *dtau, double *dx, double *dpose, double *dintr,
+                  double *dtau_abs, double *dx_abs, double *dpose_abs, double *dintr_abs)
 {
     const int C = pts->channels;
     const int64_t n = pts->n;
@@ -485,6 +527,8 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
     if (dx_abs) memset(dx_abs, 0, sizeof(double) * (size_t)(3 * n));
     if (dpose) memset(dpose, 0, sizeof(double) * (size_t)(6 * n_views));
     if (dpose_abs) memset(dpose_abs, 0, sizeof(double) * (size_t)(6 * n_views));
+    if (dintr) memset(dintr, 0, sizeof(double) * (size_t)(12 * n_views));
+    if (dintr_abs) memset(dintr_abs, 0, sizeof(double) * (size_t)(12 * n_views));
     int64_t Gbase = 0;
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
@@ -545,6 +589,15 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                 double a = R[0 + k] * w[0] + R[3 + k] * w[1] + R[6 + k] * w[2];
                 if (dx) dx[k * n + i] += a;
                 if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
+            }
+            if (dintr || dintr_abs) {
+                /* NEXT-1: d theta = Jt^T g (layer-0 pixel gradient, R17) */
+                double Jt[24];
+                orc_intrinsics_jacobian(c, proj, Jt);
+                for (int k = 0; k < 12; ++k) {
+                    if (dintr) dintr[v * 12 + k] += Jt[k] * gu + Jt[12 + k] * gv;
+                    if (dintr_abs) dintr_abs[v * 12 + k] += (ga[0] + ga[1]) * fabs(Jt[k]) + (ga[2] + ga[3]) * fabs(Jt[12 + k]);
+                }
             }
             if (dpose || dpose_abs) {
                 /* Eq. 17 left perturbation: dXc/dxi = [I | -[Xc]x] -> (w, Xc x w) (R19) */

@@ -82,9 +82,11 @@ def lib():
                                             C.c_uint64, C.c_void_p, C.c_void_p]
         _lib.orc_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_project_f64.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
+        _lib.orc_intrinsics_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_backward.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params),
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
 
 
@@ -257,10 +259,20 @@ def project_f64(cam, Xc) -> np.ndarray:
     return uv
 
 
+def intrinsics_jacobian(cam, Xc) -> np.ndarray:
+    """d(u0, v0)/d(fx, fy, cx, cy, k1..k6, p1, p2) at camera point Xc (NEXT-1), shape (2, 12)."""
+    X = np.ascontiguousarray(Xc, dtype=np.float32)
+    J = np.zeros(24, dtype=np.float64)
+    cs = camera_struct(cam)
+    lib().orc_intrinsics_jacobian(C.byref(cs), X.ctypes.data, J.ctypes.data)
+    return J.reshape(2, 12)
+
+
 class Backward:
-    def __init__(self, dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs):
+    def __init__(self, dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr=None, dintr_abs=None):
         self.dtau, self.dx, self.dpose = dtau, dx, dpose
         self.dtau_abs, self.dx_abs, self.dpose_abs = dtau_abs, dx_abs, dpose_abs
+        self.dintr, self.dintr_abs = dintr, dintr_abs
 
 
 def backward(pts: Points, cams, poses, params, fwd: Forward, G: np.ndarray) -> Backward:
@@ -271,10 +283,11 @@ def backward(pts: Points, cams, poses, params, fwd: Forward, G: np.ndarray) -> B
     dtau = np.empty((n, Cc)); dtau_abs = np.empty((n, Cc))
     dx = np.empty((3, n)); dx_abs = np.empty((3, n))
     dpose = np.empty((V, 6)); dpose_abs = np.empty((V, 6))
+    dintr = np.empty((V, 12)); dintr_abs = np.empty((V, 12))
     G = np.ascontiguousarray(G, dtype=np.float32)
     keys = np.ascontiguousarray(fwd.keys, dtype=np.uint64)
     lib().orc_backward(C.byref(pts.s), V, ca, pa, C.byref(ps), keys.ctypes.data,
                        np.ascontiguousarray(fwd.count).ctypes.data, np.ascontiguousarray(fwd.image).ctypes.data,
-                       G.ctypes.data, dtau.ctypes.data, dx.ctypes.data, dpose.ctypes.data,
-                       dtau_abs.ctypes.data, dx_abs.ctypes.data, dpose_abs.ctypes.data)
-    return Backward(dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs)
+                       G.ctypes.data, dtau.ctypes.data, dx.ctypes.data, dpose.ctypes.data, dintr.ctypes.data,
+                       dtau_abs.ctypes.data, dx_abs.ctypes.data, dpose_abs.ctypes.data, dintr_abs.ctypes.data)
+    return Backward(dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr, dintr_abs)

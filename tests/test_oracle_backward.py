@@ -243,3 +243,84 @@ def test_pose_gradient_is_left_tangent_chain_rule():
             e = np.zeros(3); e[k] = 1e-6
             rot[k] += w[:, j] @ (_rodrigues(e) @ Xc - _rodrigues(-e) @ Xc) / 2e-6
     np.testing.assert_allclose(bwd.dpose[0, 3:], rot, rtol=1e-6, atol=1e-9)
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-1: camera-intrinsics gradient from the same ghost (g_u, g_v) (Eq. 8 into the camera model C of
+# Eq. 2; the paper optimizes the camera model, Fig. 4)
+# --------------------------------------------------------------------------- #
+THETA = ["fx", "fy", "cx", "cy", "k1", "k2", "k3", "k4", "k5", "k6", "p1", "p2"]
+
+
+def _perturbed(cam, j, h):
+    """(camera with parameter j moved by ~h, the actual fp32 value of that parameter)."""
+    if j < 4:
+        v = float(F(getattr(cam, THETA[j]) + h))
+        return dataclasses.replace(cam, **{THETA[j]: v}), v
+    if j < 10:
+        k = list(cam.k); k[j - 4] = float(F(k[j - 4] + h))
+        return dataclasses.replace(cam, k=tuple(k)), k[j - 4]
+    p = list(cam.p); p[j - 10] = float(F(p[j - 10] + h))
+    return dataclasses.replace(cam, p=tuple(p)), p[j - 10]
+
+
+@pytest.mark.parametrize("model", [S.PINHOLE, S.OPENCV8])
+def test_intrinsics_jacobian_matches_finite_differences(model):
+    """d(u0, v0)/d theta against central differences of the continuous fp64 projection with perturbed
+    camera parameters (a pin independent of the closed form's algebra)."""
+    cam = S.pinhole(640, 480) if model == S.PINHOLE else S.opencv_camera(640, 480, seed=5)
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        X = np.array([rng.uniform(-0.6, 0.6), rng.uniform(-0.45, 0.45), 1.0], F) * F(rng.uniform(0.5, 4.0))
+        Jt = O.intrinsics_jacobian(cam, X)
+        for j in range(12):
+            h = 2.0 ** -4 if j < 4 else 2.0 ** -12  # camera parameters are fp32: divide by the actual step
+            cp, vp = _perturbed(cam, j, h)
+            cm, vm = _perturbed(cam, j, -h)
+            d = (O.project_f64(cp, X.astype(np.float64)) - O.project_f64(cm, X.astype(np.float64))) / (vp - vm)
+            if model == S.PINHOLE and j >= 4:
+                assert not Jt[:, j].any() and not d.any()  # the pinhole has no distortion parameters
+            np.testing.assert_allclose(Jt[:, j], d, rtol=1e-5, atol=1e-6 * max(1.0, np.abs(d).max()))
+
+
+def test_intrinsics_gradient_ramp_closed_form():
+    """Linear ramp (g_u = -G c exactly, R15): ghosts at layer-0 columns 16 (xn = 0) and 20 (xn = 1/2) give
+    dL/dcx = sum g_u, dL/dfx = sum g_u xn, dL/dfy = dL/dcy = 0."""
+    cam = _cam(32, 8, 8.0, 16.0, 4.0)
+    c = 1.0 / 64
+    render = [_at_pixel(cam, u, 4, 2.0) for u in range(32)]
+    feats = [[c * u] for u in range(32)]
+    for col, xn in ((16, 0.0), (20, 0.5)):
+        pts, gids = arrange(render, [_at_pixel(cam, col, 4, 1.0)], GPRM, feats, [[c * col]])
+        fwd = O.forward(pts, [cam], [IDENT], GPRM)
+        G = _grad_image(cam, 1, 1, 0.0)
+        G[0, 4 * 32: 5 * 32] = 1.0
+        bwd = O.backward(pts, [cam], [IDENT], GPRM, fwd, G)
+        gu = -1.0 * c
+        np.testing.assert_allclose(bwd.dintr[0, :4], [gu * xn, 0.0, gu, 0.0], atol=1e-12)
+        assert not bwd.dintr[0, 4:].any()
+
+
+def test_intrinsics_gradient_sums_pinhole_chain_rule_per_ghost():
+    """Pinhole: per ghost, w = J^T g with J = [[fx/z, 0, -fx x/z^2], [0, fy/z, -fy y/z^2]] (R21) is
+    invertible for (g_u, g_v) from w = R dx (pinned above); then d theta = sum (g_u xn, g_v yn, g_u, g_v)."""
+    room = S.make_room(4.0)
+    cloud = S.room_cloud(4000, room, 2, seed=8)
+    pts = O.Points.from_cloud(cloud)
+    pts = O.Points(pts.pos, np.full(pts.n, 0.02, F), pts.feat)
+    cams, poses = [S.pinhole(80, 60)], S.room_poses(1, room, seed=9)
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.3, seed=3)
+    fwd = O.forward(pts, cams, poses, prm)
+    G = S.grad_pyramid(1, 2, fwd.count.shape[1], seed=12).numpy()
+    bwd = O.backward(pts, cams, poses, prm, fwd, G)
+    R = poses[0].R.astype(np.float64)
+    ghosts = np.nonzero(np.abs(bwd.dx).sum(0))[0]
+    assert len(ghosts) > 20
+    ref = np.zeros(4)
+    for i in ghosts:
+        Xc = O.project(cams[0], poses[0], *pts.pos[:, i])[1].astype(np.float64)
+        w = R @ bwd.dx[:, i]
+        gu, gv = w[0] * Xc[2] / cams[0].fx, w[1] * Xc[2] / cams[0].fy
+        ref += [gu * Xc[0] / Xc[2], gv * Xc[1] / Xc[2], gu, gv]
+    np.testing.assert_allclose(bwd.dintr[0, :4], ref, rtol=1e-6, atol=1e-9)
+    assert not bwd.dintr[0, 4:].any()
