@@ -186,14 +186,17 @@ ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n
  * It produces
  *   d_feat [n][C]: sum over views/layers of G/|Lambda| for rendered points (ghosts 0),
  *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17),
- *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment).
- * Any of d_feat / d_pos / d_pose may be NULL.  params->grad_accumulate selects
+ *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment),
+ *   d_intrinsics [V][12]: sum over ghosts of (d(u0,v0)/d theta)^T g, theta = (fx, fy, cx, cy,
+ *                 k1..k6, p1, p2) of the view's camera (the camera model C of Eq. 2, optimized by
+ *                 the paper: Fig. 4); 0 for the distortion entries of a pinhole camera.
+ * Any of d_feat / d_pos / d_pose / d_intrinsics may be NULL.  params->grad_accumulate selects
  * overwrite or add.  Points, cameras, poses and params must equal the forward's.
  * Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_WORKSPACE_TOO_SMALL, ADOP_ERR_CUDA. */
 ADOP_API adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image,
-                                    float *d_feat, float *d_pos, double *d_pose,
+                                    float *d_feat, float *d_pos, double *d_pose, double *d_intrinsics,
                                     void *workspace, size_t workspace_bytes, void *stream);
 
 /* Debug / parity: per point and view, bit l (l < L) = valid, in bounds and kept

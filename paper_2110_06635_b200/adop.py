@@ -82,7 +82,8 @@ def lib():
         L.adop_rasterize_backward.restype = C.c_int
         L.adop_rasterize_backward.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose),
                                               P(adop_params), P(adop_pyramid), P(C.c_void_p), C.c_void_p,
-                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                                              C.c_void_p]
         L.adop_point_masks.restype = C.c_int
         L.adop_point_masks.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params),
                                        C.c_void_p, C.c_void_p]
@@ -296,11 +297,12 @@ def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None):
 
 def rasterize_backward(points, cams, poses, params, pyrs, grads: Sequence[torch.Tensor], ws,
                        d_feat: Optional[torch.Tensor], d_pos: Optional[torch.Tensor],
-                       d_pose: Optional[torch.Tensor], stream=None):
+                       d_pose: Optional[torch.Tensor], d_intr: Optional[torch.Tensor] = None, stream=None):
+    """d_intr: optional [V][12] float64 camera-intrinsics gradient (fx, fy, cx, cy, k1..k6, p1, p2)."""
     c = _Call(points, cams, poses, params, pyrs)
     g = (C.c_void_p * c.V)(*[t.data_ptr() for t in grads])
     _check(lib().adop_rasterize_backward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, g,
-                                         _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), ws.ptr, ws.nbytes,
+                                         _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), _ptr(d_intr), ws.ptr, ws.nbytes,
                                          _stream(stream)))
 
 
@@ -322,7 +324,7 @@ class Renderer:
     """
 
     def __init__(self, cloud, cams, poses, params, global_offset: int = 0, record_capacity: Optional[int] = None,
-                 device=None):
+                 device=None, intrinsics: bool = False):
         device = cloud.pos.device if device is None else device
         self.cams, self.poses, self.sparams = list(cams), list(poses), params
         self.points = Points.from_cloud(cloud, global_offset)
@@ -333,7 +335,8 @@ class Renderer:
             record_capacity = default_record_capacity(self.points.n, len(self.cams), params.layers, params.discard)
         self.ws = Workspace(self.points, self.cams, self.params, device, record_capacity)
         self.device = device
-        self.d_feat = self.d_pos = self.d_pose = None
+        self.d_feat = self.d_pos = self.d_pose = self.d_intr = None
+        self.intrinsics = intrinsics  # backward also produces d_intr [V][12] (NEXT-1)
 
     def forward(self, stream=None):
         rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream)
@@ -344,12 +347,14 @@ class Renderer:
         self.d_feat = torch.empty(n, self.C, dtype=torch.float32, device=self.device)
         self.d_pos = torch.empty(3, n, dtype=torch.float32, device=self.device)
         self.d_pose = torch.empty(len(self.cams), 6, dtype=torch.float64, device=self.device)
+        if self.intrinsics:
+            self.d_intr = torch.empty(len(self.cams), 12, dtype=torch.float64, device=self.device)
 
     def backward(self, grads: Sequence[torch.Tensor], stream=None):
         if self.d_feat is None:
             self.alloc_grads()
         rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,
-                           self.d_feat, self.d_pos, self.d_pose, stream)
+                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, stream)
         return self.d_feat, self.d_pos, self.d_pose
 
     def masks(self, stream=None) -> torch.Tensor:

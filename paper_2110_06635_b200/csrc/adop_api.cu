@@ -50,7 +50,7 @@ constexpr uint32_t kStreamGhost = 1, kStreamDiscard = 2;
 constexpr size_t kHeaderBytes = 4096;  // WsHeader at 0, PlaneTab[16] at 256, LayerDesc[16] at 2304
 constexpr int64_t kRecordSlack = 1 << 20;  // >= resident warps x 256-slot record chunks
 constexpr int kMaxBwdBlocks = 2048;
-constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 6 * sizeof(double);
+constexpr size_t kPartialBytes = (size_t)kMaxBwdBlocks * ADOP_MAX_VIEWS_PER_LAUNCH * 18 * sizeof(double);
 
 int32_t layer_size(int32_t s, int l) { return (int32_t)((s + (1 << l) - 1) >> l); }
 
@@ -504,8 +504,8 @@ adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, c
 adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image, float *d_feat,
-                                    float *d_pos, double *d_pose, void *workspace, size_t workspace_bytes,
-                                    void *stream) {
+                                    float *d_pos, double *d_pose, double *d_intrinsics, void *workspace,
+                                    size_t workspace_bytes, void *stream) {
     Ws ws;
     adop_status s = prologue(points, n_views, cameras, poses, params, fwd_views, workspace, workspace_bytes, true, ws);
     if (s) return s;
@@ -516,6 +516,7 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     if (d_feat && !aligned(d_feat, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_feat misaligned");
     if (d_pos && !aligned(d_pos, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pos misaligned");
     if (d_pose && !aligned(d_pose, 8)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pose misaligned");
+    if (d_intrinsics && !aligned(d_intrinsics, 8)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_intrinsics misaligned");
     int model;
     if (!uniform_model(n_views, cameras, model))
         return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
@@ -526,10 +527,16 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     a.tag = call_tag(points, n_views, cameras, poses, params, fwd_views, workspace_bytes);
     a.d_feat = d_feat;
     a.d_pos = d_pos;
+    a.d_intr = d_intrinsics;
+    a.nterms = d_intrinsics ? 18 : 6;
     if (points->n == 0) {
         if (d_pose && !params->grad_accumulate) {
             int e = (int)cudaMemsetAsync(d_pose, 0, sizeof(double) * 6 * n_views, (cudaStream_t)stream);
             if (e) return cuda_status(e, "memset d_pose");
+        }
+        if (d_intrinsics && !params->grad_accumulate) {
+            int e = (int)cudaMemsetAsync(d_intrinsics, 0, sizeof(double) * 12 * n_views, (cudaStream_t)stream);
+            if (e) return cuda_status(e, "memset d_intrinsics");
         }
         return ok();
     }

@@ -111,7 +111,9 @@ struct RasterArgs {
     int64_t rec_capacity;  // in 16-B slots
     void *tables;          // backward pixel tables, per view [P][prow] floats
     int32_t prow;          // pixel-table row stride in floats: 4 + C rounded up to a multiple of 4
-    double *pose_partials; // [gridDim.x][nviews][6]
+    double *pose_partials; // [gridDim.x][nviews][nterms]
+    int32_t nterms;        // structural terms per view: 6 (pose) or 18 (pose + 12 intrinsics, NEXT-1)
+    double *d_intr;        // backward: [V][12] intrinsics gradient or NULL
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
     unsigned long long tag;// fingerprint of this call's inputs (host); 0 = records not reusable by the backward

@@ -935,6 +935,44 @@ __device__ __forceinline__ void jacobian(const ViewDesc &v, const Proj &p, float
     J[3] = a1 * D10; J[4] = a1 * D11; J[5] = -a1 * (D10 * xn + D11 * yn);
 }
 
+// Structural terms of one ghost in one view, per view accumulated in fp64 (R20): t[0..6) = the tangent
+// pose terms (w, Xc x w) (Eq. 17 left increment, R19); with nt = kNT, t[6..18) = the camera-intrinsics
+// terms (d(u0,v0)/d theta)^T g (NEXT-1), theta = (fx, fy, cx, cy, k1..k6, p1, p2), g = (g_u, g_v) in
+// layer-0 pixels (R17); the pinhole model has no distortion parameters (those terms are 0).
+constexpr int kNI = 12;
+constexpr int kNT = 6 + kNI;
+template <int MODEL>
+__device__ __forceinline__ void struct_terms(const ViewDesc &v, const Proj &p, float gu, float gv, float w0, float w1,
+                                             float w2, int nt, double *t) {
+    t[0] = w0; t[1] = w1; t[2] = w2;
+    t[3] = (double)(p.Y * w2 - p.Z * w1);
+    t[4] = (double)(p.Z * w0 - p.X * w2);
+    t[5] = (double)(p.X * w1 - p.Y * w0);
+    if (nt <= 6) return;
+    const float xn = p.X * p.iz, yn = p.Y * p.iz;
+    float xd = xn, yd = yn;
+#pragma unroll
+    for (int k = 4; k < kNI; ++k) t[6 + k] = 0.0;
+    if (MODEL == 1) {  // camera model R6: u0 = fx xd + cx, xd = xn rad + 2 p1 xn yn + p2 (r2 + 2 xn^2), ...
+        const float r2 = xn * xn + yn * yn, r4 = r2 * r2, r6 = r4 * r2;
+        const float num = 1.f + v.k[0] * r2 + v.k[1] * r4 + v.k[2] * r6;
+        const float den = 1.f + v.k[3] * r2 + v.k[4] * r4 + v.k[5] * r6;
+        const float idn = 1.f / den, rad = num * idn;
+        xd = xn * rad + 2.f * v.p[0] * xn * yn + v.p[1] * (r2 + 2.f * xn * xn);
+        yd = yn * rad + v.p[0] * (r2 + 2.f * yn * yn) + 2.f * v.p[1] * xn * yn;
+        const float a = gu * v.fx, b = gv * v.fy, s = a * xn + b * yn;  // g . d(u0,v0)/d rad
+        const float q = -s * num * idn * idn;
+        t[10] = (double)(s * r2 * idn); t[11] = (double)(s * r4 * idn); t[12] = (double)(s * r6 * idn);  // k1..k3
+        t[13] = (double)(q * r2); t[14] = (double)(q * r4); t[15] = (double)(q * r6);                   // k4..k6
+        t[16] = (double)(a * 2.f * xn * yn + b * (r2 + 2.f * yn * yn));                                 // p1
+        t[17] = (double)(a * (r2 + 2.f * xn * xn) + b * 2.f * xn * yn);                                 // p2
+    }
+    t[6] = (double)(gu * xd);  // fx
+    t[7] = (double)(gv * yd);  // fy
+    t[8] = gu;                 // cx
+    t[9] = gv;                 // cy
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
@@ -943,8 +981,9 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 template <int MODEL, bool VEC, int CT>
 __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ RasterArgs a) {
-    __shared__ double spose[ADOP_MAX_VIEWS_PER_LAUNCH * 6];
-    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x) spose[t] = 0.0;
+    __shared__ double spose[ADOP_MAX_VIEWS_PER_LAUNCH * kNT];
+    const int NT = a.nterms;
+    for (int t = threadIdx.x; t < a.nviews * NT; t += blockDim.x) spose[t] = 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int C = CT > 0 ? CT : a.channels;
@@ -1012,6 +1051,9 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                 }
                 if (!__any_sync(kFull, gc)) continue;
                 float w0 = 0.f, w1 = 0.f, w2 = 0.f;
+                double tt[kNT];
+#pragma unroll
+                for (int k = 0; k < kNT; ++k) tt[k] = 0.0;
                 if (gc) {
                     float J[6];
                     jacobian<MODEL>(v, p, J);
@@ -1021,17 +1063,12 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                     dxx += v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2;  // dx = R^T w
                     dxy += v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2;
                     dxz += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
+                    struct_terms<MODEL>(v, p, gu, gv, w0, w1, w2, NT, tt);
                 }
-                // tangent pose gradient (w, Xc x w) (Eq. 17 left increment, R19): warp sum in fp64
-                double t6[6];
-                t6[0] = w0; t6[1] = w1; t6[2] = w2;
-                t6[3] = gc ? (double)(p.Y * w2 - p.Z * w1) : 0.0;
-                t6[4] = gc ? (double)(p.Z * w0 - p.X * w2) : 0.0;
-                t6[5] = gc ? (double)(p.X * w1 - p.Y * w0) : 0.0;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) {
-                    const double s = warp_sum(t6[k]);
-                    if (lane == 0) atomicAdd(&spose[vs * 6 + k], s);
+                // pose (+ intrinsics) terms: warp sum in fp64
+                for (int k = 0; k < NT; ++k) {
+                    const double s = warp_sum(tt[k]);
+                    if (lane == 0) atomicAdd(&spose[vs * NT + k], s);
                 }
             }
             if (in) {
@@ -1054,8 +1091,8 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x)
-        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = spose[t];
+    for (int t = threadIdx.x; t < a.nviews * NT; t += blockDim.x)
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * NT + t] = spose[t];
 }
 
 // --------------------------------------------------------------------------- //
@@ -1234,10 +1271,10 @@ __device__ __forceinline__ void tex_hit(const RasterArgs &a, const ViewDesc &v, 
 }
 
 // ghost: image gradient over its kept layers (Eqs. 9-11), chain rule (Eq. 8) -> dx (atomics), and the
-// pose terms (w, Xc x w) returned for the caller's reduction.
+// nt structural terms (struct_terms) returned for the caller's reduction.
 template <int MODEL, int CT>
 __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc &v, const Proj &p, int nk,
-                                            int64_t idx, double *t6) {
+                                            int64_t idx, int nt, double *tt, float *g = nullptr) {
     const int C = CT > 0 ? CT : a.channels;
     float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
     for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + idx * C + c);
@@ -1258,11 +1295,54 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
         red_add(a.d_pos + a.n + idx, v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2);
         red_add(a.d_pos + 2 * a.n + idx, v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2);
     }
-    t6[0] = w0; t6[1] = w1; t6[2] = w2;
-    t6[3] = (double)(p.Y * w2 - p.Z * w1);
-    t6[4] = (double)(p.Z * w0 - p.X * w2);
-    t6[5] = (double)(p.X * w1 - p.Y * w0);
+    struct_terms<MODEL>(v, p, gu, gv, w0, w1, w2, nt, tt);
+    if (g) {
+        g[0] = gu;
+        g[1] = gv;
+    }
     return true;
+}
+
+// A ghost whose list slot could not be reserved (record region full) is processed by the sweep itself.
+// The pose terms stay inline as before; the intrinsics terms (NEXT-1, only when requested) are added
+// out of line so their registers do not weigh on the sweep.
+template <int MODEL>
+__device__ __forceinline__ void intr_inline(const RasterArgs &a, const ViewDesc &v, int vs, const Proj &p, float gu,
+                                            float gv) {
+    double *row = a.pose_partials + ((int64_t)a.inline_row * a.nviews + vs) * kNT + 6;
+    const float xn = p.X * p.iz, yn = p.Y * p.iz;
+    float xd = xn, yd = yn;
+    if (MODEL == 1) {  // as struct_terms, one term at a time (no term array in the sweep's registers)
+        const float r2 = xn * xn + yn * yn, r4 = r2 * r2, r6 = r4 * r2;
+        const float num = 1.f + v.k[0] * r2 + v.k[1] * r4 + v.k[2] * r6;
+        const float den = 1.f + v.k[3] * r2 + v.k[4] * r4 + v.k[5] * r6;
+        const float idn = 1.f / den, rad = num * idn;
+        xd = xn * rad + 2.f * v.p[0] * xn * yn + v.p[1] * (r2 + 2.f * xn * xn);
+        yd = yn * rad + v.p[0] * (r2 + 2.f * yn * yn) + 2.f * v.p[1] * xn * yn;
+        const float a0 = gu * v.fx, b0 = gv * v.fy, s = a0 * xn + b0 * yn, q = -s * num * idn * idn;
+        atomicAdd(row + 4, (double)(s * r2 * idn));
+        atomicAdd(row + 5, (double)(s * r4 * idn));
+        atomicAdd(row + 6, (double)(s * r6 * idn));
+        atomicAdd(row + 7, (double)(q * r2));
+        atomicAdd(row + 8, (double)(q * r4));
+        atomicAdd(row + 9, (double)(q * r6));
+        atomicAdd(row + 10, (double)(a0 * 2.f * xn * yn + b0 * (r2 + 2.f * yn * yn)));
+        atomicAdd(row + 11, (double)(a0 * (r2 + 2.f * xn * xn) + b0 * 2.f * xn * yn));
+    }
+    atomicAdd(row + 0, (double)(gu * xd));
+    atomicAdd(row + 1, (double)(gv * yd));
+    atomicAdd(row + 2, (double)gu);
+    atomicAdd(row + 3, (double)gv);
+}
+template <int MODEL, int CT>
+__device__ __forceinline__ void ghost_inline(const RasterArgs &a, const ViewDesc &v, int vs, const Proj &p, int nk,
+                                             int64_t i) {
+    double t6[6];
+    float g[2];
+    if (!ghost_point<MODEL, CT>(a, v, p, nk, i, 6, t6, g)) return;
+    const int NT = a.nterms;
+    for (int k = 0; k < 6; ++k) atomicAdd(&a.pose_partials[((int64_t)a.inline_row * a.nviews + vs) * NT + k], t6[k]);
+    if (NT == kNT) intr_inline<MODEL>(a, v, vs, p, g[0], g[1]);
 }
 
 // Sweep candidate: exact projection and discard, then emit the rendered hits to the texture list (mode 0
@@ -1314,9 +1394,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
         r[0] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X), __float_as_uint(p.Y));
         r[1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), 0u);
     } else {
-        double t6[6];
-        if (ghost_point<MODEL, CT>(a, v, p, nk, i, t6))
-            for (int k = 0; k < 6; ++k) atomicAdd(&a.pose_partials[((int64_t)a.inline_row * a.nviews + vs) * 6 + k], t6[k]);
+        ghost_inline<MODEL, CT>(a, v, vs, p, nk, i);
     }
 }
 
@@ -1334,11 +1412,12 @@ __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ Ra
 
 // ghost list consumer: one thread per (ghost, view) (balanced); pose terms warp-reduced in fp64 into
 // per-warp shared slots, per-block partials reduced by k_pose_reduce in a fixed order.
-template <int MODEL, int CT>
+// NT = 6 (pose) or kNT (pose + intrinsics).
+template <int MODEL, int CT, int NT>
 __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant__ RasterArgs a) {
-    __shared__ double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * 6];
+    __shared__ double wpose[kWarps][ADOP_MAX_VIEWS_PER_LAUNCH * NT];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * 6; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
+    for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * NT; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
     __syncthreads();
     // the sweep's ghost list: the back of the record region
     const unsigned long long back = *(volatile unsigned long long *)&a.hdr->back_ok;
@@ -1347,7 +1426,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x; r0 < total; r0 += stride) {
         const unsigned long long r = r0 + threadIdx.x;
-        double t6[6] = {0, 0, 0, 0, 0, 0};
+        double t6[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) t6[k] = 0.0;
         int vs = -1;
         if (r < total) {
             const uint4 e1 = __ldcs(list + 2 * r + 1);
@@ -1363,7 +1444,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
                 p.Y = __uint_as_float(e0.w);
                 p.Z = __uint_as_float(e1.x);
                 p.iz = __frcp_rn(p.Z);
-                if (!ghost_point<MODEL, CT>(a, v, p, nk, (int64_t)e1.y, t6)) vs = -1;
+                if (!ghost_point<MODEL, CT>(a, v, p, nk, (int64_t)e1.y, NT, t6)) vs = -1;
             }
         }
         // warp reduction per distinct view present in the warp (usually one)
@@ -1373,18 +1454,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
             const int vv = __shfl_sync(kFull, vs, leader);
             const bool mine = vs == vv;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) {
+            for (int k = 0; k < NT; ++k) {
                 const double sum = warp_sum(mine ? t6[k] : 0.0);
-                if (lane == 0) wpose[wid][vv * 6 + k] += sum;
+                if (lane == 0) wpose[wid][vv * NT + k] += sum;
             }
             pending &= ~__ballot_sync(kFull, mine);
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < a.nviews * 6; t += blockDim.x) {
+    for (int t = threadIdx.x; t < a.nviews * NT; t += blockDim.x) {
         double acc = 0.0;
         for (int w = 0; w < kWarps; ++w) acc += wpose[w][t];
-        a.pose_partials[(int64_t)blockIdx.x * a.nviews * 6 + t] = acc;
+        a.pose_partials[(int64_t)blockIdx.x * a.nviews * NT + t] = acc;
     }
 }
 
@@ -1560,11 +1641,15 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
     list_close<true>(a, cg, lane);
 }
 
-// d_pose[t] (+)= sum over blocks of the partials, fixed order (deterministic).
-__global__ void __launch_bounds__(256) k_pose_reduce(const double *partials, int nblocks, int nvals, double *d_pose,
-                                                     int accumulate) {
+// Column t = view * nt + j of the per-block partials, summed over blocks in a fixed order (deterministic):
+// j < 6 -> d_pose[view][j], else d_intr[view][j - 6]; a NULL output is skipped.
+__global__ void __launch_bounds__(256) k_pose_reduce(const double *partials, int nblocks, int nviews, int nt,
+                                                     double *d_pose, double *d_intr, int accumulate) {
     __shared__ double s[256];
-    const int t = blockIdx.x;
+    const int t = blockIdx.x, view = t / nt, j = t % nt;
+    double *out = j < 6 ? (d_pose ? d_pose + view * 6 + j : nullptr) : (d_intr ? d_intr + view * kNI + (j - 6) : nullptr);
+    if (!out) return;
+    const int nvals = nviews * nt;
     double acc = 0.0;
     for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partials[(int64_t)b * nvals + t];
     s[threadIdx.x] = acc;
@@ -1573,7 +1658,7 @@ __global__ void __launch_bounds__(256) k_pose_reduce(const double *partials, int
         if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) d_pose[t] = accumulate ? d_pose[t] + s[0] : s[0];
+    if (threadIdx.x == 0) *out = accumulate ? *out + s[0] : s[0];
 }
 
 // --------------------------------------------------------------------------- //
@@ -1709,7 +1794,9 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         int g = resident_grid(k, sms, kWarps * 128, a.n);
         if (g > grid_cap) g = grid_cap;
         k<<<g, kThreads, 0, s>>>(a);
-        if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, g, a.nviews * 6, d_pose, a.grad_accumulate);
+        if (d_pose || a.d_intr)
+            k_pose_reduce<<<a.nviews * a.nterms, 256, 0, s>>>(a.pose_partials, g, a.nviews, a.nterms, d_pose, a.d_intr,
+                                                              a.grad_accumulate);
         return (int)cudaGetLastError();
     }
     RasterArgs b = a;
@@ -1734,7 +1821,8 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
         if (bx < 1) bx = 1;
         k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np, a.hdr,
-                                                a.pose_partials + (int64_t)gg * a.nviews * 6, a.nviews * 6, a.tag);
+                                                a.pose_partials + (int64_t)gg * a.nviews * a.nterms, a.nviews * a.nterms,
+                                                a.tag);
     }
     {   // per-pixel tables
         int64_t bx = (maxP + kThreads - 1) / kThreads;
@@ -1757,8 +1845,13 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         }
     }
     if (a.d_feat) k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
-    k_bwd_ghost<MODEL, CT><<<gg, kThreads, 0, s>>>(b);
-    if (d_pose) k_pose_reduce<<<a.nviews * 6, 256, 0, s>>>(a.pose_partials, gg + 1, a.nviews * 6, d_pose, a.grad_accumulate);
+    if (a.nterms == kNT)  // the intrinsics terms cost 12 more fp64 warp sums per ghost: only when requested
+        k_bwd_ghost<MODEL, CT, kNT><<<gg, kThreads, 0, s>>>(b);
+    else
+        k_bwd_ghost<MODEL, CT, 6><<<gg, kThreads, 0, s>>>(b);
+    if (d_pose || a.d_intr)
+        k_pose_reduce<<<a.nviews * a.nterms, 256, 0, s>>>(a.pose_partials, gg + 1, a.nviews, a.nterms, d_pose, a.d_intr,
+                                                          a.grad_accumulate);
     return (int)cudaGetLastError();
 }
 

@@ -19,10 +19,10 @@ from paper_2110_06635_b200 import adop as A
 from paper_2110_06635_b200 import scene as S
 
 
-def run_gpu(cloud, cams, poses, params, record_capacity=None, grads=None, global_offset=0):
+def run_gpu(cloud, cams, poses, params, record_capacity=None, grads=None, global_offset=0, intrinsics=True):
     dev = torch.device("cuda")
     r = A.Renderer(cloud.to(dev), cams, poses, params, global_offset=global_offset,
-                   record_capacity=record_capacity)
+                   record_capacity=record_capacity, intrinsics=intrinsics)
     r.forward()
     if grads is not None:
         r.backward([g.to(dev) for g in grads])
@@ -79,6 +79,14 @@ def compare_backward(r, bwd, ctx="", check_feat=True, check_pos=True, views=None
     err = np.abs(g - bwd.dpose)
     tol = 1e-6 + 1e-5 * np.maximum(np.abs(bwd.dpose), 1e-2 * bwd.dpose_abs)
     assert np.all(err <= tol), f"{ctx} d_pose err {err} tol {tol}\ngpu {g}\noracle {bwd.dpose}"
+    if getattr(r, "d_intr", None) is not None and bwd.dintr is not None:
+        # NEXT-1 intrinsics gradient: same tolerance form as d_pose (R20)
+        g = r.d_intr.cpu().numpy()
+        if views is not None:
+            g = g[list(views)]
+        err = np.abs(g - bwd.dintr)
+        tol = 1e-6 + 1e-5 * np.maximum(np.abs(bwd.dintr), 1e-2 * bwd.dintr_abs)
+        assert np.all(err <= tol), f"{ctx} d_intr err {err} tol {tol}\ngpu {g}\noracle {bwd.dintr}"
 
 
 def grads_for(cams, layers, C, seed=S.SEED_GRADS):

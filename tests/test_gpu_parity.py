@@ -127,19 +127,21 @@ def test_record_overflow_falls_back_to_restreaming():
 
 
 def test_backward_null_outputs():
-    """Any of d_feat / d_pos / d_pose may be NULL (include/adop.h); the others are unchanged."""
+    """Any of d_feat / d_pos / d_pose / d_intrinsics may be NULL (include/adop.h); the others are unchanged."""
     w = S.workload(2, n=60_000)
     dev = torch.device("cuda")
     G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, w.cloud.channels)]
-    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params)
+    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params, intrinsics=True)
     r.forward()
     f1, p1, q1 = [t.clone() for t in r.backward(G)]
-    for drop in range(3):
-        outs = [torch.full_like(f1, 7.0), torch.full_like(p1, 7.0), torch.full_like(q1, 7.0)]
-        args = [None if k == drop else outs[k] for k in range(3)]
+    i1 = r.d_intr.clone()
+    assert i1[:, 4:].abs().sum() > 0  # OpenCV8 camera: distortion terms present
+    for drop in range(4):
+        outs = [torch.full_like(t, 7.0) for t in (f1, p1, q1, i1)]
+        args = [None if k == drop else outs[k] for k in range(4)]
         A.rasterize_backward(r.points, r.cams, r.poses, r.params, r.pyrs, G, r.ws, *args)
         torch.cuda.synchronize()
-        for k, ref in enumerate((f1, p1, q1)):
+        for k, ref in enumerate((f1, p1, q1, i1)):
             if k == drop:
                 assert (outs[k] == 7.0).all()
             else:
@@ -159,6 +161,17 @@ def test_grad_accumulate_adds():
     torch.testing.assert_close(r.d_feat, 2 * f1)
     torch.testing.assert_close(r.d_pos, 2 * p1)
     torch.testing.assert_close(r.d_pose, 2 * q1)
+
+
+def test_intrinsics_gradient_pinhole_zero_distortion_terms():
+    """NEXT-1 on a pinhole camera: the 8 distortion entries are exactly 0, the rest match the oracle."""
+    w = S.workload(1, n=120_000, n_views=2)
+    prm = dataclasses.replace(w.params, ghost_rate=0.25)
+    G = grads_for(w.cameras, prm.layers, w.cloud.channels)
+    r = run_gpu(w.cloud, w.cameras, w.poses, prm, grads=G)
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, prm, grads=G)
+    assert (r.d_intr[:, 4:] == 0).all() and r.d_intr[:, :4].abs().sum() > 0
+    compare_backward(r, bwd, ctx="pinhole intrinsics")
 
 
 def test_phase_split_point_sharding_on_one_gpu():
@@ -234,7 +247,7 @@ def test_full_config3_100M_forward_vs_oracle():
 def test_full_config2_10M_fwd_bwd_vs_oracle():
     w = _cloud_on_gpu(2)
     G = grads_for(w.cameras, w.params.layers, w.cloud.channels)
-    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params)
+    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params, intrinsics=True)
     r.forward()
     r.backward([g.cuda() for g in G])
     torch.cuda.synchronize()
