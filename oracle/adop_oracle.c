@@ -59,7 +59,13 @@ typedef struct {
     float z_near;       /* R7 */
     uint64_t seed;
     int32_t view_id_base;
+    int32_t log_descriptors; /* NEXT-2: tau stored as log, linearized by exp() when rasterized */
 } orc_params;
+
+typedef struct {             /* NEXT-2: spherical environment map E of Eq. 7, R29 */
+    const float *data;       /* [height][width][C] equirectangular, NULL = constant background (R18) */
+    int32_t width, height;
+} orc_env;
 
 typedef struct {
     int64_t n;
@@ -249,6 +255,86 @@ static float key_depth(uint64_t key)
     return m;
 }
 
+/* Linear-space descriptor channel (logarithmic descriptors are converted to linear space
+ * during rasterization): exp(tau) in fp64 for log descriptors, tau otherwise. */
+static double desc_lin(const orc_params *pr, float t) { return pr->log_descriptors ? exp((double)t) : (double)t; }
+
+/* ------------------------------------------------------------------------- */
+/* Environment map (NEXT-2), reading R29.                                    */
+/* C^{-1}: layer-l pixel centre (u, v) -> layer-0 continuous pixel (u 2^l,   */
+/* v 2^l) (inverse of Eq. 2's 2^-l) -> normalized camera coordinates: the    */
+/* pinhole inverse, then for OpenCV8 8 Newton steps on the distortion map    */
+/* of R6 started at the distorted coordinates.  World direction d = R^T      */
+/* (xn, yn, 1) (Eq. 7's E(R^T C^{-1}(u, v))).  Equirectangular lookup:       */
+/* lon = atan2(d_x, d_z), lat = atan2(d_y, hypot(d_x, d_z)),                 */
+/* s = (lon / 2pi + 1/2) W - 1/2, t = (lat / pi + 1/2) H - 1/2, bilinear,    */
+/* columns wrapped, rows clamped.                                            */
+/* ------------------------------------------------------------------------- */
+static void distort_f64(const orc_camera *c, double xn, double yn, double *xd, double *yd, double D[2][2])
+{
+    const double k1 = c->k[0], k2 = c->k[1], k3 = c->k[2], k4 = c->k[3], k5 = c->k[4], k6 = c->k[5];
+    const double p1 = c->p[0], p2 = c->p[1];
+    double r2 = xn * xn + yn * yn;
+    double num = 1.0 + k1 * r2 + k2 * r2 * r2 + k3 * r2 * r2 * r2;
+    double den = 1.0 + k4 * r2 + k5 * r2 * r2 + k6 * r2 * r2 * r2;
+    double rad = num / den;
+    *xd = xn * rad + 2.0 * p1 * xn * yn + p2 * (r2 + 2.0 * xn * xn);
+    *yd = yn * rad + p1 * (r2 + 2.0 * yn * yn) + 2.0 * p2 * xn * yn;
+    double dnum = k1 + 2.0 * k2 * r2 + 3.0 * k3 * r2 * r2;
+    double dden = k4 + 2.0 * k5 * r2 + 3.0 * k6 * r2 * r2;
+    double drad = (dnum * den - num * dden) / (den * den);
+    D[0][0] = rad + 2.0 * xn * xn * drad + 2.0 * p1 * yn + 6.0 * p2 * xn;
+    D[0][1] = 2.0 * xn * yn * drad + 2.0 * p1 * xn + 2.0 * p2 * yn;
+    D[1][0] = D[0][1];
+    D[1][1] = rad + 2.0 * yn * yn * drad + 6.0 * p1 * yn + 2.0 * p2 * xn;
+}
+
+void orc_unproject(const orc_camera *c, double u0, double v0, double *xn, double *yn)
+{
+    double xd = (u0 - (double)c->cx) / (double)c->fx, yd = (v0 - (double)c->cy) / (double)c->fy;
+    double x = xd, y = yd;
+    if (c->model == 1) {
+        for (int it = 0; it < 8; ++it) {
+            double fx_, fy_, D[2][2];
+            distort_f64(c, x, y, &fx_, &fy_, D);
+            double rx = fx_ - xd, ry = fy_ - yd;
+            double det = D[0][0] * D[1][1] - D[0][1] * D[1][0];
+            x -= (D[1][1] * rx - D[0][1] * ry) / det;
+            y -= (-D[1][0] * rx + D[0][0] * ry) / det;
+        }
+    }
+    *xn = x;
+    *yn = y;
+}
+
+/* Bilinear lookup of E in world direction d: 4 texel indices (texel = row * W + col) and weights. */
+void orc_env_taps(const orc_env *e, const double *d, int64_t *idx, double *w)
+{
+    const double PI = 3.14159265358979323846;
+    double lon = atan2(d[0], d[2]), lat = atan2(d[1], sqrt(d[0] * d[0] + d[2] * d[2]));
+    double s = (lon / (2.0 * PI) + 0.5) * e->width - 0.5, t = (lat / PI + 0.5) * e->height - 0.5;
+    double s0 = floor(s), t0 = floor(t), fs = s - s0, ft = t - t0;
+    int64_t c0 = (int64_t)s0, r0 = (int64_t)t0;
+    int64_t cols[2] = {((c0 % e->width) + e->width) % e->width, (((c0 + 1) % e->width) + e->width) % e->width};
+    int64_t rows[2] = {r0 < 0 ? 0 : (r0 >= e->height ? e->height - 1 : r0),
+                       r0 + 1 < 0 ? 0 : (r0 + 1 >= e->height ? e->height - 1 : r0 + 1)};
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            idx[a * 2 + b] = rows[a] * e->width + cols[b];
+            w[a * 2 + b] = (a ? ft : 1.0 - ft) * (b ? fs : 1.0 - fs);
+        }
+}
+
+/* World direction of layer-l pixel (u, v) of a view (R29). */
+void orc_env_dir(const orc_camera *c, const orc_pose *P, int l, int64_t u, int64_t v, double *d)
+{
+    double xn, yn;
+    orc_unproject(c, ldexp((double)u, l), ldexp((double)v, l), &xn, &yn);
+    const double dc[3] = {xn, yn, 1.0};
+    for (int k = 0; k < 3; ++k)  /* R^T dc */
+        d[k] = (double)P->R[0 + k] * dc[0] + (double)P->R[3 + k] * dc[1] + (double)P->R[6 + k] * dc[2];
+}
+
 /* ------------------------------------------------------------------------- */
 /* Forward pass 1: depth-only render pass (§4.5) = per-pixel min of  */
 /* the packed keys over the render set (Eq. 6's min_z with R8 tie rule).     */
@@ -311,7 +397,7 @@ void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera 
                 if (!(m & (1u << l))) continue;
                 int64_t q = layer_offset(c->width, c->height, l) + pix[l];
                 if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
-                for (int ch = 0; ch < C; ++ch) av[q * C + ch] += (double)pts->feat[i * C + ch];
+                for (int ch = 0; ch < C; ++ch) av[q * C + ch] += desc_lin(pr, pts->feat[i * C + ch]);
                 cv[q] += 1.0;
             }
         }
@@ -323,20 +409,36 @@ void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera 
 /* background E (constant vector, R18) when Lambda is empty.  image layout:  */
 /* [V][C*P], layer l planar [C][h_l][w_l] starting at C*off_l.               */
 /* ------------------------------------------------------------------------- */
-void orc_forward_resolve(int32_t n_views, const orc_camera *cams, const orc_params *pr, int32_t C,
-                         const double *accum, const double *count, const float *bg, double *image)
+void orc_forward_resolve(int32_t n_views, const orc_camera *cams, const orc_pose *poses, const orc_params *pr,
+                         int32_t C, const double *accum, const double *count, const float *bg, const orc_env *env,
+                         double *image)
 {
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
         int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
         for (int l = 0; l < pr->layers; ++l) {
             int64_t off = layer_offset(c->width, c->height, l);
-            int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
+            int32_t wl = layer_w(c->width, l);
+            int64_t hw = (int64_t)wl * layer_w(c->height, l);
             for (int64_t j = 0; j < hw; ++j) {
                 int64_t q = off + j;
                 double n = count[(int64_t)v * P + q];
+                double bgv[32];
+                if (n == 0.0) {  /* Eq. 7 first case: E(R^T C^{-1}(u, v)), or the constant E of R18 */
+                    for (int ch = 0; ch < C; ++ch) bgv[ch] = bg ? (double)bg[ch] : 0.0;
+                    if (env && env->data) {
+                        double d[3], w[4];
+                        int64_t idx[4];
+                        orc_env_dir(c, &poses[v], l, j % wl, j / wl, d);
+                        orc_env_taps(env, d, idx, w);
+                        for (int ch = 0; ch < C; ++ch) {
+                            bgv[ch] = 0.0;
+                            for (int k = 0; k < 4; ++k) bgv[ch] += w[k] * (double)env->data[idx[k] * C + ch];
+                        }
+                    }
+                }
                 for (int ch = 0; ch < C; ++ch) {
-                    double val = n > 0.0 ? accum[((int64_t)v * P + q) * C + ch] / n : (bg ? (double)bg[ch] : 0.0);
+                    double val = n > 0.0 ? accum[((int64_t)v * P + q) * C + ch] / n : bgv[ch];
                     image[(int64_t)v * C * P + C * off + ch * hw + j] = val;
                 }
             }
@@ -346,11 +448,12 @@ void orc_forward_resolve(int32_t n_views, const orc_camera *cams, const orc_para
 
 /* Full forward: Eq. 1 I_l = Phi_l(...) for all layers and views. */
 void orc_forward(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
-                 const orc_params *pr, const float *bg, uint64_t *keys, double *accum, double *count, double *image)
+                 const orc_params *pr, const float *bg, const orc_env *env, uint64_t *keys, double *accum,
+                 double *count, double *image)
 {
     orc_forward_depth(pts, n_views, cams, poses, pr, keys);
     orc_forward_blend(pts, n_views, cams, poses, pr, keys, accum, count);
-    orc_forward_resolve(n_views, cams, pr, pts->channels, accum, count, bg, image);
+    orc_forward_resolve(n_views, cams, poses, pr, pts->channels, accum, count, bg, env, image);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -358,8 +461,8 @@ void orc_forward(const orc_points *pts, int32_t n_views, const orc_camera *cams,
 /* when the ghost (descriptor tau, depth z) is virtually shifted onto q.     */
 /* Returns the case number 1..4.                                             */
 /* ------------------------------------------------------------------------- */
-int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double n_q, uint64_t key_q,
-                       const double *I_q, double *delta)
+static int induced_change_d(int32_t C, const double *tau, float z, float alpha, double n_q, uint64_t key_q,
+                            const double *I_q, double *delta)
 {
     float onepa = 1.0f + alpha;
     float m_q = key_depth(key_q);
@@ -369,7 +472,7 @@ int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double
     else if (z * onepa < m_q) kase = 3;             /* shifted point fully in front */
     else kase = 4;                                  /* fuzzy co-visible: blend mean changes */
     for (int ch = 0; ch < C; ++ch) {
-        double t = (double)tau[ch];
+        double t = tau[ch];
         switch (kase) {
         case 1: case 3: delta[ch] = t - I_q[ch]; break;
         case 2: delta[ch] = 0.0; break;
@@ -377,6 +480,14 @@ int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double
         }
     }
     return kase;
+}
+
+int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double n_q, uint64_t key_q,
+                       const double *I_q, double *delta)
+{
+    double t[32];
+    for (int ch = 0; ch < C; ++ch) t[ch] = (double)tau[ch];
+    return induced_change_d(C, t, z, alpha, n_q, key_q, I_q, delta);
 }
 
 /* Projection Jacobian d(u0,v0)/dXc (R21), fp64 at the fp32 camera point.   */
@@ -468,7 +579,7 @@ void orc_intrinsics_jacobian(const orc_camera *c, const float *Xc, double *Jt)
 /* Ghost image-space gradient at layer l, pixel (u,v) (Eqs. 9-11, R14-R16):
  * g = (g_u, g_v) in layer-l pixels; gabs = per-direction sums of |G.Delta|/2. */
 static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, int64_t local, int32_t C,
-                             const float *tau, float z, const uint64_t *kv, const double *cv, const double *img,
+                             const double *tau, float z, const uint64_t *kv, const double *cv, const double *img,
                              const float *Gv, int64_t P, double *g, double *gabs)
 {
     int32_t wl = layer_w(c->width, l), hl = layer_w(c->height, l);
@@ -485,13 +596,13 @@ static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, i
         if (qu < 0 || qu >= wl || qv < 0 || qv >= hl) continue; /* neighbour outside: no term (R14) */
         int64_t qj = qv * wl + qu;
         for (int ch = 0; ch < C; ++ch) Iq[ch] = img[C * off + ch * hw + qj];
-        int kase = orc_induced_change(C, tau, z, pr->alpha, cv[off + qj], kv[off + qj], Iq, delta);
+        int kase = induced_change_d(C, tau, z, pr->alpha, cv[off + qj], kv[off + qj], Iq, delta);
         /* magnitude scale for tolerances: sum_c |G| (|tau| + |I|) times the case factor */
         double fac = kase == 2 ? 0.0 : (kase == 4 ? 1.0 / (cv[off + qj] + 1.0) : 1.0);
         for (int ch = 0; ch < C; ++ch) {
             double gq = (double)Gv[C * off + ch * hw + qj];
             d[k] += gq * delta[ch];
-            dabs[k] += fabs(gq) * (fabs((double)tau[ch]) + fabs(Iq[ch])) * fac;
+            dabs[k] += fabs(gq) * (fabs(tau[ch]) + fabs(Iq[ch])) * fac;
         }
     }
     g[0] = 0.5 * (d[0] - d[1]);   /* Eq. 10 with the signed central difference (R15) */
@@ -509,13 +620,19 @@ static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, i
 /*   dintr [V][12] intrinsics gradient (NEXT-1): sum over ghosts of          */
 /*                 (d(u0,v0)/d theta)^T (g_u, g_v), theta as in              */
 /*                 orc_intrinsics_jacobian                                   */
+/*   denv [H][W][C] environment-map gradient (NEXT-2; "straightforward",     */
+/*                 P:L253): every empty pixel's G scattered to its 4         */
+/*                 bilinear taps (R29); only with env                        */
 /* and the per-element sums of |terms| used to scale tolerances (R20).       */
+/* Log descriptors (NEXT-2): the texture gradient carries d exp(tau)/d tau   */
+/* and the ghosts' Eq. 11 uses the linear descriptor exp(tau).               */
 /* Any output pointer may be NULL.                                           */
 /* ------------------------------------------------------------------------- */
 void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
-                  const orc_params *pr, const uint64_t *keys, const double *count, const double *image,
-                  const float *G, double *dtau, double *dx, double *dpose, double *dintr,
-                  double *dtau_abs, double *dx_abs, double *dpose_abs, double *dintr_abs)
+                  const orc_params *pr, const orc_env *env, const uint64_t *keys, const double *count,
+                  const double *image, const float *G, double *dtau, double *dx, double *dpose, double *dintr,
+                  double *denv, double *dtau_abs, double *dx_abs, double *dpose_abs, double *dintr_abs,
+                  double *denv_abs)
 {
     const int C = pts->channels;
     const int64_t n = pts->n;
@@ -529,6 +646,9 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
     if (dpose_abs) memset(dpose_abs, 0, sizeof(double) * (size_t)(6 * n_views));
     if (dintr) memset(dintr, 0, sizeof(double) * (size_t)(12 * n_views));
     if (dintr_abs) memset(dintr_abs, 0, sizeof(double) * (size_t)(12 * n_views));
+    const int64_t nenv = (env && env->data) ? (int64_t)env->width * env->height * C : 0;
+    if (denv) memset(denv, 0, sizeof(double) * (size_t)nenv);
+    if (denv_abs) memset(denv_abs, 0, sizeof(double) * (size_t)nenv);
     int64_t Gbase = 0;
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
@@ -539,10 +659,32 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
         const double *img = image + Gbase;
         const float *Gv = G + Gbase;
         Gbase += (int64_t)C * P;
+        if (nenv && (denv || denv_abs)) {
+            /* environment map: I = sum_k w_k E[idx_k] on empty pixels -> dE[idx_k] += w_k G */
+            for (int l = 0; l < pr->layers; ++l) {
+                int64_t off = layer_offset(c->width, c->height, l);
+                int32_t wl = layer_w(c->width, l);
+                int64_t hw = (int64_t)wl * layer_w(c->height, l);
+                for (int64_t j = 0; j < hw; ++j) {
+                    if (cv[off + j] != 0.0) continue;
+                    double d[3], w[4];
+                    int64_t idx[4];
+                    orc_env_dir(c, Pz, l, j % wl, j / wl, d);
+                    orc_env_taps(env, d, idx, w);
+                    for (int k = 0; k < 4; ++k)
+                        for (int ch = 0; ch < C; ++ch) {
+                            double t = w[k] * (double)Gv[C * off + ch * hw + j];
+                            if (denv) denv[idx[k] * C + ch] += t;
+                            if (denv_abs) denv_abs[idx[k] * C + ch] += fabs(t);
+                        }
+                }
+            }
+        }
         for (int64_t i = 0; i < n; ++i) {
             unsigned m = point_mask(pts, i, c, Pz, pr, (uint32_t)(pr->view_id_base + v), pix, proj);
             if (!(m & 0x7Fu)) continue;
-            const float *tau = pts->feat + i * C;
+            double tau[32];  /* linear-space descriptor */
+            for (int ch = 0; ch < C; ++ch) tau[ch] = desc_lin(pr, pts->feat[i * C + ch]);
             if (!(m & 0x80u)) {
                 /* rendered point: texture gradient of Eq. 7, dI/dtau = 1/|Lambda| (R24) */
                 for (int l = 0; l < pr->layers; ++l) {
@@ -552,7 +694,8 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                     if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
                     int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
                     for (int ch = 0; ch < C; ++ch) {
-                        double t = (double)Gv[C * off + ch * hw + pix[l]] / cv[q];
+                        /* d tau_lin / d tau = exp(tau) = tau_lin for log descriptors, 1 otherwise */
+                        double t = (double)Gv[C * off + ch * hw + pix[l]] / cv[q] * (pr->log_descriptors ? tau[ch] : 1.0);
                         if (dtau) dtau[i * C + ch] += t;
                         if (dtau_abs) dtau_abs[i * C + ch] += fabs(t);
                     }

@@ -45,7 +45,11 @@ class _Pose(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("layers", C.c_int32), ("alpha", C.c_float), ("discard", C.c_int32), ("gamma", C.c_float),
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
-                ("view_id_base", C.c_int32)]
+                ("view_id_base", C.c_int32), ("log_descriptors", C.c_int32)]
+
+
+class _Env(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32)]
 
 
 class _Points(C.Structure):
@@ -75,18 +79,21 @@ def lib():
         _lib.orc_forward_depth.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params), C.c_void_p]
         _lib.orc_forward_blend.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params), C.c_void_p,
                                            C.c_void_p, C.c_void_p]
-        _lib.orc_forward_resolve.argtypes = [C.c_int32, P(_Camera), P(_Params), C.c_int32, C.c_void_p,
-                                             C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_forward_resolve.argtypes = [C.c_int32, P(_Camera), P(_Pose), P(_Params), C.c_int32, C.c_void_p,
+                                             C.c_void_p, C.c_void_p, P(_Env), C.c_void_p]
+        _lib.orc_unproject.argtypes = [P(_Camera), C.c_double, C.c_double, P(C.c_double), P(C.c_double)]
+        _lib.orc_env_taps.argtypes = [P(_Env), C.c_void_p, C.c_void_p, C.c_void_p]
+        _lib.orc_env_dir.argtypes = [P(_Camera), P(_Pose), C.c_int, C.c_int64, C.c_int64, C.c_void_p]
         _lib.orc_induced_change.restype = C.c_int
         _lib.orc_induced_change.argtypes = [C.c_int32, C.c_void_p, C.c_float, C.c_float, C.c_double,
                                             C.c_uint64, C.c_void_p, C.c_void_p]
         _lib.orc_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_project_f64.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_intrinsics_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
-        _lib.orc_backward.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params),
+        _lib.orc_backward.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params), P(_Env),
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
 
 
@@ -124,7 +131,20 @@ def params_struct(p) -> _Params:
     s = _Params()
     s.layers, s.alpha, s.discard, s.gamma = int(p.layers), p.alpha, int(bool(p.discard)), p.gamma
     s.ghost_rate, s.z_near, s.seed, s.view_id_base = p.ghost_rate, p.z_near, int(p.seed), int(p.view_id_base)
+    s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
     return s
+
+
+class Env:
+    """Host copy of params.env_map ([H][W][C] float32) as the oracle's orc_env (NULL data if none)."""
+
+    def __init__(self, params):
+        e = getattr(params, "env_map", None)
+        self.arr = None if e is None else np.ascontiguousarray(
+            e.cpu().numpy() if hasattr(e, "cpu") else e, dtype=np.float32)
+        self.s = _Env()
+        if self.arr is not None:
+            self.s.data, self.s.height, self.s.width = self.arr.ctypes.data, self.arr.shape[0], self.arr.shape[1]
 
 
 class Points:
@@ -213,24 +233,54 @@ def forward_blend(pts: Points, cams, poses, params, keys: np.ndarray):
     return accum, count
 
 
-def forward_resolve(cams, params, channels: int, accum: np.ndarray, count: np.ndarray, bg=None) -> np.ndarray:
+def forward_resolve(cams, params, channels: int, accum: np.ndarray, count: np.ndarray, bg=None,
+                    poses=None) -> np.ndarray:
     V, P = count.shape
+    if poses is None:
+        poses = [None] * V
     ca = (_Camera * V)(*[camera_struct(c) for c in cams])
+    pa = (_Pose * V)(*[pose_struct(p) if p is not None else _Pose() for p in poses])
     ps = params_struct(params)
+    env = Env(params)
+    assert env.arr is None or all(p is not None for p in poses), "an environment map needs the poses"
     image = np.empty((V, channels * P), dtype=np.float64)
     bga = None if bg is None else np.ascontiguousarray(bg, dtype=np.float32)
     accum = np.ascontiguousarray(accum, dtype=np.float64)
     count = np.ascontiguousarray(count, dtype=np.float64)
-    lib().orc_forward_resolve(V, ca, C.byref(ps), channels, accum.ctypes.data, count.ctypes.data, _ptr(bga),
-                              image.ctypes.data)
+    lib().orc_forward_resolve(V, ca, pa, C.byref(ps), channels, accum.ctypes.data, count.ctypes.data, _ptr(bga),
+                              C.byref(env.s), image.ctypes.data)
     return image
+
+
+def unproject(cam, u0: float, v0: float):
+    """C^{-1} of R29: layer-0 continuous pixel -> normalized camera coordinates (xn, yn)."""
+    x, y = C.c_double(), C.c_double()
+    cs = camera_struct(cam)
+    lib().orc_unproject(C.byref(cs), float(u0), float(v0), C.byref(x), C.byref(y))
+    return x.value, y.value
+
+
+def env_dir(cam, pose, l: int, u: int, v: int) -> np.ndarray:
+    d = np.zeros(3)
+    cs, ps = camera_struct(cam), pose_struct(pose)
+    lib().orc_env_dir(C.byref(cs), C.byref(ps), l, u, v, d.ctypes.data)
+    return d
+
+
+def env_taps(env_map, d):
+    """(texel indices row * W + col, bilinear weights) of direction d in env_map [H][W][C] (R29)."""
+    e = Env(type("P", (), {"env_map": env_map})())
+    dd = np.ascontiguousarray(d, dtype=np.float64)
+    idx, w = np.zeros(4, dtype=np.int64), np.zeros(4)
+    lib().orc_env_taps(C.byref(e.s), dd.ctypes.data, idx.ctypes.data, w.ctypes.data)
+    return idx, w
 
 
 def forward(pts: Points, cams, poses, params) -> Forward:
     """Eq. 1 for every view and layer: keys [V][P] u64, accum [V][P][C], count [V][P], image [V][C*P]."""
     keys = forward_depth(pts, cams, poses, params)
     accum, count = forward_blend(pts, cams, poses, params, keys)
-    image = forward_resolve(cams, params, pts.C, accum, count, params.background)
+    image = forward_resolve(cams, params, pts.C, accum, count, params.background, poses)
     return Forward(keys, accum, count, image)
 
 
@@ -269,10 +319,12 @@ def intrinsics_jacobian(cam, Xc) -> np.ndarray:
 
 
 class Backward:
-    def __init__(self, dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr=None, dintr_abs=None):
+    def __init__(self, dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr=None, dintr_abs=None, denv=None,
+                 denv_abs=None):
         self.dtau, self.dx, self.dpose = dtau, dx, dpose
         self.dtau_abs, self.dx_abs, self.dpose_abs = dtau_abs, dx_abs, dpose_abs
         self.dintr, self.dintr_abs = dintr, dintr_abs
+        self.denv, self.denv_abs = denv, denv_abs
 
 
 def backward(pts: Points, cams, poses, params, fwd: Forward, G: np.ndarray) -> Backward:
@@ -284,10 +336,15 @@ def backward(pts: Points, cams, poses, params, fwd: Forward, G: np.ndarray) -> B
     dx = np.empty((3, n)); dx_abs = np.empty((3, n))
     dpose = np.empty((V, 6)); dpose_abs = np.empty((V, 6))
     dintr = np.empty((V, 12)); dintr_abs = np.empty((V, 12))
+    env = Env(params)
+    denv = denv_abs = None
+    if env.arr is not None:
+        denv, denv_abs = np.empty(env.arr.shape), np.empty(env.arr.shape)
     G = np.ascontiguousarray(G, dtype=np.float32)
     keys = np.ascontiguousarray(fwd.keys, dtype=np.uint64)
-    lib().orc_backward(C.byref(pts.s), V, ca, pa, C.byref(ps), keys.ctypes.data,
+    lib().orc_backward(C.byref(pts.s), V, ca, pa, C.byref(ps), C.byref(env.s), keys.ctypes.data,
                        np.ascontiguousarray(fwd.count).ctypes.data, np.ascontiguousarray(fwd.image).ctypes.data,
                        G.ctypes.data, dtau.ctypes.data, dx.ctypes.data, dpose.ctypes.data, dintr.ctypes.data,
-                       dtau_abs.ctypes.data, dx_abs.ctypes.data, dpose_abs.ctypes.data, dintr_abs.ctypes.data)
-    return Backward(dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr, dintr_abs)
+                       _ptr(denv), dtau_abs.ctypes.data, dx_abs.ctypes.data, dpose_abs.ctypes.data,
+                       dintr_abs.ctypes.data, _ptr(denv_abs))
+    return Backward(dtau, dx, dpose, dtau_abs, dx_abs, dpose_abs, dintr, dintr_abs, denv, denv_abs)

@@ -95,6 +95,8 @@ class Params:
     seed: int = SEED_STEP
     view_id_base: int = 0
     background: Optional[List[float]] = None  # constant E; None -> zeros
+    log_descriptors: bool = False  # NEXT-2: tau stored as log, exp() when rasterized
+    env_map: Optional[object] = None  # NEXT-2: [H][W][C] float32 equirectangular E of Eq. 7 (R29); None -> background
 
 
 # --------------------------------------------------------------------------- #
