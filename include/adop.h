@@ -115,6 +115,11 @@ typedef struct {
     int32_t view_id_base;   /* global id of view 0 of this call (beta is keyed by it)       */
     const float *background;/* host [C] constant environment colour E (R18), NULL = zeros   */
     int32_t grad_accumulate;/* backward: 0 overwrite d_feat/d_pos/d_pose, 1 add into them   */
+    int32_t log_descriptors;/* tau stored as log, exp() when rasterized (NEXT-2) */
+    const float *env_map;   /* DEVICE [env_height][env_width][C] equirectangular environment
+                               map E of Eq. 7 sampled for empty pixels
+                               (R29), or NULL -> constant `background`          */
+    int32_t env_width, env_height;
 } adop_params;
 
 /* Buffers of one view (device).  See layouts above. */
@@ -189,15 +194,19 @@ ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n
  *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment),
  *   d_intrinsics [V][12]: sum over ghosts of (d(u0,v0)/d theta)^T g, theta = (fx, fy, cx, cy,
  *                 k1..k6, p1, p2) of the view's camera (the camera model C of Eq. 2, optimized by
- *                 the paper: Fig. 4); 0 for the distortion entries of a pinhole camera.
- * Any of d_feat / d_pos / d_pose / d_intrinsics may be NULL.  params->grad_accumulate selects
+ *                 the paper: Fig. 4); 0 for the distortion entries of a pinhole camera,
+ *   d_env [env_height][env_width][C]: environment-map gradient, every empty pixel's G
+ *                 scattered to its bilinear taps ("straightforward"); requires env_map.
+ * With log_descriptors the texture gradient includes d exp(tau)/d tau and the ghosts' Eq. 11
+ * uses the linear descriptor exp(tau).
+ * Any of d_feat / d_pos / d_pose / d_intrinsics / d_env may be NULL.  params->grad_accumulate selects
  * overwrite or add.  Points, cameras, poses and params must equal the forward's.
  * Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_WORKSPACE_TOO_SMALL, ADOP_ERR_CUDA. */
 ADOP_API adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image,
                                     float *d_feat, float *d_pos, double *d_pose, double *d_intrinsics,
-                                    void *workspace, size_t workspace_bytes, void *stream);
+                                    float *d_env, void *workspace, size_t workspace_bytes, void *stream);
 
 /* Debug / parity: per point and view, bit l (l < L) = valid, in bounds and kept
  * by the discard test at layer l; bit 7 = ghost.  mask: device uint8 [V][n]. */

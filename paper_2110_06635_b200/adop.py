@@ -54,7 +54,9 @@ class adop_pose(C.Structure):
 class adop_params(C.Structure):
     _fields_ = [("layers", C.c_int32), ("alpha", C.c_float), ("discard", C.c_int32), ("gamma", C.c_float),
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
-                ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32)]
+                ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32),
+                ("log_descriptors", C.c_int32), ("env_map", C.c_void_p), ("env_width", C.c_int32),
+                ("env_height", C.c_int32)]
 
 
 class adop_pyramid(C.Structure):
@@ -82,8 +84,8 @@ def lib():
         L.adop_rasterize_backward.restype = C.c_int
         L.adop_rasterize_backward.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose),
                                               P(adop_params), P(adop_pyramid), P(C.c_void_p), C.c_void_p,
-                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
-                                              C.c_void_p]
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_size_t, C.c_void_p]
         L.adop_point_masks.restype = C.c_int
         L.adop_point_masks.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params),
                                        C.c_void_p, C.c_void_p]
@@ -165,6 +167,16 @@ class Params:
         self._bg = (C.c_float * channels)(*bg) if bg is not None else None
         s.background = C.cast(self._bg, C.c_void_p) if self._bg is not None else None
         s.grad_accumulate = int(getattr(p, "grad_accumulate", 0))
+        s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
+        env = getattr(p, "env_map", None)
+        self.env = None
+        if env is not None:  # device [H][W][C] float32 (NEXT-2)
+            env = torch.as_tensor(env, dtype=torch.float32)
+            if not env.is_cuda:
+                env = env.cuda()
+            self.env = env.contiguous()
+            assert self.env.dim() == 3 and self.env.shape[2] == channels
+            s.env_map, s.env_height, s.env_width = self.env.data_ptr(), self.env.shape[0], self.env.shape[1]
         self.s = s
         self.layers = int(p.layers)
 
@@ -297,12 +309,15 @@ def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None):
 
 def rasterize_backward(points, cams, poses, params, pyrs, grads: Sequence[torch.Tensor], ws,
                        d_feat: Optional[torch.Tensor], d_pos: Optional[torch.Tensor],
-                       d_pose: Optional[torch.Tensor], d_intr: Optional[torch.Tensor] = None, stream=None):
-    """d_intr: optional [V][12] float64 camera-intrinsics gradient (fx, fy, cx, cy, k1..k6, p1, p2)."""
+                       d_pose: Optional[torch.Tensor], d_intr: Optional[torch.Tensor] = None,
+                       d_env: Optional[torch.Tensor] = None, stream=None):
+    """d_intr: optional [V][12] float64 camera-intrinsics gradient (fx, fy, cx, cy, k1..k6, p1, p2);
+    d_env: optional [H][W][C] float32 environment-map gradient (needs params.env_map)."""
     c = _Call(points, cams, poses, params, pyrs)
     g = (C.c_void_p * c.V)(*[t.data_ptr() for t in grads])
     _check(lib().adop_rasterize_backward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, g,
-                                         _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), _ptr(d_intr), ws.ptr, ws.nbytes,
+                                         _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), _ptr(d_intr), _ptr(d_env), ws.ptr,
+                                         ws.nbytes,
                                          _stream(stream)))
 
 
@@ -335,7 +350,7 @@ class Renderer:
             record_capacity = default_record_capacity(self.points.n, len(self.cams), params.layers, params.discard)
         self.ws = Workspace(self.points, self.cams, self.params, device, record_capacity)
         self.device = device
-        self.d_feat = self.d_pos = self.d_pose = self.d_intr = None
+        self.d_feat = self.d_pos = self.d_pose = self.d_intr = self.d_env = None
         self.intrinsics = intrinsics  # backward also produces d_intr [V][12] (NEXT-1)
 
     def forward(self, stream=None):
@@ -349,12 +364,14 @@ class Renderer:
         self.d_pose = torch.empty(len(self.cams), 6, dtype=torch.float64, device=self.device)
         if self.intrinsics:
             self.d_intr = torch.empty(len(self.cams), 12, dtype=torch.float64, device=self.device)
+        if self.params.env is not None:
+            self.d_env = torch.empty_like(self.params.env)
 
     def backward(self, grads: Sequence[torch.Tensor], stream=None):
         if self.d_feat is None:
             self.alloc_grads()
         rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,
-                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, stream)
+                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, self.d_env, stream)
         return self.d_feat, self.d_pos, self.d_pose
 
     def masks(self, stream=None) -> torch.Tensor:

@@ -99,6 +99,13 @@ adop_status check_params(const adop_params *pr) {
     if (!(pr->z_near >= 0.0f) || !std::isfinite(pr->z_near))
         return fail(ADOP_ERR_INVALID_ARGUMENT, "z_near must be finite and >= 0");
     if (pr->view_id_base < 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "view_id_base < 0");
+    if (pr->env_map) {
+        if (pr->env_width < 1 || pr->env_height < 1)
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "env_map: width/height < 1");
+        if ((int64_t)pr->env_width * pr->env_height >= (int64_t)1 << 31)
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "env_map too large");
+        if (!aligned(pr->env_map, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "env_map misaligned");
+    }
     return ok();
 }
 
@@ -196,7 +203,8 @@ uint64_t call_tag(const adop_points *pts, int32_t n_views, const adop_camera *ca
     f.add(cams, sizeof(adop_camera) * (size_t)n_views);
     f.add(poses, sizeof(adop_pose) * (size_t)n_views);
     f.put(pr->layers); f.put(pr->alpha); f.put(pr->discard); f.put(pr->gamma); f.put(pr->ghost_rate);
-    f.put(pr->z_near); f.put(pr->seed); f.put(pr->view_id_base);
+    f.put(pr->z_near); f.put(pr->seed); f.put(pr->view_id_base); f.put(pr->log_descriptors);
+    f.put(pr->env_map); f.put(pr->env_width); f.put(pr->env_height);
     for (int v = 0; views && v < n_views; ++v) f.put(views[v].keys);
     return f.h | 1ull;
 }
@@ -234,6 +242,10 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         a.dyn_tiles = mode;
     }
     for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
+    a.log_desc = pr->log_descriptors ? 1 : 0;
+    a.env = pr->env_map;
+    a.env_w = pr->env_map ? pr->env_width : 0;
+    a.env_h = pr->env_map ? pr->env_height : 0;
     if (ws) {
         a.hdr = ws->hdr;
         a.planes = reinterpret_cast<PlaneTab *>(reinterpret_cast<char *>(ws->hdr) + 256);
@@ -252,6 +264,7 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         std::memcpy(d.R, poses[v].R, sizeof(d.R));
         std::memcpy(d.t, poses[v].t, sizeof(d.t));
         d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+        d.model = c.model;
         if (c.model == ADOP_OPENCV8) {
             std::memcpy(d.k, c.k, sizeof(d.k));
             std::memcpy(d.p, c.p, sizeof(d.p));
@@ -504,8 +517,8 @@ adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, c
 adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image, float *d_feat,
-                                    float *d_pos, double *d_pose, double *d_intrinsics, void *workspace,
-                                    size_t workspace_bytes, void *stream) {
+                                    float *d_pos, double *d_pose, double *d_intrinsics, float *d_env,
+                                    void *workspace, size_t workspace_bytes, void *stream) {
     Ws ws;
     adop_status s = prologue(points, n_views, cameras, poses, params, fwd_views, workspace, workspace_bytes, true, ws);
     if (s) return s;
@@ -517,6 +530,8 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     if (d_pos && !aligned(d_pos, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pos misaligned");
     if (d_pose && !aligned(d_pose, 8)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_pose misaligned");
     if (d_intrinsics && !aligned(d_intrinsics, 8)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_intrinsics misaligned");
+    if (d_env && !params->env_map) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_env given without an env_map");
+    if (d_env && !aligned(d_env, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "d_env misaligned");
     int model;
     if (!uniform_model(n_views, cameras, model))
         return fail(ADOP_ERR_UNSUPPORTED, "all views of one call must use the same camera model");
@@ -529,6 +544,7 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
     a.d_pos = d_pos;
     a.d_intr = d_intrinsics;
     a.nterms = d_intrinsics ? 18 : 6;
+    a.d_env = d_env;
     if (points->n == 0) {
         if (d_pose && !params->grad_accumulate) {
             int e = (int)cudaMemsetAsync(d_pose, 0, sizeof(double) * 6 * n_views, (cudaStream_t)stream);
@@ -537,6 +553,10 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
         if (d_intrinsics && !params->grad_accumulate) {
             int e = (int)cudaMemsetAsync(d_intrinsics, 0, sizeof(double) * 12 * n_views, (cudaStream_t)stream);
             if (e) return cuda_status(e, "memset d_intrinsics");
+        }
+        if (d_env) {  // every pixel is background: E still gets its gradient
+            int e = launch_env_grad(a, stream);
+            if (e) return cuda_status(e, "env gradient launch");
         }
         return ok();
     }

@@ -181,6 +181,55 @@ __device__ __forceinline__ int layer_pixel(const VD &v, const Proj &p, int l, in
     return pv * v.wl[l] + pu;
 }
 
+// Linear-space descriptor channel (NEXT-2): exp(tau) for log descriptors.
+__device__ __forceinline__ float desc_lin(const RasterArgs &a, float t) { return a.log_desc ? expf(t) : t; }
+
+// Environment map E of Eq. 7 (NEXT-2, reading R29): bilinear taps (texel = row * W + col) and weights of
+// layer-l pixel (u, v): layer-0 (u 2^l, v 2^l), C^-1 (pinhole inverse; OpenCV8: 8 Newton steps on R6's
+// distortion map from the distorted coordinates), d = R^T (xn, yn, 1), lon = atan2(dx, dz),
+// lat = atan2(dy, hypot(dx, dz)), s = (lon / 2pi + 1/2) W - 1/2, t = (lat / pi + 1/2) H - 1/2; columns
+// wrap, rows clamp.  Continuous in (u, v) -> compared with the oracle's fp64 within tolerance.
+__device__ __forceinline__ void env_taps(const RasterArgs &a, const ViewDesc &v, int l, int u, int vv, int idx[4],
+                                         float w[4]) {
+    const float u0 = ldexpf((float)u, l), v0 = ldexpf((float)vv, l);
+    const float xd = (u0 - v.cx) / v.fx, yd = (v0 - v.cy) / v.fy;
+    float x = xd, y = yd;
+    if (v.model == ADOP_OPENCV8) {
+        for (int it = 0; it < 8; ++it) {
+            const float r2 = x * x + y * y;
+            const float num = 1.f + r2 * (v.k[0] + r2 * (v.k[1] + r2 * v.k[2]));
+            const float den = 1.f + r2 * (v.k[3] + r2 * (v.k[4] + r2 * v.k[5]));
+            const float dnum = v.k[0] + r2 * (2.f * v.k[1] + 3.f * r2 * v.k[2]);
+            const float dden = v.k[3] + r2 * (2.f * v.k[4] + 3.f * r2 * v.k[5]);
+            const float rad = num / den, drad = (dnum * den - num * dden) / (den * den);
+            const float fx_ = x * rad + 2.f * v.p[0] * x * y + v.p[1] * (r2 + 2.f * x * x);
+            const float fy_ = y * rad + v.p[0] * (r2 + 2.f * y * y) + 2.f * v.p[1] * x * y;
+            const float D00 = rad + 2.f * x * x * drad + 2.f * v.p[0] * y + 6.f * v.p[1] * x;
+            const float D01 = 2.f * x * y * drad + 2.f * v.p[0] * x + 2.f * v.p[1] * y;
+            const float D11 = rad + 2.f * y * y * drad + 6.f * v.p[0] * y + 2.f * v.p[1] * x;
+            const float rx = fx_ - xd, ry = fy_ - yd, idet = 1.f / (D00 * D11 - D01 * D01);
+            x -= (D11 * rx - D01 * ry) * idet;
+            y -= (-D01 * rx + D00 * ry) * idet;
+        }
+    }
+    const float dx = v.R[0] * x + v.R[3] * y + v.R[6], dy = v.R[1] * x + v.R[4] * y + v.R[7];
+    const float dz = v.R[2] * x + v.R[5] * y + v.R[8];
+    const float lon = atan2f(dx, dz), lat = atan2f(dy, sqrtf(dx * dx + dz * dz));
+    const float s = (lon * 0.15915494309189535f + 0.5f) * (float)a.env_w - 0.5f;
+    const float t = (lat * 0.3183098861837907f + 0.5f) * (float)a.env_h - 0.5f;
+    const float s0 = floorf(s), t0 = floorf(t), fs = s - s0, ft = t - t0;
+    int c0 = (int)s0 % a.env_w;
+    if (c0 < 0) c0 += a.env_w;
+    const int c1 = c0 + 1 == a.env_w ? 0 : c0 + 1;
+    const int r0i = (int)t0;
+    const int r0 = r0i < 0 ? 0 : (r0i >= a.env_h ? a.env_h - 1 : r0i);
+    const int r1 = r0i + 1 < 0 ? 0 : (r0i + 1 >= a.env_h ? a.env_h - 1 : r0i + 1);
+    idx[0] = r0 * a.env_w + c0; w[0] = (1.f - ft) * (1.f - fs);
+    idx[1] = r0 * a.env_w + c1; w[1] = (1.f - ft) * fs;
+    idx[2] = r1 * a.env_w + c0; w[2] = ft * (1.f - fs);
+    idx[3] = r1 * a.env_w + c1; w[3] = ft * fs;
+}
+
 __device__ __forceinline__ uint64_t depth_key(float Z, uint32_t gi) {
     return ((uint64_t)__float_as_uint(Z) << 32) | gi;  // R8
 }

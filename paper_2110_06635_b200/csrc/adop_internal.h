@@ -20,6 +20,7 @@ struct ViewDesc {
     float k[6];
     float p[2];
     float r2_max;
+    int32_t model;         // ADOP_PINHOLE / ADOP_OPENCV8 (runtime use: C^-1 of the environment map)
     float feff;            // fl(fl(fx + fy) * 0.5): focal length of the discard radius (R10)
     float ulo, uhi, vlo, vhi;  // conservative pre-cull window (pixels, all layers)
     float r2cull;          // OpenCV8 pre-cull on X^2+Y^2 <= r2cull Z^2
@@ -106,6 +107,10 @@ struct RasterArgs {
     uint32_t ghost_salt;
     int32_t grad_accumulate;
     float bg[ADOP_MAX_CHANNELS];
+    int32_t log_desc;      // NEXT-2: descriptors stored as log, linearized with exp()
+    const float *env;      // NEXT-2: environment map [env_h][env_w][C] (device) or NULL (R18 constant bg)
+    int32_t env_w, env_h;
+    float *d_env;          // backward: [env_h][env_w][C] environment-map gradient or NULL
     WsHeader *hdr;
     Record *records;       // record region: survivor records (front) + ghost list (back), see WsHeader
     int64_t rec_capacity;  // in 16-B slots
@@ -132,6 +137,7 @@ int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream
 int launch_resolve(const RasterArgs &a, void *stream);
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
 int launch_masks(const RasterArgs &a, int model, void *stream);
+int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed first unless grad_accumulate)
 int backward_grid(int sms);
 
 }  // namespace adop

@@ -177,9 +177,13 @@ __device__ __forceinline__ void accumulate_feature(const RasterArgs &a, const Vi
     float *acc = v.accum + (int64_t)pix * C;
     if (VEC4) {
         const uint64_t pol = policy_evict_first();
-        for (int c = 0; c < C; c += 4) red_add_v4(acc + c, ld_once4(f + c, pol));
+        for (int c = 0; c < C; c += 4) {
+            float4 t = ld_once4(f + c, pol);
+            if (a.log_desc) t = make_float4(expf(t.x), expf(t.y), expf(t.z), expf(t.w));
+            red_add_v4(acc + c, t);
+        }
     } else {
-        for (int c = 0; c < C; ++c) red_add(acc + c, __ldg(f + c));
+        for (int c = 0; c < C; ++c) red_add(acc + c, desc_lin(a, __ldg(f + c)));
     }
     red_add(v.count + pix, 1.0f);
 }
@@ -764,6 +768,21 @@ __global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ Rast
     }
 }
 
+// Environment-map background of channels c0..c0+3 at layer-l pixel j (NEXT-2, R29).
+__device__ __forceinline__ void env_bg4(const RasterArgs &a, const ViewDesc &v, int l, int j, int c0, float out[4]) {
+    int idx[4];
+    float w[4];
+    env_taps(a, v, l, j % v.wl[l], j / v.wl[l], idx, w);
+    const int C = a.channels;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+        float e = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) e = fmaf(w[k], __ldg(a.env + (int64_t)idx[k] * C + c0 + cc), e);
+        out[cc] = e;
+    }
+}
+
 // --------------------------------------------------------------------------- //
 // resolve: Eq. 7 (mean or background), planar per-layer output
 // --------------------------------------------------------------------------- //
@@ -793,9 +812,11 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (cn[q] > 0.0f) acc = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
                     const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+                    float bgv[4] = {a.bg[c0], a.bg[c0 + 1], a.bg[c0 + 2], a.bg[c0 + 3]};
+                    if (a.env && !(cn[q] > 0.0f)) env_bg4(a, v, l, (int)(j + q), c0, bgv);
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc)
-                        o[cc][q] = cn[q] > 0.0f ? __fdiv_rn(av[cc], cn[q]) : a.bg[c0 + cc];
+                        o[cc][q] = cn[q] > 0.0f ? __fdiv_rn(av[cc], cn[q]) : bgv[cc];
                 }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc)
@@ -814,6 +835,17 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
         const float cnt = __ldcs(v.count + p);
         float *img = v.image + (int64_t)C * v.off[l] + j;
         const float *acc = v.accum + p * C;
+        if (a.env && !(cnt > 0.0f)) {  // Eq. 7 first case: E(R^T C^-1(u, v)) (NEXT-2)
+            int idx[4];
+            float w[4];
+            env_taps(a, v, l, (int)(j % v.wl[l]), (int)(j / v.wl[l]), idx, w);
+            for (int c = 0; c < C; ++c) {
+                float e = 0.f;
+                for (int k = 0; k < 4; ++k) e = fmaf(w[k], __ldg(a.env + (int64_t)idx[k] * C + c), e);
+                __stcs(img + c * hw, e);
+            }
+            continue;
+        }
         for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fdiv_rn(acc[c], cnt) : a.bg[c]);
     }
 }
@@ -865,7 +897,7 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
     }
     const int C = a.channels, RS = a.prow;
     float *rows = const_cast<float *>(v.prow);
-    const bool v4 = (C & 3) == 0 && (reinterpret_cast<uintptr_t>(v.accum) & 15) == 0;
+    const bool v4 = (C & 3) == 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
         int l = 0;
@@ -878,31 +910,33 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
         float *row = rows + p * RS;
         const float cnt = __ldcs(v.count + p);
         const unsigned long long key = __ldcs(reinterpret_cast<const unsigned long long *>(v.keys) + p);
+        const float *Iv = v.image + (int64_t)C * v.off[l] + j;  // I exactly as k_resolve wrote it
         float S = 0.0f;
-        if (v4) {  // 16-B accum reads and row writes (C % 4 == 0)
+        if (v4) {  // 16-B row writes (C % 4 == 0)
             for (int c = 0; c < C; c += 4) {
                 const float4 g = make_float4(__ldcs(G + c * hw), __ldcs(G + (c + 1) * hw), __ldcs(G + (c + 2) * hw),
                                              __ldcs(G + (c + 3) * hw));
-                float4 I;
-                if (cnt > 0.0f) {
-                    const float4 sa = __ldcs(reinterpret_cast<const float4 *>(v.accum + p * C + c));
-                    I = make_float4(__fdiv_rn(sa.x, cnt), __fdiv_rn(sa.y, cnt), __fdiv_rn(sa.z, cnt),
-                                    __fdiv_rn(sa.w, cnt));
-                } else {
-                    I = make_float4(a.bg[c], a.bg[c + 1], a.bg[c + 2], a.bg[c + 3]);
-                }
-                S = fmaf(g.x, I.x, S);
-                S = fmaf(g.y, I.y, S);
-                S = fmaf(g.z, I.z, S);
-                S = fmaf(g.w, I.w, S);
+                S = fmaf(g.x, __ldcs(Iv + c * hw), S);
+                S = fmaf(g.y, __ldcs(Iv + (c + 1) * hw), S);
+                S = fmaf(g.z, __ldcs(Iv + (c + 2) * hw), S);
+                S = fmaf(g.w, __ldcs(Iv + (c + 3) * hw), S);
                 __stcg(reinterpret_cast<float4 *>(row + 4 + c), g);
             }
         } else {
             for (int c = 0; c < C; ++c) {
                 const float g = __ldcs(G + c * hw);
-                const float I = cnt > 0.0f ? __fdiv_rn(__ldcs(v.accum + p * C + c), cnt) : a.bg[c];
-                S = fmaf(g, I, S);
+                S = fmaf(g, __ldcs(Iv + c * hw), S);
                 row[4 + c] = g;
+            }
+        }
+        if (a.d_env && !(cnt > 0.0f)) {  // NEXT-2: dL/dE of the empty pixel's bilinear taps
+            int idx[4];
+            float w[4];
+            env_taps(a, v, l, (int)(j % v.wl[l]), (int)(j / v.wl[l]), idx, w);
+            for (int c = 0; c < C; ++c) {
+                const float g = row[4 + c];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) red_add(a.d_env + (int64_t)idx[k] * C + c, w[k] * g);
             }
         }
         __stcg(reinterpret_cast<uint4 *>(row),
@@ -1029,13 +1063,16 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                         const float *G = v.grad + (int64_t)C * v.off[l] + loc;
                         if (CT > 0) {
 #pragma unroll
-                            for (int c = 0; c < CR; ++c) dt[c] += __fdiv_rn(__ldg(G + c * hw), cnt);
+                            for (int c = 0; c < CR; ++c)
+                                dt[c] += __fdiv_rn(__ldg(G + c * hw), cnt) * (a.log_desc ? expf(__ldg(a.feat + i * C + c)) : 1.0f);
                         } else if (a.d_feat) {
-                            for (int c = 0; c < C; ++c) a.d_feat[i * C + c] += __fdiv_rn(__ldg(G + c * hw), cnt);
+                            for (int c = 0; c < C; ++c)
+                                a.d_feat[i * C + c] += __fdiv_rn(__ldg(G + c * hw), cnt) *
+                                                       (a.log_desc ? expf(__ldg(a.feat + i * C + c)) : 1.0f);
                         }
                     } else {
                         if (!tau_loaded) {
-                            for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + i * C + c);
+                            for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + i * C + c));
                             tau_loaded = true;
                         }
                         // Eqs. 9-11: signed central differences over the 4-neighbourhood (R14, R15)
@@ -1111,7 +1148,8 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
 // rendered hits when they were written by a call with the same inputs (tag) and did not
 // overflow -> the texture gradient consumes them and the sweep only collects ghosts (mode 1); otherwise
 // the sweep re-renders every point into fresh lists (mode 0).  Either way the ghost list starts empty.
-__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m, WsHeader *hdr,
+__global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m, float *r, int64_t rn,
+                                                   WsHeader *hdr,
                                                    double *inline_row, int inline_len, unsigned long long tag) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0 && hdr) {
@@ -1130,9 +1168,9 @@ __global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q
     }
     if (inline_row && tid < inline_len) inline_row[tid] = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    float *bufs[2] = {p, q};
-    const int64_t lens[2] = {n, m};
-    for (int b = 0; b < 2; ++b) {
+    float *bufs[3] = {p, q, r};
+    const int64_t lens[3] = {n, m, rn};
+    for (int b = 0; b < 3; ++b) {
         float *x = bufs[b];
         const int64_t len = lens[b];
         if (!x) continue;
@@ -1267,6 +1305,11 @@ __device__ __forceinline__ void tex_hit(const RasterArgs &a, const ViewDesc &v, 
     const uint4 e = __ldcg(reinterpret_cast<const uint4 *>(row));
     if (!(z <= fmul(a.onepa, __uint_as_float(e.x)))) return;  // fuzzy test (Eq. 6, R9)
     const int C = a.channels;
+    if (a.log_desc) {  // d exp(tau)/d tau = exp(tau) (NEXT-2)
+        for (int c = 0; c < C; ++c)
+            red_add(a.d_feat + idx * C + c, __fdiv_rn(__ldcg(row + 4 + c), __uint_as_float(e.y)) * expf(__ldg(a.feat + idx * C + c)));
+        return;
+    }
     red_add_row(a.d_feat + idx * C, row + 4, C, __uint_as_float(e.y));
 }
 
@@ -1277,7 +1320,7 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
                                             int64_t idx, int nt, double *tt, float *g = nullptr) {
     const int C = CT > 0 ? CT : a.channels;
     float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
-    for (int c = 0; c < C; ++c) tau[c] = __ldg(a.feat + idx * C + c);
+    for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + idx * C + c));  // linear space
     float gu = 0.f, gv = 0.f;
     bool gc = false;
     for (int l = 0; l < nk; ++l) {
@@ -1776,6 +1819,32 @@ int launch_resolve(const RasterArgs &a, void *stream) {
     return (int)cudaGetLastError();
 }
 
+// The argument block with the backward's pixel-table pointers (workspace table region).
+static RasterArgs with_tables(const RasterArgs &a) {
+    RasterArgs b = a;
+    char *base = reinterpret_cast<char *>(a.tables);
+    int64_t off = 0;
+    b.prow = 4 + ((a.channels + 3) & ~3);  // row stride in floats (16-B multiple)
+    for (int v = 0; v < a.nviews; ++v) {
+        b.v[v].prow = reinterpret_cast<const float *>(base + off);
+        off += (int64_t)a.v[v].pixels * b.prow * (int64_t)sizeof(float);
+    }
+    return b;
+}
+
+int launch_env_grad(const RasterArgs &a, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!a.d_env || !a.tables) return (int)cudaErrorInvalidValue;
+    if (!a.grad_accumulate)
+        cudaMemsetAsync(a.d_env, 0, sizeof(float) * (size_t)a.env_w * a.env_h * a.channels, s);
+    int64_t maxP = 1;
+    for (int v = 0; v < a.nviews; ++v) maxP = a.v[v].pixels > maxP ? a.v[v].pixels : maxP;
+    int64_t bx = (maxP + kThreads - 1) / kThreads;
+    if (bx > 2048) bx = 2048;
+    k_bwd_prep<<<dim3((unsigned)bx, (unsigned)a.nviews), kThreads, 0, s>>>(with_tables(a));
+    return (int)cudaGetLastError();
+}
+
 int backward_grid(int sms) {
     int g = sms * 8;
     return g > kMaxBwdBlocks ? kMaxBwdBlocks : g;
@@ -1789,7 +1858,14 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     const bool fast = VEC && a.tables != nullptr && a.rec_capacity >= 4 * kChunk &&
                       (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
                       (!a.radius || (reinterpret_cast<uintptr_t>(a.radius) & 15) == 0);
+    RasterArgs b = with_tables(a);
+    b.grad_accumulate = 1;  // every kernel below adds into the (zeroed or caller's) gradients
+    const int64_t n_env = a.d_env ? (int64_t)a.env_w * a.env_h * a.channels : 0;
     if (!fast) {  // planar fused sweep (unaligned inputs or a small workspace)
+        if (a.d_env) {  // the environment-map gradient comes from the pixel-table pass
+            int e = launch_env_grad(a, stream);
+            if (e) return e;
+        }
         auto k = k_backward<MODEL, VEC, CT>;
         int g = resident_grid(k, sms, kWarps * 128, a.n);
         if (g > grid_cap) g = grid_cap;
@@ -1798,16 +1874,6 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
             k_pose_reduce<<<a.nviews * a.nterms, 256, 0, s>>>(a.pose_partials, g, a.nviews, a.nterms, d_pose, a.d_intr,
                                                               a.grad_accumulate);
         return (int)cudaGetLastError();
-    }
-    RasterArgs b = a;
-    b.grad_accumulate = 1;  // every kernel below adds into the (zeroed or caller's) gradients
-    // pixel tables in their own workspace region
-    char *base = reinterpret_cast<char *>(a.tables);
-    int64_t off = 0;
-    b.prow = 4 + ((a.channels + 3) & ~3);  // row stride in floats (16-B multiple)
-    for (int v = 0; v < a.nviews; ++v) {
-        b.v[v].prow = reinterpret_cast<const float *>(base + off);
-        off += (int64_t)a.v[v].pixels * b.prow * (int64_t)sizeof(float);
     }
     // ghost-list kernel grid (its per-block pose partials) and the inline-overflow row after them
     int gg = sms * 4;
@@ -1820,7 +1886,9 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         int64_t bx = (mx / 4 + kThreads - 1) / kThreads;
         if (bx > (int64_t)sms * 8) bx = (int64_t)sms * 8;
         if (bx < 1) bx = 1;
-        k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np, a.hdr,
+        const int64_t ne = fill ? n_env : 0;
+        k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np,
+                                                ne ? a.d_env : nullptr, ne, a.hdr,
                                                 a.pose_partials + (int64_t)gg * a.nviews * a.nterms, a.nviews * a.nterms,
                                                 a.tag);
     }

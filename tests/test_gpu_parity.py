@@ -365,3 +365,49 @@ def test_backward_consumes_forward_lists_or_resweeps():
     r.forward()  # a fresh forward makes the lists consumable again
     r.backward(G)
     assert _hdr(r.ws)["mode"] == 1
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-2: environment map (R29) and logarithmic descriptors
+# --------------------------------------------------------------------------- #
+def smooth_env(H, W, C, seed=0):
+    """Low-frequency equirectangular map (so fp32-vs-fp64 direction differences stay far below tolerance)."""
+    rng = np.random.default_rng(seed)
+    lon = (np.arange(W) + 0.5) / W * 2 * np.pi - np.pi
+    lat = (np.arange(H) + 0.5) / H * np.pi - np.pi / 2
+    LA, LO = np.meshgrid(lat, lon, indexing="ij")
+    chans = [0.5 + 0.3 * np.sin(LO + rng.uniform(0, 6)) * np.cos(LA) + 0.1 * np.sin(2 * LA + rng.uniform(0, 6))
+             for _ in range(C)]
+    return np.stack(chans, -1).astype(np.float32)
+
+
+@pytest.mark.parametrize("cfg,log", [(0, False), (0, True), (2, False), (2, True)])
+def test_env_map_and_log_descriptors_fwd_bwd(cfg, log):
+    w = S.workload(cfg, n=60_000 if cfg else None)
+    C = w.cloud.channels
+    prm = dataclasses.replace(w.params, discard=True, ghost_rate=0.3, log_descriptors=log,
+                              env_map=smooth_env(32, 64, C, seed=cfg))
+    cloud = w.cloud
+    if cfg == 0:
+        cloud = dataclasses.replace(w.cloud, radius=torch.full_like(w.cloud.radius, 0.02))
+    if log:  # descriptors in log space (U(0,1) -> [-1.5, 0.5])
+        cloud = dataclasses.replace(cloud, feat=cloud.feat * 2 - 1.5)
+    G = grads_for(w.cameras, prm.layers, C)
+    r = run_gpu(cloud, w.cameras, w.poses, prm, grads=G)
+    _, fwd, bwd = run_oracle(cloud, w.cameras, w.poses, prm, grads=G)
+    compare_forward(r, fwd, ctx=f"env cfg{cfg} log={log}")
+    compare_backward(r, bwd, ctx=f"env cfg{cfg} log={log}")
+    assert r.d_env is not None and r.d_env.abs().sum() > 0
+    assert np.abs(bwd.dx).sum() > 0 and np.abs(bwd.dtau).sum() > 0
+
+
+def test_env_map_gradient_with_empty_cloud():
+    cam = S.pinhole(64, 48)
+    cloud = S.Cloud(torch.zeros(3, 0), torch.zeros(0), torch.zeros(0, 4))
+    prm = S.Params(layers=3, env_map=smooth_env(16, 32, 4, seed=3))
+    G = grads_for([cam], 3, 4)
+    r = run_gpu(cloud, [cam], [S.tiny_pose()], prm, grads=G)
+    _, fwd, bwd = run_oracle(cloud, [cam], [S.tiny_pose()], prm, grads=G)
+    compare_forward(r, fwd, ctx="env empty")
+    compare_backward(r, bwd, ctx="env empty", check_feat=False, check_pos=False)
+    assert r.d_env.abs().sum() > 0
