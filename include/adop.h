@@ -120,6 +120,9 @@ typedef struct {
                                map E of Eq. 7 sampled for empty pixels
                                (R29), or NULL -> constant `background`          */
     int32_t env_width, env_height;
+    int32_t spatial_rendered;/* backward: 0 = ghost gradients (spatial gradients for ghosts only,
+                               §4.3, Fig. 4); 1 = ghost gradients disabled, the §6.2 baseline
+                               (L584-590): Eqs. 9-11 for the rendered points (R31)  */
 } adop_params;
 
 /* Buffers of one view (device).  See layouts above. */
@@ -190,7 +193,8 @@ ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n
  * the unaligned path) every point is re-projected.  Results are the same either way.
  * It produces
  *   d_feat [n][C]: sum over views/layers of G/|Lambda| for rendered points (ghosts 0),
- *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17),
+ *   d_pos  [3][n]: ghost points only: R^T J^T g, g from Eqs. 9-11 (R14-R17) (rendered points
+ *                  instead with params->spatial_rendered),
  *   d_pose [V][6]: sum over ghosts of (w, Xc x w), w = J^T g (Eq. 17 left increment),
  *   d_intrinsics [V][12]: sum over ghosts of (d(u0,v0)/d theta)^T g, theta = (fx, fy, cx, cy,
  *                 k1..k6, p1, p2) of the view's camera (the camera model C of Eq. 2, optimized by

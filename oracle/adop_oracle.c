@@ -60,6 +60,9 @@ typedef struct {
     uint64_t seed;
     int32_t view_id_base;
     int32_t log_descriptors; /* NEXT-2: tau stored as log, linearized by exp() when rasterized */
+    int32_t spatial_rendered;/* NEXT-3 (R31): 0 = ghost gradients (spatial gradients for ghosts only, §4.3);
+                                1 = ghost gradients disabled (the §6.2 baseline): Eqs. 9-11
+                                for the rendered points, none for ghosts */
 } orc_params;
 
 typedef struct {             /* NEXT-2: spherical environment map E of Eq. 7, R29 */
@@ -700,9 +703,12 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                         if (dtau_abs) dtau_abs[i * C + ch] += fabs(t);
                     }
                 }
-                continue;
+                if (!pr->spatial_rendered) continue;
+            } else if (pr->spatial_rendered) {
+                continue;  /* ghost gradients disabled: ghosts take no part at all */
             }
-            /* ghost point: image-space gradient summed over layers in layer-0 pixels (R17) */
+            /* spatial gradient (ghost point, or a rendered point with ghost gradients disabled): image-space
+             * gradient of Eqs. 9-11 summed over layers in layer-0 pixels (R17) */
             double gu = 0.0, gv = 0.0, ga[4] = {0, 0, 0, 0};
             for (int l = 0; l < pr->layers; ++l) {
                 if (!(m & (1u << l))) continue;

@@ -45,7 +45,7 @@ class _Pose(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("layers", C.c_int32), ("alpha", C.c_float), ("discard", C.c_int32), ("gamma", C.c_float),
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
-                ("view_id_base", C.c_int32), ("log_descriptors", C.c_int32)]
+                ("view_id_base", C.c_int32), ("log_descriptors", C.c_int32), ("spatial_rendered", C.c_int32)]
 
 
 class _Env(C.Structure):
@@ -132,6 +132,7 @@ def params_struct(p) -> _Params:
     s.layers, s.alpha, s.discard, s.gamma = int(p.layers), p.alpha, int(bool(p.discard)), p.gamma
     s.ghost_rate, s.z_near, s.seed, s.view_id_base = p.ghost_rate, p.z_near, int(p.seed), int(p.view_id_base)
     s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
+    s.spatial_rendered = int(bool(getattr(p, "spatial_rendered", False)))
     return s
 
 

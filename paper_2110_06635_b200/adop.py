@@ -56,7 +56,7 @@ class adop_params(C.Structure):
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
                 ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32),
                 ("log_descriptors", C.c_int32), ("env_map", C.c_void_p), ("env_width", C.c_int32),
-                ("env_height", C.c_int32)]
+                ("env_height", C.c_int32), ("spatial_rendered", C.c_int32)]
 
 
 class adop_pyramid(C.Structure):
@@ -168,6 +168,7 @@ class Params:
         s.background = C.cast(self._bg, C.c_void_p) if self._bg is not None else None
         s.grad_accumulate = int(getattr(p, "grad_accumulate", 0))
         s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
+        s.spatial_rendered = int(bool(getattr(p, "spatial_rendered", False)))
         env = getattr(p, "env_map", None)
         self.env = None
         if env is not None:  # device [H][W][C] float32 (NEXT-2)

@@ -243,6 +243,7 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     }
     for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
     a.log_desc = pr->log_descriptors ? 1 : 0;
+    a.spatial_rendered = pr->spatial_rendered ? 1 : 0;
     a.env = pr->env_map;
     a.env_w = pr->env_map ? pr->env_width : 0;
     a.env_h = pr->env_map ? pr->env_height : 0;

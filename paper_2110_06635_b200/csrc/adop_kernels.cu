@@ -1057,8 +1057,8 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                     if (!ghost) {
                         // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
                         const int q = v.off[l] + loc;
-                        if (!fuzzy_pass(p.Z, v.keys[q], a.onepa)) continue;
                         const float cnt = v.count[q];
+                        if (fuzzy_pass(p.Z, v.keys[q], a.onepa)) {
                         const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
                         const float *G = v.grad + (int64_t)C * v.off[l] + loc;
                         if (CT > 0) {
@@ -1070,7 +1070,9 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                                 a.d_feat[i * C + c] += __fdiv_rn(__ldg(G + c * hw), cnt) *
                                                        (a.log_desc ? expf(__ldg(a.feat + i * C + c)) : 1.0f);
                         }
-                    } else {
+                        }
+                    }
+                    if (a.spatial_rendered ? !ghost : ghost) {  // spatial gradient (R22 / R31)
                         if (!tau_loaded) {
                             for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + i * C + c));
                             tau_loaded = true;
@@ -1427,7 +1429,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
             }
         }
     }
-    const bool gh = nk > 0 && ghost;
+    const bool gh = nk > 0 && (a.spatial_rendered ? !ghost : ghost);  // spatial-gradient list (R22 / R31)
     const unsigned bg = __ballot_sync(kFull, gh);
     if (bg == 0u) return;
     const unsigned long long slot = list_take<true>(a, cg, bg, gh, lane, lt);
@@ -1601,7 +1603,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         if (GO) {
             // mode 1: only ghosts (~rho of the points) are left to find -- compact them, then pre-cull and
             // project only those, 32 per warp iteration (every lane busy)
-            const uint32_t gm = ghosts & (uint32_t)vmask;
+            const uint32_t gm = (a.spatial_rendered ? ~ghosts : ghosts) & (uint32_t)vmask;  // R22 / R31
             int gn = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -1630,7 +1632,8 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                         bool cand = in && precull_fma_z<MODEL>(v, x, y, z, Zf, mz);
                         if (a.discard) cand = cand && maybe_kept(a, v, rw, Zf, mz, gi);
                         if (__any_sync(kFull, cand))
-                            bwd_emit<MODEL, CT>(a, v, vs, cand, true, x, y, z, rw, base + e, gi, ct, cg, false, lane, lt);
+                            bwd_emit<MODEL, CT>(a, v, vs, cand, !a.spatial_rendered, x, y, z, rw, base + e, gi, ct, cg,
+                                                false, lane, lt);
                     }
                 }
             }

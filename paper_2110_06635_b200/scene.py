@@ -97,6 +97,7 @@ class Params:
     background: Optional[List[float]] = None  # constant E; None -> zeros
     log_descriptors: bool = False  # NEXT-2: tau stored as log, exp() when rasterized
     env_map: Optional[object] = None  # NEXT-2: [H][W][C] float32 equirectangular E of Eq. 7 (R29); None -> background
+    spatial_rendered: bool = False  # NEXT-3: ghost gradients disabled, Eqs. 9-11 for rendered points (R31)
 
 
 # --------------------------------------------------------------------------- #

@@ -411,3 +411,15 @@ def test_env_map_gradient_with_empty_cloud():
     compare_forward(r, fwd, ctx="env empty")
     compare_backward(r, bwd, ctx="env empty", check_feat=False, check_pos=False)
     assert r.d_env.abs().sum() > 0
+
+
+@pytest.mark.parametrize("ghost,cfg", [(0.0, 2), (0.25, 2), (0.0, 1)])
+def test_spatial_gradients_for_rendered_points(ghost, cfg):
+    """NEXT-3 (R31): ghost gradients disabled (the §6.2 baseline): Eqs. 9-11 for the rendered points."""
+    w = S.workload(cfg, n=80_000, n_views=2 if cfg == 1 else None)
+    prm = dataclasses.replace(w.params, ghost_rate=ghost, spatial_rendered=True)
+    G = grads_for(w.cameras, prm.layers, w.cloud.channels)
+    r = run_gpu(w.cloud, w.cameras, w.poses, prm, grads=G)
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, prm, grads=G)
+    compare_backward(r, bwd, ctx=f"spatial_rendered rho={ghost}")
+    assert np.count_nonzero(np.abs(bwd.dx).sum(0)) > 1000

@@ -324,3 +324,54 @@ def test_intrinsics_gradient_sums_pinhole_chain_rule_per_ghost():
         ref += [gu * Xc[0] / Xc[2], gv * Xc[1] / Xc[2], gu, gv]
     np.testing.assert_allclose(bwd.dintr[0, :4], ref, rtol=1e-6, atol=1e-9)
     assert not bwd.dintr[0, 4:].any()
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-3 (R31): ghost gradients disabled -- the §6.2 baseline: Eqs. 9-11 for rendered points
+# --------------------------------------------------------------------------- #
+def test_spatial_rendered_equals_ghost_gradient_of_the_same_point():
+    """Eq. 11 only reads the NEIGHBOUR pixels' state (R14), which a point never changes (it lands on its own
+    pixel), so the rendered-point spatial gradient of point i equals the ghost gradient i gets when it is
+    made a ghost instead -- exactly; the texture gradients of the other points are unchanged."""
+    cam = _cam(32, 8, 8.0, 16.0, 4.0)
+    c = 1.0 / 64
+    render = [_at_pixel(cam, u, 4, 2.0) for u in range(32)] + [_at_pixel(cam, u, 3, 2.5) for u in range(0, 32, 3)]
+    feats = [[c * u] for u in range(32)] + [[0.3]] * 11
+    probe = _at_pixel(cam, 16.2, 4.1, 1.0)
+    prm_t = dataclasses.replace(GPRM, spatial_rendered=True)
+    G = _grad_image(cam, 1, 1, 0.0)
+    G[0, :] = np.linspace(-1, 1, G.shape[1], dtype=F)
+    # (a) probe rendered, ghost gradients disabled
+    pts_a, _ = arrange(render + [probe], [], GPRM, feats + [[c * 16]], [])
+    fwd_a = O.forward(pts_a, [cam], [IDENT], prm_t)
+    b_a = O.backward(pts_a, [cam], [IDENT], prm_t, fwd_a, G)
+    ia = pts_a.n - 1
+    while pts_a.pos[2, ia] < 0:
+        ia -= 1
+    # (b) probe as a ghost, ghost gradients on
+    pts_b, gids = arrange(render, [probe], GPRM, feats, [[c * 16]])
+    fwd_b = O.forward(pts_b, [cam], [IDENT], GPRM)
+    b_b = O.backward(pts_b, [cam], [IDENT], GPRM, fwd_b, G)
+    assert np.abs(b_b.dx[:, gids[0]]).sum() > 0
+    np.testing.assert_array_equal(b_a.dx[:, ia], b_b.dx[:, gids[0]])
+    # every rendered point now has a spatial gradient (incl. the ramp points), the pose sums them all
+    assert np.count_nonzero(np.abs(b_a.dx).sum(0)) > 20
+    assert b_a.dtau[ia, 0] != 0.0  # and keeps its texture gradient
+
+
+def test_spatial_rendered_mode_gives_ghosts_nothing():
+    room = S.make_room(4.0)
+    cloud = S.room_cloud(4000, room, 2, seed=8)
+    pts = O.Points.from_cloud(cloud)
+    pts = O.Points(pts.pos, np.full(pts.n, 0.02, F), pts.feat)
+    cams, poses = [S.pinhole(80, 60)], S.room_poses(1, room, seed=9)
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.3, seed=3)
+    prm_t = dataclasses.replace(prm, spatial_rendered=True)
+    fwd = O.forward(pts, cams, poses, prm)
+    G = S.grad_pyramid(1, 2, fwd.count.shape[1], seed=12).numpy()
+    b = O.backward(pts, cams, poses, prm, fwd, G)
+    bt = O.backward(pts, cams, poses, prm_t, fwd, G)
+    np.testing.assert_array_equal(bt.dtau, b.dtau)  # texture gradients do not depend on the mode
+    ghost = np.array([O.is_ghost(prm, i) for i in range(pts.n)])
+    assert not bt.dx[:, ghost].any() and np.abs(bt.dx[:, ~ghost]).sum() > 0
+    assert not b.dx[:, ~ghost].any()
