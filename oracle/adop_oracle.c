@@ -63,6 +63,8 @@ typedef struct {
     int32_t spatial_rendered;/* NEXT-3 (R31): 0 = ghost gradients (spatial gradients for ghosts only, §4.3);
                                 1 = ghost gradients disabled (the §6.2 baseline): Eqs. 9-11
                                 for the rendered points, none for ghosts */
+    int32_t normal_culling;  /* NEXT-3, Eq. 5, R32: 0 off; +1 keep iff (Rn).Xc > 0 (as printed);
+                                -1 keep iff (Rn).Xc < 0 (the flipped orientation) */
 } orc_params;
 
 typedef struct {             /* NEXT-2: spherical environment map E of Eq. 7, R29 */
@@ -79,6 +81,7 @@ typedef struct {
     float radius_uniform;
     const float *feat;     /* [n][C] */
     int32_t channels;
+    const float *normal;   /* NEXT-3: SoA [3][pos_stride] point normals n of Eq. 1, or NULL */
 } orc_points;
 
 #define ORC_SENTINEL 0x7FFFFFFFFFFFFFFFULL /* R8: empty pixel */
@@ -224,6 +227,16 @@ static unsigned point_mask(const orc_points *pts, int64_t i, const orc_camera *c
     float x = pos[i], y = pos[pts->pos_stride + i], z = pos[2 * pts->pos_stride + i];
     unsigned m = orc_is_ghost(pr, gi) ? 0x80u : 0u;
     if (!orc_project(c, P, x, y, z, pr->z_near, proj)) return m;
+    if (pr->normal_culling && pts->normal) {
+        /* Eq. 5 as R32: sign of (R n) . Xc in the pinned fp32 order of R1 (|Xc| > 0 drops out) */
+        const float *nv = pts->normal;
+        float nx = nv[i], ny = nv[pts->pos_stride + i], nz = nv[2 * pts->pos_stride + i];
+        float ncx = (P->R[0] * nx + P->R[1] * ny) + P->R[2] * nz;
+        float ncy = (P->R[3] * nx + P->R[4] * ny) + P->R[5] * nz;
+        float ncz = (P->R[6] * nx + P->R[7] * ny) + P->R[8] * nz;
+        float dot = (ncx * proj[0] + ncy * proj[1]) + ncz * proj[2];
+        if (!(pr->normal_culling > 0 ? dot > 0.0f : dot < 0.0f)) return m;
+    }
     int nk = keep_layers(pr, c, point_radius(pts, i), proj[5], view, gi);
     for (int l = 0; l < pr->layers; ++l) {
         pix[l] = layer_pixel(c, proj[3], proj[4], l);

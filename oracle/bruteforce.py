@@ -78,13 +78,24 @@ def project(cam, pose, x: F, y: F, z: F, z_near: F):
     return X, Y, Z, u0, v0, iz
 
 
-def forward(pos, radius, feat, cam, pose, params, view: int = 0, global_offset: int = 0):
+def forward(pos, radius, feat, cam, pose, params, view: int = 0, global_offset: int = 0, normal=None):
     """Per-pixel definition of Eqs. 2-7 for one view -> (keys, count, image[C*P])."""
     with np.errstate(all="ignore"):
-        return _forward(pos, radius, feat, cam, pose, params, view, global_offset)
+        return _forward(pos, radius, feat, cam, pose, params, view, global_offset, normal)
 
 
-def _forward(pos, radius, feat, cam, pose, params, view, global_offset):
+def normal_kept(pose, n, X: F, Y: F, Z: F, mode: int) -> bool:
+    """Eq. 5 with reading R32: sign of (R n) . Xc, pinned fp32 order; mode +1 as printed, -1 flipped."""
+    R = np.asarray(pose.R, dtype=F).reshape(9)
+    nx, ny, nz = F(n[0]), F(n[1]), F(n[2])
+    ncx = F(F(F(R[0] * nx) + F(R[1] * ny)) + F(R[2] * nz))
+    ncy = F(F(F(R[3] * nx) + F(R[4] * ny)) + F(R[5] * nz))
+    ncz = F(F(F(R[6] * nx) + F(R[7] * ny)) + F(R[8] * nz))
+    dot = F(F(F(ncx * X) + F(ncy * Y)) + F(ncz * Z))
+    return bool(dot > 0) if mode > 0 else bool(dot < 0)
+
+
+def _forward(pos, radius, feat, cam, pose, params, view, global_offset, normal):
     L = params.layers
     n = pos.shape[1]
     C = feat.shape[1]
@@ -108,6 +119,9 @@ def _forward(pos, radius, feat, cam, pose, params, view, global_offset):
         if pr is None:
             continue
         X, Y, Z, u0, v0, iz = pr
+        mode = int(getattr(params, "normal_culling", 0))
+        if mode and normal is not None and not normal_kept(pose, normal[:, i], X, Y, Z, mode):
+            continue
         nkeep = L
         if params.discard:
             feff = F(F(F(cam.fx) + F(cam.fy)) * F(0.5))

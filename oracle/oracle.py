@@ -45,7 +45,8 @@ class _Pose(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("layers", C.c_int32), ("alpha", C.c_float), ("discard", C.c_int32), ("gamma", C.c_float),
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
-                ("view_id_base", C.c_int32), ("log_descriptors", C.c_int32), ("spatial_rendered", C.c_int32)]
+                ("view_id_base", C.c_int32), ("log_descriptors", C.c_int32), ("spatial_rendered", C.c_int32),
+                ("normal_culling", C.c_int32)]
 
 
 class _Env(C.Structure):
@@ -55,7 +56,7 @@ class _Env(C.Structure):
 class _Points(C.Structure):
     _fields_ = [("n", C.c_int64), ("global_offset", C.c_int64), ("pos_stride", C.c_int64),
                 ("pos", C.c_void_p), ("radius", C.c_void_p), ("radius_uniform", C.c_float),
-                ("feat", C.c_void_p), ("channels", C.c_int32)]
+                ("feat", C.c_void_p), ("channels", C.c_int32), ("normal", C.c_void_p)]
 
 
 _lib = None
@@ -133,6 +134,7 @@ def params_struct(p) -> _Params:
     s.ghost_rate, s.z_near, s.seed, s.view_id_base = p.ghost_rate, p.z_near, int(p.seed), int(p.view_id_base)
     s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
     s.spatial_rendered = int(bool(getattr(p, "spatial_rendered", False)))
+    s.normal_culling = int(getattr(p, "normal_culling", 0))
     return s
 
 
@@ -152,8 +154,10 @@ class Points:
     """Host-side point shard: keeps the numpy arrays alive while the struct points at them."""
 
     def __init__(self, pos: np.ndarray, radius: Optional[np.ndarray], feat: np.ndarray,
-                 global_offset: int = 0, radius_uniform: float = 0.0):
+                 global_offset: int = 0, radius_uniform: float = 0.0, normal: Optional[np.ndarray] = None):
         self.pos = np.ascontiguousarray(pos, dtype=np.float32)
+        self.normal = None if normal is None else np.ascontiguousarray(normal, dtype=np.float32)
+        assert self.normal is None or self.normal.shape == self.pos.shape
         self.radius = None if radius is None else np.ascontiguousarray(radius, dtype=np.float32)
         self.feat = np.ascontiguousarray(feat, dtype=np.float32)
         self.n = self.pos.shape[1]
@@ -162,11 +166,14 @@ class Points:
         s.n, s.global_offset, s.pos_stride = self.n, int(global_offset), self.n
         s.pos, s.radius, s.radius_uniform = _ptr(self.pos), _ptr(self.radius), radius_uniform
         s.feat, s.channels = _ptr(self.feat), self.C
+        s.normal = _ptr(self.normal)
         self.s = s
 
     @staticmethod
     def from_cloud(cloud, global_offset: int = 0) -> "Points":
-        return Points(cloud.pos.cpu().numpy(), cloud.radius.cpu().numpy(), cloud.feat.cpu().numpy(), global_offset)
+        nrm = getattr(cloud, "normal", None)
+        return Points(cloud.pos.cpu().numpy(), cloud.radius.cpu().numpy(), cloud.feat.cpu().numpy(), global_offset,
+                      normal=None if nrm is None else nrm.cpu().numpy())
 
 
 def _arrays(cams, poses):

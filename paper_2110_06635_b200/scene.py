@@ -68,6 +68,7 @@ class Cloud:
     pos: torch.Tensor      # (3, N) float32 SoA: rows x, y, z
     radius: torch.Tensor   # (N,) float32 world radius
     feat: torch.Tensor     # (N, C) float32 neural descriptor tau
+    normal: Optional[torch.Tensor] = None  # (3, N) float32 SoA unit normals n of Eq. 1 (Eq. 5 culling), optional
 
     @property
     def n(self) -> int:
@@ -78,10 +79,12 @@ class Cloud:
         return int(self.feat.shape[1])
 
     def to(self, device) -> "Cloud":
-        return Cloud(self.pos.to(device), self.radius.to(device), self.feat.to(device))
+        return Cloud(self.pos.to(device), self.radius.to(device), self.feat.to(device),
+                     None if self.normal is None else self.normal.to(device))
 
     def slice(self, a: int, b: int) -> "Cloud":
-        return Cloud(self.pos[:, a:b].contiguous(), self.radius[a:b].contiguous(), self.feat[a:b].contiguous())
+        return Cloud(self.pos[:, a:b].contiguous(), self.radius[a:b].contiguous(), self.feat[a:b].contiguous(),
+                     None if self.normal is None else self.normal[:, a:b].contiguous())
 
 
 @dataclasses.dataclass
@@ -98,6 +101,7 @@ class Params:
     log_descriptors: bool = False  # NEXT-2: tau stored as log, exp() when rasterized
     env_map: Optional[object] = None  # NEXT-2: [H][W][C] float32 equirectangular E of Eq. 7 (R29); None -> background
     spatial_rendered: bool = False  # NEXT-3: ghost gradients disabled, Eqs. 9-11 for rendered points (R31)
+    normal_culling: int = 0  # NEXT-3: Eq. 5 (R32): 0 off, +1 keep (Rn).Xc > 0 as printed, -1 flipped
 
 
 # --------------------------------------------------------------------------- #
@@ -144,6 +148,7 @@ def room_cloud(n: int, room: Room, channels: int = 4, noise: float = 0.005, radi
     radii = torch.tensor(room.radii, dtype=torch.float32, device=device)
     g = _gen(seed, device)
     pos = torch.empty(3, n, dtype=torch.float32, device=device)
+    nrm = torch.empty(3, n, dtype=torch.float32, device=device)
     for a in range(0, n, chunk):
         b = min(n, a + chunk)
         m = b - a
@@ -165,12 +170,17 @@ def room_cloud(n: int, room: Room, channels: int = 4, noise: float = 0.005, radi
         sid = (surf - 6).clamp(min=0)
         sph = centers[sid].T + radii[sid] * d
         p = torch.where((surf >= 6).unsqueeze(0), sph, p)
+        # normals (no random draws): walls face the room's inside, spheres outward
+        nw = torch.zeros(3, m, dtype=torch.float32, device=device)
+        for ax in range(3):
+            nw[ax] = torch.where((axis == ax) & (surf < 6), -sign, nw[ax])
+        nrm[:, a:b] = torch.where((surf >= 6).unsqueeze(0), d, nw)
         p += torch.randn(3, m, generator=g, device=device) * noise
         pos[:, a:b] = p
     gf = _gen(seed + SEED_FEATURES, device)
     feat = torch.rand(n, channels, generator=gf, device=device, dtype=torch.float32)
     rad = torch.full((n,), radius, dtype=torch.float32, device=device)
-    return Cloud(pos, rad, feat)
+    return Cloud(pos, rad, feat, nrm)
 
 
 def _split_bits(x: torch.Tensor) -> torch.Tensor:
@@ -210,7 +220,8 @@ def _ragged_arange(lens: torch.Tensor) -> torch.Tensor:
 
 
 def apply_order(cloud: Cloud, perm: torch.Tensor) -> Cloud:
-    return Cloud(cloud.pos[:, perm].contiguous(), cloud.radius[perm].contiguous(), cloud.feat[perm].contiguous())
+    return Cloud(cloud.pos[:, perm].contiguous(), cloud.radius[perm].contiguous(), cloud.feat[perm].contiguous(),
+                 None if cloud.normal is None else cloud.normal[:, perm].contiguous())
 
 
 # --------------------------------------------------------------------------- #

@@ -396,3 +396,47 @@ def test_ghost_split_fraction_and_invisibility():
     fwd3 = O.forward(pts3, [cam2], [IDENT], dataclasses.replace(prm, ghost_rate=0.0))
     assert g.sum() > 100
     assert np.array_equal(fwd.keys, fwd3.keys) and np.array_equal(fwd.image, fwd3.image)
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-3: normal culling, Eq. 5 with reading R32
+# --------------------------------------------------------------------------- #
+def _with_normals(pts, normal):
+    return O.Points(pts.pos, pts.radius, pts.feat, int(pts.s.global_offset), normal=normal)
+
+
+def test_normal_culling_closed_form():
+    """A point on the optical axis at z = 2 (Xc = (0,0,2)) with normal (0,0,-1) (facing the camera):
+    (R n).Xc = -2 < 0 -> culled by Eq. 5 as printed (+1), kept by the flipped test (-1); (0,0,+1) the reverse."""
+    cam = _cam(16, 16, 8.0)
+    for nz, keep_printed in ((-1.0, False), (1.0, True)):
+        pts = _with_normals(_points(np.array([[0.0, 0.0, 2.0]], F), np.ones((1, 1), F), None),
+                            np.array([[0.0], [0.0], [nz]], F))
+        for mode, kept in ((0, True), (1, keep_printed), (-1, not keep_printed)):
+            m = O.point_masks(pts, [cam], [IDENT], S.Params(layers=2, discard=False, normal_culling=mode))[0]
+            assert bool(m[0] & 1) == kept, (nz, mode)
+
+
+@pytest.mark.parametrize("seed,model,mode", [(30, S.PINHOLE, 1), (31, S.PINHOLE, -1), (32, S.OPENCV8, -1)])
+def test_normal_culling_equals_bruteforce_and_removal(seed, model, mode):
+    pts, cam, prm = _random_scene(seed, model=model, discard=True, rho=0.2)
+    rng = np.random.default_rng(seed)
+    nrm = rng.normal(size=(3, pts.n)).astype(F)
+    nrm /= np.linalg.norm(nrm, axis=0, keepdims=True)
+    pts = _with_normals(pts, nrm)
+    prm = dataclasses.replace(prm, normal_culling=mode)
+    fwd = O.forward(pts, [cam], [IDENT], prm)
+    keys, count, image = BF.forward(pts.pos, pts.radius, pts.feat, cam, IDENT, prm, view=0,
+                                    global_offset=int(pts.s.global_offset), normal=nrm)
+    assert np.array_equal(fwd.keys[0], keys) and np.array_equal(fwd.count[0], count)
+    np.testing.assert_allclose(fwd.image[0], image, rtol=0, atol=1e-12)
+    # culled points take no part: same result as moving them behind the camera
+    culled = [i for i in range(pts.n)
+              if (r := BF.project(cam, IDENT, *pts.pos[:, i], F(0.0))) is not None
+              and not BF.normal_kept(IDENT, nrm[:, i], r[0], r[1], r[2], mode)]
+    assert len(culled) > 100
+    pos2 = pts.pos.copy()
+    pos2[2, culled] = -1.0
+    off = O.forward(O.Points(pos2, pts.radius, pts.feat, int(pts.s.global_offset)), [cam], [IDENT],
+                    dataclasses.replace(prm, normal_culling=0))
+    assert np.array_equal(fwd.keys, off.keys) and np.array_equal(fwd.count, off.count)
