@@ -83,6 +83,8 @@ typedef struct {
     float radius_uniform;   /* used when radius == NULL                                     */
     const float *feat;      /* device [n][C] neural descriptor tau                         */
     int32_t channels;       /* C, 1..32                                                     */
+    const float *normal;    /* device SoA [3][pos_stride] normals n of Eq. 1 (Eq. 5 culling),
+                               or NULL; required when params->normal_culling != 0        */
 } adop_points;
 
 /* Camera model C of Eq. 2 (R6): pinhole, or OpenCV rational 8-coefficient distortion
@@ -123,6 +125,9 @@ typedef struct {
     int32_t spatial_rendered;/* backward: 0 = ghost gradients (spatial gradients for ghosts only,
                                §4.3, Fig. 4); 1 = ghost gradients disabled, the §6.2 baseline
                                (L584-590): Eqs. 9-11 for the rendered points (R31)  */
+    int32_t normal_culling; /* Eq. 5 (L208) normal culling, R32: 0 off; +1 keep points
+                               with (R n).(R x + t) > 0 as printed; -1 keep < 0 (the flipped
+                               orientation: outward normals facing the camera)              */
 } adop_params;
 
 /* Buffers of one view (device).  See layouts above. */

@@ -38,7 +38,7 @@ class AdopError(RuntimeError):
 class adop_points(C.Structure):
     _fields_ = [("n", C.c_int64), ("global_offset", C.c_int64), ("pos_stride", C.c_int64),
                 ("pos", C.c_void_p), ("radius", C.c_void_p), ("radius_uniform", C.c_float),
-                ("feat", C.c_void_p), ("channels", C.c_int32)]
+                ("feat", C.c_void_p), ("channels", C.c_int32), ("normal", C.c_void_p)]
 
 
 class adop_camera(C.Structure):
@@ -56,7 +56,7 @@ class adop_params(C.Structure):
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
                 ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32),
                 ("log_descriptors", C.c_int32), ("env_map", C.c_void_p), ("env_width", C.c_int32),
-                ("env_height", C.c_int32), ("spatial_rendered", C.c_int32)]
+                ("env_height", C.c_int32), ("spatial_rendered", C.c_int32), ("normal_culling", C.c_int32)]
 
 
 class adop_pyramid(C.Structure):
@@ -119,21 +119,25 @@ class Points:
     """adop_points over torch CUDA tensors (keeps them alive).  pos: (3, N) or (3, stride) float32."""
 
     def __init__(self, pos: torch.Tensor, radius: Optional[torch.Tensor], feat: torch.Tensor,
-                 global_offset: int = 0, radius_uniform: float = 0.0, n: Optional[int] = None):
+                 global_offset: int = 0, radius_uniform: float = 0.0, n: Optional[int] = None,
+                 normal: Optional[torch.Tensor] = None):
         assert pos.dtype == torch.float32 and pos.dim() == 2 and pos.shape[0] == 3 and pos.stride(1) == 1
         assert feat.dtype == torch.float32 and feat.dim() == 2 and feat.is_contiguous()
-        self.pos, self.radius, self.feat = pos, radius, feat
+        # normals (Eq. 5 culling) share the positions' SoA stride
+        assert normal is None or (normal.dtype == torch.float32 and normal.shape[0] == 3 and normal.stride() == pos.stride())
+        self.pos, self.radius, self.feat, self.normal = pos, radius, feat, normal
         self.n = int(feat.shape[0]) if n is None else int(n)
         self.channels = int(feat.shape[1])
         s = adop_points()
         s.n, s.global_offset, s.pos_stride = self.n, int(global_offset), int(pos.stride(0))
         s.pos, s.radius, s.radius_uniform = _ptr(pos), _ptr(radius), float(radius_uniform)
         s.feat, s.channels = _ptr(feat), self.channels
+        s.normal = _ptr(normal)
         self.s = s
 
     @staticmethod
     def from_cloud(cloud, global_offset: int = 0) -> "Points":
-        return Points(cloud.pos, cloud.radius, cloud.feat, global_offset)
+        return Points(cloud.pos, cloud.radius, cloud.feat, global_offset, normal=getattr(cloud, "normal", None))
 
 
 def camera_struct(cam) -> adop_camera:
@@ -169,6 +173,7 @@ class Params:
         s.grad_accumulate = int(getattr(p, "grad_accumulate", 0))
         s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
         s.spatial_rendered = int(bool(getattr(p, "spatial_rendered", False)))
+        s.normal_culling = int(getattr(p, "normal_culling", 0))
         env = getattr(p, "env_map", None)
         self.env = None
         if env is not None:  # device [H][W][C] float32 (NEXT-2)

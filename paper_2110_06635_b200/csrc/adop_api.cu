@@ -84,6 +84,13 @@ adop_status check_points(const adop_points *pts, bool need_feat) {
         return fail(ADOP_ERR_INVALID_ARGUMENT, "radius_uniform must be finite and >= 0");
     if (need_feat && !pts->feat) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->feat is NULL");
     if (pts->feat && !aligned(pts->feat, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "feat not aligned");
+    if (pts->normal && !aligned(pts->normal, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "normal not aligned");
+    return ok();
+}
+
+adop_status check_culling(const adop_points *pts, const adop_params *pr) {
+    if (pr->normal_culling && pts->n > 0 && !pts->normal)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "normal_culling needs points->normal");
     return ok();
 }
 
@@ -204,7 +211,8 @@ uint64_t call_tag(const adop_points *pts, int32_t n_views, const adop_camera *ca
     f.add(poses, sizeof(adop_pose) * (size_t)n_views);
     f.put(pr->layers); f.put(pr->alpha); f.put(pr->discard); f.put(pr->gamma); f.put(pr->ghost_rate);
     f.put(pr->z_near); f.put(pr->seed); f.put(pr->view_id_base); f.put(pr->log_descriptors);
-    f.put(pr->env_map); f.put(pr->env_width); f.put(pr->env_height);
+    f.put(pr->env_map); f.put(pr->env_width); f.put(pr->env_height); f.put(pr->normal_culling);
+    f.put(pts->normal);
     for (int v = 0; views && v < n_views; ++v) f.put(views[v].keys);
     return f.h | 1ull;
 }
@@ -244,6 +252,10 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     for (int c = 0; c < pts->channels; ++c) a.bg[c] = pr->background ? pr->background[c] : 0.0f;
     a.log_desc = pr->log_descriptors ? 1 : 0;
     a.spatial_rendered = pr->spatial_rendered ? 1 : 0;
+    a.normal_cull = pr->normal_culling > 0 ? 1 : (pr->normal_culling < 0 ? -1 : 0);
+    a.nrm = pts->normal;
+    a.nrm_stride = pts->pos_stride;
+    if (!pts->normal) a.normal_cull = 0;
     a.env = pr->env_map;
     a.env_w = pr->env_map ? pr->env_width : 0;
     a.env_h = pr->env_map ? pr->env_height : 0;
@@ -404,6 +416,7 @@ adop_status prologue(const adop_points *points, int32_t n_views, const adop_came
     adop_status s;
     if ((s = check_params(params))) return s;
     if ((s = check_points(points, need_feat))) return s;
+    if ((s = check_culling(points, params))) return s;
     if ((s = check_views(n_views, cameras, poses, params, views, points->channels, true))) return s;
     if ((s = carve_workspace(workspace, workspace_bytes,
                              table_bytes(n_views, cameras, params->layers, points->channels), ws)))
@@ -571,6 +584,7 @@ adop_status adop_point_masks(const adop_points *points, int32_t n_views, const a
     adop_status s;
     if ((s = check_params(params))) return s;
     if ((s = check_points(points, false))) return s;
+    if ((s = check_culling(points, params))) return s;
     if ((s = check_views(n_views, cameras, poses, params, nullptr, points->channels, false))) return s;
     if (!mask && points->n > 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "mask is NULL");
     int model;

@@ -181,6 +181,20 @@ __device__ __forceinline__ int layer_pixel(const VD &v, const Proj &p, int l, in
     return pv * v.wl[l] + pu;
 }
 
+// Normal culling, Eq. 5 with reading R32: sign of (R n) . Xc in the pinned fp32 order of R1
+// (|Xc| > 0 drops out); normal_cull +1 keeps (Rn).Xc > 0 as printed, -1 keeps < 0.  The normal is gathered
+// only here, on the exact path of the points that survived the pre-cull.
+__device__ __forceinline__ bool normal_keep(const RasterArgs &a, const ViewDesc &v, int64_t i, float X, float Y,
+                                            float Z) {
+    if (a.normal_cull == 0) return true;
+    const float nx = __ldg(a.nrm + i), ny = __ldg(a.nrm + a.nrm_stride + i), nz = __ldg(a.nrm + 2 * a.nrm_stride + i);
+    const float ncx = fadd(fadd(fmul(v.R[0], nx), fmul(v.R[1], ny)), fmul(v.R[2], nz));
+    const float ncy = fadd(fadd(fmul(v.R[3], nx), fmul(v.R[4], ny)), fmul(v.R[5], nz));
+    const float ncz = fadd(fadd(fmul(v.R[6], nx), fmul(v.R[7], ny)), fmul(v.R[8], nz));
+    const float dot = fadd(fadd(fmul(ncx, X), fmul(ncy, Y)), fmul(ncz, Z));
+    return a.normal_cull > 0 ? dot > 0.0f : dot < 0.0f;
+}
+
 // Linear-space descriptor channel (NEXT-2): exp(tau) for log descriptors.
 __device__ __forceinline__ float desc_lin(const RasterArgs &a, float t) { return a.log_desc ? expf(t) : t; }
 

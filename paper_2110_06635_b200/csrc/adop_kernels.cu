@@ -213,7 +213,8 @@ __device__ __forceinline__ void stream_sweep(const RasterArgs &a) {
             for (int vs = 0; vs < a.nviews; ++vs) {
                 const ViewDesc &v = a.v[vs];
                 Proj p;
-                const bool ok = live && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p);
+                const bool ok = live && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p) &&
+                                normal_keep(a, v, i, p.X, p.Y, p.Z);
                 if (MODE == MODE_MASKS) {
                     unsigned m = ghost ? 0x80u : 0u;
                     if (ok) {
@@ -501,7 +502,7 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     int nk = 0;
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
+        if (p.Z > a.z_near && p.Z <= 3.402823466e38f && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
             p.iz = __frcp_rn(p.Z);
             nk = keep_layers(a, v, rw, p.iz, gi);
         }
@@ -1044,7 +1045,8 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
             for (int vs = 0; vs < a.nviews; ++vs) {
                 const ViewDesc &v = a.v[vs];
                 Proj p;
-                const bool ok = in && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p);
+                const bool ok = in && project_point<MODEL>(v, a.z_near, px[j], py[j], pz[j], p) &&
+                                normal_keep(a, v, i, p.X, p.Y, p.Z);
                 if (!__any_sync(kFull, ok)) continue;
                 const int nk = ok ? keep_layers(a, v, pr[j], p.iz, gi) : 0;
                 float gu = 0.f, gv = 0.f;
@@ -1400,7 +1402,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     int nk = 0;
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (p.Z > a.z_near && p.Z <= 3.402823466e38f) {
+        if (p.Z > a.z_near && p.Z <= 3.402823466e38f && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
             p.iz = __frcp_rn(p.Z);
             nk = keep_layers(a, v, rw, p.iz, gi);
             if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;

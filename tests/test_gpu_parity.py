@@ -423,3 +423,25 @@ def test_spatial_gradients_for_rendered_points(ghost, cfg):
     _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, prm, grads=G)
     compare_backward(r, bwd, ctx=f"spatial_rendered rho={ghost}")
     assert np.count_nonzero(np.abs(bwd.dx).sum(0)) > 1000
+
+
+@pytest.mark.parametrize("mode,cfg", [(1, 2), (-1, 2), (-1, 1), (-1, 0)])
+def test_normal_culling_fwd_bwd(mode, cfg):
+    """NEXT-3: Eq. 5 normal culling (R32) -- keys/counts/masks bit-exact, gradients within tolerance."""
+    w = S.workload(cfg, n=80_000 if cfg else None, n_views=2 if cfg == 1 else None)
+    cloud = w.cloud
+    if cloud.normal is None:  # configs[0] (uniform cube): random unit normals
+        g = torch.Generator().manual_seed(9)
+        nrm = torch.randn(3, cloud.n, generator=g)
+        cloud = dataclasses.replace(cloud, normal=nrm / nrm.norm(dim=0, keepdim=True))
+    prm = dataclasses.replace(w.params, ghost_rate=0.25, normal_culling=mode)
+    G = grads_for(w.cameras, prm.layers, cloud.channels)
+    r = run_gpu(cloud, w.cameras, w.poses, prm, grads=G)
+    _, fwd, bwd = run_oracle(cloud, w.cameras, w.poses, prm, grads=G)
+    compare_forward(r, fwd, ctx=f"normal culling {mode}")
+    compare_backward(r, bwd, ctx=f"normal culling {mode}")
+    m = r.masks().cpu().numpy()
+    om = O.point_masks(O.Points.from_cloud(cloud.to("cpu")), w.cameras, w.poses, prm)
+    assert np.array_equal(m, om)
+    base = run_gpu(cloud, w.cameras, w.poses, dataclasses.replace(prm, normal_culling=0))
+    assert (r.pyrs[0].count.sum() < base.pyrs[0].count.sum()).item()  # something was culled
