@@ -229,6 +229,30 @@ ADOP_API adop_status adop_point_masks(const adop_points *points, int32_t n_views
 ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream,
                                  int64_t *records, int64_t *ghost_entries, int32_t *overflowed);
 
+/* ---- Preprocessing before the hot path (untimed setup) ------------- */
+
+/* Scratch bytes of the preprocessing calls for n points and Morton blocks of `block` points. */
+ADOP_API adop_status adop_prep_workspace_size(int64_t n, int32_t block, size_t *bytes);
+
+/* Blocked Morton shuffle (§4.5; R34): positions quantized to 21 bits per
+ * axis over the cloud's bounding box (fp32, pinned order), 63-bit Morton codes, stable sort by
+ * (code, index), blocks of `block` points ordered by (hash(seed, block), block).  perm: device
+ * int64 [n], perm[j] = the old index of the point that goes to position j.  points->n in [1, 2^31).
+ * workspace: 256-byte aligned, adop_prep_workspace_size bytes.  Enqueued on `stream`. */
+ADOP_API adop_status adop_blocked_morton_order(const adop_points *points, int32_t block, uint64_t seed, int64_t *perm,
+                                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* dst.x[j] = src.x[perm[j]] for positions, radii, descriptors and normals present in both
+ * (device buffers; dst must match src's n, channels and pos_stride; dst->pos etc. are written). */
+ADOP_API adop_status adop_apply_order(const adop_points *src, const int64_t *perm, const adop_points *dst,
+                             void *stream);
+
+/* World radius r_world of every point "inside its local neighborhood" (§4.4; R33):
+ * the median distance to its k nearest other points (1 <= k <= 32, n >= k + 1), floored at
+ * 1e-9 x the bounding-box diagonal; exact (ring search over Morton cells).  radius: device [n]. */
+ADOP_API adop_status adop_knn_radius(const adop_points *points, int32_t k, float *radius, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
 /* Thread-local description of the last non-OK status ("" if none). */
 ADOP_API const char *adop_last_error(void);
 

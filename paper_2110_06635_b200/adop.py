@@ -97,6 +97,15 @@ def lib():
         L.adop_workspace_stats.restype = C.c_int
         L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int64),
                                            P(C.c_int32)]
+        L.adop_prep_workspace_size.restype = C.c_int
+        L.adop_prep_workspace_size.argtypes = [C.c_int64, C.c_int32, P(C.c_size_t)]
+        L.adop_blocked_morton_order.restype = C.c_int
+        L.adop_blocked_morton_order.argtypes = [P(adop_points), C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                C.c_size_t, C.c_void_p]
+        L.adop_apply_order.restype = C.c_int
+        L.adop_apply_order.argtypes = [P(adop_points), C.c_void_p, P(adop_points), C.c_void_p]
+        L.adop_knn_radius.restype = C.c_int
+        L.adop_knn_radius.argtypes = [P(adop_points), C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.adop_last_error.restype = C.c_char_p
         L.adop_version.restype = C.c_char_p
         _lib = L
@@ -331,6 +340,48 @@ def point_masks(points, cams, poses, params, mask: torch.Tensor, stream=None):
     c = _Call(points, cams, poses, params, None)
     _check(lib().adop_point_masks(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), mask.data_ptr(),
                                   _stream(stream)))
+
+
+# --------------------------------------------------------------------------- #
+# preprocessing (NEXT-4): blocked Morton shuffle, kNN world radius
+# --------------------------------------------------------------------------- #
+def _prep_ws(n: int, block: int, device):
+    size = C.c_size_t(0)
+    _check(lib().adop_prep_workspace_size(int(n), int(block), C.byref(size)))
+    buf = torch.empty(int(size.value) + 256, dtype=torch.uint8, device=device)
+    return buf, (buf.data_ptr() + 255) // 256 * 256, int(size.value)
+
+
+def blocked_morton_order(points: Points, block: int = 1024, seed: int = 0, stream=None) -> torch.Tensor:
+    """int64 permutation of the blocked Morton shuffle (R34): perm[j] = old index."""
+    dev = points.pos.device
+    buf, ptr, size = _prep_ws(points.n, block, dev)
+    perm = torch.empty(points.n, dtype=torch.int64, device=dev)
+    _check(lib().adop_blocked_morton_order(C.byref(points.s), int(block), int(seed), perm.data_ptr(), ptr, size,
+                                           _stream(stream)))
+    del buf  # torch's caching allocator only reuses the block for work ordered after this stream's
+    return perm
+
+
+def apply_order(points: Points, perm: torch.Tensor, stream=None) -> Points:
+    """A new Points whose arrays are points' arrays gathered by perm (positions, radii, descriptors, normals)."""
+    pos = torch.empty_like(points.pos)
+    rad = None if points.radius is None else torch.empty_like(points.radius)
+    feat = torch.empty_like(points.feat)
+    nrm = None if points.normal is None else torch.empty_like(points.normal)
+    dst = Points(pos, rad, feat, int(points.s.global_offset), float(points.s.radius_uniform), points.n, normal=nrm)
+    _check(lib().adop_apply_order(C.byref(points.s), perm.data_ptr(), C.byref(dst.s), _stream(stream)))
+    return dst
+
+
+def knn_radius(points: Points, k: int = 8, stream=None) -> torch.Tensor:
+    """r_world (R33): median distance to the k nearest neighbours, float32 [n]."""
+    dev = points.pos.device
+    buf, ptr, size = _prep_ws(points.n, 1, dev)
+    r = torch.empty(points.n, dtype=torch.float32, device=dev)
+    _check(lib().adop_knn_radius(C.byref(points.s), int(k), r.data_ptr(), ptr, size, _stream(stream)))
+    del buf  # (as above)
+    return r
 
 
 def version() -> str:

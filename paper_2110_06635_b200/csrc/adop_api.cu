@@ -15,8 +15,16 @@
 using namespace adop;
 
 namespace {
-
 thread_local char g_err[512] = "";
+}  // namespace
+
+// shared with adop_prep.cu: record the last error message (thread-local) and return s
+adop_status adop::set_status(adop_status s, const char *msg) {
+    std::snprintf(g_err, sizeof(g_err), "%s", msg ? msg : "");
+    return s;
+}
+
+namespace {
 
 adop_status fail(adop_status s, const char *fmt, ...) {
     va_list ap;

@@ -142,6 +142,7 @@ int launch_resolve(const RasterArgs &a, void *stream);
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
 int launch_masks(const RasterArgs &a, int model, void *stream);
 int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed first unless grad_accumulate)
+adop_status set_status(adop_status s, const char *msg);  // thread-local last-error message (adop_api.cu)
 int backward_grid(int sms);
 
 }  // namespace adop
