@@ -789,7 +789,8 @@ __device__ __forceinline__ void env_bg4(const RasterArgs &a, const ViewDesc &v, 
 // --------------------------------------------------------------------------- //
 // Groups of 4 consecutive pixels of one layer (host guarantees off_l and h_l*w_l are multiples of 4
 // when VEC4): one 16-B count load, accum read only for covered pixels, one 16-B store per channel plane.
-template <bool VEC4>
+// ENV: empty pixels sample the environment map (NEXT-2); a separate instance keeps the plain path lean.
+template <bool VEC4, bool ENV>
 __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     const int C = a.channels;
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
                     if (cn[q] > 0.0f) acc = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
                     const float av[4] = {acc.x, acc.y, acc.z, acc.w};
                     float bgv[4] = {a.bg[c0], a.bg[c0 + 1], a.bg[c0 + 2], a.bg[c0 + 3]};
-                    if (a.env && !(cn[q] > 0.0f)) env_bg4(a, v, l, (int)(j + q), c0, bgv);
+                    if (ENV && !(cn[q] > 0.0f)) env_bg4(a, v, l, (int)(j + q), c0, bgv);
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc)
                         o[cc][q] = cn[q] > 0.0f ? __fdiv_rn(av[cc], cn[q]) : bgv[cc];
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
         const float cnt = __ldcs(v.count + p);
         float *img = v.image + (int64_t)C * v.off[l] + j;
         const float *acc = v.accum + p * C;
-        if (a.env && !(cnt > 0.0f)) {  // Eq. 7 first case: E(R^T C^-1(u, v)) (NEXT-2)
+        if (ENV && !(cnt > 0.0f)) {  // Eq. 7 first case: E(R^T C^-1(u, v)) (NEXT-2)
             int idx[4];
             float w[4];
             env_taps(a, v, l, (int)(j % v.wl[l]), (int)(j / v.wl[l]), idx, w);
@@ -1817,10 +1818,14 @@ int launch_resolve(const RasterArgs &a, void *stream) {
             if ((a.v[v].off[l] & 3) || (((int64_t)a.v[v].wl[l] * a.v[v].hl[l]) & 3)) v4 = false;
         if (a.v[v].pixels & 3) v4 = false;
     }
-    if (v4)
-        k_resolve<true><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
-    else
-        k_resolve<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(a);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a.env) {
+        if (v4) k_resolve<true, true><<<grid, kThreads, 0, s>>>(a);
+        else k_resolve<false, true><<<grid, kThreads, 0, s>>>(a);
+    } else {
+        if (v4) k_resolve<true, false><<<grid, kThreads, 0, s>>>(a);
+        else k_resolve<false, false><<<grid, kThreads, 0, s>>>(a);
+    }
     return (int)cudaGetLastError();
 }
 
