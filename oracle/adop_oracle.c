@@ -38,7 +38,8 @@
 #include <float.h>
 
 typedef struct {
-    int32_t width, height, model; /* model 0 = pinhole, 1 = OpenCV rational 8-coefficient (R6) */
+    int32_t width, height, model; /* model 0 = pinhole, 1 = OpenCV rational 8-coefficient (R6),
+                                     2 = equidistant fisheye with distance depth (R35; r2_max holds theta_max) */
     float fx, fy, cx, cy;
     float k[6];
     float p[2];
@@ -151,6 +152,28 @@ int orc_is_ghost(const orc_params *pr, uint32_t gi)
 /* Pinned fp32 order (R1, R2, R6).  Returns 1 if the point is valid (R7).    */
 /* out: [0..2] = Xc, [3] = u0, [4] = v0, [5] = 1/z                            */
 /* ------------------------------------------------------------------------- */
+/* R35: atan(t) for t in [0, 1] as t * P(t^2), a fixed degree-9 polynomial (max error 1e-7 rad) evaluated
+ * by Horner in fp32 with one rounding per operation -- the GPU evaluates the same operations, so the
+ * fisheye's pixel decisions stay bit-identical. */
+static float atan01(float t)
+{
+    static const float c[10] = {-0.0015244261594489217f, 0.009669913910329342f, -0.028764614835381508f,
+                                0.05541255697607994f, -0.08245089650154114f, 0.10893233865499496f,
+                                -0.14251546561717987f, 0.1999710500240326f, -0.33333227038383484f, 1.0f};
+    float u = t * t, p = c[0];
+    for (int k = 1; k < 10; ++k) p = p * u + c[k];
+    return t * p;
+}
+/* angle in [0, pi] of (x, y) with y >= 0 (R35) */
+float orc_atan2p(float y, float x)
+{
+    const float PI = 3.14159265358979f, HALF_PI = 1.57079632679490f;
+    float ax = fabsf(x), a;
+    if (y <= ax) a = ax > 0.0f ? atan01(y / ax) : 0.0f;
+    else a = HALF_PI - atan01(ax / y);
+    return x >= 0.0f ? a : PI - a;
+}
+
 int orc_project(const orc_camera *c, const orc_pose *P, float x, float y, float z, float z_near, float *out)
 {
     const float *R = P->R, *t = P->t;
@@ -158,6 +181,23 @@ int orc_project(const orc_camera *c, const orc_pose *P, float x, float y, float 
     float Y = ((R[3] * x + R[4] * y) + R[5] * z) + t[1];
     float Z = ((R[6] * x + R[7] * y) + R[8] * z) + t[2];
     out[0] = X; out[1] = Y; out[2] = Z;
+    out[6] = Z;  /* the depth of keys / Eq. 6 (R4): camera z, or the distance for the fisheye */
+    if (c->model == 2) {
+        /* R35 equidistant fisheye: theta = angle to the optical axis, r_d = f theta, depth = |Xc| */
+        float rho2 = X * X + Y * Y;
+        float d = sqrtf(rho2 + Z * Z);
+        out[6] = d;
+        if (!(d > z_near && d <= FLT_MAX)) return 0;
+        float rho = sqrtf(rho2);
+        float th = orc_atan2p(rho, Z);
+        if (!(th <= c->r2_max)) return 0;  /* outside the field of view theta_max */
+        float s = rho > 0.0f ? th / rho : 0.0f;
+        float xd = X * s, yd = Y * s;
+        out[3] = c->fx * xd + c->cx;
+        out[4] = c->fy * yd + c->cy;
+        out[5] = 1.0f / d;
+        return 1;
+    }
     if (!(Z > z_near && Z <= FLT_MAX)) return 0; /* behind camera / non-finite: culled (R7) */
     float iz = 1.0f / Z;
     float xn = X * iz, yn = Y * iz;
@@ -249,7 +289,7 @@ void orc_point_masks(const orc_points *pts, int32_t n_views, const orc_camera *c
                      const orc_params *pr, uint8_t *mask /*[V][n]*/)
 {
     int64_t pix[8];
-    float proj[6];
+    float proj[7];
     for (int v = 0; v < n_views; ++v)
         for (int64_t i = 0; i < pts->n; ++i)
             mask[(int64_t)v * pts->n + i] =
@@ -345,8 +385,16 @@ void orc_env_taps(const orc_env *e, const double *d, int64_t *idx, double *w)
 void orc_env_dir(const orc_camera *c, const orc_pose *P, int l, int64_t u, int64_t v, double *d)
 {
     double xn, yn;
-    orc_unproject(c, ldexp((double)u, l), ldexp((double)v, l), &xn, &yn);
-    const double dc[3] = {xn, yn, 1.0};
+    double dc[3];
+    if (c->model == 2) {  /* R35: theta = |(xd, yd)|, direction (sin theta xd / theta, sin theta yd / theta, cos theta) */
+        double xd = (ldexp((double)u, l) - (double)c->cx) / (double)c->fx;
+        double yd = (ldexp((double)v, l) - (double)c->cy) / (double)c->fy;
+        double th = sqrt(xd * xd + yd * yd), s = th > 0.0 ? sin(th) / th : 1.0;
+        dc[0] = s * xd; dc[1] = s * yd; dc[2] = cos(th);
+    } else {
+        orc_unproject(c, ldexp((double)u, l), ldexp((double)v, l), &xn, &yn);
+        dc[0] = xn; dc[1] = yn; dc[2] = 1.0;
+    }
     for (int k = 0; k < 3; ++k)  /* R^T dc */
         d[k] = (double)P->R[0 + k] * dc[0] + (double)P->R[3 + k] * dc[1] + (double)P->R[6 + k] * dc[2];
 }
@@ -360,7 +408,7 @@ void orc_forward_depth(const orc_points *pts, int32_t n_views, const orc_camera 
                        const orc_params *pr, uint64_t *keys)
 {
     int64_t pix[8];
-    float proj[6];
+    float proj[7];
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
         int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
@@ -369,7 +417,7 @@ void orc_forward_depth(const orc_points *pts, int32_t n_views, const orc_camera 
         for (int64_t i = 0; i < pts->n; ++i) {
             unsigned m = point_mask(pts, i, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
             if (m & 0x80u) continue; /* ghosts are not rendered */
-            uint64_t key = depth_key(proj[2], (uint32_t)(pts->global_offset + i));
+            uint64_t key = depth_key(proj[6], (uint32_t)(pts->global_offset + i));
             for (int l = 0; l < pr->layers; ++l) {
                 if (!(m & (1u << l))) continue;
                 int64_t q = layer_offset(c->width, c->height, l) + pix[l];
@@ -396,7 +444,7 @@ void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera 
                        const orc_params *pr, const uint64_t *keys, double *accum, double *count)
 {
     int64_t pix[8];
-    float proj[6];
+    float proj[7];
     const int C = pts->channels;
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
@@ -412,7 +460,7 @@ void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera 
             for (int l = 0; l < pr->layers; ++l) {
                 if (!(m & (1u << l))) continue;
                 int64_t q = layer_offset(c->width, c->height, l) + pix[l];
-                if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
+                if (!fuzzy_pass(proj[6], kv[q], pr->alpha)) continue;
                 for (int ch = 0; ch < C; ++ch) av[q * C + ch] += desc_lin(pr, pts->feat[i * C + ch]);
                 cv[q] += 1.0;
             }
@@ -510,6 +558,22 @@ int orc_induced_change(int32_t C, const float *tau, float z, float alpha, double
 void orc_jacobian(const orc_camera *c, const float *Xc, double *J /* 2x3 row-major */)
 {
     double X = Xc[0], Y = Xc[1], Z = Xc[2];
+    if (c->model == 2) {
+        /* R35 equidistant: u0 = fx g X + cx, v0 = fy g Y + cy, g = theta / rho, theta = atan2(rho, Z) */
+        double rho2 = X * X + Y * Y, rho = sqrt(rho2), d2 = rho2 + Z * Z;
+        double g, A;
+        if (rho < 1e-6 * fabs(Z) && Z > 0) {  /* series at the optical axis */
+            g = (1.0 - rho2 / (3.0 * Z * Z)) / Z;
+            A = -2.0 / (3.0 * Z * Z * Z);
+        } else {
+            double th = atan2(rho, Z);
+            g = th / rho;
+            A = Z / (rho2 * d2) - th / (rho2 * rho);
+        }
+        J[0] = c->fx * (g + X * X * A); J[1] = c->fx * X * Y * A; J[2] = -c->fx * X / d2;
+        J[3] = c->fy * X * Y * A; J[4] = c->fy * (g + Y * Y * A); J[5] = -c->fy * Y / d2;
+        return;
+    }
     double xn = X / Z, yn = Y / Z;
     /* dn/dXc = [[1/Z, 0, -X/Z^2], [0, 1/Z, -Y/Z^2]] */
     double N[2][3] = {{1.0 / Z, 0.0, -X / (Z * Z)}, {0.0, 1.0 / Z, -Y / (Z * Z)}};
@@ -539,6 +603,13 @@ void orc_jacobian(const orc_camera *c, const float *Xc, double *J /* 2x3 row-maj
  * Jacobian by finite differences. */
 void orc_project_f64(const orc_camera *c, const double *Xc, double *uv)
 {
+    if (c->model == 2) {
+        double rho = sqrt(Xc[0] * Xc[0] + Xc[1] * Xc[1]), th = atan2(rho, Xc[2]);
+        double g = rho > 0.0 ? th / rho : 1.0 / Xc[2];
+        uv[0] = c->fx * g * Xc[0] + c->cx;
+        uv[1] = c->fy * g * Xc[1] + c->cy;
+        return;
+    }
     double xn = Xc[0] / Xc[2], yn = Xc[1] / Xc[2];
     double xd = xn, yd = yn;
     if (c->model == 1) {
@@ -565,6 +636,12 @@ void orc_intrinsics_jacobian(const orc_camera *c, const float *Xc, double *Jt)
     double xn = (double)Xc[0] / (double)Xc[2], yn = (double)Xc[1] / (double)Xc[2];
     for (int k = 0; k < 24; ++k) Jt[k] = 0.0;
     double xd = xn, yd = yn;
+    if (c->model == 2) {  /* R35: xd = g X, yd = g Y (no distortion parameters) */
+        double X = Xc[0], Y = Xc[1], rho = sqrt(X * X + Y * Y), th = atan2(rho, (double)Xc[2]);
+        double g = rho > 0.0 ? th / rho : 1.0 / (double)Xc[2];
+        xd = g * X;
+        yd = g * Y;
+    }
     if (c->model == 1) {
         double r2 = xn * xn + yn * yn;
         double r[3] = {r2, r2 * r2, r2 * r2 * r2};
@@ -653,7 +730,7 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
     const int C = pts->channels;
     const int64_t n = pts->n;
     int64_t pix[8];
-    float proj[6];
+    float proj[7];
     if (dtau) memset(dtau, 0, sizeof(double) * (size_t)(n * C));
     if (dtau_abs) memset(dtau_abs, 0, sizeof(double) * (size_t)(n * C));
     if (dx) memset(dx, 0, sizeof(double) * (size_t)(3 * n));
@@ -707,7 +784,7 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                     if (!(m & (1u << l))) continue;
                     int64_t off = layer_offset(c->width, c->height, l);
                     int64_t q = off + pix[l];
-                    if (!fuzzy_pass(proj[2], kv[q], pr->alpha)) continue;
+                    if (!fuzzy_pass(proj[6], kv[q], pr->alpha)) continue;
                     int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
                     for (int ch = 0; ch < C; ++ch) {
                         /* d tau_lin / d tau = exp(tau) = tau_lin for log descriptors, 1 otherwise */
@@ -726,7 +803,7 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
             for (int l = 0; l < pr->layers; ++l) {
                 if (!(m & (1u << l))) continue;
                 double g[2], gabs[4];
-                ghost_layer_grad(c, pr, l, pix[l], C, tau, proj[2], kv, cv, img, Gv, P, g, gabs);
+                ghost_layer_grad(c, pr, l, pix[l], C, tau, proj[6], kv, cv, img, Gv, P, g, gabs);
                 double s = ldexp(1.0, -l);
                 gu += s * g[0]; gv += s * g[1];
                 for (int k = 0; k < 4; ++k) ga[k] += s * gabs[k];

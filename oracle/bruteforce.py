@@ -43,12 +43,46 @@ def round_half_away(x: F) -> F:
     return F(t)
 
 
+ATAN_C = [F(v) for v in (-0.0015244261594489217, 0.009669913910329342, -0.028764614835381508, 0.05541255697607994,
+                          -0.08245089650154114, 0.10893233865499496, -0.14251546561717987, 0.1999710500240326,
+                          -0.33333227038383484, 1.0)]
+
+
+def atan2p(y: F, x: F) -> F:
+    """R35: angle in [0, pi] of (x, y), y >= 0, from the fixed degree-9 polynomial (fp32, one rounding per op)."""
+    def a01(t):
+        u, p = F(t * t), ATAN_C[0]
+        for c in ATAN_C[1:]:
+            p = F(F(p * u) + c)
+        return F(t * p)
+    ax = F(abs(x))
+    if y <= ax:
+        a = a01(F(y / ax)) if ax > 0 else F(0.0)
+    else:
+        a = F(F(1.57079632679490) - a01(F(ax / y)))
+    return a if x >= 0 else F(F(3.14159265358979) - a)
+
+
 def project(cam, pose, x: F, y: F, z: F, z_near: F):
+    """-> (X, Y, Z, u0, v0, 1/depth, depth) or None (pinned fp32)."""
     R = np.asarray(pose.R, dtype=F).reshape(9)
     t = np.asarray(pose.t, dtype=F)
     X = F(F(F(R[0] * x) + F(R[1] * y)) + F(R[2] * z)) + t[0]
     Y = F(F(F(R[3] * x) + F(R[4] * y)) + F(R[5] * z)) + t[1]
     Z = F(F(F(R[6] * x) + F(R[7] * y)) + F(R[8] * z)) + t[2]
+    if cam.model == 2:  # equidistant fisheye, distance depth (R35)
+        rho2 = F(F(X * X) + F(Y * Y))
+        d = F(np.sqrt(F(rho2 + F(Z * Z))))
+        if not (d > z_near and d <= np.finfo(F).max):
+            return None
+        rho = F(np.sqrt(rho2))
+        th = atan2p(rho, Z)
+        if not (th <= F(cam.r2_max)):
+            return None
+        s = F(th / rho) if rho > 0 else F(0.0)
+        u0 = F(F(F(cam.fx) * F(X * s)) + F(cam.cx))
+        v0 = F(F(F(cam.fy) * F(Y * s)) + F(cam.cy))
+        return X, Y, Z, u0, v0, F(F(1.0) / d), d
     if not (Z > z_near and Z <= np.finfo(F).max):
         return None
     iz = F(F(1.0) / Z)
@@ -75,7 +109,7 @@ def project(cam, pose, x: F, y: F, z: F, z_near: F):
         yd = F(F(F(yn * rad) + F(p[0] * a3)) + F(p[1] * a1))
     u0 = F(F(F(cam.fx) * xd) + F(cam.cx))
     v0 = F(F(F(cam.fy) * yd) + F(cam.cy))
-    return X, Y, Z, u0, v0, iz
+    return X, Y, Z, u0, v0, iz, Z
 
 
 def forward(pos, radius, feat, cam, pose, params, view: int = 0, global_offset: int = 0, normal=None):
@@ -118,7 +152,7 @@ def _forward(pos, radius, feat, cam, pose, params, view, global_offset, normal):
         pr = project(cam, pose, F(pos[0, i]), F(pos[1, i]), F(pos[2, i]), F(params.z_near))
         if pr is None:
             continue
-        X, Y, Z, u0, v0, iz = pr
+        X, Y, Z, u0, v0, iz, D = pr
         mode = int(getattr(params, "normal_culling", 0))
         if mode and normal is not None and not normal_kept(pose, normal[:, i], X, Y, Z, mode):
             continue
@@ -133,14 +167,14 @@ def _forward(pos, radius, feat, cam, pose, params, view, global_offset, normal):
                 if not (F(a * a) > om):
                     break
                 nkeep += 1
-        zb = int(np.array([Z], dtype=F).view(np.uint32)[0])
+        zb = int(np.array([D], dtype=F).view(np.uint32)[0])
         key = (zb << 32) | (gi & 0xFFFFFFFF)
         for l in range(nkeep):
             wl, hl, o = dims[l]
             s = F(2.0 ** -l)
             ru, rv = round_half_away(F(u0 * s)), round_half_away(F(v0 * s))
             if ru >= 0 and ru < F(wl) and rv >= 0 and rv < F(hl):
-                hits.setdefault((l, int(rv) * wl + int(ru)), []).append((key, Z, i))
+                hits.setdefault((l, int(rv) * wl + int(ru)), []).append((key, D, i))
     keys = np.full(P, SENTINEL, dtype=np.uint64)
     count = np.zeros(P, dtype=np.float64)
     image = np.zeros(C * P, dtype=np.float64)

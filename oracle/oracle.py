@@ -197,8 +197,8 @@ def is_ghost(params, gi: int) -> bool:
 
 
 def project(cam, pose, x, y, z, z_near=0.0):
-    """-> (valid, Xc[3], u0, v0, 1/z) for one point, pinned fp32 (Eq. 2, R1/R2/R6)."""
-    out = np.zeros(6, dtype=np.float32)
+    """-> (valid, Xc[3], u0, v0, 1/depth) for one point, pinned fp32 (Eq. 2, R1/R2/R6/R35)."""
+    out = np.zeros(7, dtype=np.float32)
     cs, ps = camera_struct(cam), pose_struct(pose)
     ok = lib().orc_project(C.byref(cs), C.byref(ps), x, y, z, z_near, out.ctypes.data)
     return bool(ok), out[:3].copy(), float(out[3]), float(out[4]), float(out[5])

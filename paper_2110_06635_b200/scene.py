@@ -38,6 +38,7 @@ import torch
 
 PINHOLE = 0
 OPENCV8 = 1
+FISHEYE = 2  # equidistant fisheye, distance depth (R35); Camera.r2_max holds theta_max (radians)
 
 # Seeds (proposed and fixed here).
 SEED_SCENE, SEED_POSES, SEED_CAMERAS, SEED_FEATURES, SEED_GRADS, SEED_STEP = 2110, 6635, 3, 4, 5, 6
@@ -254,6 +255,14 @@ def distortion_r2_max(cam: Camera, steps: int = 1 << 16) -> float:
     bad = (den <= 0.05) | np.concatenate([[False], np.diff(rho) <= 0])
     last = int(np.argmax(bad)) - 1 if bad.any() else steps
     return float(np.float32(r2[max(last, 0)]))
+
+
+def fisheye_camera(width: int, height: int, fov_deg: float = 180.0) -> Camera:
+    """Equidistant fisheye (R35) whose image circle theta_max = fov/2 touches the shorter image side."""
+    th = math.radians(fov_deg) / 2.0
+    f = float(np.float32(min(width, height) / 2.0 / th))
+    return Camera(width, height, FISHEYE, f, f, float(np.float32(width / 2.0)), float(np.float32(height / 2.0)),
+                  r2_max=float(np.float32(th)))
 
 
 def opencv_camera(width: int, height: int, seed: int = SEED_CAMERAS) -> Camera:
