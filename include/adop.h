@@ -67,7 +67,7 @@ typedef enum {
     ADOP_ERR_CUDA = 5
 } adop_status;
 
-enum { ADOP_PINHOLE = 0, ADOP_OPENCV8 = 1 };
+enum { ADOP_PINHOLE = 0, ADOP_OPENCV8 = 1, ADOP_FISHEYE = 2 };
 
 #define ADOP_MAX_LAYERS 8
 #define ADOP_MAX_CHANNELS 32
@@ -92,7 +92,9 @@ typedef struct {
  * denominator are culled.  Host memory. */
 typedef struct {
     int32_t width, height;  /* layer-0 image size, >= 1                                     */
-    int32_t model;          /* ADOP_PINHOLE or ADOP_OPENCV8                                  */
+    int32_t model;          /* ADOP_PINHOLE, ADOP_OPENCV8, or ADOP_FISHEYE: equidistant
+                               r_d = f theta with the distance |Xc| as depth (L214; DESIGN.md
+                               R35), r2_max = theta_max in (0, pi]                          */
     float fx, fy, cx, cy;   /* pixels; pixel centres at integer coordinates                 */
     float k[6];             /* k1..k6 (OpenCV8)                                             */
     float p[2];             /* p1, p2 (OpenCV8)                                             */

@@ -126,7 +126,9 @@ adop_status check_params(const adop_params *pr) {
 
 adop_status check_camera(const adop_camera *c, int v, int layers) {
     if (c->width < 1 || c->height < 1) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: width/height < 1", v);
-    if (c->model != ADOP_PINHOLE && c->model != ADOP_OPENCV8)
+    if (c->model == ADOP_FISHEYE && !(c->r2_max > 0.0f && c->r2_max <= 3.14159265f))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: fisheye theta_max (r2_max) must be in (0, pi]", v);
+    if (c->model != ADOP_PINHOLE && c->model != ADOP_OPENCV8 && c->model != ADOP_FISHEYE)
         return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: unknown camera model %d", v, c->model);
     if (!std::isfinite(c->fx) || !std::isfinite(c->fy) || !std::isfinite(c->cx) || !std::isfinite(c->cy))
         return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: non-finite intrinsics", v);
@@ -291,6 +293,12 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
             std::memcpy(d.p, c.p, sizeof(d.p));
             d.r2_max = c.r2_max;
             d.r2cull = std::isinf(c.r2_max) ? c.r2_max : (float)((double)c.r2_max * (1.0 + 1.0 / 4096.0));
+        } else if (c.model == ADOP_FISHEYE) {
+            // R35: r2_max holds theta_max; up to 1.5 rad the pre-cull is the cone X^2 + Y^2 <= tan^2 Z^2 (with
+            // slack for the 1e-7-accurate atan), beyond it (a field of view near or over 180 degrees) none
+            d.r2_max = c.r2_max;
+            const double tt = std::tan((double)c.r2_max);
+            d.r2cull = c.r2_max <= 1.5f ? (float)(tt * tt * (1.0 + 1.0 / 1024.0)) : INFINITY;
         } else {
             d.r2_max = INFINITY;
             d.r2cull = INFINITY;
@@ -336,6 +344,13 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
                 for (int k = 0; k < 4; ++k) dc[k] = 1.0;  // no lateral bound
             }
             nc[4][2] = 1.0;
+            if (c.model == ADOP_FISHEYE) {  // the depth is the distance: valid points only have Z >= 0 (narrow)
+                dc[4] = 0.0;
+                if (std::isinf(d.r2cull)) {  // wide: no half-space at all
+                    nc[4][2] = 0.0;
+                    dc[4] = 1.0;
+                }
+            }
             const double T = std::fabs((double)poses[v].t[0]) + std::fabs((double)poses[v].t[1]) +
                              std::fabs((double)poses[v].t[2]);
             const float *R = poses[v].R;

@@ -43,8 +43,43 @@ __device__ __forceinline__ uint32_t h24(uint32_t salt, uint32_t gi) { return mix
 struct Proj {
     float X, Y, Z;  // camera-space point (R1)
     float u0, v0;   // layer-0 continuous pixel coordinates
-    float iz;       // 1 / Z (IEEE)
+    float iz;       // 1 / D (IEEE)
+    float D;        // depth of keys and Eq. 6 (R4): Z, or the distance |Xc| for the fisheye (R35)
 };
+
+// R35: atan(t), t in [0, 1], as t * P(t^2) with the fixed degree-9 polynomial of DESIGN.md R35, Horner in fp32
+// with one rounding per operation (identical to the oracle's), and the angle in [0, pi] of (x, y), y >= 0.
+__device__ __forceinline__ float atan01(float t) {
+    const float c[10] = {-0.0015244261594489217f, 0.009669913910329342f, -0.028764614835381508f,
+                         0.05541255697607994f, -0.08245089650154114f, 0.10893233865499496f,
+                         -0.14251546561717987f, 0.1999710500240326f, -0.33333227038383484f, 1.0f};
+    const float u = __fmul_rn(t, t);
+    float p = c[0];
+#pragma unroll
+    for (int k = 1; k < 10; ++k) p = __fadd_rn(__fmul_rn(p, u), c[k]);
+    return __fmul_rn(t, p);
+}
+__device__ __forceinline__ float atan2p(float y, float x) {
+    const float ax = fabsf(x);
+    float a;
+    if (y <= ax) a = ax > 0.0f ? atan01(__fdiv_rn(y, ax)) : 0.0f;
+    else a = __fsub_rn(1.57079632679490f, atan01(__fdiv_rn(ax, y)));
+    return x >= 0.0f ? a : __fsub_rn(3.14159265358979f, a);
+}
+
+// Validity (R7 / R35) and the depth D of a camera point; sets p.D and p.iz = 1/D.  Pinned fp32.
+template <int MODEL>
+__device__ __forceinline__ bool depth_valid(Proj &p, float z_near) {
+    if (MODEL == 2) {
+        const float rho2 = __fadd_rn(__fmul_rn(p.X, p.X), __fmul_rn(p.Y, p.Y));
+        p.D = __fsqrt_rn(__fadd_rn(rho2, __fmul_rn(p.Z, p.Z)));
+    } else {
+        p.D = p.Z;
+    }
+    if (!(p.D > z_near && p.D <= 3.402823466e38f)) return false;
+    p.iz = __frcp_rn(p.D);
+    return true;
+}
 
 // Xc = R x + t in the pinned order ((r0 x + r1 y) + r2 z) + t (R1).
 __device__ __forceinline__ void to_camera(const ViewDesc &v, float x, float y, float z, float &X, float &Y,
@@ -58,6 +93,7 @@ __device__ __forceinline__ void to_camera(const ViewDesc &v, float x, float y, f
 // per-layer test would accept).  Z > z_near already holds.
 template <int MODEL>
 __device__ __forceinline__ bool precull_pass(const ViewDesc &v, float X, float Y, float Z) {
+    if (MODEL == 2 && !(v.r2cull <= 3.402823466e38f)) return true;  // fisheye wider than 180 degrees
     if (MODEL == 0) {
         float su = fmaf(v.fx, X, v.cx * Z);
         float sv = fmaf(v.fy, Y, v.cy * Z);
@@ -83,6 +119,8 @@ __device__ __forceinline__ bool precull_fma(const ViewDesc &v, float x, float y,
         const float d0 = fmaf(-v.ulo, Z, su), d1 = fmaf(v.uhi, Z, -su);
         const float d2 = fmaf(-v.vlo, Z, sv), d3 = fmaf(v.vhi, Z, -sv);
         return fminf(fminf(d0, d1), fminf(d2, d3)) >= -m;
+    } else if (MODEL == 2 && !(v.r2cull <= 3.402823466e38f)) {
+        return true;  // fisheye wider than 180 degrees: no cone
     } else {
         // |Xp| >= |Xf| - m etc.: (|Xf|-m)+^2 + (|Yf|-m)+^2 <= r2cull (|Zf|+m)^2 is implied by the exact test
         const float ax = fmaxf(fabsf(X) - m, 0.0f), ay = fmaxf(fabsf(Y) - m, 0.0f), az = fabsf(Z) + m;
@@ -99,6 +137,7 @@ __device__ __forceinline__ bool precull_fma_z(const ViewDesc &v, float x, float 
     const float m = fmaf(v.fk, fabsf(x) + fabsf(y) + fabsf(z), v.fkt);
     Zo = Z;
     mo = m;
+    if (MODEL == 2 && !(v.r2cull <= 3.402823466e38f)) return true;  // fisheye wider than 180 degrees
     if (MODEL == 0) {
         const float su = fmaf(v.fx, X, v.cx * Z);
         const float sv = fmaf(v.fy, Y, v.cy * Z);
@@ -114,6 +153,15 @@ __device__ __forceinline__ bool precull_fma_z(const ViewDesc &v, float x, float 
 // Exact projection to layer-0 pixels given p.X, p.Y, p.Z (pinned) and p.iz = 1/Z (R2, R6).
 template <int MODEL>
 __device__ __forceinline__ bool project_uv(const ViewDesc &v, Proj &p) {
+    if (MODEL == 2) {  // R35 equidistant: theta = atan2(rho, Z) <= theta_max, r_d = f theta
+        const float rho = __fsqrt_rn(__fadd_rn(__fmul_rn(p.X, p.X), __fmul_rn(p.Y, p.Y)));
+        const float th = atan2p(rho, p.Z);
+        if (!(th <= v.r2_max)) return false;
+        const float s = rho > 0.0f ? __fdiv_rn(th, rho) : 0.0f;
+        p.u0 = fadd(fmul(v.fx, fmul(p.X, s)), v.cx);
+        p.v0 = fadd(fmul(v.fy, fmul(p.Y, s)), v.cy);
+        return true;
+    }
     float xn = fmul(p.X, p.iz), yn = fmul(p.Y, p.iz);
     float xd = xn, yd = yn;
     if (MODEL == 1) {
@@ -136,20 +184,13 @@ __device__ __forceinline__ bool project_uv(const ViewDesc &v, Proj &p) {
     return true;
 }
 
-// Exact projection after the pre-cull (R2, R6): returns false if culled.
-template <int MODEL>
-__device__ __forceinline__ bool project_exact(const ViewDesc &v, Proj &p) {
-    p.iz = __frcp_rn(p.Z);
-    return project_uv<MODEL>(v, p);
-}
-
-// Full projection of a point: validity (R7), pre-cull, exact projection.
+// Full projection of a point: validity (R7 / R35), pre-cull, exact projection.
 template <int MODEL>
 __device__ __forceinline__ bool project_point(const ViewDesc &v, float z_near, float x, float y, float z, Proj &p) {
     to_camera(v, x, y, z, p.X, p.Y, p.Z);
-    if (!(p.Z > z_near && p.Z <= 3.402823466e38f)) return false;
+    if (!depth_valid<MODEL>(p, z_near)) return false;
     if (!precull_pass<MODEL>(v, p.X, p.Y, p.Z)) return false;
-    return project_exact<MODEL>(v, p);
+    return project_uv<MODEL>(v, p);
 }
 
 // Eq. 12 (L344) as R10/R11: number of leading layers at which the point is kept.
@@ -207,8 +248,13 @@ __device__ __forceinline__ void env_taps(const RasterArgs &a, const ViewDesc &v,
                                          float w[4]) {
     const float u0 = ldexpf((float)u, l), v0 = ldexpf((float)vv, l);
     const float xd = (u0 - v.cx) / v.fx, yd = (v0 - v.cy) / v.fy;
-    float x = xd, y = yd;
-    if (v.model == ADOP_OPENCV8) {
+    float x = xd, y = yd, zc = 1.f;
+    if (v.model == 2) {  // R35: theta = |(xd, yd)|, direction (sin theta xd / theta, sin theta yd / theta, cos theta)
+        const float th = sqrtf(xd * xd + yd * yd), s = th > 0.f ? sinf(th) / th : 1.f;
+        x = s * xd;
+        y = s * yd;
+        zc = cosf(th);
+    } else if (v.model == ADOP_OPENCV8) {
         for (int it = 0; it < 8; ++it) {
             const float r2 = x * x + y * y;
             const float num = 1.f + r2 * (v.k[0] + r2 * (v.k[1] + r2 * v.k[2]));
@@ -226,8 +272,8 @@ __device__ __forceinline__ void env_taps(const RasterArgs &a, const ViewDesc &v,
             y -= (-D01 * rx + D00 * ry) * idet;
         }
     }
-    const float dx = v.R[0] * x + v.R[3] * y + v.R[6], dy = v.R[1] * x + v.R[4] * y + v.R[7];
-    const float dz = v.R[2] * x + v.R[5] * y + v.R[8];
+    const float dx = v.R[0] * x + v.R[3] * y + v.R[6] * zc, dy = v.R[1] * x + v.R[4] * y + v.R[7] * zc;
+    const float dz = v.R[2] * x + v.R[5] * y + v.R[8] * zc;
     const float lon = atan2f(dx, dz), lat = atan2f(dy, sqrtf(dx * dx + dz * dz));
     const float s = (lon * 0.15915494309189535f + 0.5f) * (float)a.env_w - 0.5f;
     const float t = (lat * 0.3183098861837907f + 0.5f) * (float)a.env_h - 0.5f;

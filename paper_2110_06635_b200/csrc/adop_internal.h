@@ -49,7 +49,7 @@ struct GhostEntry {  // one (ghost point, view) kept at >= 1 layer (§4.3), 32 b
     float Z;
     uint32_t idx;    // shard-local point index
     uint32_t vsnk;   // view slot | kept layers << 8 (0xFFFFFFFF: dead entry)
-    uint32_t pad;
+    float D;         // depth of keys / Eq. 6: Z, or the distance for the fisheye (R35)
 };
 constexpr int kResvBackShift = 40;
 

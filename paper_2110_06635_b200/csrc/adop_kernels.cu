@@ -229,7 +229,7 @@ __device__ __forceinline__ void stream_sweep(const RasterArgs &a) {
                 }
                 if (!__any_sync(kFull, ok)) continue;
                 const int nk = ok ? keep_layers(a, v, pr[j], p.iz, gi) : 0;
-                const uint64_t key = depth_key(p.Z, gi);
+                const uint64_t key = depth_key(p.D, gi);
 #pragma unroll
                 for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {
                     if (l >= a.layers) break;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void stream_sweep(const RasterArgs &a) {
                             if (hit) {
                                 Record r;
                                 r.pix = pix;
-                                r.zbits = __float_as_uint(p.Z);
+                                r.zbits = __float_as_uint(p.D);
                                 r.idx = (uint32_t)i;
                                 r.view = (uint32_t)vs;
                                 sbuf[wid][wcount + __popc(b & lt)] = r;
@@ -253,7 +253,7 @@ __device__ __forceinline__ void stream_sweep(const RasterArgs &a) {
                             wcount += __popc(b);
                         }
                     } else {  // MODE_BLEND: re-streamed accumulate (only after a record overflow)
-                        if (hit && fuzzy_pass(p.Z, v.keys[pix], a.onepa)) accumulate_feature<VEC4>(a, v, i, pix);
+                        if (hit && fuzzy_pass(p.D, v.keys[pix], a.onepa)) accumulate_feature<VEC4>(a, v, i, pix);
                     }
                 }
             }
@@ -502,17 +502,14 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     int nk = 0;
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (p.Z > a.z_near && p.Z <= 3.402823466e38f && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
-            p.iz = __frcp_rn(p.Z);
-            nk = keep_layers(a, v, rw, p.iz, gi);
-        }
+        if (depth_valid<MODEL>(p, a.z_near) && normal_keep(a, v, i, p.X, p.Y, p.Z)) nk = keep_layers(a, v, rw, p.iz, gi);
     }
     if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
     const unsigned b = __ballot_sync(kFull, nk > 0);
     if (b == 0u) return;
     if (nk > 0) {
         const int slot = qn + __popc(b & lt);
-        q.e[slot] = make_float4(p.u0, p.v0, p.Z, __uint_as_float((uint32_t)i));
+        q.e[slot] = make_float4(p.u0, p.v0, p.D, __uint_as_float((uint32_t)i));
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
     qn += __popc(b);
@@ -946,8 +943,32 @@ __global__ void __launch_bounds__(kThreads) k_bwd_prep(const __grid_constant__ R
     }
 }
 
+// R35 equidistant fisheye: g = theta / rho (u0 = fx g X + cx), and A = dg/dX / X = dg/dY / Y.  For
+// t = rho / Z < 0.3 A uses the series of (t - (1 + t^2) atan t) / t^3 (the direct form cancels in fp32).
+__device__ __forceinline__ void fisheye_gA(const Proj &p, float &g, float &A) {
+    const float X = p.X, Y = p.Y, Z = p.Z;
+    const float rho2 = X * X + Y * Y, rho = sqrtf(rho2), d2 = rho2 + Z * Z;
+    const float th = atan2f(rho, Z);
+    g = rho > 0.f ? th / rho : 1.f / Z;
+    if (Z > 0.f && rho < 0.3f * Z) {
+        const float t2 = rho2 / (Z * Z);
+        const float h = -2.f / 3.f + t2 * (2.f / 15.f + t2 * (-2.f / 35.f + t2 * (2.f / 63.f)));
+        A = h / (Z * d2);
+    } else {
+        A = (Z * rho - th * d2) / (rho2 * rho * d2);
+    }
+}
+
 template <int MODEL>
 __device__ __forceinline__ void jacobian(const ViewDesc &v, const Proj &p, float J[6]) {
+    if (MODEL == 2) {
+        float g, A;
+        fisheye_gA(p, g, A);
+        const float X = p.X, Y = p.Y, d2 = X * X + Y * Y + p.Z * p.Z;
+        J[0] = v.fx * (g + X * X * A); J[1] = v.fx * X * Y * A; J[2] = -v.fx * X / d2;
+        J[3] = v.fy * X * Y * A; J[4] = v.fy * (g + Y * Y * A); J[5] = -v.fy * Y / d2;
+        return;
+    }
     const float iz = p.iz, xn = p.X * iz, yn = p.Y * iz;
     // dn/dXc = [[iz, 0, -xn iz], [0, iz, -yn iz]]
     float D00 = 1.f, D01 = 0.f, D10 = 0.f, D11 = 1.f;
@@ -985,7 +1006,13 @@ __device__ __forceinline__ void struct_terms(const ViewDesc &v, const Proj &p, f
     t[4] = (double)(p.Z * w0 - p.X * w2);
     t[5] = (double)(p.X * w1 - p.Y * w0);
     if (nt <= 6) return;
-    const float xn = p.X * p.iz, yn = p.Y * p.iz;
+    float xn = p.X * p.iz, yn = p.Y * p.iz;
+    if (MODEL == 2) {  // R35: xd = g X, yd = g Y; no distortion parameters
+        float g, A;
+        fisheye_gA(p, g, A);
+        xn = g * p.X;
+        yn = g * p.Y;
+    }
     float xd = xn, yd = yn;
 #pragma unroll
     for (int k = 4; k < kNI; ++k) t[6 + k] = 0.0;
@@ -1061,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                         // texture gradient: dI/dtau = 1/|Lambda| for members of Lambda (R24)
                         const int q = v.off[l] + loc;
                         const float cnt = v.count[q];
-                        if (fuzzy_pass(p.Z, v.keys[q], a.onepa)) {
+                        if (fuzzy_pass(p.D, v.keys[q], a.onepa)) {
                         const int64_t hw = (int64_t)v.wl[l] * v.hl[l];
                         const float *G = v.grad + (int64_t)C * v.off[l] + loc;
                         if (CT > 0) {
@@ -1081,10 +1108,10 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                             tau_loaded = true;
                         }
                         // Eqs. 9-11: signed central differences over the 4-neighbourhood (R14, R15)
-                        const float dup = neighbour_term<CT>(a, v, l, pu + 1, pv, p.Z, tau);
-                        const float dum = neighbour_term<CT>(a, v, l, pu - 1, pv, p.Z, tau);
-                        const float dvp = neighbour_term<CT>(a, v, l, pu, pv + 1, p.Z, tau);
-                        const float dvm = neighbour_term<CT>(a, v, l, pu, pv - 1, p.Z, tau);
+                        const float dup = neighbour_term<CT>(a, v, l, pu + 1, pv, p.D, tau);
+                        const float dum = neighbour_term<CT>(a, v, l, pu - 1, pv, p.D, tau);
+                        const float dvp = neighbour_term<CT>(a, v, l, pu, pv + 1, p.D, tau);
+                        const float dvm = neighbour_term<CT>(a, v, l, pu, pv - 1, p.D, tau);
                         const float s = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
                         gu += s * (dup - dum);
                         gv += s * (dvp - dvm);
@@ -1331,7 +1358,7 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
     for (int l = 0; l < nk; ++l) {
         int pu, pv;
         if (layer_pixel(v, p, l, pu, pv) < 0) continue;
-        ghost_layer<CT>(a, v, l, pu, pv, p.Z, tau, gu, gv);
+        ghost_layer<CT>(a, v, l, pu, pv, p.D, tau, gu, gv);
         gc = true;
     }
     if (!gc) return false;
@@ -1358,7 +1385,13 @@ template <int MODEL>
 __device__ __forceinline__ void intr_inline(const RasterArgs &a, const ViewDesc &v, int vs, const Proj &p, float gu,
                                             float gv) {
     double *row = a.pose_partials + ((int64_t)a.inline_row * a.nviews + vs) * kNT + 6;
-    const float xn = p.X * p.iz, yn = p.Y * p.iz;
+    float xn = p.X * p.iz, yn = p.Y * p.iz;
+    if (MODEL == 2) {
+        float g, A;
+        fisheye_gA(p, g, A);
+        xn = g * p.X;
+        yn = g * p.Y;
+    }
     float xd = xn, yd = yn;
     if (MODEL == 1) {  // as struct_terms, one term at a time (no term array in the sweep's registers)
         const float r2 = xn * xn + yn * yn, r4 = r2 * r2, r6 = r4 * r2;
@@ -1403,8 +1436,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     int nk = 0;
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (p.Z > a.z_near && p.Z <= 3.402823466e38f && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
-            p.iz = __frcp_rn(p.Z);
+        if (depth_valid<MODEL>(p, a.z_near) && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
             nk = keep_layers(a, v, rw, p.iz, gi);
             if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
         }
@@ -1426,9 +1458,9 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
             if (hit) {
                 if (slot != kNoSlot)
                     reinterpret_cast<uint4 *>(a.records)[slot] =
-                        make_uint4(q, __float_as_uint(p.Z), (uint32_t)i, (uint32_t)vs);  // Record
+                        make_uint4(q, __float_as_uint(p.D), (uint32_t)i, (uint32_t)vs);  // Record
                 else
-                    tex_hit(a, v, q, p.Z, i);
+                    tex_hit(a, v, q, p.D, i);
             }
         }
     }
@@ -1440,7 +1472,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     if (slot != kNoSlot) {  // GhostEntry
         uint4 *r = reinterpret_cast<uint4 *>(a.records) + slot;
         r[0] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X), __float_as_uint(p.Y));
-        r[1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), 0u);
+        r[1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), __float_as_uint(p.D));
     } else {
         ghost_inline<MODEL, CT>(a, v, vs, p, nk, i);
     }
@@ -1491,7 +1523,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
                 p.X = __uint_as_float(e0.z);
                 p.Y = __uint_as_float(e0.w);
                 p.Z = __uint_as_float(e1.x);
-                p.iz = __frcp_rn(p.Z);
+                p.D = __uint_as_float(e1.w);  // the depth of Eq. 6 (R4 / R35)
+                p.iz = __frcp_rn(p.D);
                 if (!ghost_point<MODEL, CT>(a, v, p, nk, (int64_t)e1.y, NT, t6)) vs = -1;
             }
         }
@@ -1780,6 +1813,7 @@ static int launch_depth_t(const RasterArgs &a, int sms, void *stream) {
 
 int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream) {
     if (model == 0) return vec ? launch_depth_t<0, true>(a, sms, stream) : launch_depth_t<0, false>(a, sms, stream);
+    if (model == 2) return vec ? launch_depth_t<2, true>(a, sms, stream) : launch_depth_t<2, false>(a, sms, stream);
     return vec ? launch_depth_t<1, true>(a, sms, stream) : launch_depth_t<1, false>(a, sms, stream);
 }
 
@@ -1799,6 +1833,10 @@ int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream
     if (model == 0) {
         if (vec) return v4 ? launch_blend_t<0, true, true>(a, sms, stream) : launch_blend_t<0, true, false>(a, sms, stream);
         return v4 ? launch_blend_t<0, false, true>(a, sms, stream) : launch_blend_t<0, false, false>(a, sms, stream);
+    }
+    if (model == 2) {
+        if (vec) return v4 ? launch_blend_t<2, true, true>(a, sms, stream) : launch_blend_t<2, true, false>(a, sms, stream);
+        return v4 ? launch_blend_t<2, false, true>(a, sms, stream) : launch_blend_t<2, false, false>(a, sms, stream);
     }
     if (vec) return v4 ? launch_blend_t<1, true, true>(a, sms, stream) : launch_blend_t<1, true, false>(a, sms, stream);
     return v4 ? launch_blend_t<1, false, true>(a, sms, stream) : launch_blend_t<1, false, false>(a, sms, stream);
@@ -1943,6 +1981,8 @@ static int launch_backward_c(const RasterArgs &a, int sms, int grid_cap, double 
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid_cap, double *d_pose, void *stream) {
     if (model == 0) return vec ? launch_backward_c<0, true>(a, sms, grid_cap, d_pose, stream)
                                : launch_backward_c<0, false>(a, sms, grid_cap, d_pose, stream);
+    if (model == 2) return vec ? launch_backward_c<2, true>(a, sms, grid_cap, d_pose, stream)
+                               : launch_backward_c<2, false>(a, sms, grid_cap, d_pose, stream);
     return vec ? launch_backward_c<1, true>(a, sms, grid_cap, d_pose, stream)
                : launch_backward_c<1, false>(a, sms, grid_cap, d_pose, stream);
 }
@@ -1954,6 +1994,8 @@ int launch_masks(const RasterArgs &a, int model, void *stream) {
     if (g > 65535) g = 65535;
     if (model == 0)
         k_stream<0, false, MODE_MASKS, false><<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else if (model == 2)
+        k_stream<2, false, MODE_MASKS, false><<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(a);
     else
         k_stream<1, false, MODE_MASKS, false><<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();

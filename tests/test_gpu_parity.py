@@ -445,3 +445,48 @@ def test_normal_culling_fwd_bwd(mode, cfg):
     assert np.array_equal(m, om)
     base = run_gpu(cloud, w.cameras, w.poses, dataclasses.replace(prm, normal_culling=0))
     assert (r.pyrs[0].count.sum() < base.pyrs[0].count.sum()).item()  # something was culled
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-3: equidistant fisheye with distance depth (R35)
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("fov,ghost,views", [(120.0, 0.25, 1), (200.0, 0.25, 1), (179.0, 0.0, 3)])
+def test_fisheye_fwd_bwd(fov, ghost, views):
+    room = S.make_room(10.0)
+    cloud = S.room_cloud(150_000, room, channels=4, seed=21)
+    cloud = dataclasses.replace(cloud, radius=torch.full_like(cloud.radius, 0.05))  # ~1 px splats: most kept
+    cams = [S.fisheye_camera(160, 120, fov) for _ in range(views)]
+    poses = S.room_poses(views, room, seed=8)
+    prm = S.Params(layers=4, discard=True, ghost_rate=ghost, seed=5, background=[0.5, 0.25, -0.5, 1.0])
+    G = grads_for(cams, prm.layers, 4)
+    r = run_gpu(cloud, cams, poses, prm, grads=G if ghost else None)
+    _, fwd, bwd = run_oracle(cloud, cams, poses, prm, grads=G if ghost else None)
+    compare_forward(r, fwd, ctx=f"fisheye {fov}")
+    if ghost:
+        compare_backward(r, bwd, ctx=f"fisheye {fov}")
+        assert np.abs(bwd.dx).sum() > 0 and (r.d_intr[:, 4:] == 0).all()
+    m = r.masks().cpu().numpy()
+    assert np.array_equal(m, O.point_masks(O.Points.from_cloud(cloud), cams, poses, prm))
+    assert (fwd.count > 0).sum() > 5000
+
+
+@pytest.mark.parametrize("fov", [120.0, 200.0])
+def test_fisheye_precull_is_conservative(fov):
+    """Points on rings just inside / outside theta_max at tiny to huge distances: never dropped by the
+    pre-culls (cone + warp box for the narrow lens, none for the wide one)."""
+    cam = S.fisheye_camera(64, 64, fov)
+    th_max = cam.r2_max
+    rng = np.random.default_rng(3)
+    th = np.concatenate([th_max + np.array([-1e-3, -1e-5, -1e-7, 0.0, 1e-7, 1e-5]), rng.uniform(0, th_max, 50)])
+    ph = np.linspace(0, 2 * np.pi, 64, endpoint=False)
+    ds = np.array([1e-3, 0.5, 3.0, 1e3, 1e5])
+    T, Ph, D = [a.ravel() for a in np.meshgrid(th, ph, ds)]
+    xyz = np.stack([D * np.sin(T) * np.cos(Ph), D * np.sin(T) * np.sin(Ph), D * np.cos(T)]).astype(np.float32)
+    n = xyz.shape[1]
+    cloud = S.Cloud(torch.from_numpy(xyz), torch.full((n,), 0.01), torch.rand(n, 4, generator=torch.Generator().manual_seed(2)))
+    prm = S.Params(layers=5, discard=False)
+    pose = S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))
+    r = run_gpu(cloud, [cam], [pose], prm)
+    _, fwd, _ = run_oracle(cloud, [cam], [pose], prm)
+    compare_forward(r, fwd, ctx=f"fisheye precull {fov}")
+    assert (fwd.count > 0).sum() > 300
