@@ -21,7 +21,7 @@ import torch
 from . import build as _build
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libadop.so")
+LIB_PATH = os.environ.get("ADOP_LIB", os.path.join(PKG, "libadop.so"))  # ADOP_LIB: a tuning variant
 MAX_VIEWS = 16
 SENTINEL = 0x7FFFFFFFFFFFFFFF
 
@@ -70,7 +70,7 @@ def lib():
     """Load libadop.so (building it first if the sources are newer).  Raises if it cannot be loaded."""
     global _lib
     if _lib is None:
-        if _build.needs_build():
+        if LIB_PATH == _build.LIB and _build.needs_build():
             _build.build()
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"libadop.so not found at {LIB_PATH}; run python -m paper_2110_06635_b200.build")

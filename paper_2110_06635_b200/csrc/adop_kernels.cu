@@ -285,7 +285,15 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 //      packed key (§4.5, R8) and survivor records, written straight to global memory into per-warp
 //      chunks of kChunk slots reserved with one atomic (unused slots are marked dead).
 // --------------------------------------------------------------------------- //
-constexpr int kStages = 2;
+constexpr int kStages = 2;   // backward sweep ring depth
+#ifndef ADOP_DSTAGES
+#define ADOP_DSTAGES 2
+#endif
+#ifndef ADOP_DCTAS
+#define ADOP_DCTAS 3
+#endif
+constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flight per warp)
+constexpr int kDCTAs = ADOP_DCTAS;      // depth sweep CTAs per SM
 constexpr int kSW = 8;               // warps per CTA of the TMA sweeps (3 CTAs x 8 warps per SM)
 constexpr int kST = kSW * 32;
 constexpr int kWTile = 256;  // points per warp tile (8 per lane)
@@ -360,9 +368,9 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 
 
 struct DepthSmem {
-    float pos[kStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
-    uint64_t bar[kSW][kStages];          // per-warp TMA completion barriers
-    int tile[kSW][kStages];              // tile claimed into each stage (dynamic claiming)
+    float pos[kDStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
+    uint64_t bar[kSW][kDStages];          // per-warp TMA completion barriers
+    int tile[kSW][kDStages];              // tile claimed into each stage (dynamic claiming)
     WarpQueue q[kSW];
     uint8_t cand[kSW][kWTile];           // compacted candidate list of the warp tile (tile offsets)
 };
@@ -644,10 +652,10 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
     }
 }
 
-static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / 3, "depth sweep: 3 CTAs per SM must fit in shared memory");
+static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / kDCTAs, "depth sweep: kDCTAs CTAs per SM must fit in shared memory");
 
 template <int MODEL, int VM>
-__global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ RasterArgs a) {
+__global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
     const int rows = staged_r ? 4 : 3;
     const bool dyn = a.dyn_tiles & 1;
     if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
+        for (int st = 0; st < kDStages; ++st) mbar_init(&sm.bar[wid][st], 1);
         fence_mbar_init();
     }
     __syncwarp();
@@ -698,7 +706,7 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
             if (rows == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
         }
     };
-    for (int st = 0; st < kStages; ++st) issue(st);
+    for (int st = 0; st < kDStages; ++st) issue(st);
     __syncwarp();
     WarpQueue &q = sm.q[wid];
     int qn = 0;
@@ -707,7 +715,7 @@ __global__ void __launch_bounds__(kST, 3) k_depth_async(const __grid_constant__ 
     c.left = 0;
     uint32_t phase = 0u;
     int t_cons = (int)blockIdx.x * kSW + wid;
-    for (int st = 0;; st = (st + 1) & (kStages - 1)) {
+    for (int st = 0;; st = st + 1 == kDStages ? 0 : st + 1) {
         int t;
         if (dyn) {
             t = *(volatile int *)&sm.tile[wid][st];
