@@ -85,6 +85,11 @@ typedef struct {
     int32_t channels;       /* C, 1..32                                                     */
     const float *normal;    /* device SoA [3][pos_stride] normals n of Eq. 1 (Eq. 5 culling),
                                or NULL; required when params->normal_culling != 0        */
+    const float *tile_bounds;/* device [ceil(n/256)][8] per-256-point-tile bounding boxes
+                               (adop_tile_bounds) or NULL.  When given, the depth pass
+                               neither loads nor processes tiles whose box meets no view's
+                               frustum (results are identical; for static clouds rendered
+                               many times).  Must describe the current positions.          */
 } adop_points;
 
 /* Camera model C of Eq. 2 (R6): pinhole, or OpenCV rational 8-coefficient distortion
@@ -227,9 +232,15 @@ ADOP_API adop_status adop_point_masks(const adop_points *points, int32_t n_views
 /* List statistics of `workspace` (synchronizes `stream`); any output may be NULL:
  * records: survivor-record slots of the last depth pass (including dead chunk tails),
  * ghost_entries: ghost-list entries of the last backward (including dead chunk tails),
- * overflowed: whether the depth pass's records did not fit the record region. */
+ * overflowed: whether the depth pass's records did not fit the record region,
+ * tiles_read: with tile_bounds, the 256-point tiles the last depth pass loaded. */
 ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream,
-                                 int64_t *records, int64_t *ghost_entries, int32_t *overflowed);
+                                 int64_t *records, int64_t *ghost_entries, int32_t *overflowed,
+                                 int64_t *tiles_read);
+
+/* Bounding box of every 256-point tile of `points` (lo x, y, z, 0, hi x, y, z, 0; NaN coordinates
+ * ignored): bounds = device float [ceil(n/256)][8], 16-byte aligned.  Enqueued on `stream`. */
+ADOP_API adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *stream);
 
 /* ---- Preprocessing before the hot path (untimed setup) ------------- */
 

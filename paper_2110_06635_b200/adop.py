@@ -38,7 +38,7 @@ class AdopError(RuntimeError):
 class adop_points(C.Structure):
     _fields_ = [("n", C.c_int64), ("global_offset", C.c_int64), ("pos_stride", C.c_int64),
                 ("pos", C.c_void_p), ("radius", C.c_void_p), ("radius_uniform", C.c_float),
-                ("feat", C.c_void_p), ("channels", C.c_int32), ("normal", C.c_void_p)]
+                ("feat", C.c_void_p), ("channels", C.c_int32), ("normal", C.c_void_p), ("tile_bounds", C.c_void_p)]
 
 
 class adop_camera(C.Structure):
@@ -96,7 +96,9 @@ def lib():
                                           P(C.c_size_t)]
         L.adop_workspace_stats.restype = C.c_int
         L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int64),
-                                           P(C.c_int32)]
+                                           P(C.c_int32), P(C.c_int64)]
+        L.adop_tile_bounds.restype = C.c_int
+        L.adop_tile_bounds.argtypes = [P(adop_points), C.c_void_p, C.c_void_p]
         L.adop_prep_workspace_size.restype = C.c_int
         L.adop_prep_workspace_size.argtypes = [C.c_int64, C.c_int32, P(C.c_size_t)]
         L.adop_blocked_morton_order.restype = C.c_int
@@ -142,7 +144,19 @@ class Points:
         s.pos, s.radius, s.radius_uniform = _ptr(pos), _ptr(radius), float(radius_uniform)
         s.feat, s.channels = _ptr(feat), self.channels
         s.normal = _ptr(normal)
+        self.bounds = None
         self.s = s
+
+    def enable_tile_culling(self, stream=None) -> "Points":
+        """Compute per-tile bounds (adop_tile_bounds) so the depth pass skips tiles outside every view.
+        Call again after the positions change."""
+        if self.bounds is None:
+            self.bounds = torch.empty((self.n + 255) // 256 * 8 + 4, dtype=torch.float32, device=self.pos.device)
+        ptr = (self.bounds.data_ptr() + 15) // 16 * 16
+        self.s.tile_bounds = None
+        _check(lib().adop_tile_bounds(C.byref(self.s), ptr, _stream(stream)))
+        self.s.tile_bounds = ptr
+        return self
 
     @staticmethod
     def from_cloud(cloud, global_offset: int = 0) -> "Points":
@@ -262,9 +276,10 @@ class Workspace:
 
     def stats3(self, stream=None):
         """(survivor record slots, ghost-list entries of the last backward, overflowed)."""
-        rec, gh, of = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+        rec, gh, of, tr = C.c_int64(0), C.c_int64(0), C.c_int32(0), C.c_int64(0)
         _check(lib().adop_workspace_stats(self.ptr, self.nbytes, _stream(stream), C.byref(rec), C.byref(gh),
-                                          C.byref(of)))
+                                          C.byref(of), C.byref(tr)))
+        self.tiles_read = int(tr.value)
         return int(rec.value), int(gh.value), bool(of.value)
 
 

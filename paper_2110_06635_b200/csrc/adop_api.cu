@@ -93,6 +93,8 @@ adop_status check_points(const adop_points *pts, bool need_feat) {
     if (need_feat && !pts->feat) return fail(ADOP_ERR_INVALID_ARGUMENT, "points->feat is NULL");
     if (pts->feat && !aligned(pts->feat, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "feat not aligned");
     if (pts->normal && !aligned(pts->normal, 4)) return fail(ADOP_ERR_INVALID_ARGUMENT, "normal not aligned");
+    if (pts->tile_bounds && !aligned(pts->tile_bounds, 16))
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "tile_bounds not 16-byte aligned");
     return ok();
 }
 
@@ -264,6 +266,7 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     a.spatial_rendered = pr->spatial_rendered ? 1 : 0;
     a.normal_cull = pr->normal_culling > 0 ? 1 : (pr->normal_culling < 0 ? -1 : 0);
     a.nrm = pts->normal;
+    a.tbounds = pts->tile_bounds;
     a.nrm_stride = pts->pos_stride;
     if (!pts->normal) a.normal_cull = 0;
     a.env = pr->env_map;
@@ -622,8 +625,20 @@ adop_status adop_point_masks(const adop_points *points, int32_t n_views, const a
     return ok();
 }
 
+adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *stream) {
+    adop_status s;
+    if ((s = check_points(points, false))) return s;
+    if (points->n > 0 && !bounds) return fail(ADOP_ERR_INVALID_ARGUMENT, "bounds is NULL");
+    if (bounds && !aligned(bounds, 16)) return fail(ADOP_ERR_INVALID_ARGUMENT, "bounds not 16-byte aligned");
+    if (points->n == 0) return ok();
+    int e = launch_tile_bounds(points->pos, points->pos + points->pos_stride, points->pos + 2 * points->pos_stride,
+                               points->n, bounds, stream);
+    if (e) return cuda_status(e, "tile bounds launch");
+    return ok();
+}
+
 adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, void *stream, int64_t *records,
-                                 int64_t *ghost_entries, int32_t *overflowed) {
+                                 int64_t *ghost_entries, int32_t *overflowed, int64_t *tiles_read) {
     if (!workspace || workspace_bytes < kHeaderBytes) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad workspace");
     WsHeader h;
     cudaError_t e = cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
@@ -631,6 +646,7 @@ adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, 
     if (e != cudaSuccess) return cuda_status((int)e, "workspace stats");
     if (records) *records = (int64_t)h.front_ok;
     if (ghost_entries) *ghost_entries = (int64_t)(h.back_ok / 2);
+    if (tiles_read) *tiles_read = (int64_t)h.tiles_read;
     if (overflowed) *overflowed = h.overflow;
     return ok();
 }

@@ -67,6 +67,7 @@ struct WsHeader {
     unsigned long long tag;        // fingerprint of the call that wrote the lists (0: not reusable)
     unsigned long long front_ok;   // slots of the front list (survivor / texture records)
     unsigned long long back_ok;    // slots of the back list (ghost entries, 2 slots each)
+    unsigned long long tiles_read; // tile culling: tiles the depth pass loaded
     unsigned long long tiles_fwd;  // dynamic tile counters of the depth and backward sweeps
     unsigned long long tiles_bwd;
 };
@@ -126,6 +127,7 @@ struct RasterArgs {
     int32_t inline_row;    // pose-partials row for inline (list overflow) ghost contributions
     int32_t dyn_tiles;     // bit 0: depth sweep, bit 1: backward sweep use dynamic tile claiming
     unsigned long long tag;// fingerprint of this call's inputs (host); 0 = records not reusable by the backward
+    const float *tbounds;  // tile culling: per-256-point-tile AABBs [ntiles][8] (adop_tile_bounds) or NULL
     PlaneTab *planes;      // [nviews] in the workspace header area
     LayerDesc *ldesc;      // [nviews] in the workspace header area
     float *d_feat;
@@ -142,6 +144,7 @@ int launch_resolve(const RasterArgs &a, void *stream);
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
 int launch_masks(const RasterArgs &a, int model, void *stream);
 int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed first unless grad_accumulate)
+int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n, float *out, void *stream);
 adop_status set_status(adop_status s, const char *msg);  // thread-local last-error message (adop_api.cu)
 int backward_grid(int sms);
 

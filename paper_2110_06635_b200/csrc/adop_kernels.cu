@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
             a.hdr->overflow = 0;
             a.hdr->tag = a.tag;
             a.hdr->tiles_fwd = 0ull;
+            a.hdr->tiles_read = 0ull;
         }
         if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for tile_views
             const int k = threadIdx.x;
@@ -370,10 +371,50 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 struct DepthSmem {
     float pos[kDStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
     uint64_t bar[kSW][kDStages];          // per-warp TMA completion barriers
-    int tile[kSW][kDStages];              // tile claimed into each stage (dynamic claiming)
+    int tile[kSW][kDStages];              // tile claimed into each stage (dynamic claiming / tile culling)
+    uint32_t tviews[kSW][kDStages];       // tile culling: views whose frustum meets the tile's bounds
     WarpQueue q[kSW];
     uint8_t cand[kSW][kWTile];           // compacted candidate list of the warp tile (tile offsets)
 };
+
+// Tile culling with precomputed per-tile bounds (adop_tile_bounds): the views whose (widened) frustum may
+// contain a point of tile t, as a warp-uniform mask (lane v tests view v; the same conservative half-space
+// test as the per-lane boxes).  Tiles without any view are neither loaded nor processed.
+__device__ __forceinline__ uint32_t bounds_views(const RasterArgs &a, int t, int lane) {
+    const float4 lo = __ldg(reinterpret_cast<const float4 *>(a.tbounds) + 2 * t);
+    const float4 hi = __ldg(reinterpret_cast<const float4 *>(a.tbounds) + 2 * t + 1);
+    const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+    if (!(l[0] <= h[0])) return 0u;  // no valid point in the tile
+    Box w;
+    float ext = 0.0f;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        w.c[ax] = 0.5f * (l[ax] + h[ax]);
+        w.e[ax] = 0.5f * (h[ax] - l[ax]) * 1.0000002f;  // covers the rounding of c -+ e
+        ext += fmaxf(fabsf(l[ax]), fabsf(h[ax]));
+    }
+    w.B = ext;
+    bool in = false;
+    if (lane < a.nviews) {
+        const PlaneTab &v = a.planes[lane];
+        bool out = false;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const float4 P = __ldg(&v.pl[k]);
+            const float2 M = __ldg(&v.pm[k]);
+            float val = P.w;
+            val = fmaf(P.x, w.c[0], val);
+            val = fmaf(fabsf(P.x), w.e[0], val);
+            val = fmaf(P.y, w.c[1], val);
+            val = fmaf(fabsf(P.y), w.e[1], val);
+            val = fmaf(P.z, w.c[2], val);
+            val = fmaf(fabsf(P.z), w.e[2], val);
+            out |= val < -fmaf(M.x, w.B, M.y);
+        }
+        in = !out;
+    }
+    return __ballot_sync(kFull, in);
+}
 
 __device__ __forceinline__ void init_layer_descs(const RasterArgs &a, LayerDesc *ld) {
     constexpr int F = 3 * ADOP_MAX_LAYERS + 1;
@@ -595,7 +636,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 template <int MODEL, int VM>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
-                                            uint8_t *cl, int lane, unsigned lt) {
+                                            uint8_t *cl, int lane, unsigned lt, uint32_t pre_views) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     uint32_t live = (uint32_t)vmask;
     if (a.ghost_thr != 0u) {  // ghosts take no part in the depth test (§4.3)
@@ -604,7 +645,8 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
     }
     const Box box = lane_box(rows, lane, vmask);
-    uint32_t views = VM == 2 ? tile_views(a, box, lane) : (VM == 0 ? 1u : (1u << a.nviews) - 1u);
+    uint32_t views = pre_views != 0xFFFFFFFFu ? pre_views
+                     : (VM == 2 ? tile_views(a, box, lane) : (VM == 0 ? 1u : (1u << a.nviews) - 1u));
 #pragma unroll 1
     while (views) {
         const int vs = VM == 0 ? 0 : __ffs(views) - 1;  // VM 0: compile-time view 0 (constant-bank operands)
@@ -665,6 +707,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     const bool staged_r = a.discard && a.radius != nullptr;
     const int rows = staged_r ? 4 : 3;
     const bool dyn = a.dyn_tiles & 1;
+    const bool tcull = a.tbounds != nullptr;  // the claimed tile goes through shared memory (sm.tile)
     if (lane == 0) {
         for (int st = 0; st < kDStages; ++st) mbar_init(&sm.bar[wid][st], 1);
         fence_mbar_init();
@@ -683,14 +726,39 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     // lane 0 claims the stage's next tile and streams its rows with the TMA engine (L2 evict-first):
     // x, y, z in one 2-D tensor copy (or three 1-D bulk copies), r_world in a 1-D bulk copy
     auto issue = [&](int st) {
-        if (lane != 0) return;
         int t;
-        if (dyn) {
-            t = (int)tc.take(&a.hdr->tiles_fwd);
+        if (tcull) {  // warp-collective: skip tiles that meet no view's frustum (never loaded)
+            uint32_t views;
+            for (;;) {
+                if (lane == 0) {
+                    if (dyn) {
+                        t = (int)tc.take(&a.hdr->tiles_fwd);
+                    } else {
+                        t = t_next;
+                        t_next += stride;
+                    }
+                }
+                t = __shfl_sync(kFull, t, 0);
+                if (t >= ntiles) {
+                    views = 0u;
+                    break;
+                }
+                views = bounds_views(a, t, lane);
+                if (views) break;
+            }
+            if (lane != 0) return;
             sm.tile[wid][st] = t;
+            sm.tviews[wid][st] = views;
+            if (t < ntiles) atomicAdd(&a.hdr->tiles_read, 1ull);
         } else {
-            t = t_next;
-            t_next += stride;
+            if (lane != 0) return;
+            if (dyn) {
+                t = (int)tc.take(&a.hdr->tiles_fwd);
+                sm.tile[wid][st] = t;
+            } else {
+                t = t_next;
+                t_next += stride;
+            }
         }
         if (t < nfull) {
             const uint32_t bar = bar_s + 8u * st, dst = pos_s + kStageBytes * st;
@@ -717,8 +785,10 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     int t_cons = (int)blockIdx.x * kSW + wid;
     for (int st = 0;; st = st + 1 == kDStages ? 0 : st + 1) {
         int t;
-        if (dyn) {
+        uint32_t pre_views = 0xFFFFFFFFu;
+        if (dyn || tcull) {
             t = *(volatile int *)&sm.tile[wid][st];
+            if (tcull) pre_views = *(volatile uint32_t *)&sm.tviews[wid][st];
         } else {
             t = t_cons;
             t_cons += stride;
@@ -743,13 +813,52 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
             }
             __syncwarp();
         }
-        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt);
+        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views);
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
     }
     if (qn > 0) drain(a, a.ldesc, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
+}
+
+// Per-tile bounds for tile culling: warp per 256-point tile, AABB of its finite points (lo.xyz, -, hi.xyz, -).
+__global__ void __launch_bounds__(kThreads) k_tile_bounds(const float *x, const float *y, const float *z, int64_t n,
+                                                          float4 *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + kWTile - 1) / kWTile;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x / 32) {
+        float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int k = lane; k < kWTile; k += 32) {
+            const int64_t i = t * kWTile + k;
+            if (i >= n) break;
+            const float p[3] = {x[i], y[i], z[i]};
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                lo[ax] = fminf(lo[ax], p[ax]);  // NaN coordinates are ignored (such points are invalid, R7)
+                hi[ax] = fmaxf(hi[ax], p[ax]);
+            }
+        }
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            lo[ax] = ord2f(__reduce_min_sync(kFull, f2ord(lo[ax])));
+            hi[ax] = ord2f(__reduce_max_sync(kFull, f2ord(hi[ax])));
+        }
+        if (lane == 0) {
+            out[2 * t] = make_float4(lo[0], lo[1], lo[2], 0.f);
+            out[2 * t + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+        }
+    }
+}
+
+int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n, float *out, void *stream) {
+    const int64_t ntiles = (n + kWTile - 1) / kWTile;
+    int64_t g = (ntiles * 32 + kThreads - 1) / kThreads;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    k_tile_bounds<<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(x, y, z, n, reinterpret_cast<float4 *>(out));
+    return (int)cudaGetLastError();
 }
 
 // --------------------------------------------------------------------------- //

@@ -490,3 +490,37 @@ def test_fisheye_precull_is_conservative(fov):
     _, fwd, _ = run_oracle(cloud, [cam], [pose], prm)
     compare_forward(r, fwd, ctx=f"fisheye precull {fov}")
     assert (fwd.count > 0).sum() > 300
+
+
+# --------------------------------------------------------------------------- #
+# tile culling with precomputed tile bounds (adop_tile_bounds): identical results
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("idx,n,views,bwd", [(3, 2_000_000, 1, False), (1, 400_000, 4, False), (4, 300_000, 16, True),
+                                             (2, 300_000, 1, True)])
+def test_tile_culling_is_exact(idx, n, views, bwd):
+    w = S.workload(idx, n=n, n_views=views if idx != 4 else None)
+    dev = torch.device("cuda")
+    cloud = w.cloud.to(dev)
+    G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, cloud.channels)] if bwd else None
+    plain = A.Renderer(cloud, w.cameras, w.poses, w.params)
+    plain.forward()
+    culled = A.Renderer(cloud, w.cameras, w.poses, w.params)
+    culled.points.enable_tile_culling()
+    culled.forward()
+    if bwd:
+        plain.backward(G)
+        culled.backward(G)
+    torch.cuda.synchronize()
+    culled.ws.stats3()
+    ntiles = (cloud.n + 255) // 256
+    assert 0 < culled.ws.tiles_read < ntiles
+    for p, q in zip(plain.pyrs, culled.pyrs):
+        assert torch.equal(p.keys, q.keys) and torch.equal(p.count, q.count)
+        torch.testing.assert_close(p.image, q.image, rtol=1e-5, atol=1e-6)
+    if bwd:
+        torch.testing.assert_close(plain.d_feat, culled.d_feat, rtol=1e-5, atol=1e-6)
+        torch.testing.assert_close(plain.d_pos, culled.d_pos, rtol=1e-4, atol=1e-6)
+    if idx == 2:  # and against the oracle
+        _, fwd, ob = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=[g.cpu() for g in G])
+        compare_forward(culled, fwd, ctx="tile culling")
+        compare_backward(culled, ob, ctx="tile culling")
