@@ -347,11 +347,15 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
                 for (int k = 0; k < 4; ++k) dc[k] = 1.0;  // no lateral bound
             }
             nc[4][2] = 1.0;
+            d.zplane = 1;
+            d.zoff = pr->z_near;
             if (c.model == ADOP_FISHEYE) {  // the depth is the distance: valid points only have Z >= 0 (narrow)
                 dc[4] = 0.0;
+                d.zoff = 0.0f;
                 if (std::isinf(d.r2cull)) {  // wide: no half-space at all
                     nc[4][2] = 0.0;
                     dc[4] = 1.0;
+                    d.zplane = 0;
                 }
             }
             const double T = std::fabs((double)poses[v].t[0]) + std::fabs((double)poses[v].t[1]) +

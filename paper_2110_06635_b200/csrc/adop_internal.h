@@ -27,6 +27,8 @@ struct ViewDesc {
     float fk, fkt;         // FMA pre-cull margin: m = fk * (|x|+|y|+|z|) + fkt
     float pl[5][4];        // conservative world-space frustum planes n.p + d >= 0 (warp-box cull)
     float pm[5][2];        // their margins: m = pm0 * sum_a max|p_a| + pm1 (+ 2^-16 |terms|)
+    int32_t zplane;        // plane 4 is the depth half-space Z + (pl[4][3] - t_z) >= 0 (all but the wide fisheye)
+    float zoff;            // Z = plane-4 value + zoff (z_near; 0 for the fisheye)
     uint32_t discard_salt; // hash salt of (seed, DISCARD, view id) (R11)
     int32_t wl[ADOP_MAX_LAYERS], hl[ADOP_MAX_LAYERS], off[ADOP_MAX_LAYERS];
     int32_t pixels;        // P

@@ -294,6 +294,10 @@ constexpr int kStages = 2;   // backward sweep ring depth
 #define ADOP_DCTAS 3
 #endif
 constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flight per warp)
+#ifndef ADOP_PREFILTER
+#define ADOP_PREFILTER 1
+#endif
+constexpr bool kPrefilter = ADOP_PREFILTER;  // depth sweep: hash-first discard prefilter (see depth_lane8)
 constexpr int kDCTAs = ADOP_DCTAS;      // depth sweep CTAs per SM
 constexpr int kSW = 8;               // warps per CTA of the TMA sweeps (3 CTAs x 8 warps per SM)
 constexpr int kST = kSW * 32;
@@ -652,8 +656,45 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         const int vs = VM == 0 ? 0 : __ffs(views) - 1;  // VM 0: compile-time view 0 (constant-bank operands)
         views &= views - 1u;
         const ViewDesc &v = a.v[vs];
-        if (__all_sync(kFull, box_culled(v, box))) continue;  // every lane's box is outside (warp-uniform)
+        const bool lane_out = box_culled(v, box);
+        if (__all_sync(kFull, lane_out)) continue;  // every lane's box is outside (warp-uniform)
         uint32_t m = 0u;
+        if (kPrefilter && a.discard && v.zplane) {
+            // Discard prefilter (Eq. 12 on a lane bound): the near plane's minimum over the lane box bounds every
+            // point's depth from below (margins as box_culled), so r_screen <= r_max = gamma r_w,max f_eff / z_lo
+            // and a point can be kept at layer 0 -- hence at any layer -- only if 1 - beta < r_max^2, i.e. its
+            // hash h > H = 2^24 (1 - r_max^2) (with slack).  Only those go to the exact path; no per-point
+            // frustum pre-cull (the exact path's bounds test decides).
+            float vmin = v.pl[4][3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                vmin = fmaf(v.pl[4][ax], box.c[ax], vmin);
+                vmin = fmaf(-fabsf(v.pl[4][ax]), box.e[ax], vmin);
+            }
+            const float zlo = (vmin - fmaf(v.pm[4][0], box.B, v.pm[4][1])) * 0.9999f + v.zoff;
+            float rwmax = a.radius_uniform;
+            if (staged_r) {
+                const float4 R0 = lane_row(rows[3], lane, 0), R1 = lane_row(rows[3], lane, 1);
+                rwmax = fmaxf(fmaxf(fmaxf(R0.x, R0.y), fmaxf(R0.z, R0.w)), fmaxf(fmaxf(R1.x, R1.y), fmaxf(R1.z, R1.w)));
+            }
+            bool all = true;
+            uint32_t H = 0u;
+            if (zlo > 0.0f) {
+                const float rmax = a.gamma * rwmax * v.feff / zlo;
+                const float qk = rmax * rmax * 1.004f;
+                if (qk < 1.0f) {
+                    const float hf = 16777216.0f * (1.0f - qk);
+                    if (hf > 4.0f) {
+                        H = (uint32_t)hf - 2u;
+                        all = false;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                m |= ((all || h24(v.discard_salt, a.goff + (uint32_t)pidx(j)) > H) ? 1u : 0u) << j;
+            if (lane_out) m = 0u;
+        } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const float4 X = lane_row(rows[0], lane, h), Y = lane_row(rows[1], lane, h), Z = lane_row(rows[2], lane, h);
@@ -669,6 +710,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
                 if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)pidx(4 * h + j));
                 m |= (cand ? 1u : 0u) << (4 * h + j);
             }
+        }
         }
         m &= live;
         if (!__any_sync(kFull, m != 0u)) continue;

@@ -513,14 +513,56 @@ def test_tile_culling_is_exact(idx, n, views, bwd):
     torch.cuda.synchronize()
     culled.ws.stats3()
     ntiles = (cloud.n + 255) // 256
-    assert 0 < culled.ws.tiles_read < ntiles
+    assert 0 < culled.ws.tiles_read <= ntiles
+    if views == 1:
+        assert culled.ws.tiles_read < ntiles  # one view sees only part of the cloud
     for p, q in zip(plain.pyrs, culled.pyrs):
         assert torch.equal(p.keys, q.keys) and torch.equal(p.count, q.count)
         torch.testing.assert_close(p.image, q.image, rtol=1e-5, atol=1e-6)
     if bwd:
+        # fp32 atomic sums in another order (cancellation in d_pos): tolerance scaled by the field's magnitude
         torch.testing.assert_close(plain.d_feat, culled.d_feat, rtol=1e-5, atol=1e-6)
-        torch.testing.assert_close(plain.d_pos, culled.d_pos, rtol=1e-4, atol=1e-6)
+        torch.testing.assert_close(plain.d_pos, culled.d_pos, rtol=1e-4, atol=1e-5 * float(plain.d_pos.abs().max()))
     if idx == 2:  # and against the oracle
         _, fwd, ob = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=[g.cpu() for g in G])
         compare_forward(culled, fwd, ctx="tile culling")
         compare_backward(culled, ob, ctx="tile culling")
+
+
+@pytest.mark.parametrize("model", [S.PINHOLE, S.OPENCV8, S.FISHEYE])
+def test_discard_prefilter_is_conservative(model):
+    """One point per layer-0 pixel (so every kept point owns its key) with radii putting gamma r_screen in
+    [0.2, 1.3]: thousands of keep / discard decisions near 1 - beta; the depth pass's hash-first discard
+    prefilter (a lane bound on r_screen) must never drop a point the exact test keeps -- keys bit-exact."""
+    rng = np.random.default_rng(23)
+    w, h = 256, 192
+    if model == S.FISHEYE:
+        cam = S.fisheye_camera(w, h, 120.0)
+    else:
+        cam = S.Camera(w, h, S.PINHOLE, 128.0, 128.0, 128.0, 96.0)
+        if model == S.OPENCV8:
+            cam = dataclasses.replace(cam, model=S.OPENCV8, k=(0.01, -0.02, 0.0, 0.005, 0.0, 0.0), p=(0.001, -0.001))
+            cam = dataclasses.replace(cam, r2_max=S.distortion_r2_max(cam))
+    us, vs = np.meshgrid(np.arange(w), np.arange(h))
+    z = rng.uniform(0.5, 40.0, us.size)
+    if model == S.FISHEYE:
+        xd, yd = (us.ravel() - cam.cx) / cam.fx, (vs.ravel() - cam.cy) / cam.fy
+        th = np.hypot(xd, yd)
+        keep = th < cam.r2_max * 0.98
+        s = np.where(th > 0, np.sin(th) / np.maximum(th, 1e-12), 1.0)
+        xyz = np.stack([s * xd * z, s * yd * z, np.cos(th) * z])[:, keep]
+        z = z[keep]
+    else:
+        xyz = np.stack([(us.ravel() - cam.cx) / cam.fx * z, (vs.ravel() - cam.cy) / cam.fy * z, z])
+    f = (cam.fx + cam.fy) / 2
+    rad = rng.uniform(0.2, 1.3, z.size) / 1.5 * z / f   # gamma r_screen in [0.2, 1.3]
+    perm = rng.permutation(z.size)
+    cloud = S.Cloud(torch.from_numpy(np.ascontiguousarray(xyz[:, perm], dtype=np.float32)),
+                    torch.from_numpy(np.ascontiguousarray(rad[perm], dtype=np.float32)),
+                    torch.rand(z.size, 4, generator=torch.Generator().manual_seed(4)))
+    prm = S.Params(layers=4, discard=True, seed=77)
+    pose = S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))
+    r = run_gpu(cloud, [cam], [pose], prm)
+    _, fwd, _ = run_oracle(cloud, [cam], [pose], prm)
+    compare_forward(r, fwd, ctx=f"prefilter {model}")
+    assert 0.2 < (fwd.count[0][: w * h] > 0).mean() < 0.95
