@@ -297,6 +297,12 @@ constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flig
 #ifndef ADOP_PREFILTER
 #define ADOP_PREFILTER 1
 #endif
+#ifndef ADOP_LAYER_UNROLL
+#define ADOP_LAYER_UNROLL 0  // measured: the rolled layer loop halves the kernel (icache) and is faster
+#endif
+#ifndef ADOP_DRAIN_NOINLINE
+#define ADOP_DRAIN_NOINLINE 0
+#endif
 constexpr bool kPrefilter = ADOP_PREFILTER;  // depth sweep: hash-first discard prefilter (see depth_lane8)
 constexpr int kDCTAs = ADOP_DCTAS;      // depth sweep CTAs per SM
 constexpr int kSW = 8;               // warps per CTA of the TMA sweeps (3 CTAs x 8 warps per SM)
@@ -506,7 +512,11 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
     Proj p;
     p.u0 = u0;
     p.v0 = v0;
+#if ADOP_LAYER_UNROLL
 #pragma unroll
+#else
+#pragma unroll 1
+#endif
     for (int l = 0; l < ADOP_MAX_LAYERS; ++l) {
         if (l >= a.layers) break;
         int pu, pv;
@@ -528,8 +538,12 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
 }
 
 // Process `cnt` (<= 32) entries from the top of the queue, one per lane (each with its own view slot).
-__device__ __forceinline__ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int cnt,
-                                      RecChunk &c, int lane, unsigned lt) {
+#if ADOP_DRAIN_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int cnt, RecChunk &c, int lane, unsigned lt) {
     __syncwarp();
     int nk = 0, vs = 0;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -637,7 +651,7 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
 
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
-template <int MODEL, int VM>
+template <int MODEL, int VM, bool DISC>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
                                             uint8_t *cl, int lane, unsigned lt, uint32_t pre_views) {
@@ -659,7 +673,8 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         const bool lane_out = box_culled(v, box);
         if (__all_sync(kFull, lane_out)) continue;  // every lane's box is outside (warp-uniform)
         uint32_t m = 0u;
-        if (kPrefilter && a.discard && v.zplane) {
+        // DISC = stochastic discarding on (a separate instance: each keeps only the code it runs)
+        if (kPrefilter && DISC && (MODEL != 2 || v.zplane)) {
             // Discard prefilter (Eq. 12 on a lane bound): the near plane's minimum over the lane box bounds every
             // point's depth from below (margins as box_culled), so r_screen <= r_max = gamma r_w,max f_eff / z_lo
             // and a point can be kept at layer 0 -- hence at any layer -- only if 1 - beta < r_max^2, i.e. its
@@ -707,7 +722,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             for (int j = 0; j < 4; ++j) {
                 float Zf, mz;
                 bool cand = precull_fma_z<MODEL>(v, xs[j], ys[j], zs[j], Zf, mz);
-                if (a.discard) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)pidx(4 * h + j));
+                if (DISC) cand &= maybe_kept(a, v, rs[j], Zf, mz, a.goff + (uint32_t)pidx(4 * h + j));
                 m |= (cand ? 1u : 0u) << (4 * h + j);
             }
         }
@@ -738,7 +753,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
 
 static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / kDCTAs, "depth sweep: kDCTAs CTAs per SM must fit in shared memory");
 
-template <int MODEL, int VM>
+template <int MODEL, int VM, bool DISC>
 __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     DepthSmem &sm = *reinterpret_cast<DepthSmem *>(smem_raw);
@@ -855,7 +870,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
             }
             __syncwarp();
         }
-        depth_lane8<MODEL, VM>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views);
+        depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views);
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
@@ -1942,10 +1957,13 @@ int launch_clear(const RasterArgs &a, int what, void *stream) {
 
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
-    auto k = k_depth_async<MODEL, VM>;
+    auto k = a.discard ? k_depth_async<MODEL, VM, true> : k_depth_async<MODEL, VM, false>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem));
+        cudaFuncSetAttribute(k_depth_async<MODEL, VM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(DepthSmem));
+        cudaFuncSetAttribute(k_depth_async<MODEL, VM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(DepthSmem));
         attr = true;
     }
     int per_sm = 0;
