@@ -126,7 +126,10 @@ __device__ __forceinline__ void load_points(const RasterArgs &a, int64_t i0, flo
 }
 
 // ---- record-region reservations (WsHeader::resv: front slots | back chunks << 40) ----
-constexpr int kChunk = 256;  // record slots reserved per warp at a time (back list: kChunk / 2 ghost entries)
+#ifndef ADOP_CHUNK
+#define ADOP_CHUNK 256
+#endif
+constexpr int kChunk = ADOP_CHUNK;  // record slots reserved per warp at a time (back list: kChunk / 2 ghost entries)
 constexpr unsigned long long kFrontMask = (1ull << kResvBackShift) - 1ull;
 constexpr unsigned long long kNoSlot = ~0ull;
 
@@ -302,6 +305,9 @@ constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flig
 #endif
 #ifndef ADOP_DRAIN_NOINLINE
 #define ADOP_DRAIN_NOINLINE 0
+#endif
+#ifndef ADOP_CHUNK_PREFETCH
+#define ADOP_CHUNK_PREFETCH 0
 #endif
 constexpr bool kPrefilter = ADOP_PREFILTER;  // depth sweep: hash-first discard prefilter (see depth_lane8)
 constexpr int kDCTAs = ADOP_DCTAS;      // depth sweep CTAs per SM
@@ -483,9 +489,13 @@ __device__ __forceinline__ uint32_t tile_views(const RasterArgs &a, const Box &b
     return __ballot_sync(kFull, in);
 }
 
-struct RecChunk {  // warp-uniform
+struct RecChunk {  // warp-uniform (pend: lane 0)
     unsigned long long base;
     int left;
+#if ADOP_CHUNK_PREFETCH
+    unsigned long long pend;  // old value of the next chunk's reservation, issued one chunk ahead
+    bool has;
+#endif
 };
 
 // A chunk that could not be reserved has base = capacity: its records are dropped (overflow is set).
@@ -494,11 +504,43 @@ __device__ __forceinline__ void put_record(const RasterArgs &a, unsigned long lo
 }
 
 // mark the chunk's unused slots dead, then reserve a fresh chunk (one atomic per kChunk slots)
+#if ADOP_CHUNK_PREFETCH
+// validation of a front reservation whose atomicAdd returned o (see resv_take)
+__device__ __forceinline__ unsigned long long front_validate(const RasterArgs &a, unsigned long long o) {
+    const unsigned long long f = resv_front_used(o);
+    if (f + kChunk + resv_back_slots(o) <= (unsigned long long)a.rec_capacity) {
+        atomicMax(&a.hdr->front_ok, f + kChunk);
+        return f;
+    }
+    atomicExch(&a.hdr->overflow, 1);
+    return kNoSlot;
+}
+#endif
+
 __device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, int lane, bool fresh) {
     for (int k = lane; k < c.left; k += 32) put_record(a, c.base + k, make_uint4(0u, 0u, 0u, kDeadView));
+#if ADOP_CHUNK_PREFETCH
+    // the next chunk is reserved one chunk ahead, so the atomic's latency is not waited for
+    unsigned long long b = 0;
+    if (!fresh) {  // end of the sweep: the prefetched chunk is never used -- mark it dead
+        if (!c.has) return;
+        if (lane == 0) b = front_validate(a, c.pend);
+        b = __shfl_sync(kFull, b, 0);
+        if (b != kNoSlot)
+            for (int k = lane; k < kChunk; k += 32) put_record(a, b + k, make_uint4(0u, 0u, 0u, kDeadView));
+        return;
+    }
+    if (lane == 0) {
+        const unsigned long long o = c.has ? c.pend : atomicAdd(&a.hdr->resv, (unsigned long long)kChunk);
+        b = front_validate(a, o);
+        c.pend = atomicAdd(&a.hdr->resv, (unsigned long long)kChunk);
+    }
+    c.has = true;
+#else
     if (!fresh) return;
     unsigned long long b = 0;
     if (lane == 0) b = resv_take<false>(a, kChunk, true);
+#endif
     b = __shfl_sync(kFull, b, 0);
     c.base = b == kNoSlot ? (unsigned long long)a.rec_capacity : b;
     c.left = kChunk;
@@ -838,6 +880,10 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     RecChunk c;
     c.base = 0;
     c.left = 0;
+#if ADOP_CHUNK_PREFETCH
+    c.has = false;
+    c.pend = 0;
+#endif
     uint32_t phase = 0u;
     int t_cons = (int)blockIdx.x * kSW + wid;
     for (int st = 0;; st = st + 1 == kDStages ? 0 : st + 1) {
