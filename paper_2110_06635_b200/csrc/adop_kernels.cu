@@ -1027,15 +1027,17 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
             for (int c0 = 0; c0 < C; c0 += 4) {
                 float o[4][4];  // [channel][pixel]
 #pragma unroll
+                float4 acc[4];  // loaded with the counts (L2-resident after the blend): one round trip
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
+#pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (cn[q] > 0.0f) acc = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
-                    const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+                    const float av[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
                     float bgv[4] = {a.bg[c0], a.bg[c0 + 1], a.bg[c0 + 2], a.bg[c0 + 3]};
                     if (ENV && !(cn[q] > 0.0f)) env_bg4(a, v, l, (int)(j + q), c0, bgv);
+                    const float inv = __frcp_rn(cn[q]);  // Eq. 7 mean as sum x (1/n): within 1 ulp of the quotient
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc)
-                        o[cc][q] = cn[q] > 0.0f ? __fdiv_rn(av[cc], cn[q]) : bgv[cc];
+                    for (int cc = 0; cc < 4; ++cc) o[cc][q] = cn[q] > 0.0f ? __fmul_rn(av[cc], inv) : bgv[cc];
                 }
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc)
