@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region (single GPU)")
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     return ap.parse_args()
@@ -152,28 +153,56 @@ def run_ours(args, rank, world, local_rank):
     ws = A.Workspace(pts, cams, ap, dev, cap)
     stream = torch.cuda.current_stream(dev)
 
-    def step(ev=None):
+    def step(ev=None, s=None):
+        s = stream if s is None else s
         if ev is not None:
-            ev[0].record(stream)
-        A.forward_depth(pts, cams, poses, ap, pyrs, ws, stream)
+            ev[0].record(s)
+        A.forward_depth(pts, cams, poses, ap, pyrs, ws, s)
         if ev is not None:
-            ev[1].record(stream)
+            ev[1].record(s)
         if world > 1:
             for p in pyrs:
                 dist.all_reduce(p.keys, op=dist.ReduceOp.MIN)
         if ev is not None:
-            ev[2].record(stream)
-        A.forward_blend(pts, cams, poses, ap, pyrs, ws, stream)
+            ev[2].record(s)
+        A.forward_blend(pts, cams, poses, ap, pyrs, ws, s)
         if ev is not None:
-            ev[3].record(stream)
+            ev[3].record(s)
         if world > 1:
             for p in pyrs:
                 dist.all_reduce(p.ac, op=dist.ReduceOp.SUM)
         if ev is not None:
-            ev[4].record(stream)
-        A.forward_resolve(pts, cams, poses, ap, pyrs, ws, stream)
+            ev[4].record(s)
+        A.forward_resolve(pts, cams, poses, ap, pyrs, ws, s)
         if ev is not None:
-            ev[5].record(stream)
+            ev[5].record(s)
+
+    # Single GPU: the frame's launches are captured once into two CUDA graphs (depth phase | blend +
+    # resolve) and replayed; the timed region holds only the replays and one event pair around each
+    # depth phase (for the roofline).  N > 1 runs the phases eagerly with the collectives in between.
+    graphs = None
+    if world == 1 and not args.no_graph:
+        gs = torch.cuda.Stream(dev)
+        gd, gr = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            step(s=gs)
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(gd, stream=gs):
+                A.forward_depth(pts, cams, poses, ap, pyrs, ws, gs)
+            with torch.cuda.graph(gr, stream=gs):
+                A.forward_blend(pts, cams, poses, ap, pyrs, ws, gs)
+                A.forward_resolve(pts, cams, poses, ap, pyrs, ws, gs)
+        torch.cuda.synchronize(dev)
+        graphs = (gd, gr)
+
+    def timed_step(ev):
+        if graphs is None:
+            step(ev)
+            return
+        ev[0].record(stream)
+        graphs[0].replay()
+        ev[1].record(stream)
+        graphs[1].replay()
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -197,17 +226,22 @@ def run_ours(args, rank, world, local_rank):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        timed_step(evs[k])
     end.record(stream)
     barrier()
     clk = clocks.stop()
     total_ms = start.elapsed_time(end)
-    ph = [[e[i].elapsed_time(e[i + 1]) for e in evs] for i in range(5)]
+    depth_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    # phase breakdown (eager, every phase bracketed by events): a separate pass after the timed region
+    bevs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(min(args.steps, 20))]
+    for e in bevs:
+        step(e)
+    barrier()
+    ph = [[e[i].elapsed_time(e[i + 1]) for e in bevs] for i in range(5)]
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
-    depth_ms = statistics.mean(ph[0])
 
     # the same frames with tile culling (precomputed per-tile bounds, adop_tile_bounds): results identical,
     # tiles outside the frustum are neither loaded nor processed (static-scene rendering)
@@ -250,7 +284,9 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"point-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "inputs (1.6 GB/GPU positions+radii) exceed the 126 MB L2; no flush needed",
                        "record_slots_per_frame": records, "record_overflow": overflow},
-            "phases_ms": {"depth": depth_ms, "key_allreduce": statistics.mean(ph[1]),
+            "timing": ("CUDA graph replays (depth | blend+resolve) with an event pair around each depth phase"
+                       if graphs is not None else "eager C-ABI calls, events around every phase"),
+            "phases_ms": {"depth": statistics.mean(ph[0]), "key_allreduce": statistics.mean(ph[1]),
                           "blend": statistics.mean(ph[2]), "accum_allreduce": statistics.mean(ph[3]),
                           "resolve": statistics.mean(ph[4])},
             "roofline": {"kernel": "depth phase (k_clear<KEYS> + k_depth_async<PINHOLE, 1 view>)", "bound": "hbm",
