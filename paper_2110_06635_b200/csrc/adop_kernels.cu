@@ -393,6 +393,43 @@ struct DepthSmem {
     uint8_t cand[kSW][kWTile];           // compacted candidate list of the warp tile (tile offsets)
 };
 
+// Tile culling, per lane: the views whose frustum may meet tile t (all views tested by this lane).
+__device__ __forceinline__ uint32_t bounds_views_lane(const RasterArgs &a, int t) {
+    const float4 lo = __ldg(reinterpret_cast<const float4 *>(a.tbounds) + 2 * t);
+    const float4 hi = __ldg(reinterpret_cast<const float4 *>(a.tbounds) + 2 * t + 1);
+    const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+    if (!(l[0] <= h[0])) return 0u;
+    Box w;
+    float ext = 0.0f;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        w.c[ax] = 0.5f * (l[ax] + h[ax]);
+        w.e[ax] = 0.5f * (h[ax] - l[ax]) * 1.0000002f;
+        ext += fmaxf(fabsf(l[ax]), fabsf(h[ax]));
+    }
+    w.B = ext;
+    uint32_t mask = 0u;
+    for (int vv = 0; vv < a.nviews; ++vv) {
+        const PlaneTab &v = a.planes[vv];
+        bool out = false;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const float4 P = __ldg(&v.pl[k]);
+            const float2 M = __ldg(&v.pm[k]);
+            float val = P.w;
+            val = fmaf(P.x, w.c[0], val);
+            val = fmaf(fabsf(P.x), w.e[0], val);
+            val = fmaf(P.y, w.c[1], val);
+            val = fmaf(fabsf(P.y), w.e[1], val);
+            val = fmaf(P.z, w.c[2], val);
+            val = fmaf(fabsf(P.z), w.e[2], val);
+            out |= val < -fmaf(M.x, w.B, M.y);
+        }
+        mask |= (out ? 0u : 1u) << vv;
+    }
+    return mask;
+}
+
 // Tile culling with precomputed per-tile bounds (adop_tile_bounds): the views whose (widened) frustum may
 // contain a point of tile t, as a warp-uniform mask (lane v tests view v; the same conservative half-space
 // test as the per-lane boxes).  Tiles without any view are neither loaded nor processed.
@@ -822,11 +859,40 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     int t_next = (int)blockIdx.x * kSW + wid;  // static order: warp w takes tiles w, w + W, ...
     TileClaim tc;
     if (dyn && lane == 0) tc.init(&a.hdr->tiles_fwd, ntiles, stride, t_next, true);
+    uint32_t win_rem = 0u, win_lmask = 0u;  // tile culling window (static claiming)
+    int win_t0 = 0;
     // lane 0 claims the stage's next tile and streams its rows with the TMA engine (L2 evict-first):
     // x, y, z in one 2-D tensor copy (or three 1-D bulk copies), r_world in a 1-D bulk copy
     auto issue = [&](int st) {
         int t;
-        if (tcull) {  // warp-collective: skip tiles that meet no view's frustum (never loaded)
+        if (tcull && !dyn) {
+            // warp-collective window scan: lane i tests tile t_next + i * stride (one round trip for 32 tiles),
+            // the visible ones are then issued one by one
+            uint32_t views = 0u;
+            for (;;) {
+                if (win_rem == 0u) {
+                    if (t_next >= ntiles) {
+                        t = ntiles;
+                        break;
+                    }
+                    const int ti = t_next + lane * stride;
+                    win_lmask = ti < ntiles ? bounds_views_lane(a, ti) : 0u;
+                    win_t0 = t_next;
+                    t_next += 32 * stride;
+                    win_rem = __ballot_sync(kFull, win_lmask != 0u);
+                    continue;
+                }
+                const int i = __ffs(win_rem) - 1;
+                win_rem &= win_rem - 1u;
+                t = win_t0 + i * stride;
+                views = __shfl_sync(kFull, win_lmask, i);
+                break;
+            }
+            if (lane != 0) return;
+            sm.tile[wid][st] = t;
+            sm.tviews[wid][st] = views;
+            if (t < ntiles) atomicAdd(&a.hdr->tiles_read, 1ull);
+        } else if (tcull) {  // dynamic claiming: tile by tile (lane v tests view v)
             uint32_t views;
             for (;;) {
                 if (lane == 0) {
