@@ -23,6 +23,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
+    "-split-compile=0",  # the optimizer's work on the kernel instances in parallel threads
     "-I", os.path.join(ROOT, "include"),
 ]
 
@@ -51,13 +52,16 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     bdir = os.path.join(PKG, "build" if out is None else "build_" + os.path.basename(out).replace(".so", ""))
     os.makedirs(bdir, exist_ok=True)
     logs = []
-    for src in sources():
+    procs = []
+    for src in sources():  # the translation units compile concurrently
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for src, obj, p in procs:
+        out, err = p.communicate()
+        logs.append(out + err)
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     target = LIB if out is None else out
