@@ -768,7 +768,8 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                         for (int ch = 0; ch < C; ++ch) {
                             double t = w[k] * (double)Gv[C * off + ch * hw + j];
                             if (denv) denv[idx[k] * C + ch] += t;
-                            if (denv_abs) denv_abs[idx[k] * C + ch] += fabs(t);
+                            /* tolerance scale: |G| per tap (the fp32 lookup's weights err by ~(W + H) 2^-22) */
+                            if (denv_abs) denv_abs[idx[k] * C + ch] += fabs((double)Gv[C * off + ch * hw + j]);
                         }
                 }
             }

@@ -80,10 +80,13 @@ def compare_backward(r, bwd, ctx="", check_feat=True, check_pos=True, views=None
     tol = 1e-6 + 1e-5 * np.maximum(np.abs(bwd.dpose), 1e-2 * bwd.dpose_abs)
     assert np.all(err <= tol), f"{ctx} d_pose err {err} tol {tol}\ngpu {g}\noracle {bwd.dpose}"
     if getattr(r, "d_env", None) is not None and bwd.denv is not None:
-        # NEXT-2 environment-map gradient: fp32 sums of w G terms, error ~ S = sum |w G|
+        # NEXT-2 environment-map gradient: fp32 sums of w G terms plus the bilinear weights' error -- the
+        # fp32 lookup coordinates err by a few ulp of the angles, i.e. ~(W + H) 2^-22 texels -- both scaled
+        # by S = sum over the texel's taps of |G|
         g = r.d_env.cpu().numpy().astype(np.float64)
+        H_, W_ = g.shape[0], g.shape[1]
         err = np.abs(g - bwd.denv)
-        tol = 1e-6 + 1e-5 * bwd.denv_abs
+        tol = 1e-6 + (1e-5 + (W_ + H_) * 2.0 ** -22) * bwd.denv_abs
         assert np.all(err <= tol), f"{ctx} d_env max excess {(err - tol).max()}"
     if getattr(r, "d_intr", None) is not None and bwd.dintr is not None:
         # NEXT-1 intrinsics gradient: same tolerance form as d_pose (R20)

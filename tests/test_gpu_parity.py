@@ -566,3 +566,27 @@ def test_discard_prefilter_is_conservative(model):
     _, fwd, _ = run_oracle(cloud, [cam], [pose], prm)
     compare_forward(r, fwd, ctx=f"prefilter {model}")
     assert 0.2 < (fwd.count[0][: w * h] > 0).mean() < 0.95
+
+
+@pytest.mark.parametrize("fov", [120.0, 200.0])
+def test_fisheye_with_env_map_log_descriptors_and_tile_culling(fov):
+    """The NEXT items together on the fisheye: environment map (fisheye C^-1), log descriptors, ghosts,
+    intrinsics, and the same frame with tile culling -- against the oracle."""
+    room = S.make_room(10.0)
+    cloud = S.room_cloud(120_000, room, channels=4, seed=31)
+    cloud = dataclasses.replace(cloud, radius=torch.full_like(cloud.radius, 0.05), feat=cloud.feat * 2 - 1.5)
+    cams = [S.fisheye_camera(128, 96, fov)]
+    poses = S.room_poses(1, room, seed=12)
+    prm = S.Params(layers=4, discard=True, ghost_rate=0.25, seed=9, log_descriptors=True,
+                   env_map=smooth_env(32, 64, 4, seed=5))
+    G = grads_for(cams, prm.layers, 4)
+    dev = torch.device("cuda")
+    r = A.Renderer(cloud.to(dev), cams, poses, prm, intrinsics=True)
+    r.points.enable_tile_culling()
+    r.forward()
+    r.backward([g.to(dev) for g in G])
+    torch.cuda.synchronize()
+    _, fwd, bwd = run_oracle(cloud, cams, poses, prm, grads=G)
+    compare_forward(r, fwd, ctx=f"fisheye+env {fov}")
+    compare_backward(r, bwd, ctx=f"fisheye+env {fov}")
+    assert r.d_env.abs().sum() > 0 and (fwd.count > 0).sum() > 1000
