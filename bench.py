@@ -384,18 +384,18 @@ def run_secondary(args, dev):
         for _ in range(3):
             one()
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        fw, bw = [], []
-        for _ in range(K):
+        # back to back (the host enqueues ahead; no synchronization between iterations)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        for ev in evs:
             ev[0].record()
             r.forward()
             ev[1].record()
             if G is not None:
                 r.backward(G)
             ev[2].record()
-            torch.cuda.synchronize()
-            fw.append(ev[0].elapsed_time(ev[1]))
-            bw.append(ev[1].elapsed_time(ev[2]))
+        torch.cuda.synchronize()
+        fw = [ev[0].elapsed_time(ev[1]) for ev in evs]
+        bw = [ev[1].elapsed_time(ev[2]) for ev in evs]
         V = len(w.cameras)
         fms, bms = statistics.median(fw), statistics.median(bw)
         res[w.name] = {"config": f"BASELINE.json configs[{idx}]", "points": w.cloud.n, "views": V,

@@ -314,8 +314,8 @@ class _Call:
         self.points, self.params = points, params
 
 
-def _phase(fn_name, points, cams, poses, params, pyrs, ws: Workspace, stream=None):
-    c = _Call(points, cams, poses, params, pyrs)
+def _phase(fn_name, points, cams, poses, params, pyrs, ws: Workspace, stream=None, call=None):
+    c = _Call(points, cams, poses, params, pyrs) if call is None else call
     fn = getattr(lib(), fn_name)
     _check(fn(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, ws.ptr, ws.nbytes,
               _stream(stream)))
@@ -333,17 +333,17 @@ def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None):
     _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream)
 
 
-def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None):
-    _phase("adop_rasterize_forward", points, cams, poses, params, pyrs, ws, stream)
+def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None, call=None):
+    _phase("adop_rasterize_forward", points, cams, poses, params, pyrs, ws, stream, call)
 
 
 def rasterize_backward(points, cams, poses, params, pyrs, grads: Sequence[torch.Tensor], ws,
                        d_feat: Optional[torch.Tensor], d_pos: Optional[torch.Tensor],
                        d_pose: Optional[torch.Tensor], d_intr: Optional[torch.Tensor] = None,
-                       d_env: Optional[torch.Tensor] = None, stream=None):
+                       d_env: Optional[torch.Tensor] = None, stream=None, call=None):
     """d_intr: optional [V][12] float64 camera-intrinsics gradient (fx, fy, cx, cy, k1..k6, p1, p2);
     d_env: optional [H][W][C] float32 environment-map gradient (needs params.env_map)."""
-    c = _Call(points, cams, poses, params, pyrs)
+    c = _Call(points, cams, poses, params, pyrs) if call is None else call
     g = (C.c_void_p * c.V)(*[t.data_ptr() for t in grads])
     _check(lib().adop_rasterize_backward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, g,
                                          _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), _ptr(d_intr), _ptr(d_env), ws.ptr,
@@ -425,8 +425,14 @@ class Renderer:
         self.d_feat = self.d_pos = self.d_pose = self.d_intr = self.d_env = None
         self.intrinsics = intrinsics  # backward also produces d_intr [V][12] (NEXT-1)
 
+    def _call(self):
+        # marshalled descriptors, built once (the cameras / poses / buffers of a Renderer are fixed)
+        if getattr(self, "_c", None) is None:
+            self._c = _Call(self.points, self.cams, self.poses, self.params, self.pyrs)
+        return self._c
+
     def forward(self, stream=None):
-        rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream)
+        rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream, self._call())
         return self.pyrs
 
     def alloc_grads(self):
@@ -443,7 +449,7 @@ class Renderer:
         if self.d_feat is None:
             self.alloc_grads()
         rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,
-                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, self.d_env, stream)
+                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, self.d_env, stream, self._call())
         return self.d_feat, self.d_pos, self.d_pose
 
     def masks(self, stream=None) -> torch.Tensor:
