@@ -58,10 +58,10 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     for src, obj, p in procs:
-        out, err = p.communicate()
-        logs.append(out + err)
+        so, se = p.communicate()
+        logs.append(so + se)
         if p.returncode != 0:
-            sys.stderr.write(out + err)
+            sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
     target = LIB if out is None else out
