@@ -1035,8 +1035,11 @@ int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n
 // --------------------------------------------------------------------------- //
 // (Measured: a separate low-register record kernel at higher occupancy moved more DRAM bytes and ran
 // slower on configs[4]; the L2 reductions, not latency, bound this pass.)
-template <int MODEL, bool VEC, bool VEC4>
-__global__ void __launch_bounds__(kThreads) k_blend(const __grid_constant__ RasterArgs a) {
+// HOCC: 6 blocks per SM (40 registers; the overflow fallback spills, it is the slow path anyway) -- one
+// view: blend phase 63 -> 58 us on configs[3]; with 16 views (configs[4]) the extra concurrency thrashes
+// L2 (forward 4.73 -> 5.17 ms), so multi-view launches keep 4 blocks per SM.
+template <int MODEL, bool VEC, bool VEC4, bool HOCC>
+__global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_constant__ RasterArgs a) {
     if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
         stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
         return;
@@ -2113,7 +2116,9 @@ static int launch_blend_t(const RasterArgs &a, int sms, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     int e = launch_clear(a, CLEAR_ACC, stream);
     if (e) return e;
-    auto k = k_blend<MODEL, VEC, VEC4>;
+    auto k = k_blend<MODEL, VEC, VEC4, false>;
+    if constexpr (VEC && VEC4)
+        if (a.nviews == 1) k = k_blend<MODEL, VEC, VEC4, true>;
     int g = resident_grid(k, sms, kWarps * 128, a.n > 0 ? a.n : 1);
     k<<<g, kThreads, 0, s>>>(a);
     return (int)cudaGetLastError();
