@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region (single GPU)")
+    ap.add_argument("--comm", choices=["nccl", "p2p"], default="nccl",
+                    help="N > 1 point sharding: NCCL all-reduces of private pyramids, or every shard reducing "
+                         "straight into rank 0's pyramid over peer memory (DESIGN.md section 8)")
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     return ap.parse_args()
@@ -152,8 +155,47 @@ def run_ours(args, rank, world, local_rank):
     cap = A.default_record_capacity(N, len(cams), prm.layers, prm.discard)
     ws = A.Workspace(pts, cams, ap, dev, cap)
     stream = torch.cuda.current_stream(dev)
+    p2p = world > 1 and args.comm == "p2p"
+    rd_pyrs = pyrs  # buffers this rank reads back (count, image): a non-owner's own under p2p
+    if p2p:  # rank 0's pyramid is shared: the others map its keys / accum / count (CUDA IPC)
+        ap.s.shared_pyramid = 1
+        obj = [[(A.ipc_export(p.keys), A.ipc_export(p.accum), A.ipc_export(p.count)) for p in pyrs]
+               if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        if rank != 0:
+            own = rd_pyrs = pyrs
+            pyrs = [A.PeerPyramid(A.ipc_open(*k), A.ipc_open(*a), A.ipc_open(*c), q.image.data_ptr(), q.width,
+                                  q.height, q.layers) for (k, a, c), q in zip(obj[0], own)]
+
+    def p2p_step(ev=None):  # same event slots as step(): the barriers take the collectives' places
+        def sync_barrier():
+            torch.cuda.synchronize(dev)
+            dist.barrier(device_ids=[local_rank])
+        if ev is not None:
+            ev[0].record(stream)
+        if rank == 0:
+            A.clear_pyramid(cams, prm.layers, C, pyrs, stream)
+        sync_barrier()
+        A.forward_depth(pts, cams, poses, ap, pyrs, ws, stream)
+        if ev is not None:
+            ev[1].record(stream)
+        sync_barrier()
+        if ev is not None:
+            ev[2].record(stream)
+        A.forward_blend(pts, cams, poses, ap, pyrs, ws, stream)
+        if ev is not None:
+            ev[3].record(stream)
+        sync_barrier()
+        if ev is not None:
+            ev[4].record(stream)
+        if rank == 0:
+            A.forward_resolve(pts, cams, poses, ap, pyrs, ws, stream)
+        if ev is not None:
+            ev[5].record(stream)
 
     def step(ev=None, s=None):
+        if p2p:
+            return p2p_step(ev)
         s = stream if s is None else s
         if ev is not None:
             ev[0].record(s)
@@ -269,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
         #   keys 8 B per pixel written once (survivor records are this design's intermediate, not counted);
         #   frame: B_fwd = N (12 + 4) + N_blend 4C + P (8 + 4C + 4), N_blend = sum of the counts.
         alg = N * 16 + P * 8
-        n_blend = int(sum(float(p.count.sum()) for p in pyrs))
+        n_blend = int(sum(float(p.count.sum()) for p in rd_pyrs))
         alg_frame = N * 16 + n_blend * 4 * C + P * (8 + 4 * C + 4)
         peak, peak_src = peaks()
         achieved = alg / (depth_ms * 1e-3) / 1e9
@@ -281,7 +323,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": WORKLOAD, "points_per_gpu": N, "points_total": N * world, "channels": C,
                        "layers": prm.layers, "resolution": "1920x1080", "views": 1, "discard": True,
                        "gamma": prm.gamma, "alpha": prm.alpha,
-                       "parallelism": f"point-sharded x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"point-sharded x{world} ({args.comm})" if world > 1 else "single GPU"),
                        "l2": "inputs (1.6 GB/GPU positions+radii) exceed the 126 MB L2; no flush needed",
                        "record_slots_per_frame": records, "record_overflow": overflow},
             "timing": ("CUDA graph replays (depth | blend+resolve) with an event pair around each depth phase"
@@ -305,7 +347,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": 5 * args.steps,
             "clocks": clk,
         }
-    return out, (dev, step, pts, cloud, cams, poses, prm, pyrs, ws, stream, barrier, N, C)
+    return out, (dev, step, pts, cloud, cams, poses, prm, rd_pyrs, ws, stream, barrier, N, C)
 
 
 def run_e2e(args, ctx, rank, world, local_rank):

@@ -135,6 +135,13 @@ typedef struct {
     int32_t normal_culling; /* Eq. 5 (L208) normal culling, R32: 0 off; +1 keep points
                                with (R n).(R x + t) > 0 as printed; -1 keep < 0 (the flipped
                                orientation: outward normals facing the camera)              */
+    int32_t shared_pyramid; /* point sharding over peer memory: 1 = the
+                               keys / accum / count buffers of `views` are ONE pyramid shared by
+                               every shard (e.g. the owner's, opened with adop_ipc_open); the
+                               phases then do not clear them -- the owner calls
+                               adop_clear_pyramid once per frame and the caller orders the
+                               phases of all shards (depth of every shard before any blend,
+                               every blend before the owner's resolve).  0 = private pyramid. */
 } adop_params;
 
 /* Buffers of one view (device).  See layouts above. */
@@ -241,6 +248,26 @@ ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspac
 /* Bounding box of every 256-point tile of `points` (lo x, y, z, 0, hi x, y, z, 0; NaN coordinates
  * ignored): bounds = device float [ceil(n/256)][8], 16-byte aligned.  Enqueued on `stream`. */
 ADOP_API adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *stream);
+
+/* ---- Point sharding over peer memory (NVLink P2P / CUDA IPC) ---------- */
+
+/* keys <- sentinel, accum <- 0, count <- 0 for every view of `views` (device buffers of
+ * adop_pyramid_pixels(w, h, layers) pixels, C channels): the owner's once-per-frame reset of a
+ * shared pyramid.  Enqueued on `stream`.  Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_CUDA. */
+ADOP_API adop_status adop_clear_pyramid(int32_t n_views, const adop_camera *cameras, int32_t layers, int32_t channels,
+                               const adop_pyramid *views, void *stream);
+
+/* Export device memory to another process: `handle` (64 bytes, host) names the allocation that
+ * contains `ptr`, `offset` is ptr's byte offset in it (cudaIpcGetMemHandle + the allocation base). */
+ADOP_API adop_status adop_ipc_export(const void *ptr, unsigned char handle[64], uint64_t *offset);
+
+/* Map an exported allocation into this process (peer access enabled lazily): *base = the mapped
+ * allocation (pass it to adop_ipc_close), *ptr = base + offset.  One mapping per allocation and
+ * process: the caller caches it (opening the same handle twice fails). */
+ADOP_API adop_status adop_ipc_open(const unsigned char handle[64], uint64_t offset, void **base, void **ptr);
+
+/* Unmap an allocation mapped by adop_ipc_open. */
+ADOP_API adop_status adop_ipc_close(void *base);
 
 /* ---- Preprocessing before the hot path (untimed setup) ------------- */
 

@@ -14,7 +14,7 @@ import ctypes as C
 import dataclasses
 import math
 import os
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 
@@ -56,7 +56,8 @@ class adop_params(C.Structure):
                 ("ghost_rate", C.c_float), ("z_near", C.c_float), ("seed", C.c_uint64),
                 ("view_id_base", C.c_int32), ("background", C.c_void_p), ("grad_accumulate", C.c_int32),
                 ("log_descriptors", C.c_int32), ("env_map", C.c_void_p), ("env_width", C.c_int32),
-                ("env_height", C.c_int32), ("spatial_rendered", C.c_int32), ("normal_culling", C.c_int32)]
+                ("env_height", C.c_int32), ("spatial_rendered", C.c_int32), ("normal_culling", C.c_int32),
+                ("shared_pyramid", C.c_int32)]
 
 
 class adop_pyramid(C.Structure):
@@ -97,6 +98,14 @@ def lib():
         L.adop_workspace_stats.restype = C.c_int
         L.adop_workspace_stats.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, P(C.c_int64), P(C.c_int64),
                                            P(C.c_int32), P(C.c_int64)]
+        L.adop_clear_pyramid.restype = C.c_int
+        L.adop_clear_pyramid.argtypes = [C.c_int32, P(adop_camera), C.c_int32, C.c_int32, P(adop_pyramid), C.c_void_p]
+        L.adop_ipc_export.restype = C.c_int
+        L.adop_ipc_export.argtypes = [C.c_void_p, C.c_char_p, P(C.c_uint64)]
+        L.adop_ipc_open.restype = C.c_int
+        L.adop_ipc_open.argtypes = [C.c_char_p, C.c_uint64, P(C.c_void_p), P(C.c_void_p)]
+        L.adop_ipc_close.restype = C.c_int
+        L.adop_ipc_close.argtypes = [C.c_void_p]
         L.adop_tile_bounds.restype = C.c_int
         L.adop_tile_bounds.argtypes = [P(adop_points), C.c_void_p, C.c_void_p]
         L.adop_prep_workspace_size.restype = C.c_int
@@ -197,6 +206,7 @@ class Params:
         s.log_descriptors = int(bool(getattr(p, "log_descriptors", False)))
         s.spatial_rendered = int(bool(getattr(p, "spatial_rendered", False)))
         s.normal_culling = int(getattr(p, "normal_culling", 0))
+        s.shared_pyramid = int(bool(getattr(p, "shared_pyramid", False)))
         env = getattr(p, "env_map", None)
         self.env = None
         if env is not None:  # device [H][W][C] float32 (NEXT-2)
@@ -240,6 +250,55 @@ class Pyramid:
             off += -(-self.width // (1 << k)) * -(-self.height // (1 << k))
         wl, hl = -(-self.width // (1 << l)), -(-self.height // (1 << l))
         return self.image[channels * off: channels * (off + wl * hl)].view(channels, hl, wl)
+
+
+class PeerPyramid:
+    """A view's pyramid whose keys / accum / count live in another process's memory (CUDA IPC, peer
+    access over NVLink; point sharding).  The image pointer is this process's own
+    (only the owner resolves)."""
+
+    def __init__(self, keys: int, accum: int, count: int, image: int, width: int, height: int, layers: int):
+        self.keys_ptr, self.accum_ptr, self.count_ptr, self.image_ptr = keys, accum, count, image
+        self.width, self.height, self.layers = width, height, layers
+
+    def struct(self) -> adop_pyramid:
+        s = adop_pyramid()
+        s.image, s.count, s.keys, s.accum = self.image_ptr, self.count_ptr, self.keys_ptr, self.accum_ptr
+        return s
+
+
+def clear_pyramid(cams, layers: int, channels: int, pyrs, stream=None):
+    """keys <- sentinel, accum, count <- 0 (the owner's reset of a shared pyramid)."""
+    ca = (adop_camera * len(cams))(*[camera_struct(c) for c in cams])
+    pa = (adop_pyramid * len(pyrs))(*[p.struct() for p in pyrs])
+    _check(lib().adop_clear_pyramid(len(cams), ca, int(layers), int(channels), pa, _stream(stream)))
+
+
+def ipc_export(t: torch.Tensor) -> Tuple[bytes, int]:
+    """(64-byte handle of the allocation holding t, byte offset of t in it)."""
+    h = C.create_string_buffer(64)
+    off = C.c_uint64(0)
+    _check(lib().adop_ipc_export(t.data_ptr(), h, C.byref(off)))
+    return h.raw, int(off.value)
+
+
+_ipc_maps = {}
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Device pointer of an exported tensor in this process (one mapping per allocation, cached)."""
+    base = _ipc_maps.get(handle)
+    if base is None:
+        b, p = C.c_void_p(0), C.c_void_p(0)
+        _check(lib().adop_ipc_open(handle, 0, C.byref(b), C.byref(p)))
+        base = _ipc_maps[handle] = int(b.value)
+    return base + int(offset)
+
+
+def ipc_close_all():
+    for base in _ipc_maps.values():
+        _check(lib().adop_ipc_close(base))
+    _ipc_maps.clear()
 
 
 def alloc_pyramids(cams, layers: int, channels: int, device) -> List[Pyramid]:

@@ -265,6 +265,7 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
     a.log_desc = pr->log_descriptors ? 1 : 0;
     a.spatial_rendered = pr->spatial_rendered ? 1 : 0;
     a.normal_cull = pr->normal_culling > 0 ? 1 : (pr->normal_culling < 0 ? -1 : 0);
+    a.clear_pyr = pr->shared_pyramid ? 0 : 1;
     a.nrm = pts->normal;
     a.tbounds = pts->tile_bounds;
     a.nrm_stride = pts->pos_stride;
@@ -638,6 +639,68 @@ adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *str
     int e = launch_tile_bounds(points->pos, points->pos + points->pos_stride, points->pos + 2 * points->pos_stride,
                                points->n, bounds, stream);
     if (e) return cuda_status(e, "tile bounds launch");
+    return ok();
+}
+
+adop_status adop_clear_pyramid(int32_t n_views, const adop_camera *cameras, int32_t layers, int32_t channels,
+                               const adop_pyramid *views, void *stream) {
+    if (!cameras || !views) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 1 || n_views > ADOP_MAX_VIEWS_PER_LAUNCH)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "n_views = %d not in [1, %d]", n_views, ADOP_MAX_VIEWS_PER_LAUNCH);
+    if (layers < 1 || layers > ADOP_MAX_LAYERS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad layers");
+    if (channels < 1 || channels > ADOP_MAX_CHANNELS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad channels");
+    for (int v = 0; v < n_views; ++v) {
+        const int64_t P = adop_pyramid_pixels(cameras[v].width, cameras[v].height, layers);
+        if (P <= 0) return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: bad width/height", v);
+        if (!views[v].keys || !views[v].accum || !views[v].count)
+            return fail(ADOP_ERR_INVALID_ARGUMENT, "view %d: NULL pyramid buffer", v);
+        int e = launch_clear_pyr(views[v].keys, views[v].accum, views[v].count, P, channels, stream);
+        if (e) return cuda_status(e, "clear pyramid launch");
+    }
+    return ok();
+}
+
+adop_status adop_ipc_export(const void *ptr, unsigned char handle[64], uint64_t *offset) {
+    if (!ptr || !handle || !offset) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    if (!range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return fail(ADOP_ERR_CUDA, "cuMemGetAddressRange unavailable");
+        }
+        range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return fail(ADOP_ERR_CUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void *)base);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+    *offset = (uint64_t)((CUdeviceptr)ptr - base);
+    return ok();
+}
+
+adop_status adop_ipc_open(const unsigned char handle[64], uint64_t offset, void **base, void **ptr) {
+    if (!handle || !base || !ptr) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void *b = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcOpenMemHandle");
+    *base = b;
+    *ptr = static_cast<char *>(b) + offset;
+    return ok();
+}
+
+adop_status adop_ipc_close(void *base) {
+    if (!base) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaError_t e = cudaIpcCloseMemHandle(base);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcCloseMemHandle");
     return ok();
 }
 

@@ -111,6 +111,7 @@ struct RasterArgs {
     int32_t grad_accumulate;
     float bg[ADOP_MAX_CHANNELS];
     int32_t spatial_rendered;  // NEXT-3 (R31): spatial gradients for rendered points instead of ghosts
+    int32_t clear_pyr;     // 1: the phases clear keys / accum / count; 0: shared pyramid (adop_clear_pyramid)
     int32_t normal_cull;   // NEXT-3, Eq. 5 (R32): 0 off, +1 / -1 sign of (R n).Xc that is kept
     const float *nrm;      // normals SoA [3][nrm_stride] (device) when normal_cull != 0
     int64_t nrm_stride;
@@ -146,6 +147,7 @@ int launch_resolve(const RasterArgs &a, void *stream);
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
 int launch_masks(const RasterArgs &a, int model, void *stream);
 int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed first unless grad_accumulate)
+int launch_clear_pyr(uint64_t *keys, float *accum, float *count, int64_t P, int C, void *stream);
 int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n, float *out, void *stream);
 adop_status set_status(adop_status s, const char *msg);  // thread-local last-error message (adop_api.cu)
 int backward_grid(int sms);

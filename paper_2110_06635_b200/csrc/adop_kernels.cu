@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
     if (WHAT == CLEAR_KEYS) {
         const unsigned long long sentinel = 0x7FFFFFFFFFFFFFFFull;
         unsigned long long *k = reinterpret_cast<unsigned long long *>(v.keys);
-        if ((reinterpret_cast<uintptr_t>(k) & 15) == 0) {
+        if (!a.clear_pyr) {  // shared pyramid: the owner's adop_clear_pyramid reset it
+        } else if ((reinterpret_cast<uintptr_t>(k) & 15) == 0) {
             for (int64_t q = tid; q < P / 2; q += stride)
                 reinterpret_cast<ulonglong2 *>(k)[q] = make_ulonglong2(sentinel, sentinel);
             for (int64_t q = (P / 2) * 2 + tid; q < P; q += stride) k[q] = sentinel;
@@ -989,6 +990,26 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     }
     if (qn > 0) drain(a, a.ldesc, q, qn, qn, c, lane, lt);
     rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
+}
+
+// Shared-pyramid reset (adop_clear_pyramid): keys <- sentinel, accum / count <- 0.
+__global__ void __launch_bounds__(kThreads) k_clear_pyr(unsigned long long *keys, float *accum, float *count, int64_t P,
+                                                        int C) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P; q += stride) {
+        keys[q] = 0x7FFFFFFFFFFFFFFFull;
+        count[q] = 0.0f;
+        for (int c = 0; c < C; ++c) accum[q * C + c] = 0.0f;
+    }
+}
+
+int launch_clear_pyr(uint64_t *keys, float *accum, float *count, int64_t P, int C, void *stream) {
+    int64_t g = (P + kThreads - 1) / kThreads;
+    if (g > 148 * 8) g = 148 * 8;
+    if (g < 1) g = 1;
+    k_clear_pyr<<<(unsigned)g, kThreads, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long *>(keys), accum,
+                                                                   count, P, C);
+    return (int)cudaGetLastError();
 }
 
 // Per-tile bounds for tile culling: warp per 256-point tile, AABB of its finite points (lo.xyz, -, hi.xyz, -).
@@ -2114,8 +2135,10 @@ int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream
 template <int MODEL, bool VEC, bool VEC4>
 static int launch_blend_t(const RasterArgs &a, int sms, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    int e = launch_clear(a, CLEAR_ACC, stream);
-    if (e) return e;
+    if (a.clear_pyr) {  // a shared pyramid was reset by its owner (adop_clear_pyramid)
+        int e = launch_clear(a, CLEAR_ACC, stream);
+        if (e) return e;
+    }
     auto k = k_blend<MODEL, VEC, VEC4, false>;
     if constexpr (VEC && VEC4)
         if (a.nviews == 1) k = k_blend<MODEL, VEC, VEC4, true>;

@@ -12,7 +12,13 @@ The paper is single-GPU.  The north star adds two partitionings 
   whole cloud; after the backward the point gradients d_feat ++ d_pos are SUM all-reduced in one buffer,
   d_pose rows are all-gathered.
 
-Both functions only sequence collectives between phase calls: the phases themselves are the C-ABI
+* Point sharding over peer memory (`PeerPointSharding`, `point_sharded_forward_p2p`): instead of two
+  all-reduces of full private pyramids, every shard's depth pass min-reduces its keys and every blend
+  sum-reduces its descriptors straight into ONE pyramid owned by one rank (CUDA IPC mapping; red.min /
+  red.add over NVLink from inside the kernels), so each frame moves only the touched pixels and the
+  exchange overlaps the kernels' own work; host barriers order the phases across ranks.
+
+The functions only sequence collectives between phase calls: the phases themselves are the C-ABI
 entry points (CudaPhases) -- or any object with the same methods (the CPU tests plug the oracle's
 phase functions in to check this host logic with world_size 2 on gloo).
 """
@@ -79,6 +85,54 @@ def view_sharded_step(phases, grad_points: torch.Tensor, d_pose_local: torch.Ten
     return torch.cat([g[: b - a] for g, (a, b) in zip(gathered, counts)], dim=0)
 
 
+def point_sharded_forward_p2p(phases, owner: int, group=None):
+    """One frame of point sharding over a shared (peer-memory) pyramid: the owner resets it; every shard's
+    depth pass min-reduces into it; after all of them, every shard's blend sum-reduces into it; after all
+    of those the owner resolves.  Each step ends with the rank's stream synchronized and a barrier."""
+    rank = dist.get_rank()
+    if rank == owner:
+        phases.clear()
+    phases.sync()
+    dist.barrier(group=group)
+    phases.depth()
+    phases.sync()
+    dist.barrier(group=group)
+    phases.blend()
+    phases.sync()
+    dist.barrier(group=group)
+    if rank == owner:
+        phases.resolve()
+
+
+class PeerPointSharding:
+    """Points the renderer of this rank (its shard, with its global_offset) at the owner's pyramid: the
+    owner exports the keys / accum / count allocations (adop_ipc_export), the others map them
+    (adop_ipc_open; peer access over NVLink between GPUs) and render into them with
+    adop_params.shared_pyramid = 1.  Non-owners keep their own image buffer (only the owner resolves)."""
+
+    def __init__(self, renderer, owner: int = 0, group=None):
+        from . import adop as A
+        self.r = renderer
+        self.owner = owner
+        rank = dist.get_rank()
+        renderer.params.s.shared_pyramid = 1
+        obj = [None]
+        if rank == owner:
+            obj = [[(A.ipc_export(p.keys), A.ipc_export(p.accum), A.ipc_export(p.count)) for p in renderer.pyrs]]
+        dist.broadcast_object_list(obj, src=owner, group=group)
+        if rank != owner:
+            self.own = renderer.pyrs  # keeps this rank's (unused) buffers alive for the image pointer
+            renderer.pyrs = [A.PeerPyramid(A.ipc_open(*k), A.ipc_open(*a), A.ipc_open(*c), p.image.data_ptr(),
+                                           p.width, p.height, p.layers)
+                             for (k, a, c), p in zip(obj[0], self.own)]
+            renderer._c = None  # the cached marshalled call holds the old pyramid pointers
+
+    def close(self):
+        from . import adop as A
+        if dist.get_rank() != self.owner:
+            A.ipc_close_all()
+
+
 class CudaPhases:
     """The C-ABI phases of one rank (paper_2110_06635_b200.adop) bound to its buffers."""
 
@@ -100,6 +154,14 @@ class CudaPhases:
         from . import adop as A
         r = self.r
         A.forward_resolve(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws)
+
+    def clear(self):
+        from . import adop as A
+        r = self.r
+        A.clear_pyramid(r.cams, r.params.layers, r.C, r.pyrs)
+
+    def sync(self):
+        torch.cuda.current_stream().synchronize()
 
     def forward(self):
         self.r.forward()

@@ -179,3 +179,97 @@ def test_view_sharded_training_gloo_ws2_equals_unsharded():
     np.testing.assert_allclose(d_pos, b.dx, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(d_pose, b.dpose, rtol=1e-12, atol=1e-12)
     assert np.abs(b.dx).sum() > 0
+
+
+# --------------------------------------------------------------------------- #
+# point sharding over a shared (peer-memory) pyramid: the orchestration of point_sharded_forward_p2p
+# --------------------------------------------------------------------------- #
+class _SharedPyr:
+    """The owner's pyramid as every rank sees it: file-backed shared tensors stand in for the IPC-mapped
+    device memory; a file lock stands in for the atomicity of the kernels' red.min / red.add."""
+
+    def __init__(self, path, P, C):
+        self.P, self.C = P, C
+        self.keys = torch.from_file(path + ".k", shared=True, size=P, dtype=torch.int64)
+        self.ac = torch.from_file(path + ".ac", shared=True, size=P * (C + 1), dtype=torch.float64)
+        self.image = torch.zeros(C * P, dtype=torch.float64)
+
+
+class SharedOraclePhases(OraclePhases):
+    def __init__(self, lock_path, *args):
+        super().__init__(*args)
+        self.lock_path = lock_path
+
+    def _locked(self, fn):
+        import fcntl
+        with open(self.lock_path, "a") as f:
+            fcntl.flock(f, fcntl.LOCK_EX)
+            try:
+                fn()
+            finally:
+                fcntl.flock(f, fcntl.LOCK_UN)
+
+    def clear(self):
+        for p in self.pyrs:
+            p.keys.fill_(np.iinfo(np.int64).max)
+            p.ac.zero_()
+
+    def sync(self):
+        pass
+
+    def depth(self):  # this shard's keys min-reduced into the shared pyramid
+        keys = O.forward_depth(self.pts, self.cams, self.poses, self.prm)
+
+        def upd():
+            for v, p in enumerate(self.pyrs):
+                p.keys.copy_(torch.minimum(p.keys, torch.from_numpy(keys[v].view(np.int64))))
+        self._locked(upd)
+
+    def blend(self):  # this shard's sums added into the shared pyramid
+        accum, count = O.forward_blend(self.pts, self.cams, self.poses, self.prm, self._keys())
+
+        def upd():
+            for v, p in enumerate(self.pyrs):
+                p.ac.add_(torch.from_numpy(np.concatenate([accum[v].ravel(), count[v]])))
+        self._locked(upd)
+
+
+def _point_sharded_p2p(rank, world, port, q, tmp):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    cloud, cams, poses, prm = _scene()
+    a, b = PL.shard_range(cloud.n, world, rank, align=256)
+    pts = O.Points.from_cloud(cloud.slice(a, b), global_offset=a)
+    P = O.pyramid_pixels(96, 64, prm.layers)
+    pyrs = [_SharedPyr(os.path.join(tmp, f"pyr{v}"), P, 3) for v in range(len(cams))]
+    ph = SharedOraclePhases(os.path.join(tmp, "lock"), pts, cams, poses, prm, pyrs)
+    for _ in range(2):  # the second frame checks the owner's per-frame reset
+        PL.point_sharded_forward_p2p(ph, owner=1)
+    if rank == 1:
+        q.put(([p.keys.numpy().copy() for p in pyrs], [p.ac.numpy().copy() for p in pyrs],
+               [p.image.numpy().copy() for p in pyrs]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_point_sharded_forward_over_a_shared_pyramid_gloo_ws2(tmp_path):
+    cloud, cams, poses, prm = _scene()
+    P = O.pyramid_pixels(96, 64, prm.layers)
+    for v in range(len(cams)):  # the owner's buffers (pre-sized backing files)
+        (tmp_path / f"pyr{v}.k").write_bytes(b"\0" * (8 * P))
+        (tmp_path / f"pyr{v}.ac").write_bytes(b"\0" * (8 * P * 4))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_point_sharded_p2p, args=(r, 2, port, q, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    keys, ac, image = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    fwd = O.forward(O.Points.from_cloud(cloud), cams, poses, prm)
+    for v in range(len(cams)):
+        assert np.array_equal(keys[v].view(np.uint64), fwd.keys[v])
+        assert np.array_equal(ac[v][P * 3:], fwd.count[v])
+        np.testing.assert_allclose(image[v], fwd.image[v], rtol=1e-12, atol=1e-12)
+    assert fwd.count.sum() > 500
