@@ -307,6 +307,23 @@ constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flig
 #ifndef ADOP_DRAIN_NOINLINE
 #define ADOP_DRAIN_NOINLINE 0
 #endif
+#ifndef ADOP_COUNTERS  // profiling build only: per-stage work counts of the depth sweep (scripts/depth_counters.py)
+#define ADOP_COUNTERS 0
+#endif
+#if ADOP_COUNTERS
+__device__ unsigned long long g_depth_counts[8];  // tiles, view-tiles kept by the box test, candidates, kept, hits
+extern "C" __attribute__((visibility("default"))) int adop_debug_depth_counts(unsigned long long *out, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_depth_counts, sizeof(g_depth_counts));
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_depth_counts, z, sizeof(z));
+    }
+    return (int)e;
+}
+#define CNT(k, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_depth_counts[k], (unsigned long long)(v)); } while (0)
+#else
+#define CNT(k, v) do { } while (0)
+#endif
 #ifndef ADOP_CHUNK_PREFETCH
 #define ADOP_CHUNK_PREFETCH 0
 #endif
@@ -610,6 +627,7 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
             continue;
         }
         const int nb = __popc(b);
+        CNT(4, nb);
         if (nb > c.left) rec_reserve(a, c, lane, true);
         if (hit) put_record(a, c.base + __popc(b & lt), make_uint4(pix, zbits, idx, (uint32_t)vs));
         c.base += nb;
@@ -660,6 +678,7 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
     qn += __popc(b);
+    CNT(3, __popc(b));
     if (qn >= 32) drain(a, ld, q, qn, 32, c, lane, lt);
 }
 
@@ -752,6 +771,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         const ViewDesc &v = a.v[vs];
         const bool lane_out = box_culled(v, box);
         if (__all_sync(kFull, lane_out)) continue;  // every lane's box is outside (warp-uniform)
+        CNT(1, 1);
         uint32_t m = 0u;
         // DISC = stochastic discarding on (a separate instance: each keeps only the code it runs)
         if (kPrefilter && DISC && (MODEL != 2 || v.zplane)) {
@@ -820,6 +840,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             cn += __popc(b);
         }
         __syncwarp();
+        CNT(2, cn);
         for (int i0 = 0; i0 < cn; i0 += 32) {
             const bool ok = i0 + lane < cn;
             const int e = ok ? cl[i0 + lane] : 0;
@@ -983,6 +1004,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
             }
             __syncwarp();
         }
+        CNT(0, 1);
         depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views);
         __syncwarp();  // every lane is done with stage st
         issue(st);
