@@ -590,3 +590,39 @@ def test_fisheye_with_env_map_log_descriptors_and_tile_culling(fov):
     compare_forward(r, fwd, ctx=f"fisheye+env {fov}")
     compare_backward(r, bwd, ctx=f"fisheye+env {fov}")
     assert r.d_env.abs().sum() > 0 and (fwd.count > 0).sum() > 1000
+
+
+def test_largest_index_range_2_31_points_ending_at_index_2_32():
+    """Maximum sizes: 2^31 + 4196 points (tile and point indices past int32, a ragged last tile, no TMA tensor
+    map past 2^31 points) whose global indices end at 2^32 - 1, the largest the packed key holds.  All but the
+    last 5000 points lie behind the camera; those 5000 are checked against the oracle (run on them alone with
+    the same global indices): keys bit-exact (index half included), counts exact, image within tolerance."""
+    n = (1 << 31) + 4196
+    tail = 5000
+    dev = torch.device("cuda")
+    goff = (1 << 32) - n
+    pos = torch.zeros(3, n, dtype=torch.float32, device=dev)
+    pos[2].fill_(-1.0)  # behind the camera: culled
+    g = torch.Generator(device="cpu").manual_seed(7)
+    vis = torch.empty(3, tail)
+    vis[0].uniform_(-1.0, 1.0, generator=g)
+    vis[1].uniform_(-0.75, 0.75, generator=g)
+    vis[2].uniform_(2.0, 4.0, generator=g)
+    pos[:, n - tail:] = vis.to(dev)
+    radius = torch.full((n,), 0.02, dtype=torch.float32, device=dev)
+    feat = torch.zeros(n, 1, dtype=torch.float32, device=dev)
+    feat[n - tail:, 0] = torch.rand(tail, generator=g).to(dev)
+    cloud = S.Cloud(pos, radius, feat)
+    cams = [S.pinhole(320, 240)]
+    poses = [S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))]
+    prm = S.Params(layers=3, discard=True, ghost_rate=0.2, seed=5, background=[0.25])
+    r = run_gpu(cloud, cams, poses, prm, record_capacity=1 << 20, global_offset=goff)
+    assert not r.ws.stats()[1]
+    sub = S.Cloud(vis.clone(), torch.full((tail,), 0.02), feat[n - tail:].cpu())
+    del cloud, pos, radius, feat
+    _, fwd, _ = run_oracle(sub, cams, poses, prm, global_offset=goff + n - tail)
+    compare_forward(r, fwd, ctx="2^31 points")
+    assert (fwd.count > 0).sum() > 1000
+    keys = keys_u64(r.pyrs[0].keys)
+    hit = keys != np.uint64(0x7FFFFFFFFFFFFFFF)
+    assert (keys[hit] & np.uint64(0xFFFFFFFF)).max() > (1 << 31)  # winners carry indices past 2^31
