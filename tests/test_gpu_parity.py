@@ -596,7 +596,8 @@ def test_largest_index_range_2_31_points_ending_at_index_2_32():
     """Maximum sizes: 2^31 + 4196 points (tile and point indices past int32, a ragged last tile, no TMA tensor
     map past 2^31 points) whose global indices end at 2^32 - 1, the largest the packed key holds.  All but the
     last 5000 points lie behind the camera; those 5000 are checked against the oracle (run on them alone with
-    the same global indices): keys bit-exact (index half included), counts exact, image within tolerance."""
+    the same global indices): keys bit-exact (index half included), counts exact, image, d_feat, d_pos, d_pose
+    and d_intr within tolerance, every other point's gradient exactly zero."""
     n = (1 << 31) + 4196
     tail = 5000
     dev = torch.device("cuda")
@@ -616,12 +617,20 @@ def test_largest_index_range_2_31_points_ending_at_index_2_32():
     cams = [S.pinhole(320, 240)]
     poses = [S.Pose(np.eye(3, dtype=np.float32), np.zeros(3, dtype=np.float32))]
     prm = S.Params(layers=3, discard=True, ghost_rate=0.2, seed=5, background=[0.25])
-    r = run_gpu(cloud, cams, poses, prm, record_capacity=1 << 20, global_offset=goff)
+    G = grads_for(cams, prm.layers, 1)
+    r = run_gpu(cloud, cams, poses, prm, record_capacity=1 << 20, global_offset=goff, grads=G)
     assert not r.ws.stats()[1]
     sub = S.Cloud(vis.clone(), torch.full((tail,), 0.02), feat[n - tail:].cpu())
     del cloud, pos, radius, feat
-    _, fwd, _ = run_oracle(sub, cams, poses, prm, global_offset=goff + n - tail)
+    _, fwd, bwd = run_oracle(sub, cams, poses, prm, global_offset=goff + n - tail, grads=G)
     compare_forward(r, fwd, ctx="2^31 points")
+    # backward: the tail's gradients against the oracle, every other point's exactly zero
+    tail_view = type("Tail", (), {})()
+    tail_view.d_feat, tail_view.d_pos = r.d_feat[n - tail:], r.d_pos[:, n - tail:]
+    tail_view.d_pose, tail_view.d_intr = r.d_pose, r.d_intr
+    compare_backward(tail_view, bwd, ctx="2^31 points")
+    assert float(r.d_feat[: n - tail].abs().max()) == 0.0 and float(r.d_pos[:, : n - tail].abs().max()) == 0.0
+    assert np.abs(bwd.dx).sum() > 0 and np.abs(bwd.dtau).sum() > 0
     assert (fwd.count > 0).sum() > 1000
     keys = keys_u64(r.pyrs[0].keys)
     hit = keys != np.uint64(0x7FFFFFFFFFFFFFFF)
