@@ -81,7 +81,10 @@ typedef struct {
     const float *pos;       /* device, SoA [3][pos_stride]                                  */
     const float *radius;    /* device [n] world radius r_world (§4.4), or NULL         */
     float radius_uniform;   /* used when radius == NULL                                     */
-    const float *feat;      /* device [n][C] neural descriptor tau                         */
+    const float *feat;      /* device [n][C] neural descriptor tau -- or pinned HOST memory
+                               (cudaHostAlloc / torch pin_memory, device-accessible through
+                               UVA): the forward then reads only the survivors' descriptors
+                               over PCIe, in place (zero-copy; bench.py's e2e)             */
     int32_t channels;       /* C, 1..32                                                     */
     const float *normal;    /* device SoA [3][pos_stride] normals n of Eq. 1 (Eq. 5 culling),
                                or NULL; required when params->normal_culling != 0        */

@@ -31,6 +31,7 @@ def test_bench_line_has_every_contract_key():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert e["copy_all"]["value"] > 0 and e["copy_all"]["h2d_bytes_per_step"] > e["h2d_bytes_per_step"]
 
 
 def test_reference_arm_line():

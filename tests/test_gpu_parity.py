@@ -635,3 +635,23 @@ def test_largest_index_range_2_31_points_ending_at_index_2_32():
     keys = keys_u64(r.pyrs[0].keys)
     hit = keys != np.uint64(0x7FFFFFFFFFFFFFFF)
     assert (keys[hit] & np.uint64(0xFFFFFFFF)).max() > (1 << 31)  # winners carry indices past 2^31
+
+
+def test_descriptors_in_pinned_host_memory():
+    """adop_points.feat in pinned host memory (zero-copy, UVA): the blend reads the survivors' descriptors in
+    place; same result as with the descriptors in HBM, and against the oracle."""
+    w = S.workload(1, n=200_004, n_views=4)
+    dev = torch.device("cuda")
+    cloud = w.cloud.to(dev)
+    ref = A.Renderer(cloud, w.cameras, w.poses, w.params)
+    ref.forward()
+    h_feat = w.cloud.feat.cpu().pin_memory()
+    r = A.Renderer(S.Cloud(cloud.pos, cloud.radius, h_feat), w.cameras, w.poses, w.params)
+    assert r.points.s.feat == h_feat.data_ptr()
+    r.forward()
+    torch.cuda.synchronize()
+    for v in range(4):
+        assert torch.equal(r.pyrs[v].keys, ref.pyrs[v].keys) and torch.equal(r.pyrs[v].count, ref.pyrs[v].count)
+        torch.testing.assert_close(r.pyrs[v].image, ref.pyrs[v].image, rtol=1e-5, atol=1e-6)
+    _, fwd, _ = run_oracle(w.cloud, w.cameras, w.poses, w.params)
+    compare_forward(r, fwd, ctx="host descriptors")
