@@ -111,11 +111,12 @@ struct RasterArgs {
     int32_t grad_accumulate;
     float bg[ADOP_MAX_CHANNELS];
     int32_t spatial_rendered;  // NEXT-3 (R31): spatial gradients for rendered points instead of ghosts
-    int32_t clear_pyr;     // 1: the phases clear keys / accum / count; 0: shared pyramid (adop_clear_pyramid)
     int32_t normal_cull;   // NEXT-3, Eq. 5 (R32): 0 off, +1 / -1 sign of (R n).Xc that is kept
     const float *nrm;      // normals SoA [3][nrm_stride] (device) when normal_cull != 0
     int64_t nrm_stride;
     int32_t log_desc;      // NEXT-2: descriptors stored as log, linearized with exp()
+    int32_t clear_pyr;     // 1: the phases clear keys / accum / count; 0: shared pyramid (adop_clear_pyramid)
+                           // (placed in the padding after log_desc: the other fields keep their offsets)
     const float *env;      // NEXT-2: environment map [env_h][env_w][C] (device) or NULL (R18 constant bg)
     int32_t env_w, env_h;
     float *d_env;          // backward: [env_h][env_w][C] environment-map gradient or NULL
