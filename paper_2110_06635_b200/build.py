@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import glob
 import os
+import re
 import subprocess
 import sys
 
@@ -23,9 +24,37 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
-    "-split-compile=0",  # the optimizer's work on the kernel instances in parallel threads
     "-I", os.path.join(ROOT, "include"),
 ]
+
+
+# nvcc -split-compile=N: the optimizer's work on the kernel instances in N parallel threads.  The split
+# also changes how the module is partitioned, and the sweeps sit at their 80-register cap: some
+# partitionings push the backward sweep into 100-350 B of local-memory spills (profiles/r01/evolution.md).
+# adop_kernels.cu is compiled with each count below and the build with the fewest spill bytes in the hot
+# instances is kept (deterministic: fixed counts, first wins ties).
+SPLITS = (16, 4)
+HOT = (  # hot instances (tests/test_build_spills.py checks their spills)
+    "_ZN4adop13k_depth_asyncILi0ELi0ELb1EEEvNS_10RasterArgsE",
+    "_ZN4adop13k_depth_asyncILi1ELi2ELb1EEEvNS_10RasterArgsE",
+    "_ZN4adop11k_bwd_sweepILi1ELi4ELb1ELb1EEEvNS_10RasterArgsE",
+    "_ZN4adop11k_bwd_sweepILi1ELi8ELb0ELb1EEEvNS_10RasterArgsE",
+    "_ZN4adop11k_bwd_ghostILi1ELi4ELi6EEEvNS_10RasterArgsE",
+    "_ZN4adop7k_blendILi0ELb1ELb1ELb1EEEvNS_10RasterArgsE",
+)
+
+
+def hot_spill_bytes(ptxas_log: str) -> int:
+    out, cur = 0, None
+    for line in ptxas_log.splitlines():
+        m = re.search(r"Function properties for (\S+)", line)
+        if m:
+            cur = m.group(1)
+            continue
+        m = re.search(r"(\d+) bytes spill stores", line)
+        if m and cur in HOT:
+            out += int(m.group(1))
+    return out
 
 
 def sources():
@@ -53,16 +82,25 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     os.makedirs(bdir, exist_ok=True)
     logs = []
     procs = []
-    for src in sources():  # the translation units compile concurrently
-        obj = os.path.join(bdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
-        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
-    for src, obj, p in procs:
+    for src in sources():  # the translation units (and split variants) compile concurrently
+        splits = SPLITS if os.path.basename(src) == "adop_kernels.cu" else SPLITS[:1]
+        for sc in splits:
+            obj = os.path.join(bdir, os.path.basename(src) + f".s{sc}.o")
+            cmd = [NVCC, *NVCC_FLAGS, f"-split-compile={sc}", *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+            procs.append((src, sc, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                                         text=True)))
+    best = {}
+    for src, sc, obj, p in procs:
         so, se = p.communicate()
-        logs.append(so + se)
         if p.returncode != 0:
             sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed on {src}")
+        score = hot_spill_bytes(so + se)
+        if src not in best or score < best[src][0]:
+            best[src] = (score, sc, obj, so + se)
+    for src in sources():
+        score, sc, obj, log = best[src]
+        logs.append(f"// {os.path.basename(src)}: -split-compile={sc} (hot-instance spill bytes {score})\n" + log)
         objs.append(obj)
     target = LIB if out is None else out
     tmp = target + f".tmp{os.getpid()}"
