@@ -210,6 +210,15 @@ __device__ __forceinline__ int keep_layers(const RasterArgs &a, const ViewDesc &
     return l;
 }
 
+// True unless the point is outside the image at every layer l < nk (then no layer_pixel call can hit):
+// round_away(u0 2^-l) is in [0, w_l) only if -2^(l-1) < u0 < (w_l - 1/2) 2^l <= w + 2^(l-1), and the widest
+// of these over l < nk is l = nk - 1.  Exact (power-of-two scalings), so dropping the point changes nothing.
+template <typename VD>
+__device__ __forceinline__ bool any_layer_in_bounds(const VD &v, const Proj &p, int nk) {
+    const float hs = __int_as_float((126 + nk) << 23);  // 2^(nk - 2) = 0.5 * 2^(nk - 1)
+    return p.u0 > -hs && p.u0 < (float)v.wl[0] + hs && p.v0 > -hs && p.v0 < (float)v.hl[0] + hs;
+}
+
 // Eqs. 3-4: layer-local pixel (u, v) and bounds.  Returns layer-local linear index or -1.
 template <typename VD>
 __device__ __forceinline__ int layer_pixel(const VD &v, const Proj &p, int l, int &pu, int &pv) {
