@@ -1775,7 +1775,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
         if (depth_valid<MODEL>(p, a.z_near) && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
             nk = keep_layers(a, v, rw, p.iz, gi);
-            if (nk > 0 && !project_uv<MODEL>(v, p)) nk = 0;
+            if (nk > 0 && !(project_uv<MODEL>(v, p) && any_layer_in_bounds(v, p, nk))) nk = 0;  // R14: no term
         }
     }
     const bool rend = tex_on && nk > 0 && !ghost && a.d_feat;
