@@ -124,3 +124,27 @@ def test_view_count_limits():
     pts, cams, poses, prm, pyrs = _valid()
     st, msg = _call(pts, cams * 17, poses * 17, prm, pyrs * 17)
     assert st == 1 and "n_views" in msg
+
+
+def test_shared_pyramid_and_ipc_arguments_rejected():
+    """adop_clear_pyramid / adop_ipc_* validate their arguments before any CUDA call."""
+    L = A.lib()
+    _, cams, _, _, pyrs = _valid()
+    ca = (A.adop_camera * 1)(A.camera_struct(cams[0]))
+    py = (A.adop_pyramid * 1)(*pyrs)
+    assert L.adop_clear_pyramid(1, None, 4, 4, py, None) == 1
+    assert L.adop_clear_pyramid(0, ca, 4, 4, py, None) == 1 and "n_views" in L.adop_last_error().decode()
+    assert L.adop_clear_pyramid(1, ca, 0, 4, py, None) == 1 and "layers" in L.adop_last_error().decode()
+    assert L.adop_clear_pyramid(1, ca, 4, 0, py, None) == 1 and "channels" in L.adop_last_error().decode()
+    bad = A.adop_pyramid()
+    bad.image, bad.count, bad.keys, bad.accum = 1 << 20, 0, 3 << 20, 4 << 20
+    assert L.adop_clear_pyramid(1, ca, 4, 4, (A.adop_pyramid * 1)(bad), None) == 1
+    assert "NULL pyramid" in L.adop_last_error().decode()
+    h = C.create_string_buffer(64)
+    off = C.c_uint64(0)
+    assert L.adop_ipc_export(None, h, C.byref(off)) == 1
+    assert L.adop_ipc_export(C.c_void_p(4096), None, C.byref(off)) == 1
+    b, p = C.c_void_p(0), C.c_void_p(0)
+    assert L.adop_ipc_open(None, 0, C.byref(b), C.byref(p)) == 1
+    assert L.adop_ipc_open(h.raw, 0, None, C.byref(p)) == 1
+    assert L.adop_ipc_close(None) == 1
