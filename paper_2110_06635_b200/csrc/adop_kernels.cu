@@ -2242,6 +2242,32 @@ int backward_grid(int sms) {
     return g > kMaxBwdBlocks ? kMaxBwdBlocks : g;
 }
 
+// Per-thread, per-device side stream and fork / join events of the backward (created on first use, never
+// destroyed; thread-local so concurrent callers never share a fork event).  NULL if creation failed: the
+// caller's stream is used alone.
+#ifndef ADOP_BWD_SIDE_STREAM
+#define ADOP_BWD_SIDE_STREAM 1
+#endif
+constexpr int kMaxDevices = 64;
+static cudaStream_t side_stream() {
+    if (!ADOP_BWD_SIDE_STREAM) return nullptr;
+    static thread_local cudaStream_t streams[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        streams[dev] = nullptr;
+    }
+    return streams[dev];
+}
+static cudaEvent_t side_event(int which) {
+    static thread_local cudaEvent_t events[kMaxDevices][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!events[dev][which]) cudaEventCreateWithFlags(&events[dev][which], cudaEventDisableTiming);
+    return events[dev][which];
+}
+
 template <int MODEL, bool VEC, int CT>
 static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double *d_pose, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
@@ -2304,11 +2330,30 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
             k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
         }
     }
-    if (a.d_feat) k_bwd_tex<<<sms * 8, kThreads, 0, s>>>(b);
+    // the two list consumers are independent (d_feat from the texture list; d_pos and the pose / intrinsics
+    // partials from the ghost list) and both latency-bound: the texture kernel runs on a side stream forked
+    // from and joined back into the caller's (event fork / join, CUDA-graph capturable).
+    // Measured: configs[2] backward 0.387 -> 0.351 ms; with 16 views (configs[4], 0.7 GB of pixel tables) the
+    // two consumers thrash L2 together (+1.5%), so large launches keep them in sequence.
+    int64_t tbytes = 0;
+    for (int v = 0; v < a.nviews; ++v) tbytes += a.v[v].pixels * a.prow * (int64_t)sizeof(float);
+    cudaStream_t side = (a.d_feat && tbytes <= (256ll << 20)) ? side_stream() : nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (side) {
+        fork = side_event(0);
+        join = side_event(1);
+        cudaEventRecord(fork, s);
+        cudaStreamWaitEvent(side, fork, 0);
+    }
+    if (a.d_feat) k_bwd_tex<<<sms * 8, kThreads, 0, side ? side : s>>>(b);
     if (a.nterms == kNT)  // the intrinsics terms cost 12 more fp64 warp sums per ghost: only when requested
         k_bwd_ghost<MODEL, CT, kNT><<<gg, kThreads, 0, s>>>(b);
     else
         k_bwd_ghost<MODEL, CT, 6><<<gg, kThreads, 0, s>>>(b);
+    if (side) {
+        cudaEventRecord(join, side);
+        cudaStreamWaitEvent(s, join, 0);
+    }
     if (d_pose || a.d_intr)
         k_pose_reduce<<<a.nviews * a.nterms, 256, 0, s>>>(a.pose_partials, gg + 1, a.nviews, a.nterms, d_pose, a.d_intr,
                                                           a.grad_accumulate);

@@ -655,3 +655,30 @@ def test_descriptors_in_pinned_host_memory():
         torch.testing.assert_close(r.pyrs[v].image, ref.pyrs[v].image, rtol=1e-5, atol=1e-6)
     _, fwd, _ = run_oracle(w.cloud, w.cameras, w.poses, w.params)
     compare_forward(r, fwd, ctx="host descriptors")
+
+
+def test_backward_captured_in_a_cuda_graph():
+    """The backward's side-stream fork / join (texture consumer beside the ghost consumer) inside CUDA-graph
+    capture: replaying the captured backward reproduces the eager one."""
+    w = S.workload(2, n=200_004)
+    dev = torch.device("cuda")
+    G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, w.cloud.channels)]
+    r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params)
+    r.forward()
+    r.backward(G)
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in (r.d_feat, r.d_pos, r.d_pose)]
+    s = torch.cuda.Stream(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        r.backward(G, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            r.backward(G, stream=s)
+    for t in (r.d_feat, r.d_pos, r.d_pose):
+        t.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    for got, ref in zip((r.d_feat, r.d_pos, r.d_pose), eager):
+        torch.testing.assert_close(got, ref, rtol=1e-5, atol=1e-6 * float(ref.abs().max()))
+    assert float(eager[0].abs().sum()) > 0 and float(eager[1].abs().sum()) > 0
