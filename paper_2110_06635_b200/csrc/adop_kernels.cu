@@ -659,9 +659,10 @@ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int 
 // Candidate part for one point and view: pinned Xc = R x + t (R1), validity (R7), exact discard (Eq. 12,
 // R10) BEFORE the projection, exact projection (R2/R6); kept points are appended to the warp queue,
 // which is drained 32 at a time.  Warp-collective.
-// PRECHECK (multi-view launches): kept points outside the image at every layer are dropped before the queue
-// (configs[4]: a quarter of the kept point-views).  On the single-view headline the extra compares cost
-// more than the few out-of-image points they save.
+// PRECHECK (multi-view launches, distortion / fisheye cameras): kept points outside the image at every layer
+// are dropped before the queue (configs[4]: a quarter of the kept point-views; with distortion the pre-cull
+// planes bound the whole valid cone, well beyond the image).  On the single-view pinhole headline the extra
+// compares cost more than the few out-of-image points they save.
 template <int MODEL, bool PRECHECK>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
                                                 float y, float z, float rw, int64_t i, uint32_t gi, const LayerDesc *ld,
@@ -848,7 +849,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             const bool ok = i0 + lane < cn;
             const int e = ok ? cl[i0 + lane] : 0;
             const float rw = staged_r ? rows[3][e] : a.radius_uniform;
-            depth_candidate<MODEL, VM != 0>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
+            depth_candidate<MODEL, VM != 0 || MODEL != 0>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
                                    a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
         }
         __syncwarp();  // the list is rewritten by the next view / tile
