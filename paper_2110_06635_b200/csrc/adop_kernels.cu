@@ -759,12 +759,9 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
                                             uint8_t *cl, int lane, unsigned lt, uint32_t pre_views) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
+    // ghosts take no part in the depth test (§4.3): their mask is hashed at the tile's first visible view
     uint32_t live = (uint32_t)vmask;
-    if (a.ghost_thr != 0u) {  // ghosts take no part in the depth test (§4.3)
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
-    }
+    bool live_done = a.ghost_thr == 0u;
     const Box box = lane_box(rows, lane, vmask);
     uint32_t views = pre_views != 0xFFFFFFFFu ? pre_views
                      : (VM == 2 ? tile_views(a, box, lane) : (VM == 0 ? 1u : (1u << a.nviews) - 1u));
@@ -830,6 +827,12 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
                 m |= (cand ? 1u : 0u) << (4 * h + j);
             }
         }
+        }
+        if (!live_done) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
+            live_done = true;
         }
         m &= live;
         if (!__any_sync(kFull, m != 0u)) continue;
