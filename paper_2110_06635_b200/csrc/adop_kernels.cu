@@ -1972,33 +1972,43 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         }
         auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
         uint32_t ghosts = 0u;
-        if (a.ghost_thr != 0u) {
+        auto hash_ghosts = [&]() {
+            if (a.ghost_thr != 0u) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
-        }
-        if (GO) {
-            // mode 1: only ghosts (~rho of the points) are left to find -- compact them, then pre-cull and
-            // project only those, 32 per warp iteration (every lane busy)
-            const uint32_t gm = (a.spatial_rendered ? ~ghosts : ghosts) & (uint32_t)vmask;  // R22 / R31
-            int gn = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool bit = (gm >> j) & 1u;
-                const unsigned b = __ballot_sync(kFull, bit);
-                if (bit) sm.gl[wid][gn + __popc(b & lt)] = (uint8_t)((j >> 2) * 128 + 4 * lane + (j & 3));
-                gn += __popc(b);
+                for (int j = 0; j < 8; ++j)
+                    if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) ghosts |= 1u << j;
             }
-            __syncwarp();
-            if (gn > 0) {
-                const Box box = lane_box(rp, lane, vmask);
-                uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
+        };
+        if (GO) {
+            // mode 1: only ghosts (~rho of the points) are left to find.  The tile's visible views come first (a
+            // culled tile costs no hashing); then the ghosts are compacted and only they are pre-culled and
+            // projected, 32 per warp iteration (every lane busy)
+            const Box box = lane_box(rp, lane, vmask);
+            uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u, vis = 0u;
 #pragma unroll 1
-                while (views) {
-                    const int vs = __ffs(views) - 1;
-                    views &= views - 1u;
+            for (uint32_t vv = views; vv; vv &= vv - 1u) {
+                const int vs = __ffs(vv) - 1;
+                if (!__all_sync(kFull, box_culled(a.v[vs], box))) vis |= 1u << vs;
+            }
+            int gn = 0;
+            if (vis) {
+                hash_ghosts();
+                const uint32_t gm = (a.spatial_rendered ? ~ghosts : ghosts) & (uint32_t)vmask;  // R22 / R31
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const bool bit = (gm >> j) & 1u;
+                    const unsigned b = __ballot_sync(kFull, bit);
+                    if (bit) sm.gl[wid][gn + __popc(b & lt)] = (uint8_t)((j >> 2) * 128 + 4 * lane + (j & 3));
+                    gn += __popc(b);
+                }
+                __syncwarp();
+            }
+            if (gn > 0) {
+#pragma unroll 1
+                while (vis) {
+                    const int vs = __ffs(vis) - 1;
+                    vis &= vis - 1u;
                     const ViewDesc &v = a.v[vs];
-                    if (__all_sync(kFull, box_culled(v, box))) continue;
                     for (int i0 = 0; i0 < gn; i0 += 32) {
                         const bool in = i0 + lane < gn;
                         const int e = in ? sm.gl[wid][i0 + lane] : 0;
@@ -2020,6 +2030,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             __syncwarp();
             continue;
         }
+        hash_ghosts();
         const Box box = lane_box(rp, lane, vmask);
         uint32_t views = MV ? tile_views(a, box, lane) : (1u << a.nviews) - 1u;
 #pragma unroll 1
