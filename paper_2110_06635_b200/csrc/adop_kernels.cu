@@ -2279,7 +2279,11 @@ static cudaEvent_t side_event(int which) {
     static thread_local cudaEvent_t events[kMaxDevices][2] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!events[dev][which]) cudaEventCreateWithFlags(&events[dev][which], cudaEventDisableTiming);
+    if (dev < 0 || dev >= kMaxDevices) return nullptr;
+    if (!events[dev][which] && cudaEventCreateWithFlags(&events[dev][which], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        events[dev][which] = nullptr;
+    }
     return events[dev][which];
 }
 
@@ -2357,6 +2361,9 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     if (side) {
         fork = side_event(0);
         join = side_event(1);
+        if (!fork || !join) side = nullptr;  // no events: stay on the caller's stream
+    }
+    if (side) {
         cudaEventRecord(fork, s);
         cudaStreamWaitEvent(side, fork, 0);
     }
