@@ -380,16 +380,17 @@ def _phase(fn_name, points, cams, poses, params, pyrs, ws: Workspace, stream=Non
               _stream(stream)))
 
 
-def forward_depth(points, cams, poses, params, pyrs, ws, stream=None):
-    _phase("adop_forward_depth", points, cams, poses, params, pyrs, ws, stream)
+def forward_depth(points, cams, poses, params, pyrs, ws, stream=None, call=None):
+    """Phase 1.  `call`: a cached _Call of the same arguments (skips the per-call marshalling)."""
+    _phase("adop_forward_depth", points, cams, poses, params, pyrs, ws, stream, call)
 
 
-def forward_blend(points, cams, poses, params, pyrs, ws, stream=None):
-    _phase("adop_forward_blend", points, cams, poses, params, pyrs, ws, stream)
+def forward_blend(points, cams, poses, params, pyrs, ws, stream=None, call=None):
+    _phase("adop_forward_blend", points, cams, poses, params, pyrs, ws, stream, call)
 
 
-def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None):
-    _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream)
+def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None, call=None):
+    _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream, call)
 
 
 def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None, call=None):

@@ -143,17 +143,17 @@ class CudaPhases:
     def depth(self):
         from . import adop as A
         r = self.r
-        A.forward_depth(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws)
+        A.forward_depth(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, call=r._call())
 
     def blend(self):
         from . import adop as A
         r = self.r
-        A.forward_blend(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws)
+        A.forward_blend(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, call=r._call())
 
     def resolve(self):
         from . import adop as A
         r = self.r
-        A.forward_resolve(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws)
+        A.forward_resolve(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, call=r._call())
 
     def clear(self):
         from . import adop as A
