@@ -36,19 +36,19 @@ NVCC_FLAGS = [
 # hot instances is kept, and another round runs (up to ROUNDS) while that is above SPILL_OK.
 SPLIT = 16
 ROUNDS = 3
-SPILL_OK = 200  # the clean build's hot-instance total: the blend's overflow fallback (slow path) and 36 B
-HOT = (  # hot instances (tests/test_build_spills.py checks their spills)
-    "_ZN4adop13k_depth_asyncILi0ELi0ELb1EEEvNS_10RasterArgsE",
-    "_ZN4adop13k_depth_asyncILi1ELi2ELb1EEEvNS_10RasterArgsE",
-    "_ZN4adop11k_bwd_sweepILi1ELi4ELb1ELb1EEEvNS_10RasterArgsE",
-    "_ZN4adop11k_bwd_sweepILi1ELi8ELb0ELb1EEEvNS_10RasterArgsE",
-    "_ZN4adop11k_bwd_ghostILi1ELi4ELi6EEEvNS_10RasterArgsE",
-    "_ZN4adop7k_blendILi0ELb1ELb1ELb1EEEvNS_10RasterArgsE",
-)
+SPILL_OK = 300  # every hot instance within its limit (an instance over its limit adds 100000)
+HOT = {  # hot instances -> accepted spill-store bytes (tests/test_build_spills.py checks the kept build)
+    "_ZN4adop13k_depth_asyncILi0ELi0ELb1EEEvNS_10RasterArgsE": 0,     # configs[3] headline depth sweep
+    "_ZN4adop13k_depth_asyncILi1ELi2ELb1EEEvNS_10RasterArgsE": 32,    # configs[4] multi-view depth sweep
+    "_ZN4adop11k_bwd_sweepILi1ELi4ELb1ELb1EEEvNS_10RasterArgsE": 0,   # configs[4] ghost-only backward sweep
+    "_ZN4adop11k_bwd_sweepILi1ELi8ELb0ELb1EEEvNS_10RasterArgsE": 40,  # configs[2] ghost-only backward sweep
+    "_ZN4adop11k_bwd_ghostILi1ELi4ELi6EEEvNS_10RasterArgsE": 0,       # configs[4] ghost consumer
+    "_ZN4adop7k_blendILi0ELb1ELb1ELb1EEEvNS_10RasterArgsE": 192,      # configs[3] blend (its overflow fallback)
+}
 
 
-def hot_spill_bytes(ptxas_log: str) -> int:
-    out, cur = 0, None
+def hot_spills(ptxas_log: str) -> dict:
+    out, cur = {}, None
     for line in ptxas_log.splitlines():
         m = re.search(r"Function properties for (\S+)", line)
         if m:
@@ -56,8 +56,14 @@ def hot_spill_bytes(ptxas_log: str) -> int:
             continue
         m = re.search(r"(\d+) bytes spill stores", line)
         if m and cur in HOT:
-            out += int(m.group(1))
+            out[cur] = int(m.group(1))
     return out
+
+
+def hot_spill_bytes(ptxas_log: str) -> int:
+    """Total spill-store bytes of the hot instances, plus a large penalty per instance over its limit."""
+    sp = hot_spills(ptxas_log)
+    return sum(sp.values()) + sum(100000 for k, v in sp.items() if v > HOT[k])
 
 
 def sources():

@@ -11,13 +11,7 @@ import pytest
 from paper_2110_06635_b200 import build as B
 
 LOG = os.path.join(B.PKG, "build", "ptxas.log")
-HOT = {
-    "_ZN4adop13k_depth_asyncILi0ELi0ELb1EEEvNS_10RasterArgsE": 0,    # configs[3] headline depth sweep
-    "_ZN4adop13k_depth_asyncILi1ELi2ELb1EEEvNS_10RasterArgsE": 32,   # configs[4] multi-view depth sweep
-    "_ZN4adop11k_bwd_sweepILi1ELi4ELb1ELb1EEEvNS_10RasterArgsE": 0,  # configs[4] ghost-only backward sweep
-    "_ZN4adop11k_bwd_sweepILi1ELi8ELb0ELb1EEEvNS_10RasterArgsE": 40,  # configs[2] ghost-only backward sweep
-    "_ZN4adop11k_bwd_ghostILi1ELi4ELi6EEEvNS_10RasterArgsE": 0,      # configs[4] ghost consumer
-}
+HOT = B.HOT
 
 
 def _spills():
