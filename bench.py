@@ -254,6 +254,7 @@ def run_ours(args, rank, world, local_rank):
         graphs[0].replay()
         ev[1].record(stream)
         graphs[1].replay()
+        ev[5].record(stream)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -283,6 +284,8 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     total_ms = start.elapsed_time(end)
     depth_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    per_step = sorted(e[0].elapsed_time(e[5]) for e in evs)  # frame by frame (each frame's own event pair)
+    q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]
     # phase breakdown (eager, every phase bracketed by events): a separate pass after the timed region
     bevs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(min(args.steps, 20))]
     for e in bevs:
@@ -337,6 +340,9 @@ def run_ours(args, rank, world, local_rank):
                        "record_slots_per_frame": records, "record_overflow": overflow},
             "timing": ("CUDA graph replays (depth | blend+resolve) with an event pair around each depth phase"
                        if graphs is not None else "eager C-ABI calls, events around every phase"),
+            "ms_per_step_stats": {"median": statistics.median(per_step), "p10": q(0.1), "p90": q(0.9),
+                                  "min": per_step[0], "max": per_step[-1], "frames": len(per_step),
+                                  "note": "per-frame event pairs; ms_per_step is the whole timed region / steps"},
             "phases_ms": {"depth": statistics.mean(ph[0]), "key_allreduce": statistics.mean(ph[1]),
                           "blend": statistics.mean(ph[2]), "accum_allreduce": statistics.mean(ph[3]),
                           "resolve": statistics.mean(ph[4])},
@@ -417,20 +423,33 @@ def run_e2e(args, ctx, rank, world, local_rank):
 
 
 def cpu_baseline(args, ctx):
-    """The CPU oracle (oracle/adop_oracle.c, single-threaded, as it stands) on a bounded sample."""
-    import numpy as np
+    """The CPU oracle (oracle/adop_oracle.c, as it stands) on bounded samples of the same cloud: once with one
+    thread and once with OpenMP on all host cores (per-point work in parallel, reductions serial in point
+    order: the results do not depend on the thread count).  `value` is the all-core rate."""
     from oracle import oracle as O
     dev, step, pts, cloud, cams, poses, prm, pyrs, ws, stream, barrier, N, C = ctx
-    n_s = min(args.cpu_sample, N)
-    sub = cloud.slice(0, n_s).to("cpu")
-    opts = O.Points.from_cloud(sub)
-    t0 = time.perf_counter()
-    O.forward(opts, cams, poses, prm)
-    dt = time.perf_counter() - t0
-    return {"value": n_s / dt, "unit": "points/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {n_s:,} points of the blocked-Morton-shuffled cloud (random spatial blocks), "
-                      f"1 view 1920x1080, 5 layers: full oracle forward (depth, blend, resolve), {dt:.2f} s",
-            "seconds": dt}
+
+    def run(n_s, threads):
+        used = O.set_threads(threads)
+        opts = O.Points.from_cloud(cloud.slice(0, n_s).to("cpu"))
+        t0 = time.perf_counter()
+        O.forward(opts, cams, poses, prm)
+        return time.perf_counter() - t0, used
+
+    n1 = min(args.cpu_sample // 5, N)
+    dt1, _ = run(n1, 1)
+    # size the all-core sample for ~10 s at the expected rate, capped at the whole cloud
+    cores = os.cpu_count() or 1
+    n_all = int(min(N, max(n1, 10.0 * n1 / dt1 * max(1.0, 0.5 * cores))))
+    dt, used = run(n_all, 0)
+    O.set_threads(1)
+    return {"value": n_all / dt, "unit": "points/s", "cores": used, "kind": "oracle",
+            "os_cpu_count": cores, "omp_threads": used,
+            "sample": f"first {n_all:,} points of the blocked-Morton-shuffled cloud (random spatial blocks), 1 view "
+                      f"1920x1080, 5 layers: full oracle forward (depth, blend, resolve) on {used} threads, {dt:.2f} s",
+            "seconds": dt, "ms_per_frame_100M": dt / n_all * N * 1e3,
+            "single_thread": {"value": n1 / dt1, "cores": 1, "points": n1, "seconds": dt1,
+                              "ms_per_frame_100M": dt1 / n1 * N * 1e3}}
 
 
 def run_secondary(args, dev):
@@ -535,6 +554,7 @@ def run_reference(args, rank, world):
     sub = w.cloud.slice(0, n_s).to("cpu")
     del w.cloud
     opts = O.Points.from_cloud(sub)
+    threads = O.set_threads(0)  # the box's host cores (results do not depend on the count)
     for _ in range(args.warmup):
         O.forward(opts, w.cameras, w.poses, w.params)
     t0 = time.perf_counter()
@@ -546,8 +566,10 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "points_per_gpu": args.points, "sample_points_per_step": n_s},
-            "cpu_baseline": {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {n_s:,} points of configs[3]'s cloud per step, full oracle forward"},
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "oracle",
+                             "os_cpu_count": os.cpu_count(),
+                             "sample": f"first {n_s:,} points of configs[3]'s cloud per step, full oracle forward "
+                                       f"on {threads} threads"},
             "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

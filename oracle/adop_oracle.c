@@ -26,6 +26,14 @@
  * (§4.2 "straightforward"), ghost image-space gradient (Eqs. 9-11, §4.3),
  * chain rule to points and tangent-space pose (Eq. 8, Eq. 17).
  *
+ * Threads: OpenMP over points in chunks of ORC_CHUNK.  Every
+ * per-point quantity (projection, masks, pixels, per-point gradients) is
+ * computed in parallel into per-point slots of the chunk; every quantity that
+ * is a reduction over points (depth keys, blend sums and counts, pose and
+ * intrinsics gradients) is then reduced SERIALLY in point order.  The results
+ * are therefore bit-identical to the single-threaded program for any thread
+ * count (tests/test_oracle_threads.py checks it).
+ *
  * Parity pins: tests/test_oracle_*.py (closed forms, brute force, finite
  * differences, worked values).  Parity unpinned: none of the functions below
  * is unpinned; the *usefulness* of ghost gradients (paper §6.2) is not a
@@ -36,6 +44,27 @@
 #include <stdlib.h>
 #include <string.h>
 #include <float.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_CHUNK ((int64_t)1 << 18) /* points per parallel chunk */
+
+static int orc_threads = 1;
+
+/* Thread count of every parallel loop below (>= 1); returns the count in effect. */
+int orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    orc_threads = n >= 1 ? n : omp_get_num_procs();
+#else
+    (void)n;
+    orc_threads = 1;
+#endif
+    return orc_threads;
+}
+
+int orc_get_threads(void) { return orc_threads; }
 
 typedef struct {
     int32_t width, height, model; /* model 0 = pinhole, 1 = OpenCV rational 8-coefficient (R6),
@@ -288,12 +317,46 @@ static unsigned point_mask(const orc_points *pts, int64_t i, const orc_camera *c
 void orc_point_masks(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
                      const orc_params *pr, uint8_t *mask /*[V][n]*/)
 {
-    int64_t pix[8];
-    float proj[7];
-    for (int v = 0; v < n_views; ++v)
-        for (int64_t i = 0; i < pts->n; ++i)
+    for (int v = 0; v < n_views; ++v) {
+        #pragma omp parallel for schedule(static) num_threads(orc_threads)
+        for (int64_t i = 0; i < pts->n; ++i) {
+            int64_t pix[8];
+            float proj[7];
             mask[(int64_t)v * pts->n + i] =
                 (uint8_t)point_mask(pts, i, &cams[v], &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
+        }
+    }
+}
+
+/* Per-point slots of one chunk [i0, i0 + cnt): mask, pixels per layer and projection of every point, computed
+ * in parallel (a map: each point writes only its own slot).  The callers reduce over the slots serially. */
+typedef struct {
+    uint8_t *mask;  /* [ORC_CHUNK] */
+    int64_t *pix;   /* [ORC_CHUNK][8] */
+    float *proj;    /* [ORC_CHUNK][8] (orc_project's 7 outputs) */
+} orc_chunk;
+
+static int chunk_alloc(orc_chunk *ch)
+{
+    ch->mask = (uint8_t *)malloc((size_t)ORC_CHUNK);
+    ch->pix = (int64_t *)malloc(sizeof(int64_t) * 8 * (size_t)ORC_CHUNK);
+    ch->proj = (float *)malloc(sizeof(float) * 8 * (size_t)ORC_CHUNK);
+    return ch->mask && ch->pix && ch->proj;
+}
+
+static void chunk_free(orc_chunk *ch)
+{
+    free(ch->mask);
+    free(ch->pix);
+    free(ch->proj);
+}
+
+static void chunk_masks(const orc_points *pts, int64_t i0, int64_t cnt, const orc_camera *c, const orc_pose *P,
+                        const orc_params *pr, uint32_t view, orc_chunk *ch)
+{
+    #pragma omp parallel for schedule(static) num_threads(orc_threads)
+    for (int64_t j = 0; j < cnt; ++j)
+        ch->mask[j] = (uint8_t)point_mask(pts, i0 + j, c, P, pr, view, ch->pix + 8 * j, ch->proj + 8 * j);
 }
 
 static uint64_t depth_key(float Z, uint32_t gi)
@@ -407,24 +470,29 @@ void orc_env_dir(const orc_camera *c, const orc_pose *P, int l, int64_t u, int64
 void orc_forward_depth(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
                        const orc_params *pr, uint64_t *keys)
 {
-    int64_t pix[8];
-    float proj[7];
+    orc_chunk ch;
+    if (!chunk_alloc(&ch)) abort();
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
         int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
         uint64_t *kv = keys + (int64_t)v * P;
         for (int64_t p = 0; p < P; ++p) kv[p] = ORC_SENTINEL;
-        for (int64_t i = 0; i < pts->n; ++i) {
-            unsigned m = point_mask(pts, i, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
-            if (m & 0x80u) continue; /* ghosts are not rendered */
-            uint64_t key = depth_key(proj[6], (uint32_t)(pts->global_offset + i));
-            for (int l = 0; l < pr->layers; ++l) {
-                if (!(m & (1u << l))) continue;
-                int64_t q = layer_offset(c->width, c->height, l) + pix[l];
-                if (key < kv[q]) kv[q] = key;
+        for (int64_t i0 = 0; i0 < pts->n; i0 += ORC_CHUNK) {
+            int64_t cnt = pts->n - i0 < ORC_CHUNK ? pts->n - i0 : ORC_CHUNK;
+            chunk_masks(pts, i0, cnt, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), &ch);
+            for (int64_t j = 0; j < cnt; ++j) {  /* serial, point order */
+                unsigned m = ch.mask[j];
+                if (m & 0x80u) continue; /* ghosts are not rendered */
+                uint64_t key = depth_key(ch.proj[8 * j + 6], (uint32_t)(pts->global_offset + i0 + j));
+                for (int l = 0; l < pr->layers; ++l) {
+                    if (!(m & (1u << l))) continue;
+                    int64_t q = layer_offset(c->width, c->height, l) + ch.pix[8 * j + l];
+                    if (key < kv[q]) kv[q] = key;
+                }
             }
         }
     }
+    chunk_free(&ch);
 }
 
 /* Fuzzy depth test, Eq. 6, pinned as R9: z <= fl(fl(1+alpha) * m). */
@@ -443,9 +511,9 @@ static int fuzzy_pass(float z, uint64_t key, float alpha)
 void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera *cams, const orc_pose *poses,
                        const orc_params *pr, const uint64_t *keys, double *accum, double *count)
 {
-    int64_t pix[8];
-    float proj[7];
     const int C = pts->channels;
+    orc_chunk ck;
+    if (!chunk_alloc(&ck)) abort();
     for (int v = 0; v < n_views; ++v) {
         const orc_camera *c = &cams[v];
         int64_t P = orc_pyramid_pixels(c->width, c->height, pr->layers);
@@ -454,18 +522,24 @@ void orc_forward_blend(const orc_points *pts, int32_t n_views, const orc_camera 
         double *cv = count + (int64_t)v * P;
         memset(av, 0, sizeof(double) * (size_t)(P * C));
         memset(cv, 0, sizeof(double) * (size_t)P);
-        for (int64_t i = 0; i < pts->n; ++i) {
-            unsigned m = point_mask(pts, i, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), pix, proj);
-            if (m & 0x80u) continue;
-            for (int l = 0; l < pr->layers; ++l) {
-                if (!(m & (1u << l))) continue;
-                int64_t q = layer_offset(c->width, c->height, l) + pix[l];
-                if (!fuzzy_pass(proj[6], kv[q], pr->alpha)) continue;
-                for (int ch = 0; ch < C; ++ch) av[q * C + ch] += desc_lin(pr, pts->feat[i * C + ch]);
-                cv[q] += 1.0;
+        for (int64_t i0 = 0; i0 < pts->n; i0 += ORC_CHUNK) {
+            int64_t cnt = pts->n - i0 < ORC_CHUNK ? pts->n - i0 : ORC_CHUNK;
+            chunk_masks(pts, i0, cnt, c, &poses[v], pr, (uint32_t)(pr->view_id_base + v), &ck);
+            for (int64_t j = 0; j < cnt; ++j) {  /* serial, point order */
+                unsigned m = ck.mask[j];
+                if (m & 0x80u) continue;
+                int64_t i = i0 + j;
+                for (int l = 0; l < pr->layers; ++l) {
+                    if (!(m & (1u << l))) continue;
+                    int64_t q = layer_offset(c->width, c->height, l) + ck.pix[8 * j + l];
+                    if (!fuzzy_pass(ck.proj[8 * j + 6], kv[q], pr->alpha)) continue;
+                    for (int ch = 0; ch < C; ++ch) av[q * C + ch] += desc_lin(pr, pts->feat[i * C + ch]);
+                    cv[q] += 1.0;
+                }
             }
         }
     }
+    chunk_free(&ck);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -484,7 +558,8 @@ void orc_forward_resolve(int32_t n_views, const orc_camera *cams, const orc_pose
             int64_t off = layer_offset(c->width, c->height, l);
             int32_t wl = layer_w(c->width, l);
             int64_t hw = (int64_t)wl * layer_w(c->height, l);
-            for (int64_t j = 0; j < hw; ++j) {
+            #pragma omp parallel for schedule(static) num_threads(orc_threads)
+            for (int64_t j = 0; j < hw; ++j) {  /* each pixel writes only its own outputs */
                 int64_t q = off + j;
                 double n = count[(int64_t)v * P + q];
                 double bgv[32];
@@ -704,6 +779,99 @@ static void ghost_layer_grad(const orc_camera *c, const orc_params *pr, int l, i
     gabs[2] = 0.5 * dabs[2]; gabs[3] = 0.5 * dabs[3];
 }
 
+/* One point of the backward in one view (the loop body of orc_backward): texture gradient of a rendered point
+ * into dtau[i] (R24), spatial gradient (ghost, or rendered point with spatial_rendered) into dx[i] (R17, R21),
+ * and its pose / intrinsics terms into slot: [0] = 1 if any, [1..6] d_pose, [7..12] their scales,
+ * [13..24] d_intrinsics, [25..36] their scales.  Writes only point i's entries and its own slot. */
+#define SLOT 37
+static void backward_point(const orc_points *pts, int64_t i, unsigned m, const int64_t *pix, const float *proj,
+                           const orc_camera *c, const orc_pose *Pz, const orc_params *pr, const uint64_t *kv,
+                           const double *cv, const double *img, const float *Gv, int64_t P, double *dtau,
+                           double *dx, double *dtau_abs, double *dx_abs, int want_intr, double *slot)
+{
+    const int C = pts->channels;
+    const int64_t n = pts->n;
+    slot[0] = 0.0;
+    if (!(m & 0x7Fu)) return;
+    double tau[32];  /* linear-space descriptor */
+    for (int ch = 0; ch < C; ++ch) tau[ch] = desc_lin(pr, pts->feat[i * C + ch]);
+    if (!(m & 0x80u)) {
+        /* rendered point: texture gradient of Eq. 7, dI/dtau = 1/|Lambda| (R24) */
+        for (int l = 0; l < pr->layers; ++l) {
+            if (!(m & (1u << l))) continue;
+            int64_t off = layer_offset(c->width, c->height, l);
+            int64_t q = off + pix[l];
+            if (!fuzzy_pass(proj[6], kv[q], pr->alpha)) continue;
+            int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
+            for (int ch = 0; ch < C; ++ch) {
+                /* d tau_lin / d tau = exp(tau) = tau_lin for log descriptors, 1 otherwise */
+                double t = (double)Gv[C * off + ch * hw + pix[l]] / cv[q] * (pr->log_descriptors ? tau[ch] : 1.0);
+                if (dtau) dtau[i * C + ch] += t;
+                if (dtau_abs) dtau_abs[i * C + ch] += fabs(t);
+            }
+        }
+        if (!pr->spatial_rendered) return;
+    } else if (pr->spatial_rendered) {
+        return;  /* ghost gradients disabled: ghosts take no part at all */
+    }
+    /* spatial gradient (ghost point, or a rendered point with ghost gradients disabled): image-space
+     * gradient of Eqs. 9-11 summed over layers in layer-0 pixels (R17) */
+    double gu = 0.0, gv = 0.0, ga[4] = {0, 0, 0, 0};
+    for (int l = 0; l < pr->layers; ++l) {
+        if (!(m & (1u << l))) continue;
+        double g[2], gabs[4];
+        ghost_layer_grad(c, pr, l, pix[l], C, tau, proj[6], kv, cv, img, Gv, P, g, gabs);
+        double s = ldexp(1.0, -l);
+        gu += s * g[0]; gv += s * g[1];
+        for (int k = 0; k < 4; ++k) ga[k] += s * gabs[k];
+    }
+    double J[6];
+    orc_jacobian(c, proj, J);
+    /* w = J^T g = dL/dXc */
+    double w[3], wu[3], wv[3];
+    for (int k = 0; k < 3; ++k) {
+        w[k] = J[k] * gu + J[3 + k] * gv;
+        wu[k] = J[k];
+        wv[k] = J[3 + k];
+    }
+    const float *R = Pz->R;
+    double X[3] = {proj[0], proj[1], proj[2]};
+    /* tolerance scale: rounding errors of w live in camera space and R^T mixes them into every
+     * component, so each component's scale is the 2-norm of the term vectors R^T J^T e. */
+    double nu = sqrt(wu[0] * wu[0] + wu[1] * wu[1] + wu[2] * wu[2]);
+    double nv = sqrt(wv[0] * wv[0] + wv[1] * wv[1] + wv[2] * wv[2]);
+    for (int k = 0; k < 3; ++k) {
+        /* dx = R^T w (Xc = R x + t) */
+        double a = R[0 + k] * w[0] + R[3 + k] * w[1] + R[6 + k] * w[2];
+        if (dx) dx[k * n + i] += a;
+        if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
+    }
+    slot[0] = 1.0;
+    if (want_intr) {
+        /* NEXT-1: d theta = Jt^T g (layer-0 pixel gradient, R17) */
+        double Jt[24];
+        orc_intrinsics_jacobian(c, proj, Jt);
+        for (int k = 0; k < 12; ++k) {
+            slot[13 + k] = Jt[k] * gu + Jt[12 + k] * gv;
+            slot[25 + k] = (ga[0] + ga[1]) * fabs(Jt[k]) + (ga[2] + ga[3]) * fabs(Jt[12 + k]);
+        }
+    } else {
+        for (int k = 13; k < SLOT; ++k) slot[k] = 0.0;
+    }
+    /* Eq. 17 left perturbation: dXc/dxi = [I | -[Xc]x] -> (w, Xc x w) (R19) */
+    double cr[3] = {X[1] * w[2] - X[2] * w[1], X[2] * w[0] - X[0] * w[2], X[0] * w[1] - X[1] * w[0]};
+    double cu[3] = {X[1] * wu[2] - X[2] * wu[1], X[2] * wu[0] - X[0] * wu[2], X[0] * wu[1] - X[1] * wu[0]};
+    double cvv[3] = {X[1] * wv[2] - X[2] * wv[1], X[2] * wv[0] - X[0] * wv[2], X[0] * wv[1] - X[1] * wv[0]};
+    double ncu = sqrt(cu[0] * cu[0] + cu[1] * cu[1] + cu[2] * cu[2]);
+    double ncv = sqrt(cvv[0] * cvv[0] + cvv[1] * cvv[1] + cvv[2] * cvv[2]);
+    for (int k = 0; k < 3; ++k) {
+        slot[1 + k] = w[k];
+        slot[4 + k] = cr[k];
+        slot[7 + k] = (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
+        slot[10 + k] = (ga[0] + ga[1]) * ncu + (ga[2] + ga[3]) * ncv;
+    }
+}
+
 /* ------------------------------------------------------------------------- */
 /* Backward.  Inputs: the forward's keys/count/image (re-render) and */
 /* the upstream gradient G = dL/dI (image layout).  Outputs (overwritten):   */
@@ -729,8 +897,9 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
 {
     const int C = pts->channels;
     const int64_t n = pts->n;
-    int64_t pix[8];
-    float proj[7];
+    orc_chunk ck;
+    double *slot = (double *)malloc(sizeof(double) * SLOT * (size_t)ORC_CHUNK);
+    if (!chunk_alloc(&ck) || !slot) abort();
     if (dtau) memset(dtau, 0, sizeof(double) * (size_t)(n * C));
     if (dtau_abs) memset(dtau_abs, 0, sizeof(double) * (size_t)(n * C));
     if (dx) memset(dx, 0, sizeof(double) * (size_t)(3 * n));
@@ -774,89 +943,29 @@ void orc_backward(const orc_points *pts, int32_t n_views, const orc_camera *cams
                 }
             }
         }
-        for (int64_t i = 0; i < n; ++i) {
-            unsigned m = point_mask(pts, i, c, Pz, pr, (uint32_t)(pr->view_id_base + v), pix, proj);
-            if (!(m & 0x7Fu)) continue;
-            double tau[32];  /* linear-space descriptor */
-            for (int ch = 0; ch < C; ++ch) tau[ch] = desc_lin(pr, pts->feat[i * C + ch]);
-            if (!(m & 0x80u)) {
-                /* rendered point: texture gradient of Eq. 7, dI/dtau = 1/|Lambda| (R24) */
-                for (int l = 0; l < pr->layers; ++l) {
-                    if (!(m & (1u << l))) continue;
-                    int64_t off = layer_offset(c->width, c->height, l);
-                    int64_t q = off + pix[l];
-                    if (!fuzzy_pass(proj[6], kv[q], pr->alpha)) continue;
-                    int64_t hw = (int64_t)layer_w(c->width, l) * layer_w(c->height, l);
-                    for (int ch = 0; ch < C; ++ch) {
-                        /* d tau_lin / d tau = exp(tau) = tau_lin for log descriptors, 1 otherwise */
-                        double t = (double)Gv[C * off + ch * hw + pix[l]] / cv[q] * (pr->log_descriptors ? tau[ch] : 1.0);
-                        if (dtau) dtau[i * C + ch] += t;
-                        if (dtau_abs) dtau_abs[i * C + ch] += fabs(t);
-                    }
+        for (int64_t i0 = 0; i0 < n; i0 += ORC_CHUNK) {
+            int64_t cnt = n - i0 < ORC_CHUNK ? n - i0 : ORC_CHUNK;
+            chunk_masks(pts, i0, cnt, c, Pz, pr, (uint32_t)(pr->view_id_base + v), &ck);
+            /* map: every point writes its own d_tau / d_x entries and its pose / intrinsics terms into its slot */
+            #pragma omp parallel for schedule(static) num_threads(orc_threads)
+            for (int64_t j = 0; j < cnt; ++j)
+                backward_point(pts, i0 + j, ck.mask[j], ck.pix + 8 * j, ck.proj + 8 * j, c, Pz, pr, kv, cv, img, Gv,
+                               P, dtau, dx, dtau_abs, dx_abs, dintr || dintr_abs, slot + SLOT * j);
+            /* reduce: per-view sums over points, serially in point order */
+            for (int64_t j = 0; j < cnt; ++j) {
+                const double *sl = slot + SLOT * j;
+                if (sl[0] == 0.0) continue;
+                for (int k = 0; k < 6; ++k) {
+                    if (dpose) dpose[v * 6 + k] += sl[1 + k];
+                    if (dpose_abs) dpose_abs[v * 6 + k] += sl[7 + k];
                 }
-                if (!pr->spatial_rendered) continue;
-            } else if (pr->spatial_rendered) {
-                continue;  /* ghost gradients disabled: ghosts take no part at all */
-            }
-            /* spatial gradient (ghost point, or a rendered point with ghost gradients disabled): image-space
-             * gradient of Eqs. 9-11 summed over layers in layer-0 pixels (R17) */
-            double gu = 0.0, gv = 0.0, ga[4] = {0, 0, 0, 0};
-            for (int l = 0; l < pr->layers; ++l) {
-                if (!(m & (1u << l))) continue;
-                double g[2], gabs[4];
-                ghost_layer_grad(c, pr, l, pix[l], C, tau, proj[6], kv, cv, img, Gv, P, g, gabs);
-                double s = ldexp(1.0, -l);
-                gu += s * g[0]; gv += s * g[1];
-                for (int k = 0; k < 4; ++k) ga[k] += s * gabs[k];
-            }
-            double J[6];
-            orc_jacobian(c, proj, J);
-            /* w = J^T g = dL/dXc */
-            double w[3], wu[3], wv[3];
-            for (int k = 0; k < 3; ++k) {
-                w[k] = J[k] * gu + J[3 + k] * gv;
-                wu[k] = J[k];
-                wv[k] = J[3 + k];
-            }
-            const float *R = Pz->R;
-            double X[3] = {proj[0], proj[1], proj[2]};
-            /* tolerance scale: rounding errors of w live in camera space and R^T mixes them into every
-             * component, so each component's scale is the 2-norm of the term vectors R^T J^T e. */
-            double nu = sqrt(wu[0] * wu[0] + wu[1] * wu[1] + wu[2] * wu[2]);
-            double nv = sqrt(wv[0] * wv[0] + wv[1] * wv[1] + wv[2] * wv[2]);
-            for (int k = 0; k < 3; ++k) {
-                /* dx = R^T w (Xc = R x + t) */
-                double a = R[0 + k] * w[0] + R[3 + k] * w[1] + R[6 + k] * w[2];
-                if (dx) dx[k * n + i] += a;
-                if (dx_abs) dx_abs[k * n + i] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
-            }
-            if (dintr || dintr_abs) {
-                /* NEXT-1: d theta = Jt^T g (layer-0 pixel gradient, R17) */
-                double Jt[24];
-                orc_intrinsics_jacobian(c, proj, Jt);
                 for (int k = 0; k < 12; ++k) {
-                    if (dintr) dintr[v * 12 + k] += Jt[k] * gu + Jt[12 + k] * gv;
-                    if (dintr_abs) dintr_abs[v * 12 + k] += (ga[0] + ga[1]) * fabs(Jt[k]) + (ga[2] + ga[3]) * fabs(Jt[12 + k]);
-                }
-            }
-            if (dpose || dpose_abs) {
-                /* Eq. 17 left perturbation: dXc/dxi = [I | -[Xc]x] -> (w, Xc x w) (R19) */
-                double cr[3] = {X[1] * w[2] - X[2] * w[1], X[2] * w[0] - X[0] * w[2], X[0] * w[1] - X[1] * w[0]};
-                double cu[3] = {X[1] * wu[2] - X[2] * wu[1], X[2] * wu[0] - X[0] * wu[2], X[0] * wu[1] - X[1] * wu[0]};
-                double cvv[3] = {X[1] * wv[2] - X[2] * wv[1], X[2] * wv[0] - X[0] * wv[2], X[0] * wv[1] - X[1] * wv[0]};
-                for (int k = 0; k < 3; ++k) {
-                    if (dpose) {
-                        dpose[v * 6 + k] += w[k];
-                        dpose[v * 6 + 3 + k] += cr[k];
-                    }
-                    if (dpose_abs) {
-                        double ncu = sqrt(cu[0] * cu[0] + cu[1] * cu[1] + cu[2] * cu[2]);
-                        double ncv = sqrt(cvv[0] * cvv[0] + cvv[1] * cvv[1] + cvv[2] * cvv[2]);
-                        dpose_abs[v * 6 + k] += (ga[0] + ga[1]) * nu + (ga[2] + ga[3]) * nv;
-                        dpose_abs[v * 6 + 3 + k] += (ga[0] + ga[1]) * ncu + (ga[2] + ga[3]) * ncv;
-                    }
+                    if (dintr) dintr[v * 12 + k] += sl[13 + k];
+                    if (dintr_abs) dintr_abs[v * 12 + k] += sl[25 + k];
                 }
             }
         }
     }
+    chunk_free(&ck);
+    free(slot);
 }

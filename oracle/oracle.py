@@ -18,7 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "adop_oracle.c")
 LIB = os.path.join(HERE, "liborc.so")
-CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 SENTINEL = 0x7FFFFFFFFFFFFFFF
 STREAM_GHOST, STREAM_DISCARD = 1, 2
@@ -91,6 +91,9 @@ def lib():
         _lib.orc_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_project_f64.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
         _lib.orc_intrinsics_jacobian.argtypes = [P(_Camera), C.c_void_p, C.c_void_p]
+        _lib.orc_set_threads.restype = C.c_int
+        _lib.orc_set_threads.argtypes = [C.c_int]
+        _lib.orc_get_threads.restype = C.c_int
         _lib.orc_backward.argtypes = [P(_Points), C.c_int32, P(_Camera), P(_Pose), P(_Params), P(_Env),
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -181,6 +184,16 @@ def _arrays(cams, poses):
     ca = (_Camera * V)(*[camera_struct(c) for c in cams])
     pa = (_Pose * V)(*[pose_struct(p) for p in poses])
     return ca, pa
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's parallel loops (n <= 0: all processors); returns the count in effect.
+    Results do not depend on it (per-point map in parallel, reductions serial in point order)."""
+    return int(lib().orc_set_threads(int(n)))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
 
 
 def pyramid_pixels(w: int, h: int, layers: int) -> int:

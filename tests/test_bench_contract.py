@@ -20,7 +20,7 @@ def _line(args, timeout=900):
 
 @pytest.mark.gpu
 def test_bench_line_has_every_contract_key():
-    d = _line(["--steps", "3", "--warmup", "3", "--points", "2000000", "--no-secondary", "--no-cpu-baseline"])
+    d = _line(["--steps", "3", "--warmup", "3", "--points", "2000000", "--no-secondary"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "gpu_launches", "clocks", "e2e"):
         assert k in d, k
@@ -29,6 +29,11 @@ def test_bench_line_has_every_contract_key():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2 and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    st = d["ms_per_step_stats"]
+    assert st["frames"] == 3 and st["p10"] <= st["median"] <= st["p90"]
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["value"] > 0 and cb["cores"] == cb["omp_threads"] >= 1
+    assert cb["os_cpu_count"] == os.cpu_count() and cb["single_thread"]["cores"] == 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert e["copy_all"]["value"] > 0 and e["copy_all"]["h2d_bytes_per_step"] > e["h2d_bytes_per_step"]
@@ -37,4 +42,5 @@ def test_bench_line_has_every_contract_key():
 def test_reference_arm_line():
     d = _line(["--impl", "reference", "--steps", "1", "--warmup", "0", "--points", "300000", "--ref-sample", "50000"])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["os_cpu_count"] == os.cpu_count()
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["unit"] == d["unit"]

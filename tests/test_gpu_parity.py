@@ -256,25 +256,21 @@ def test_full_config2_10M_fwd_bwd_vs_oracle():
     compare_backward(r, bwd, ctx="config2-full")
 
 
-def test_full_config4_50M_16views_sampled_views():
-    """configs[4]: 50M points x 16 views 1024^2 in ONE fused sweep (as bench times it); the oracle checks
-    views 0 and 11 of that sweep (forward + per-view pose gradient), and the 2-view backward call."""
+def test_full_config4_50M_16views_fwd_bwd_vs_oracle():
+    """configs[4]: 50M points x 16 views 1024^2 OpenCV8 in ONE fused forward + backward (as bench times it)
+    against the (OpenMP) oracle on the same inputs: keys and counts of all 16 views bit-exact, images, and the
+    full backward -- d_feat, d_pos of all 50M points, d_pose and d_intrinsics of all 16 views."""
     w = _cloud_on_gpu(4)
     C = w.cloud.channels
     G = grads_for(w.cameras, w.params.layers, C)
-    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params)
+    r = A.Renderer(w.cloud, w.cameras, w.poses, w.params, intrinsics=True)
     r.forward()
     r.backward([g.cuda() for g in G])
     torch.cuda.synchronize()
-    sel = [0, 11]
-    cams = [w.cameras[v] for v in sel]
-    poses = [w.poses[v] for v in sel]
-    cpu = w.cloud.to("cpu")
-    for j, v in enumerate(sel):
-        prm = dataclasses.replace(w.params, view_id_base=v)
-        _, fwd, bwd = run_oracle(cpu, [cams[j]], [poses[j]], prm, grads=[G[v]])
-        compare_forward(r, fwd, views=[v], ctx=f"config4 view {v}")
-        compare_backward(r, bwd, check_feat=False, check_pos=False, views=[v], ctx=f"config4 view {v}")
+    _, fwd, bwd = run_oracle(w.cloud.to("cpu"), w.cameras, w.poses, w.params, grads=G)
+    compare_forward(r, fwd, ctx="config4-full")
+    compare_backward(r, bwd, ctx="config4-full")
+    assert np.count_nonzero(np.abs(bwd.dx).sum(0)) > 1_000_000
 
 
 @pytest.mark.parametrize("model,tight", [(S.PINHOLE, False), (S.OPENCV8, False), (S.PINHOLE, True),
