@@ -16,6 +16,7 @@ import math
 import os
 from typing import List, Optional, Sequence, Tuple
 
+import numpy as np
 import torch
 
 from . import build as _build
@@ -485,10 +486,32 @@ class Renderer:
         self.d_feat = self.d_pos = self.d_pose = self.d_intr = self.d_env = None
         self.intrinsics = intrinsics  # backward also produces d_intr [V][12] (NEXT-1)
 
+    def set_poses(self, poses):
+        """Replace the views' poses (e.g. after a pose-refinement step with d_pose)."""
+        assert len(poses) == len(self.cams)
+        self.poses = list(poses)
+
+    def set_cameras(self, cams):
+        """Replace the views' cameras (e.g. after an intrinsics step with d_intr); same image sizes."""
+        assert len(cams) == len(self.cams) and all(
+            (a.width, a.height) == (b.width, b.height) for a, b in zip(cams, self.cams))
+        self.cams = list(cams)
+
+    def _key(self):
+        # the values the marshalled descriptors are built from: poses and cameras may be replaced or edited in
+        # place between calls (refinement with d_pose / d_intr), so the cache is keyed on their values
+        k = []
+        for c, p in zip(self.cams, self.poses):
+            k.append((c.width, c.height, c.model, c.fx, c.fy, c.cx, c.cy, tuple(c.k), tuple(c.p), c.r2_max,
+                      np.asarray(p.R, dtype=np.float32).tobytes(), np.asarray(p.t, dtype=np.float32).tobytes()))
+        return tuple(k)
+
     def _call(self):
-        # marshalled descriptors, built once (the cameras / poses / buffers of a Renderer are fixed)
-        if getattr(self, "_c", None) is None:
+        # marshalled descriptors, rebuilt only when a pose or camera value changed
+        key = self._key()
+        if getattr(self, "_c", None) is None or self._ckey != key:
             self._c = _Call(self.points, self.cams, self.poses, self.params, self.pyrs)
+            self._ckey = key
         return self._c
 
     def forward(self, stream=None):
@@ -506,6 +529,9 @@ class Renderer:
             self.d_env = torch.empty_like(self.params.env)
 
     def backward(self, grads: Sequence[torch.Tensor], stream=None):
+        if getattr(self, "peer_non_owner", False):
+            raise RuntimeError("backward on a non-owner of a shared (peer-memory) pyramid: its image is never "
+                               "resolved; run the backward on the owner (the p2p point sharding is forward-only)")
         if self.d_feat is None:
             self.alloc_grads()
         rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,

@@ -115,6 +115,11 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         procs = []
     for src in sources():
         score, r, obj, log = best[src]
+        if score > SPILL_OK:  # still a hot instance over its limit after ROUNDS attempts: say which, loudly
+            # (linked anyway -- a correct but slower library beats no library; tests/test_build_spills.py fails)
+            over = {k: v for k, v in hot_spills(log).items() if v > HOT[k]}
+            sys.stderr.write(f"WARNING build: {os.path.basename(src)} kept with hot instances over their spill "
+                             f"limits after {ROUNDS} rounds: {over}\n")
         logs.append(f"// {os.path.basename(src)}: round {r} (hot-instance spill bytes {score})\n" + log)
         objs.append(obj)
     target = LIB if out is None else out

@@ -17,6 +17,7 @@
 // of the SoA rows), so every warp-collective below is warp-uniform.
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <atomic>
 
 #include "adop_device.cuh"
 
@@ -1333,6 +1334,40 @@ __device__ __forceinline__ void jacobian(const ViewDesc &v, const Proj &p, float
     J[3] = a1 * D10; J[4] = a1 * D11; J[5] = -a1 * (D10 * xn + D11 * yn);
 }
 
+// w = J^T g = dL/dXc (R21).  The distortion model's Jacobian is evaluated in fp64: near the edge of the
+// camera's valid radius (R6) the radial derivative rad + 2 r^2 drad/dr^2 nearly cancels, and an fp32 J there
+// errs by ~eps |rad| instead of ~eps |J| (measured on configs[4]: d_pos 2.4x over the R20 tolerance).
+template <int MODEL>
+__device__ __forceinline__ void chain_w(const ViewDesc &v, const Proj &p, float gu, float gv, double w[3]) {
+    if (MODEL != 1) {
+        float J[6];
+        jacobian<MODEL>(v, p, J);
+        w[0] = (double)(J[0] * gu + J[3] * gv);
+        w[1] = (double)(J[1] * gu + J[4] * gv);
+        w[2] = (double)(J[2] * gu + J[5] * gv);
+        return;
+    }
+    const double iz = 1.0 / (double)p.Z, xn = (double)p.X * iz, yn = (double)p.Y * iz;
+    const double r2 = xn * xn + yn * yn;
+    const double k0 = v.k[0], k1 = v.k[1], k2 = v.k[2], k3 = v.k[3], k4 = v.k[4], k5 = v.k[5];
+    const double num = 1.0 + r2 * (k0 + r2 * (k1 + r2 * k2));
+    const double den = 1.0 + r2 * (k3 + r2 * (k4 + r2 * k5));
+    const double dnum = k0 + r2 * (2.0 * k1 + 3.0 * r2 * k2);
+    const double dden = k3 + r2 * (2.0 * k4 + 3.0 * r2 * k5);
+    const double rad = num / den;
+    const double drad = (dnum * den - num * dden) / (den * den);
+    const double p1 = v.p[0], p2 = v.p[1];
+    const double D00 = rad + 2.0 * xn * xn * drad + 2.0 * p1 * yn + 6.0 * p2 * xn;
+    const double D01 = 2.0 * xn * yn * drad + 2.0 * p1 * xn + 2.0 * p2 * yn;
+    const double D11 = rad + 2.0 * yn * yn * drad + 6.0 * p1 * yn + 2.0 * p2 * xn;
+    const double a0 = (double)v.fx * iz * gu, a1 = (double)v.fy * iz * gv;  // g scaled by f / Z
+    // J = diag(f) D N, N = [[1, 0, -xn], [0, 1, -yn]] / Z  ->  w = N^T D^T diag(f) g
+    const double e0 = D00 * a0 + D01 * a1, e1 = D01 * a0 + D11 * a1;
+    w[0] = e0;
+    w[1] = e1;
+    w[2] = -(e0 * xn + e1 * yn);
+}
+
 // Structural terms of one ghost in one view, per view accumulated in fp64 (R20): t[0..6) = the tangent
 // pose terms (w, Xc x w) (Eq. 17 left increment, R19); with nt = kNT, t[6..18) = the camera-intrinsics
 // terms (d(u0,v0)/d theta)^T g (NEXT-1), theta = (fx, fy, cx, cy, k1..k6, p1, p2), g = (g_u, g_v) in
@@ -1340,12 +1375,12 @@ __device__ __forceinline__ void jacobian(const ViewDesc &v, const Proj &p, float
 constexpr int kNI = 12;
 constexpr int kNT = 6 + kNI;
 template <int MODEL>
-__device__ __forceinline__ void struct_terms(const ViewDesc &v, const Proj &p, float gu, float gv, float w0, float w1,
-                                             float w2, int nt, double *t) {
-    t[0] = w0; t[1] = w1; t[2] = w2;
-    t[3] = (double)(p.Y * w2 - p.Z * w1);
-    t[4] = (double)(p.Z * w0 - p.X * w2);
-    t[5] = (double)(p.X * w1 - p.Y * w0);
+__device__ __forceinline__ void struct_terms(const ViewDesc &v, const Proj &p, float gu, float gv, const double *w,
+                                             int nt, double *t) {
+    t[0] = w[0]; t[1] = w[1]; t[2] = w[2];
+    t[3] = (double)p.Y * w[2] - (double)p.Z * w[1];
+    t[4] = (double)p.Z * w[0] - (double)p.X * w[2];
+    t[5] = (double)p.X * w[1] - (double)p.Y * w[0];
     if (nt <= 6) return;
     float xn = p.X * p.iz, yn = p.Y * p.iz;
     if (MODEL == 2) {  // R35: xd = g X, yd = g Y; no distortion parameters
@@ -1460,20 +1495,16 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
                     }
                 }
                 if (!__any_sync(kFull, gc)) continue;
-                float w0 = 0.f, w1 = 0.f, w2 = 0.f;
                 double tt[kNT];
 #pragma unroll
                 for (int k = 0; k < kNT; ++k) tt[k] = 0.0;
                 if (gc) {
-                    float J[6];
-                    jacobian<MODEL>(v, p, J);
-                    w0 = J[0] * gu + J[3] * gv;  // w = J^T g = dL/dXc
-                    w1 = J[1] * gu + J[4] * gv;
-                    w2 = J[2] * gu + J[5] * gv;
-                    dxx += v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2;  // dx = R^T w
-                    dxy += v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2;
-                    dxz += v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2;
-                    struct_terms<MODEL>(v, p, gu, gv, w0, w1, w2, NT, tt);
+                    double w[3];
+                    chain_w<MODEL>(v, p, gu, gv, w);  // w = J^T g = dL/dXc
+                    dxx += (float)(v.R[0] * w[0] + v.R[3] * w[1] + v.R[6] * w[2]);  // dx = R^T w
+                    dxy += (float)(v.R[1] * w[0] + v.R[4] * w[1] + v.R[7] * w[2]);
+                    dxz += (float)(v.R[2] * w[0] + v.R[5] * w[1] + v.R[8] * w[2]);
+                    struct_terms<MODEL>(v, p, gu, gv, w, NT, tt);
                 }
                 // pose (+ intrinsics) terms: warp sum in fp64
                 for (int k = 0; k < NT; ++k) {
@@ -1703,15 +1734,14 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
         gc = true;
     }
     if (!gc) return false;
-    float J[6];
-    jacobian<MODEL>(v, p, J);
-    const float w0 = J[0] * gu + J[3] * gv, w1 = J[1] * gu + J[4] * gv, w2 = J[2] * gu + J[5] * gv;
+    double w[3];
+    chain_w<MODEL>(v, p, gu, gv, w);  // w = J^T g = dL/dXc
     if (a.d_pos) {
-        red_add(a.d_pos + idx, v.R[0] * w0 + v.R[3] * w1 + v.R[6] * w2);  // dx = R^T w
-        red_add(a.d_pos + a.n + idx, v.R[1] * w0 + v.R[4] * w1 + v.R[7] * w2);
-        red_add(a.d_pos + 2 * a.n + idx, v.R[2] * w0 + v.R[5] * w1 + v.R[8] * w2);
+        red_add(a.d_pos + idx, (float)(v.R[0] * w[0] + v.R[3] * w[1] + v.R[6] * w[2]));  // dx = R^T w
+        red_add(a.d_pos + a.n + idx, (float)(v.R[1] * w[0] + v.R[4] * w[1] + v.R[7] * w[2]));
+        red_add(a.d_pos + 2 * a.n + idx, (float)(v.R[2] * w[0] + v.R[5] * w[1] + v.R[8] * w[2]));
     }
-    struct_terms<MODEL>(v, p, gu, gv, w0, w1, w2, nt, tt);
+    struct_terms<MODEL>(v, p, gu, gv, w, nt, tt);
     if (g) {
         g[0] = gu;
         g[1] = gv;
@@ -2136,13 +2166,17 @@ int launch_clear(const RasterArgs &a, int what, void *stream) {
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
     auto k = a.discard ? k_depth_async<MODEL, VM, true> : k_depth_async<MODEL, VM, false>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_depth_async<MODEL, VM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(DepthSmem));
-        cudaFuncSetAttribute(k_depth_async<MODEL, VM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(DepthSmem));
-        attr = true;
+    // the dynamic shared-memory limit is a per-device (context) attribute: raised once per device and
+    // instance (two threads racing here both set the same value)
+    static std::atomic<unsigned long long> attr_set[2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set[a.discard ? 1 : 0].load(std::memory_order_acquire) & bit)) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DepthSmem)) !=
+            cudaSuccess)
+            return (int)cudaGetLastError();
+        attr_set[a.discard ? 1 : 0].fetch_or(bit, std::memory_order_acq_rel);
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kST, sizeof(DepthSmem));
@@ -2355,7 +2389,7 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
     // Measured: configs[2] backward 0.387 -> 0.351 ms; with 16 views (configs[4], 0.7 GB of pixel tables) the
     // two consumers thrash L2 together (+1.5%), so large launches keep them in sequence.
     int64_t tbytes = 0;
-    for (int v = 0; v < a.nviews; ++v) tbytes += a.v[v].pixels * a.prow * (int64_t)sizeof(float);
+    for (int v = 0; v < a.nviews; ++v) tbytes += a.v[v].pixels * b.prow * (int64_t)sizeof(float);
     cudaStream_t side = (a.d_feat && tbytes <= (256ll << 20)) ? side_stream() : nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
     if (side) {

@@ -108,7 +108,8 @@ class PeerPointSharding:
     """Points the renderer of this rank (its shard, with its global_offset) at the owner's pyramid: the
     owner exports the keys / accum / count allocations (adop_ipc_export), the others map them
     (adop_ipc_open; peer access over NVLink between GPUs) and render into them with
-    adop_params.shared_pyramid = 1.  Non-owners keep their own image buffer (only the owner resolves)."""
+    adop_params.shared_pyramid = 1.  Non-owners keep their own image buffer (only the owner resolves), so the
+    p2p path is forward-only on them: a backward there raises (the owner's backward is a normal one)."""
 
     def __init__(self, renderer, owner: int = 0, group=None):
         from . import adop as A
@@ -126,6 +127,9 @@ class PeerPointSharding:
                                            p.width, p.height, p.layers)
                              for (k, a, c), p in zip(obj[0], self.own)]
             renderer._c = None  # the cached marshalled call holds the old pyramid pointers
+            # forward-only on non-owners: their image buffer is never resolved (only the owner resolves), and
+            # the backward reads the image (pixel tables, Eq. 11's I_q): Renderer.backward refuses
+            renderer.peer_non_owner = True
 
     def close(self):
         from . import adop as A

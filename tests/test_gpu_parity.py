@@ -678,3 +678,32 @@ def test_backward_captured_in_a_cuda_graph():
     for got, ref in zip((r.d_feat, r.d_pos, r.d_pose), eager):
         torch.testing.assert_close(got, ref, rtol=1e-5, atol=1e-6 * float(ref.abs().max()))
     assert float(eager[0].abs().sum()) > 0 and float(eager[1].abs().sum()) > 0
+
+
+def test_pose_and_camera_updates_between_forwards():
+    """Renderer keys its marshalled descriptors on the pose / camera values: a pose replaced with set_poses(),
+    a pose edited in place and a camera replaced with set_cameras() all reach the next forward and backward."""
+    w = S.workload(2, n=150_000, n_views=2)
+    prm = w.params
+    G = grads_for(w.cameras, prm.layers, w.cloud.channels)
+    r = A.Renderer(w.cloud.to("cuda"), w.cameras, w.poses, prm, intrinsics=True)
+    r.forward()
+    room = S.make_room(10.0)
+    new_poses = S.room_poses(2, room, seed=77)
+    r.set_poses(new_poses)
+    r.forward()
+    r.backward([g.cuda() for g in G])
+    torch.cuda.synchronize()
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, new_poses, prm, grads=G)
+    compare_forward(r, fwd, ctx="set_poses")
+    compare_backward(r, bwd, ctx="set_poses")
+    # in-place edit of a translation and a new camera for view 1
+    r.poses[0].t[:] = r.poses[0].t + np.array([0.05, -0.02, 0.01], np.float32)
+    cams = [w.cameras[0], S.opencv_camera(w.cameras[1].width, w.cameras[1].height, seed=99)]
+    r.set_cameras(cams)
+    r.forward()
+    r.backward([g.cuda() for g in G])
+    torch.cuda.synchronize()
+    _, fwd, bwd = run_oracle(w.cloud, cams, r.poses, prm, grads=G)
+    compare_forward(r, fwd, ctx="in-place pose + set_cameras")
+    compare_backward(r, bwd, ctx="in-place pose + set_cameras")

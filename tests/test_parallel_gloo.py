@@ -273,3 +273,12 @@ def test_point_sharded_forward_over_a_shared_pyramid_gloo_ws2(tmp_path):
         assert np.array_equal(ac[v][P * 3:], fwd.count[v])
         np.testing.assert_allclose(image[v], fwd.image[v], rtol=1e-12, atol=1e-12)
     assert fwd.count.sum() > 500
+
+
+def test_peer_non_owner_backward_is_refused():
+    """The peer-memory point sharding is forward-only on non-owners (their image is never resolved)."""
+    import types
+    from paper_2110_06635_b200 import adop as A
+    fake = types.SimpleNamespace(peer_non_owner=True, d_feat=None)
+    with pytest.raises(RuntimeError, match="non-owner"):
+        A.Renderer.backward(fake, [])
