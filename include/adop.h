@@ -160,14 +160,18 @@ ADOP_API int64_t adop_pyramid_pixels(int32_t width, int32_t height, int32_t laye
 
 /* Workspace bytes for calls over `n_views` views (cameras: host [n_views]) of `points`.
  * Layout: 4 KiB header | pose partials | backward pixel tables (per view and pixel one
- * row {min depth, count, sum_c G I, 0, G[C]} of 16 + 4 * roundup4(C) bytes) | record region.
- * record_capacity: 16-byte slots of the record region.  The depth pass fills it from
- * the front with survivor records (one per (point, view, layer) hit of the render set)
- * and, when params->ghost_rate > 0, from the back with ghost entries (2 slots per kept
- * (ghost, view)); both are reserved per warp in chunks of 256 slots whose unused slots
- * are marked dead.  < 0 selects the worst case n * n_views * max(layers, 2) plus chunk
- * slack.  If the lists do not fit, the blend pass re-streams all points and the
- * backward re-renders them (correct, slower).
+ * row {min depth, count, sum_c G I, 0, G[C]} of 16 + 4 * roundup4(C) bytes) | record region |
+ * chunk tables.
+ * record_capacity: 16-byte slots of the record region (rounded up to 64-slot chunks).  The depth
+ * pass fills it from the front with survivor records (one per (point, view, layer) hit of the
+ * render set) and the backward sweep, when params->ghost_rate > 0, from the back with ghost
+ * entries (2 slots per kept (ghost, view)); both are reserved per warp in chunks of 64 slots whose
+ * unused slots are marked dead.  With more than 2 views every chunk holds one view's items and the
+ * chunk tables (per chunk: 1 view byte + 2 x 4-byte order entries; plus 1 KiB) let the consumers
+ * walk the lists view by view.  < 0 selects the worst case n * n_views * max(layers, 2) plus chunk
+ * slack.  If the lists do not fit, the blend pass re-streams all points and the backward
+ * re-renders them (correct, slower).
+ * Bytes = 4096 + 2048 * 16 * 18 * 8 + tables + ceil(capacity / 64) * 1033 + 1024.
  * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, n_views not in [1, 16], bad layers,
  * channels or camera sizes). */
 ADOP_API adop_status adop_workspace_size(const adop_points *points, int32_t n_views, const adop_camera *cameras,
@@ -251,6 +255,15 @@ ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspac
 /* Bounding box of every 256-point tile of `points` (lo x, y, z, 0, hi x, y, z, 0; NaN coordinates
  * ignored): bounds = device float [ceil(n/256)][8], 16-byte aligned.  Enqueued on `stream`. */
 ADOP_API adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *stream);
+
+/* Host-only diagnostic of the OpenCV8 candidate window (no GPU work): the box [xlo, xhi] x [ylo, yhi]
+ * in undistorted normalized coordinates that contains every point n with |n|^2 <= r2_max whose
+ * distorted pixel (Eq. 2 with R6) lies in the all-layer window (-2^(L-1) - 2, w + 2^(L-1) + 2) x
+ * (same for h); points outside it cannot land in any layer, so the depth and backward sweeps cull
+ * them before the distortion model.  out[4] = (xlo, xhi, ylo, yhi); *valid = 0 when no window is
+ * used for this camera (pinhole / fisheye, no finite r2_max, or an edge point failed to invert).
+ * Errors: ADOP_ERR_INVALID_ARGUMENT (NULL pointers, bad camera or layers). */
+ADOP_API adop_status adop_camera_window(const adop_camera *camera, int32_t layers, float out[4], int32_t *valid);
 
 /* ---- Point sharding over peer memory (NVLink P2P / CUDA IPC) ---------- */
 

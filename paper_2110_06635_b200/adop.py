@@ -109,6 +109,8 @@ def lib():
         L.adop_ipc_close.argtypes = [C.c_void_p]
         L.adop_tile_bounds.restype = C.c_int
         L.adop_tile_bounds.argtypes = [P(adop_points), C.c_void_p, C.c_void_p]
+        L.adop_camera_window.restype = C.c_int
+        L.adop_camera_window.argtypes = [P(adop_camera), C.c_int32, P(C.c_float), P(C.c_int32)]
         L.adop_prep_workspace_size.restype = C.c_int
         L.adop_prep_workspace_size.argtypes = [C.c_int64, C.c_int32, P(C.c_size_t)]
         L.adop_blocked_morton_order.restype = C.c_int
@@ -458,6 +460,15 @@ def knn_radius(points: Points, k: int = 8, stream=None) -> torch.Tensor:
     _check(lib().adop_knn_radius(C.byref(points.s), int(k), r.data_ptr(), ptr, size, _stream(stream)))
     del buf  # (as above)
     return r
+
+
+def camera_window(cam, layers: int):
+    """(xlo, xhi, ylo, yhi) of the OpenCV8 candidate window in undistorted normalized coordinates, or None
+    (adop_camera_window; host only)."""
+    out, valid = (C.c_float * 4)(), C.c_int32(0)
+    cs = camera_struct(cam)
+    _check(lib().adop_camera_window(C.byref(cs), int(layers), out, C.byref(valid)))
+    return tuple(out) if valid.value else None
 
 
 def version() -> str:

@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+#include <vector>
+
 #include "adop_internal.h"
 
 using namespace adop;
@@ -175,8 +178,15 @@ struct Ws {
     double *partials;
     void *tables;
     Record *records;
-    int64_t capacity;
+    int64_t capacity;   // record slots, a multiple of kListChunk
+    uint8_t *cview;     // chunk tables of the multi-view lists (after the record region)
+    uint32_t *corder0, *corder1, *ccount;
 };
+
+// Bytes of the record region per kListChunk-slot chunk: the slots, the chunk's view byte and its two order
+// entries (front / back list); plus a fixed tail for the counts and alignment.
+constexpr size_t kChunkBytes = (size_t)kListChunk * sizeof(Record) + 1 + 2 * sizeof(uint32_t);
+constexpr size_t kListTail = 1024;
 
 // Backward pixel tables: per view and pixel one row {m, count, S, 0, G[C]} of 16 + 4 * roundup4(C)
 // bytes (k_bwd_prep), 256-B rounded.
@@ -199,7 +209,17 @@ adop_status carve_workspace(void *ws, size_t bytes, size_t tbytes, Ws &out) {
     out.partials = reinterpret_cast<double *>(b + kHeaderBytes);
     out.tables = b + kHeaderBytes + kPartialBytes;
     out.records = reinterpret_cast<Record *>(b + fixed);
-    out.capacity = (int64_t)((bytes - fixed) / sizeof(Record));
+    const size_t avail = bytes - fixed;
+    const int64_t nch = avail > kListTail ? (int64_t)((avail - kListTail) / kChunkBytes) : 0;
+    out.capacity = nch * kListChunk;
+    char *t = b + fixed + (size_t)out.capacity * sizeof(Record);
+    out.cview = reinterpret_cast<uint8_t *>(t);
+    t += (nch + 15) / 16 * 16;
+    out.corder0 = reinterpret_cast<uint32_t *>(t);
+    out.corder1 = out.corder0 + nch;
+    t += (size_t)nch * 2 * sizeof(uint32_t);
+    t = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(t) + 255) & ~(uintptr_t)255);
+    out.ccount = reinterpret_cast<uint32_t *>(t);  // 2 x 64 u32, within kListTail
     return ok();
 }
 
@@ -227,6 +247,181 @@ uint64_t call_tag(const adop_points *pts, int32_t n_views, const adop_camera *ca
     f.put(pts->normal);
     for (int v = 0; views && v < n_views; ++v) f.put(views[v].keys);
     return f.h | 1ull;
+}
+
+// ---- OpenCV8 image window in undistorted normalized coordinates (the candidate window test) ----
+// W = { n : |n|^2 <= r2_max, the distortion map d(n) of R6 lands in the pixel window (ulo, uhi) x (vlo, vhi) }.
+// Its bounding box [xlo, xhi] x [ylo, yhi] is found from W's boundary, which lies on the valid circle
+// |n|^2 = r2_max (sampled, kept where d(n) is in the window) and on the preimages of the window's four edges
+// (sampled, inverted by Newton's method, kept inside the disk); the box is widened by the largest distance
+// between consecutive boundary samples.  Every point whose exact projection lands in some layer satisfies
+// xlo Z <= X <= xhi Z, ylo Z <= Y <= yhi Z (the pixel window already holds a 2-pixel margin over the fp32
+// projection's rounding).  ok = false (no window test) if an edge point inside the distorted disk fails to
+// invert, or the camera has no finite valid radius.
+struct NormWindow {
+    double xlo, xhi, ylo, yhi;
+    bool ok;
+};
+
+static void distort_jac(const adop_camera &c, double xn, double yn, double &xd, double &yd, double J[2][2]) {
+    const double k1 = c.k[0], k2 = c.k[1], k3 = c.k[2], k4 = c.k[3], k5 = c.k[4], k6 = c.k[5];
+    const double p1 = c.p[0], p2 = c.p[1];
+    const double r2 = xn * xn + yn * yn;
+    const double num = 1.0 + r2 * (k1 + r2 * (k2 + r2 * k3)), den = 1.0 + r2 * (k4 + r2 * (k5 + r2 * k6));
+    const double rad = num / den;
+    const double dnum = k1 + r2 * (2.0 * k2 + 3.0 * r2 * k3), dden = k4 + r2 * (2.0 * k5 + 3.0 * r2 * k6);
+    const double drad = (dnum * den - num * dden) / (den * den);  // d rad / d r^2
+    xd = xn * rad + 2.0 * p1 * xn * yn + p2 * (r2 + 2.0 * xn * xn);
+    yd = yn * rad + p1 * (r2 + 2.0 * yn * yn) + 2.0 * p2 * xn * yn;
+    J[0][0] = rad + 2.0 * xn * xn * drad + 2.0 * p1 * yn + 6.0 * p2 * xn;
+    J[0][1] = 2.0 * xn * yn * drad + 2.0 * p1 * xn + 2.0 * p2 * yn;
+    J[1][0] = J[0][1];
+    J[1][1] = rad + 2.0 * yn * yn * drad + 6.0 * p1 * yn + 2.0 * p2 * xn;
+}
+
+// d(n) = q by damped Newton from (x, y); true if it converged (the result may lie outside the valid disk).
+static bool newton_inverse(const adop_camera &c, double qx, double qy, double R, double R2, double &x, double &y) {
+    for (int it = 0; it < 60; ++it) {
+        double xd, yd, J[2][2];
+        distort_jac(c, x, y, xd, yd, J);
+        const double rx = xd - qx, ry = yd - qy;
+        if (std::hypot(rx, ry) <= 1e-12 * (1.0 + std::hypot(qx, qy))) return true;
+        const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        if (!(std::fabs(det) > 1e-300)) return false;
+        double sx = (J[1][1] * rx - J[0][1] * ry) / det, sy = (-J[1][0] * rx + J[0][0] * ry) / det;
+        const double sn = std::hypot(sx, sy), lim = 0.25 * (1.0 + R);
+        if (sn > lim) {  // damped step
+            sx *= lim / sn;
+            sy *= lim / sn;
+        }
+        x -= sx;
+        y -= sy;
+        if (!(x * x + y * y <= 16.0 * R2)) return false;  // left the model's domain
+    }
+    return false;
+}
+
+static NormWindow compute_window(const adop_camera &c, double ulo, double uhi, double vlo, double vhi) {
+    NormWindow w{0, 0, 0, 0, false};
+    const double R2 = c.r2_max;
+    if (!(R2 > 0.0) || !std::isfinite(R2)) return w;
+    double ax = (ulo - c.cx) / c.fx, bx = (uhi - c.cx) / c.fx, ay = (vlo - c.cy) / c.fy, by = (vhi - c.cy) / c.fy;
+    if (ax > bx) std::swap(ax, bx);
+    if (ay > by) std::swap(ay, by);
+    double lo[2] = {INFINITY, INFINITY}, hi[2] = {-INFINITY, -INFINITY}, gap = 0.0;
+    auto add = [&](double x, double y) {
+        lo[0] = std::fmin(lo[0], x); hi[0] = std::fmax(hi[0], x);
+        lo[1] = std::fmin(lo[1], y); hi[1] = std::fmax(hi[1], y);
+    };
+    // the valid circle: kept where it maps into the window
+    const int NC = 4096;
+    const double R = std::sqrt(R2);
+    std::vector<double> cx(NC), cy(NC);  // the distorted circle, a closed polygon around the distorted disk
+    for (int i = 0; i < NC; ++i) {
+        const double th = 2.0 * M_PI * i / NC, x = R * std::cos(th), y = R * std::sin(th);
+        double xd, yd, J[2][2];
+        distort_jac(c, x, y, xd, yd, J);
+        cx[i] = xd;
+        cy[i] = yd;
+        if (xd >= ax && xd <= bx && yd >= ay && yd <= by) add(x, y);
+    }
+    // q inside the distorted disk (even-odd test against the polygon scaled by 1 + 1e-5 about the origin)
+    auto in_image_of_disk = [&](double qx, double qy) {
+        const double s = 1.0 / (1.0 + 1e-5);
+        qx *= s;
+        qy *= s;
+        bool in = false;
+        for (int i = 0, j = NC - 1; i < NC; j = i++)
+            if ((cy[i] > qy) != (cy[j] > qy) && qx < (cx[j] - cx[i]) * (qy - cy[i]) / (cy[j] - cy[i]) + cx[i]) in = !in;
+        return in;
+    };
+    gap = 2.0 * M_PI * R / NC;
+    // the window's edges, inverted point by point (continuation from the previous solution)
+    const int NE = 1024;
+    for (int e = 0; e < 4; ++e) {
+        double px = 0, py = 0;
+        bool prev = false;
+        for (int i = 0; i <= NE; ++i) {
+            const double t = (double)i / NE;
+            const double qx = e == 0 ? ax + t * (bx - ax) : (e == 1 ? ax + t * (bx - ax) : (e == 2 ? ax : bx));
+            const double qy = e == 0 ? ay : (e == 1 ? by : ay + t * (by - ay));
+            // Newton from the previous edge point's preimage, then (near the fold at the valid radius, where a
+            // second preimage outside the disk exists) from q itself and from points pulled towards the centre
+            double x = 0.0, y = 0.0;
+            bool conv = false;
+            for (int start = 0; start < 4 && !(conv && x * x + y * y <= R2 * (1.0 + 1e-3)); ++start) {
+                if (start == 0 && !prev) continue;
+                const double sc = start <= 1 ? 1.0 : (start == 2 ? 0.9 : 0.6);
+                x = start == 0 ? px : sc * qx;
+                y = start == 0 ? py : sc * qy;
+                conv = newton_inverse(c, qx, qy, R, R2, x, y);
+            }
+            // at the fold (the valid radius is where the radial map stops increasing) a window point just inside
+            // the distorted disk can have its inner preimage numerically indistinguishable from the outer one:
+            // an outer preimage within 1e-3 of the circle is taken, and the box widened by twice its distance
+            const double r2 = x * x + y * y;
+            const bool in = conv && r2 <= R2 * (1.0 + 1e-3);
+            if (in && r2 > R2) gap = std::fmax(gap, 2.0 * (std::sqrt(r2) - R));
+            if (in) {
+                add(x, y);
+                if (prev) gap = std::fmax(gap, std::hypot(x - px, y - py));
+                px = x;
+                py = y;
+            } else if (in_image_of_disk(qx, qy)) {
+                return w;  // inside the distorted disk but not inverted: no window test for this camera
+            }
+            prev = in;
+        }
+    }
+    if (!(lo[0] <= hi[0])) {  // nothing of the valid disk lands in the window: an empty window
+        w.xlo = w.ylo = 1.0;
+        w.xhi = w.yhi = -1.0;
+        w.ok = true;
+        return w;
+    }
+    const double m = 2.0 * gap + 1e-6;
+    w.xlo = lo[0] - m;
+    w.xhi = hi[0] + m;
+    w.ylo = lo[1] - m;
+    w.yhi = hi[1] + m;
+    w.ok = true;
+    return w;
+}
+
+// compute_window of a camera, cached by the camera's bytes and the window (refined intrinsics recompute it)
+static NormWindow camera_window(const adop_camera &c, float ulo, float uhi, float vlo, float vhi) {
+    struct Entry {
+        adop_camera cam;
+        float win[4];
+        NormWindow w;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    const float win[4] = {ulo, uhi, vlo, vhi};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (const Entry &e : cache)
+            if (!std::memcmp(&e.cam, &c, sizeof(c)) && !std::memcmp(e.win, win, sizeof(win))) return e.w;
+    }
+    const NormWindow w = compute_window(c, ulo, uhi, vlo, vhi);
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() >= 256) cache.erase(cache.begin());
+    cache.push_back(Entry{c, {ulo, uhi, vlo, vhi}, w});
+    return w;
+}
+
+// ADOP_WINDOW=0 disables the OpenCV8 window test (A/B measurements)
+static bool window_test_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = std::getenv("ADOP_WINDOW");
+        env = e ? std::atoi(e) : 1;
+    }
+    return env != 0;
+}
+
+bool vec_path(const adop_points *pts) {
+    return pts->n > 0 && aligned(pts->pos, 16) && pts->pos_stride % 4 == 0 && (!pts->radius || aligned(pts->radius, 16));
 }
 
 void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const adop_camera *cams,
@@ -281,6 +476,25 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         static_assert(2304 + ADOP_MAX_VIEWS_PER_LAUNCH * sizeof(LayerDesc) <= kHeaderBytes, "header layout");
         a.records = ws->records;
         a.rec_capacity = ws->capacity;
+        a.cview = ws->cview;
+        a.corder[0] = ws->corder0;
+        a.corder[1] = ws->corder1;
+        a.ccount = ws->ccount;
+        // per-view chunk lists for multi-view launches (the chunk slot index must fit 32 bits)
+        a.mv_lists = (n_views > 2 && vec_path(pts) && ws->capacity >= 64 * kListChunk &&
+                      ws->capacity < ((int64_t)1 << 32) - 256) ? 1 : 0;
+        {
+            // ADOP_MV_LISTS (A/B measurements): bit 0 lists on, bit 1 view-major texture consumer, bit 2
+            // view-major ghost consumer.  Default 5: the texture gradient keeps the lists' chunk order, in which
+            // a point's records of different views sit close together (its d_feat row is reused), while the
+            // blend and the ghost consumer gain more from one view's pixel state staying in L2.
+            static int env = -1;
+            if (env < 0) {
+                const char *e = std::getenv("ADOP_MV_LISTS");
+                env = e ? std::atoi(e) : 5;
+            }
+            a.mv_lists = (a.mv_lists && (env & 1)) ? (env & 7) : 0;
+        }
         a.tables = ws->tables;
         a.pose_partials = ws->partials;
     }
@@ -313,6 +527,18 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         d.uhi = (float)c.width + lmax + 2.0f;
         d.vlo = -lmax - 2.0f;
         d.vhi = (float)c.height + lmax + 2.0f;
+        d.wn_on = 0;
+        if (c.model == ADOP_OPENCV8 && window_test_enabled()) {
+            // OpenCV8: the image window in undistorted normalized coordinates (camera_window), widened by 1e-4
+            // relative so the fp32 test X <= xhi Z of the candidate path is conservative
+            const NormWindow w = camera_window(c, d.ulo, d.uhi, d.vlo, d.vhi);
+            if (w.ok) {
+                const double b[4] = {w.xlo, w.xhi, w.ylo, w.yhi};
+                for (int k = 0; k < 4; ++k)
+                    d.wn[k] = (float)(b[k] + (k & 1 ? 1.0 : -1.0) * 1e-4 * (1.0 + std::fabs(b[k])));
+                d.wn_on = 1;
+            }
+        }
         // Margin of the FMA-evaluated pre-cull: |Xf - Xp| <= 2^-20 (|x|+|y|+|z| + max|t|) for the FMA and
         // the pinned evaluations of R x + t (|R| <= 1); the pre-cull combinations add at most
         // (|f| + |c| + |bound|) times that plus their own rounding, so 2^-18 (...) is conservative.
@@ -342,7 +568,15 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
                 std::memcpy(nc, ncam, sizeof(ncam));
             } else if (!std::isinf(d.r2cull)) {
                 const double sr = std::sqrt((double)d.r2cull) * (1.0 + 1.0 / 1024.0);
-                const double ncam[4][3] = {{-1, 0, sr}, {1, 0, sr}, {0, -1, sr}, {0, 1, sr}};
+                // the valid cone |X|, |Y| <= sr Z, tightened to the image window in normalized coordinates
+                double xlo = -sr, xhi = sr, ylo = -sr, yhi = sr;
+                if (c.model == ADOP_OPENCV8 && d.wn_on) {
+                    xlo = std::fmax(xlo, (double)d.wn[0]);
+                    xhi = std::fmin(xhi, (double)d.wn[1]);
+                    ylo = std::fmax(ylo, (double)d.wn[2]);
+                    yhi = std::fmin(yhi, (double)d.wn[3]);
+                }
+                const double ncam[4][3] = {{1, 0, -xlo}, {-1, 0, xhi}, {0, 1, -ylo}, {0, -1, yhi}};
                 std::memcpy(nc, ncam, sizeof(ncam));
             } else {
                 for (int k = 0; k < 4; ++k) dc[k] = 1.0;  // no lateral bound
@@ -432,9 +666,6 @@ void encode_pos_tmap(RasterArgs &a, const adop_points *pts) {
     a.use_tmap = r == CUDA_SUCCESS ? 1 : 0;
 }
 
-bool vec_path(const adop_points *pts) {
-    return pts->n > 0 && aligned(pts->pos, 16) && pts->pos_stride % 4 == 0 && (!pts->radius || aligned(pts->radius, 16));
-}
 
 adop_status cuda_status(int err, const char *what) {
     if (err != cudaSuccess) return fail(ADOP_ERR_CUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)err));
@@ -490,8 +721,9 @@ adop_status adop_workspace_size(const adop_points *points, int32_t n_views, cons
     // worst case n*V*max(L, 2) (a ghost entry takes 2 slots) plus slack for partially filled per-warp chunks
     const int64_t per = params->layers > 2 ? params->layers : 2;
     int64_t cap = record_capacity >= 0 ? record_capacity : points->n * (int64_t)n_views * per + kRecordSlack;
+    const size_t nch = (size_t)((cap + kListChunk - 1) / kListChunk);
     *bytes = kHeaderBytes + kPartialBytes + table_bytes(n_views, cameras, params->layers, points->channels) +
-             (size_t)cap * sizeof(Record);
+             nch * kChunkBytes + kListTail;
     return ok();
 }
 
@@ -514,6 +746,10 @@ adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const
     if (points->n > 0) {
         e = launch_depth(a, model, vec_path(points), device_sms(), stream);
         if (e) return cuda_status(e, "depth launch");
+    }
+    if (a.mv_lists) {  // multi-view: the survivor chunks in view-major order (blend, and the backward's texture list)
+        e = launch_chunk_order(a, 0, device_sms(), stream);
+        if (e) return cuda_status(e, "chunk order launch");
     }
     return ok();
 }
@@ -639,6 +875,24 @@ adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *str
     int e = launch_tile_bounds(points->pos, points->pos + points->pos_stride, points->pos + 2 * points->pos_stride,
                                points->n, bounds, stream);
     if (e) return cuda_status(e, "tile bounds launch");
+    return ok();
+}
+
+adop_status adop_camera_window(const adop_camera *camera, int32_t layers, float out[4], int32_t *valid) {
+    if (!camera || !out || !valid) return fail(ADOP_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (layers < 1 || layers > ADOP_MAX_LAYERS) return fail(ADOP_ERR_INVALID_ARGUMENT, "bad layers");
+    adop_status st = check_camera(camera, 0, layers);
+    if (st) return st;
+    *valid = 0;
+    if (camera->model != ADOP_OPENCV8 || !window_test_enabled()) return ok();
+    // the same window and widening as fill_args
+    const float lmax = (float)(1 << (layers - 1));
+    const NormWindow w = camera_window(*camera, -lmax - 2.0f, (float)camera->width + lmax + 2.0f, -lmax - 2.0f,
+                                       (float)camera->height + lmax + 2.0f);
+    if (!w.ok) return ok();
+    const double b[4] = {w.xlo, w.xhi, w.ylo, w.yhi};
+    for (int k = 0; k < 4; ++k) out[k] = (float)(b[k] + (k & 1 ? 1.0 : -1.0) * 1e-4 * (1.0 + std::fabs(b[k])));
+    *valid = 1;
     return ok();
 }
 

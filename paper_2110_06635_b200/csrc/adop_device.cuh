@@ -89,6 +89,17 @@ __device__ __forceinline__ void to_camera(const ViewDesc &v, float x, float y, f
     Z = fadd(fadd(fadd(fmul(v.R[6], x), fmul(v.R[7], y)), fmul(v.R[8], z)), v.t[2]);
 }
 
+// OpenCV8 image window in undistorted normalized coordinates (ViewDesc::wn, computed and widened on the host):
+// false only if the pinned camera point (Z > 0) cannot land in any layer.
+__device__ __forceinline__ bool in_window(const ViewDesc &v, float X, float Y, float Z) {
+    return X >= v.wn[0] * Z && X <= v.wn[1] * Z && Y >= v.wn[2] * Z && Y <= v.wn[3] * Z;
+}
+// The same test on the FMA-evaluated point with the pre-cull margin m (|Xf - Xp|, |Zf - Zp| <= m).
+__device__ __forceinline__ bool in_window_fma(const ViewDesc &v, float X, float Y, float Z, float m) {
+    return X >= fmaf(v.wn[0], Z, -m * (1.0f + fabsf(v.wn[0]))) && X <= fmaf(v.wn[1], Z, m * (1.0f + fabsf(v.wn[1]))) &&
+           Y >= fmaf(v.wn[2], Z, -m * (1.0f + fabsf(v.wn[2]))) && Y <= fmaf(v.wn[3], Z, m * (1.0f + fabsf(v.wn[3])));
+}
+
 // Conservative, division-free frustum test (never rejects a point the exact
 // per-layer test would accept).  Z > z_near already holds.
 template <int MODEL>
@@ -100,6 +111,7 @@ __device__ __forceinline__ bool precull_pass(const ViewDesc &v, float X, float Y
         return su >= v.ulo * Z && su <= v.uhi * Z && sv >= v.vlo * Z && sv <= v.vhi * Z;
     } else {
         float r2z = fmaf(X, X, Y * Y);
+        if (MODEL == 1 && v.wn_on && !in_window(v, X, Y, Z)) return false;
         return r2z <= v.r2cull * (Z * Z);
     }
 }
@@ -124,6 +136,7 @@ __device__ __forceinline__ bool precull_fma(const ViewDesc &v, float x, float y,
     } else {
         // |Xp| >= |Xf| - m etc.: (|Xf|-m)+^2 + (|Yf|-m)+^2 <= r2cull (|Zf|+m)^2 is implied by the exact test
         const float ax = fmaxf(fabsf(X) - m, 0.0f), ay = fmaxf(fabsf(Y) - m, 0.0f), az = fabsf(Z) + m;
+        if (MODEL == 1 && v.wn_on && !in_window_fma(v, X, Y, Z, m)) return false;
         return Z >= -m && fmaf(ax, ax, ay * ay) <= v.r2cull * (az * az);
     }
 }
@@ -146,6 +159,7 @@ __device__ __forceinline__ bool precull_fma_z(const ViewDesc &v, float x, float 
         return fminf(fminf(d0, d1), fminf(d2, d3)) >= -m;
     } else {
         const float ax = fmaxf(fabsf(X) - m, 0.0f), ay = fmaxf(fabsf(Y) - m, 0.0f), az = fabsf(Z) + m;
+        if (MODEL == 1 && v.wn_on && !in_window_fma(v, X, Y, Z, m)) return false;
         return Z >= -m && fmaf(ax, ax, ay * ay) <= v.r2cull * (az * az);
     }
 }

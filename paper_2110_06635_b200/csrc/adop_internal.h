@@ -36,6 +36,8 @@ struct ViewDesc {
     float *accum, *count, *image;
     const float *grad;     // backward: dL/dI (image layout)
     const float *prow;     // backward pixel table: [P] rows of RasterArgs::prow floats (k_bwd_prep)
+    float wn[4];           // OpenCV8: image window in undistorted normalized coordinates (xlo, xhi, ylo, yhi):
+    int32_t wn_on;         // every point landing in some layer has xlo Z <= X <= xhi Z, ylo Z <= Y <= yhi Z
 };
 
 struct Record {  // one (point, view, layer) hit of the render set, 16 bytes
@@ -138,13 +140,24 @@ struct RasterArgs {
     float *d_pos;          // [3][n]
     uint8_t *mask;         // point-mask debug output [V][n]
     ViewDesc v[ADOP_MAX_VIEWS_PER_LAUNCH];
+    // Multi-view work lists (nviews > 2; appended after v[] so the fields above keep their offsets): the record
+    // region is cut into kListChunk-slot chunks, every chunk of the depth pass's survivor list and of the
+    // backward's ghost list holds ONE view's items, and the consumers walk the chunks in view-major order
+    // (k_chunk_hist / k_chunk_scatter), so one view's keys, accumulators and pixel tables stay in L2.
+    uint8_t *cview;        // [rec_capacity / kListChunk] view of each chunk (written when it is reserved)
+    uint32_t *corder[2];   // view-major chunk order of the front (survivor) and back (ghost) list
+    uint32_t *ccount;      // [2][64]: per-view chunk counts [0..16], cursors [32..48], total [63]
+    int32_t mv_lists;      // bit 0: the sweeps write per-view chunks (the blend walks them view-major);
+                           // bit 1: the texture consumer walks them view-major too; bit 2: the ghost consumer
 };
+constexpr int kListChunk = 64;  // record slots per chunk of the chunk table (a 64-aligned unit of every list)
 
 // Launchers (adop_kernels.cu).  Return cudaError_t as int.
 int launch_clear(const RasterArgs &a, int what, void *stream);  // 0 keys+header, 1 accum+count
 int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream);
 int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream);
 int launch_resolve(const RasterArgs &a, void *stream);
+int launch_chunk_order(const RasterArgs &a, int list, int sms, void *stream);  // multi-view lists (mv_lists)
 int launch_backward(const RasterArgs &a, int model, bool vec, int sms, int grid, double *d_pose, void *stream);
 int launch_masks(const RasterArgs &a, int model, void *stream);
 int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed first unless grad_accumulate)

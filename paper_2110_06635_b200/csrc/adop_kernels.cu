@@ -132,6 +132,8 @@ __device__ __forceinline__ void load_points(const RasterArgs &a, int64_t i0, flo
 #define ADOP_CHUNK 256
 #endif
 constexpr int kChunk = ADOP_CHUNK;  // record slots reserved per warp at a time (back list: kChunk / 2 ghost entries)
+static_assert(kChunk % kListChunk == 0, "list chunks are reserved in units of the chunk table's kListChunk slots");
+constexpr int kPoolLane = 31;  // multi-view lists: the lane holding the warp's pool of reserved list chunks (views <= 16)
 constexpr unsigned long long kFrontMask = (1ull << kResvBackShift) - 1ull;
 constexpr unsigned long long kNoSlot = ~0ull;
 
@@ -602,7 +604,68 @@ __device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, in
     c.left = kChunk;
 }
 
+// Multi-view lists (RasterArgs::mv_lists): every kListChunk-slot chunk of the survivor list holds one view's
+// records.  Lane w of the warp keeps view w's open chunk in c.base (the next free slot; a multiple of
+// kListChunk means no room left).  The lanes of ballot b (record `rec` each, view `vs`) append to their
+// views' chunks, one view at a time (a drain usually holds one or two views); a chunk that fills up is
+// continued in a fresh one, whose view is written to the chunk table.  Warp-collective.
+__device__ __forceinline__ void mv_put(const RasterArgs &a, RecChunk &c, unsigned b, bool hit, int vs, uint4 rec,
+                                       int lane, unsigned lt) {
+    unsigned pend = b;
+    while (pend) {
+        const int w = __shfl_sync(kFull, vs, __ffs(pend) - 1);
+        const unsigned grp = __ballot_sync(kFull, hit && vs == w);
+        const int cnt = __popc(grp);
+        const unsigned long long st = __shfl_sync(kFull, c.base, w);
+        const int used = (int)(st & (kListChunk - 1));
+        const int room = used ? kListChunk - used : 0;
+        unsigned long long nb = 0;
+        if (cnt > room) {  // a fresh list chunk from the warp's pool (lane kPoolLane), refilled kChunk slots at a time
+            unsigned long long pb = __shfl_sync(kFull, c.base, kPoolLane);
+            int pl = __shfl_sync(kFull, c.left, kPoolLane);
+            if (pl <= 0) {
+                if (lane == 0) pb = resv_take<false>(a, kChunk, true);
+                pb = __shfl_sync(kFull, pb, 0);
+                pl = pb == kNoSlot ? 0 : kChunk / kListChunk;
+            }
+            if (pl > 0) {
+                nb = pb;
+                pb += kListChunk;
+                --pl;
+                if (lane == 0) a.cview[nb / kListChunk] = (uint8_t)w;
+            } else {
+                nb = (unsigned long long)a.rec_capacity;  // region full: dropped (overflow is set)
+            }
+            if (lane == kPoolLane) {
+                c.base = pb;
+                c.left = pl;
+            }
+        }
+        if (hit && vs == w) {
+            const int off = __popc(grp & lt);
+            put_record(a, off < room ? st + off : nb + (off - room), rec);
+        }
+        if (lane == w) c.base = cnt <= room ? st + cnt : nb + (cnt - room);
+        pend &= ~grp;
+    }
+}
+
+// End of a multi-view sweep: lane w marks the rest of view w's open chunk dead; the pool lane marks its unused
+// chunks dead (their chunk-table entry: no view).
+__device__ __forceinline__ void mv_close(const RasterArgs &a, const RecChunk &c, int lane) {
+    if (lane == kPoolLane) {
+        for (int k = 0; k < c.left; ++k) {
+            const unsigned long long b = c.base + (unsigned long long)k * kListChunk;
+            a.cview[b / kListChunk] = 0xFF;
+            for (int j = 0; j < kListChunk; ++j) put_record(a, b + j, make_uint4(0u, 0u, 0u, kDeadView));
+        }
+        return;
+    }
+    for (unsigned long long s = c.base; (s & (kListChunk - 1)) != 0; ++s) put_record(a, s, make_uint4(0u, 0u, 0u, kDeadView));
+}
+
 // Layers of one kept point per lane (nk = 0: idle lane).  Warp-collective.
+template <bool MV>
 __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDesc &v, int vs, int nk, float u0,
                                              float v0, uint32_t zbits, uint32_t idx, RecChunk &c, int lane,
                                              unsigned lt) {
@@ -629,6 +692,10 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
         }
         const int nb = __popc(b);
         CNT(4, nb);
+        if (MV && a.mv_lists) {
+            mv_put(a, c, b, hit, vs, make_uint4(pix, zbits, idx, (uint32_t)vs), lane, lt);
+            continue;
+        }
         if (nb > c.left) rec_reserve(a, c, lane, true);
         if (hit) put_record(a, c.base + __popc(b & lt), make_uint4(pix, zbits, idx, (uint32_t)vs));
         c.base += nb;
@@ -637,6 +704,7 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
 }
 
 // Process `cnt` (<= 32) entries from the top of the queue, one per lane (each with its own view slot).
+template <bool MV>
 #if ADOP_DRAIN_NOINLINE
 __device__ __noinline__
 #else
@@ -654,7 +722,7 @@ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int 
     }
     __syncwarp();
     qn -= cnt;
-    depth_layers(a, ld[vs], vs, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
+    depth_layers<MV>(a, ld[vs], vs, nk, e.x, e.y, __float_as_uint(e.z), __float_as_uint(e.w), c, lane, lt);
 }
 
 // Candidate part for one point and view: pinned Xc = R x + t (R1), validity (R7), exact discard (Eq. 12,
@@ -664,16 +732,35 @@ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int 
 // are dropped before the queue (configs[4]: a quarter of the kept point-views; with distortion the pre-cull
 // planes bound the whole valid cone, well beyond the image).  On the single-view pinhole headline the extra
 // compares cost more than the few out-of-image points they save.
-template <int MODEL, bool PRECHECK>
+template <int MODEL, bool PRECHECK, bool MV>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
                                                 float y, float z, float rw, int64_t i, uint32_t gi, const LayerDesc *ld,
                                                 WarpQueue &q, int &qn, RecChunk &c, int lane, unsigned lt) {
     Proj p;
     int nk = 0;
+#if ADOP_COUNTERS
+    bool c_valid = false, c_proj = false;
+#endif
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (depth_valid<MODEL>(p, a.z_near) && normal_keep(a, v, i, p.X, p.Y, p.Z)) nk = keep_layers(a, v, rw, p.iz, gi);
+        if (depth_valid<MODEL>(p, a.z_near) && (MODEL != 1 || !v.wn_on || in_window(v, p.X, p.Y, p.Z)) &&
+            normal_keep(a, v, i, p.X, p.Y, p.Z)) {
+            nk = keep_layers(a, v, rw, p.iz, gi);
+#if ADOP_COUNTERS
+            c_valid = true;
+#endif
+        }
     }
+#if ADOP_COUNTERS
+    {  // (ballots outside CNT: its argument is evaluated by lane 0 only)
+        const unsigned b_valid = __ballot_sync(kFull, c_valid), b_disc = __ballot_sync(kFull, nk > 0);
+        if (nk > 0) c_proj = project_uv<MODEL>(v, p);
+        const unsigned b_proj = __ballot_sync(kFull, c_proj);
+        CNT(5, __popc(b_valid));
+        CNT(6, __popc(b_disc));
+        CNT(7, __popc(b_proj));
+    }
+#endif
     if (nk > 0 && !(project_uv<MODEL>(v, p) && (!PRECHECK || any_layer_in_bounds(v, p, nk)))) nk = 0;
     const unsigned b = __ballot_sync(kFull, nk > 0);
     if (b == 0u) return;
@@ -684,7 +771,7 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     }
     qn += __popc(b);
     CNT(3, __popc(b));
-    if (qn >= 32) drain(a, ld, q, qn, 32, c, lane, lt);
+    if (qn >= 32) drain<MV>(a, ld, q, qn, 32, c, lane, lt);
 }
 
 
@@ -853,7 +940,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
             const bool ok = i0 + lane < cn;
             const int e = ok ? cl[i0 + lane] : 0;
             const float rw = staged_r ? rows[3][e] : a.radius_uniform;
-            depth_candidate<MODEL, VM != 0 || MODEL != 0>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
+            depth_candidate<MODEL, VM != 0 || MODEL != 0, VM == 2>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
                                    a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
         }
         __syncwarp();  // the list is rewritten by the next view / tile
@@ -1018,8 +1105,11 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
         issue(st);
         __syncwarp();
     }
-    if (qn > 0) drain(a, a.ldesc, q, qn, qn, c, lane, lt);
-    rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
+    if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
+    if (VM == 2 && a.mv_lists)
+        mv_close(a, c, lane);        // lane w: the rest of view w's chunk
+    else
+        rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
 }
 
 // Shared-pyramid reset (adop_clear_pyramid): keys <- sentinel, accum / count <- 0.
@@ -1089,21 +1179,112 @@ int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n
 // HOCC: 6 blocks per SM (40 registers; the overflow fallback spills, it is the slow path anyway) -- one
 // view: blend phase 63 -> 58 us on configs[3]; with 16 views (configs[4]) the extra concurrency thrashes
 // L2 (forward 4.73 -> 5.17 ms), so multi-view launches keep 4 blocks per SM.
+// ---- view-major order of a multi-view list's chunks (list 0: survivor records, 1: ghost entries) ----
+// Chunk range of a list in the chunk table: the front list [0, front_ok) grows from slot 0, the back list
+// [capacity - back_ok, capacity) from the top; both consist of whole kListChunk-slot chunks.
+__device__ __forceinline__ void list_chunks(const RasterArgs &a, int list, unsigned long long &c0,
+                                            unsigned long long &c1) {
+    const unsigned long long cap = (unsigned long long)a.rec_capacity;
+    if (list == 0) {
+        c0 = 0;
+        c1 = *(volatile unsigned long long *)&a.hdr->front_ok / kListChunk;
+    } else {
+        c1 = cap / kListChunk;
+        c0 = (cap - *(volatile unsigned long long *)&a.hdr->back_ok) / kListChunk;
+    }
+}
+__device__ __forceinline__ int chunk_bucket(const RasterArgs &a, unsigned long long c) {
+    const unsigned v = a.cview[c];
+    return v < (unsigned)a.nviews ? (int)v : ADOP_MAX_VIEWS_PER_LAUNCH;  // 16: not a per-view chunk
+}
+// Per-view chunk counts (ccount[list][0..16], zeroed by the launcher).
+__global__ void __launch_bounds__(kThreads) k_chunk_hist(const __grid_constant__ RasterArgs a, int list) {
+    __shared__ unsigned h[ADOP_MAX_VIEWS_PER_LAUNCH + 1];
+    if (threadIdx.x <= ADOP_MAX_VIEWS_PER_LAUNCH) h[threadIdx.x] = 0u;
+    __syncthreads();
+    unsigned long long c0, c1;
+    list_chunks(a, list, c0, c1);
+    for (unsigned long long c = c0 + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; c < c1;
+         c += (unsigned long long)gridDim.x * blockDim.x)
+        atomicAdd(&h[chunk_bucket(a, c)], 1u);
+    __syncthreads();
+    if (threadIdx.x <= ADOP_MAX_VIEWS_PER_LAUNCH && h[threadIdx.x])
+        atomicAdd(&a.ccount[list * 64 + threadIdx.x], h[threadIdx.x]);
+}
+// Scatter every chunk index to its view's segment of corder[list] (segments in view order; the order inside a
+// segment is arbitrary -- the consumers' results do not depend on it beyond fp32 summation order).
+__global__ void __launch_bounds__(kThreads) k_chunk_scatter(const __grid_constant__ RasterArgs a, int list) {
+    constexpr int NB = ADOP_MAX_VIEWS_PER_LAUNCH + 1;
+    __shared__ unsigned start[NB], h[NB], base[NB];
+    unsigned *cnt = a.ccount + list * 64;
+    if (threadIdx.x == 0) {
+        unsigned s0 = 0;
+        for (int b = 0; b < NB; ++b) {
+            start[b] = s0;
+            s0 += cnt[b];
+        }
+    }
+    unsigned long long c0, c1;
+    list_chunks(a, list, c0, c1);
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    for (unsigned long long r0 = c0 + (unsigned long long)blockIdx.x * blockDim.x; r0 < c1; r0 += stride) {
+        if (threadIdx.x < NB) h[threadIdx.x] = 0u;
+        __syncthreads();
+        const unsigned long long c = r0 + threadIdx.x;
+        int bk = -1;
+        unsigned rank = 0u;
+        if (c < c1) {
+            bk = chunk_bucket(a, c);
+            rank = atomicAdd(&h[bk], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < NB && h[threadIdx.x]) base[threadIdx.x] = atomicAdd(&cnt[32 + threadIdx.x], h[threadIdx.x]);
+        __syncthreads();
+        if (bk >= 0) a.corder[list][start[bk] + base[bk] + rank] = (uint32_t)c;
+        __syncthreads();
+    }
+}
+
+// Visit the slots of a multi-view list in view-major chunk order: warp w takes ordered chunks w, w + W, ...
+// (so the chunks in flight at any time are a narrow window of the order, mostly one view), lane k of the warp
+// takes items k, k + 32, ... of the chunk, STEP slots per item (STEP = 2 for ghost entries: one entry per lane).
+template <int STEP, typename F>
+__device__ __forceinline__ void for_ordered(const RasterArgs &a, int list, F &&f) {
+    unsigned long long c0, c1;
+    list_chunks(a, list, c0, c1);
+    const unsigned long long nch = c1 - c0;
+    const unsigned long long W = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (unsigned long long j = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nch; j += W) {
+        const unsigned long long base = (unsigned long long)a.corder[list][j] * kListChunk;
+#pragma unroll
+        for (int k = 0; k < kListChunk / (32 * STEP); ++k) f(base + (unsigned long long)STEP * (k * 32 + lane));
+    }
+}
+
+template <bool VEC4>
+__device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long long r) {
+    const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
+    if (rec.w == kDeadView) return;
+    const ViewDesc &v = a.v[rec.w];
+    const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
+    if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
+}
+
 template <int MODEL, bool VEC, bool VEC4, bool HOCC>
 __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_constant__ RasterArgs a) {
     if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
         stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
         return;
     }
+    if (a.mv_lists) {  // multi-view: the survivor chunks view by view (keys and accumulators stay in L2)
+        for_ordered<1>(a, 0, [&](unsigned long long r) { blend_record<VEC4>(a, r); });
+        return;
+    }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
-        const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
-        if (rec.w == kDeadView) continue;
-        const ViewDesc &v = a.v[rec.w];
-        const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
-        if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
-    }
+    for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride)
+        blend_record<VEC4>(a, r);
 }
 
 // Environment-map background of channels c0..c0+3 at layer-l pixel j (NEXT-2, R29).
@@ -1691,6 +1872,58 @@ __device__ __forceinline__ unsigned long long list_take(const RasterArgs &a, Lis
     return mine ? slot : kNoSlot;
 }
 
+// Multi-view ghost list (RasterArgs::mv_lists): like mv_put for the back list -- lane vs keeps view vs's open
+// chunk in c.base (next free slot; 2 slots per ghost entry); all items of a call share the warp-uniform view
+// slot vs.  Returns the lane's slot or kNoSlot (region full: processed inline).  Warp-collective.
+__device__ __forceinline__ unsigned long long mv_take_back(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
+                                                           int vs, int lane, unsigned lt) {
+    const int nb = __popc(b);
+    const unsigned long long st = __shfl_sync(kFull, c.base, vs);
+    const int used = (int)(st & (kListChunk - 1));
+    const int room = used ? (kListChunk - used) / 2 : 0;
+    unsigned long long nbase = 0;
+    if (nb > room) {  // a fresh list chunk from the warp's pool (lane kPoolLane), refilled one back reservation at a time
+        unsigned long long pb = __shfl_sync(kFull, c.base, kPoolLane);
+        int pl = __shfl_sync(kFull, c.left, kPoolLane);
+        if (pl <= 0) {
+            if (lane == 0) pb = resv_take<true>(a, kChunk, false);
+            pb = __shfl_sync(kFull, pb, 0);
+            pl = pb == kNoSlot ? 0 : kChunk / kListChunk;
+        }
+        if (pl > 0) {
+            nbase = pb;
+            pb += kListChunk;
+            --pl;
+            if (lane == 0) a.cview[nbase / kListChunk] = (uint8_t)vs;
+        } else {
+            nbase = kNoSlot;  // region full: the items are processed inline
+        }
+        if (lane == kPoolLane) {
+            c.base = pb;
+            c.left = pl;
+        }
+    }
+    const int off = __popc(b & lt);
+    const unsigned long long slot =
+        off < room ? st + 2ull * off : (nbase == kNoSlot ? kNoSlot : nbase + 2ull * (off - room));
+    if (lane == vs) c.base = nb <= room ? st + 2ull * nb : (nbase == kNoSlot ? 0ull : nbase + 2ull * (nb - room));
+    return mine ? slot : kNoSlot;
+}
+
+// End of a multi-view backward sweep: lane w marks the rest of view w's ghost chunk dead.
+__device__ __forceinline__ void mv_close_back(const RasterArgs &a, const ListChunk &c, int lane) {
+    uint4 *r = reinterpret_cast<uint4 *>(a.records);
+    if (lane == kPoolLane) {
+        for (int k = 0; k < c.left; ++k) {
+            const unsigned long long b = c.base + (unsigned long long)k * kListChunk;
+            a.cview[b / kListChunk] = 0xFF;
+            for (int j = 0; j < kListChunk; j += 2) r[b + j + 1] = make_uint4(0u, 0u, kDead, kDead);
+        }
+        return;
+    }
+    for (unsigned long long s = c.base; (s & (kListChunk - 1)) != 0; s += 2) r[s + 1] = make_uint4(0u, 0u, kDead, kDead);
+}
+
 __device__ __forceinline__ void red_add_row(float *dst, const float *src, int C, float scale) {
     if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
         for (int c = 0; c < C; c += 4) {
@@ -1799,7 +2032,7 @@ __device__ __forceinline__ void ghost_inline(const RasterArgs &a, const ViewDesc
 
 // Sweep candidate: exact projection and discard, then emit the rendered hits to the texture list (mode 0
 // only) and the ghost to the ghost list (inline processing when the region is full).  Warp-collective.
-template <int MODEL, int CT>
+template <int MODEL, int CT, bool MV>
 __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, bool ghost, float x,
                                          float y, float z, float rw, int64_t i, uint32_t gi, ListChunk &ct,
                                          ListChunk &cg, bool tex_on, int lane, unsigned lt) {
@@ -1807,7 +2040,8 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     int nk = 0;
     if (ok) {
         to_camera(v, x, y, z, p.X, p.Y, p.Z);
-        if (depth_valid<MODEL>(p, a.z_near) && normal_keep(a, v, i, p.X, p.Y, p.Z)) {
+        if (depth_valid<MODEL>(p, a.z_near) && (MODEL != 1 || !v.wn_on || in_window(v, p.X, p.Y, p.Z)) &&
+            normal_keep(a, v, i, p.X, p.Y, p.Z)) {
             nk = keep_layers(a, v, rw, p.iz, gi);
             if (nk > 0 && !(project_uv<MODEL>(v, p) && any_layer_in_bounds(v, p, nk))) nk = 0;  // R14: no term
         }
@@ -1838,7 +2072,8 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
     const bool gh = nk > 0 && (a.spatial_rendered ? !ghost : ghost);  // spatial-gradient list (R22 / R31)
     const unsigned bg = __ballot_sync(kFull, gh);
     if (bg == 0u) return;
-    const unsigned long long slot = list_take<true>(a, cg, bg, gh, lane, lt);
+    const unsigned long long slot = (MV && a.mv_lists) ? mv_take_back(a, cg, bg, gh, vs, lane, lt)
+                                                       : list_take<true>(a, cg, bg, gh, lane, lt);
     if (!gh) return;
     if (slot != kNoSlot) {  // GhostEntry
         uint4 *r = reinterpret_cast<uint4 *>(a.records) + slot;
@@ -1852,6 +2087,13 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
 // texture list consumer: one thread per hit (balanced), vector reductions into d_feat.
 __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
     const uint4 *list = reinterpret_cast<const uint4 *>(a.records);
+    if ((a.mv_lists & 2) && *(volatile int32_t *)&a.hdr->mode == 1) {  // the forward's per-view chunks, view by view
+        for_ordered<1>(a, 0, [&](unsigned long long r) {
+            const uint4 e = __ldcs(list + r);
+            if (e.w != kDead) tex_hit(a, a.v[e.w], e.x, __uint_as_float(e.y), (int64_t)e.z);
+        });
+        return;
+    }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
@@ -1870,21 +2112,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < kWarps * ADOP_MAX_VIEWS_PER_LAUNCH * NT; t += blockDim.x) (&wpose[0][0])[t] = 0.0;
     __syncthreads();
-    // the sweep's ghost list: the back of the record region
-    const unsigned long long back = *(volatile unsigned long long *)&a.hdr->back_ok;
-    const uint4 *list = reinterpret_cast<const uint4 *>(a.records) + ((unsigned long long)a.rec_capacity - back);
-    const unsigned long long total = back / 2;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x; r0 < total; r0 += stride) {
-        const unsigned long long r = r0 + threadIdx.x;
+    // one ghost entry per lane (ent = NULL: none), then the warp's fp64 reduction per distinct view present
+    // (usually one: with multi-view lists every chunk holds one view).  Warp-collective.
+    auto entry = [&](const uint4 *ent) {
         double t6[NT];
 #pragma unroll
         for (int k = 0; k < NT; ++k) t6[k] = 0.0;
         int vs = -1;
-        if (r < total) {
-            const uint4 e1 = __ldcs(list + 2 * r + 1);
+        if (ent) {
+            const uint4 e1 = __ldcs(ent + 1);
             if (e1.z != kDead) {
-                const uint4 e0 = __ldcs(list + 2 * r);
+                const uint4 e0 = __ldcs(ent);
                 vs = (int)(e1.z & 0xFF);
                 const int nk = (int)(e1.z >> 8);
                 const ViewDesc &v = a.v[vs];
@@ -1899,7 +2137,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
                 if (!ghost_point<MODEL, CT>(a, v, p, nk, (int64_t)e1.y, NT, t6)) vs = -1;
             }
         }
-        // warp reduction per distinct view present in the warp (usually one)
         unsigned pending = __ballot_sync(kFull, vs >= 0);
         while (pending) {
             const int leader = __ffs(pending) - 1;
@@ -1911,6 +2148,19 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
                 if (lane == 0) wpose[wid][vv * NT + k] += sum;
             }
             pending &= ~__ballot_sync(kFull, mine);
+        }
+    };
+    const uint4 *rec = reinterpret_cast<const uint4 *>(a.records);
+    if (a.mv_lists & 4) {  // the per-view ghost chunks, view by view (one view's pixel tables stay in L2)
+        for_ordered<2>(a, 1, [&](unsigned long long slot) { entry(rec + slot); });
+    } else {  // the sweep's ghost list: the back of the record region
+        const unsigned long long back = *(volatile unsigned long long *)&a.hdr->back_ok;
+        const uint4 *list = rec + ((unsigned long long)a.rec_capacity - back);
+        const unsigned long long total = back / 2;
+        const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+        for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x; r0 < total; r0 += stride) {
+            const unsigned long long r = r0 + threadIdx.x;
+            entry(r < total ? list + 2 * r : nullptr);
         }
     }
     __syncthreads();
@@ -2049,7 +2299,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                         bool cand = in && precull_fma_z<MODEL>(v, x, y, z, Zf, mz);
                         if (a.discard) cand = cand && maybe_kept(a, v, rw, Zf, mz, gi);
                         if (__any_sync(kFull, cand))
-                            bwd_emit<MODEL, CT>(a, v, vs, cand, !a.spatial_rendered, x, y, z, rw, base + e, gi, ct, cg,
+                            bwd_emit<MODEL, CT, MV>(a, v, vs, cand, !a.spatial_rendered, x, y, z, rw, base + e, gi, ct, cg,
                                                 false, lane, lt);
                     }
                 }
@@ -2093,7 +2343,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                 m &= m - 1u;
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const float rw = staged_r ? rp[3][e] : a.radius_uniform;
-                bwd_emit<MODEL, CT>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
+                bwd_emit<MODEL, CT, MV>(a, v, vs, ok, (ghosts >> j) & 1u, rp[0][e], rp[1][e], rp[2][e], rw, base + e,
                                     a.goff + (uint32_t)(base + e), ct, cg, tex_on, lane, lt);
             }
         }
@@ -2102,7 +2352,10 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         __syncwarp();
     }
     list_close<false>(a, ct, lane);
-    list_close<true>(a, cg, lane);
+    if (MV && a.mv_lists)
+        mv_close_back(a, cg, lane);
+    else
+        list_close<true>(a, cg, lane);
 }
 
 // Column t = view * nt + j of the per-block partials, summed over blocks in a fixed order (deterministic):
@@ -2233,6 +2486,16 @@ int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream
     }
     if (vec) return v4 ? launch_blend_t<1, true, true>(a, sms, stream) : launch_blend_t<1, true, false>(a, sms, stream);
     return v4 ? launch_blend_t<1, false, true>(a, sms, stream) : launch_blend_t<1, false, false>(a, sms, stream);
+}
+
+// View-major order of list 0 (survivor records) or 1 (ghost entries) of a multi-view launch.
+int launch_chunk_order(const RasterArgs &a, int list, int sms, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    int e = (int)cudaMemsetAsync(a.ccount + list * 64, 0, 64 * sizeof(uint32_t), s);
+    if (e) return e;
+    k_chunk_hist<<<sms, kThreads, 0, s>>>(a, list);
+    k_chunk_scatter<<<sms, kThreads, 0, s>>>(a, list);
+    return (int)cudaGetLastError();
 }
 
 int launch_resolve(const RasterArgs &a, void *stream) {
@@ -2382,6 +2645,10 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
             if (g < 1) g = 1;
             k<<<(unsigned)g, kST, sizeof(BwdSmem), s>>>(b);
         }
+    }
+    if (b.mv_lists) {  // the ghost list's per-view chunks in view-major order
+        int e = launch_chunk_order(b, 1, sms, stream);
+        if (e) return e;
     }
     // the two list consumers are independent (d_feat from the texture list; d_pos and the pose / intrinsics
     // partials from the ghost list) and both latency-bound: the texture kernel runs on a side stream forked

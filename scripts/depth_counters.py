@@ -23,8 +23,11 @@ L.adop_debug_depth_counts(out, 1)
 r.forward()
 torch.cuda.synchronize()
 L.adop_debug_depth_counts(out, 1)
-tiles, vt, cand, kept, hits = list(out)[:5]
+tiles, vt, cand, kept, hits, valid, disc, proj = list(out)[:8]
 print(f"configs[{cfg}]: {len(w.cameras)} views")
 print(f"tiles {tiles:,}  box-visible view-tiles {vt:,} ({100 * vt / max(tiles, 1):.1f}%)")
 print(f"candidates {cand:,} ({cand / max(vt, 1):.1f} per visible tile)  kept {kept:,} ({100 * kept / max(cand, 1):.1f}% "
       f"of candidates)  layer hits {hits:,} ({hits / max(kept, 1):.2f} per kept)")
+print(f"of the candidates: valid depth {valid:,} ({100 * valid / max(cand, 1):.1f}%), kept by the exact discard {disc:,} "
+      f"({100 * disc / max(cand, 1):.1f}%), inside the camera's valid radius {proj:,} ({100 * proj / max(cand, 1):.1f}%), "
+      f"in the image at some kept layer {kept:,} ({100 * kept / max(cand, 1):.1f}%)")

@@ -43,13 +43,14 @@ def test_pyramid_pixels_and_workspace_size():
     assert A.lib().adop_workspace_size(C.byref(pts), 2, cams, C.byref(prm), -1, C.byref(sz)) == 0
     P = A.pyramid_pixels(64, 32, 5)
     tables = -(-2 * P * (16 + 4 * 4) // 256) * 256  # rows of 16 + 4 roundup4(C) bytes
-    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables + (1000 * 2 * 5 + (1 << 20)) * 16
+    rec = lambda cap: -(-cap // 64) * (64 * 16 + 1 + 8) + 1024  # 64-slot chunks + chunk tables (include/adop.h)
+    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables + rec(1000 * 2 * 5 + (1 << 20))
     assert A.lib().adop_workspace_size(C.byref(pts), 2, cams, C.byref(prm), 100, C.byref(sz)) == 0
-    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables + 100 * 16
+    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables + rec(100)
     prm.layers = 1  # a ghost entry takes 2 slots: worst case n * V * max(L, 2)
     assert A.lib().adop_workspace_size(C.byref(pts), 2, cams, C.byref(prm), -1, C.byref(sz)) == 0
     tables1 = -(-2 * A.pyramid_pixels(64, 32, 1) * 32 // 256) * 256
-    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables1 + (1000 * 2 * 2 + (1 << 20)) * 16
+    assert sz.value == 4096 + 2048 * 16 * 18 * 8 + tables1 + rec(1000 * 2 * 2 + (1 << 20))
     prm.layers = 5
     assert A.lib().adop_workspace_size(C.byref(pts), 0, cams, C.byref(prm), -1, C.byref(sz)) == 1
     assert A.lib().adop_workspace_size(C.byref(pts), 2, None, C.byref(prm), -1, C.byref(sz)) == 1
