@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <atomic>
+#include <cstdlib>
 
 #include "adop_device.cuh"
 
@@ -408,6 +409,7 @@ __device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i
 struct DepthSmem {
     float pos[kDStages][kSW][4][kWTile];  // stage, warp, row (x, y, z, r_world), point of the warp tile
     uint64_t bar[kSW][kDStages];          // per-warp TMA completion barriers
+    uint64_t rbar[kSW][kDStages];         // per-warp barriers of the lazily loaded r_world row (kLazyR)
     int tile[kSW][kDStages];              // tile claimed into each stage (dynamic claiming / tile culling)
     uint32_t tviews[kSW][kDStages];       // tile culling: views whose frustum meets the tile's bounds
     WarpQueue q[kSW];
@@ -840,12 +842,34 @@ __device__ __forceinline__ bool maybe_kept(const RasterArgs &a, const ViewDesc &
     return !(zl > 0.0f) || r * r * 1.002f > om;
 }
 
+// Lazily loaded r_world row (kLazyR): the x, y, z rows of a warp tile are streamed for every tile, the r_world
+// row only for a tile that some view's box test keeps (21% of the tiles on configs[3]; r_world is only read
+// by the discard test of Eq. 12).  ensure_r issues its 1 KB bulk copy into the stage's row 3 and waits for it.
+#ifndef ADOP_LAZY_R
+#define ADOP_LAZY_R 0  // measured: no gain on configs[3] (0.3225 vs 0.3210 ms depth), slower tile culling
+#endif
+constexpr bool kLazyR = ADOP_LAZY_R;
+struct LazyR {
+    uint32_t bar, dst;  // the stage's r barrier and row-3 shared-memory address
+    const float *src;   // global r_world of the tile, or nullptr when row 3 already holds it
+    uint32_t parity;
+};
+__device__ __forceinline__ void ensure_r(LazyR &r, int lane) {
+    if (!r.src) return;
+    if (lane == 0) {
+        mbar_expect_tx_a(r.bar, kWTile * sizeof(float));
+        bulk_g2s_a(r.dst, r.src, kWTile * sizeof(float), r.bar, policy_evict_first());
+    }
+    mbar_wait_a(r.bar, r.parity);
+    r.src = nullptr;
+}
+
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
 template <int MODEL, int VM, bool DISC>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
-                                            uint8_t *cl, int lane, unsigned lt, uint32_t pre_views) {
+                                            uint8_t *cl, int lane, unsigned lt, uint32_t pre_views, LazyR &lr) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     // ghosts take no part in the depth test (§4.3): their mask is hashed at the tile's first visible view
     uint32_t live = (uint32_t)vmask;
@@ -861,6 +885,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         const bool lane_out = box_culled(v, box);
         if (__all_sync(kFull, lane_out)) continue;  // every lane's box is outside (warp-uniform)
         CNT(1, 1);
+        if (kLazyR && staged_r) ensure_r(lr, lane);
         uint32_t m = 0u;
         // DISC = stochastic discarding on (a separate instance: each keeps only the code it runs)
         if (kPrefilter && DISC && (MODEL != 2 || v.zplane)) {
@@ -962,15 +987,20 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     const bool dyn = a.dyn_tiles & 1;
     const bool tcull = a.tbounds != nullptr;  // the claimed tile goes through shared memory (sm.tile)
     if (lane == 0) {
-        for (int st = 0; st < kDStages; ++st) mbar_init(&sm.bar[wid][st], 1);
+        for (int st = 0; st < kDStages; ++st) {
+            mbar_init(&sm.bar[wid][st], 1);
+            mbar_init(&sm.rbar[wid][st], 1);
+        }
         fence_mbar_init();
     }
     __syncwarp();
     // per-warp constants of the issue path: shared-window addresses, L2 policy, tile sequence
     constexpr uint32_t kStageBytes = sizeof(sm.pos[0]), kRowBytes = kWTile * sizeof(float);
     const uint32_t bar_s = smem_addr(&sm.bar[wid][0]);
+    const uint32_t rbar_s = smem_addr(&sm.rbar[wid][0]);
     const uint32_t pos_s = smem_addr(&sm.pos[0][wid][0][0]);
-    const uint32_t txb = (uint32_t)rows * kRowBytes;
+    const int streamed = kLazyR ? 3 : rows;  // rows every tile streams (r_world lazily with kLazyR)
+    const uint32_t txb = (uint32_t)streamed * kRowBytes;
     const uint64_t pol = policy_evict_first();
     const int stride = (int)gridDim.x * kSW;
     int t_next = (int)blockIdx.x * kSW + wid;  // static order: warp w takes tiles w, w + W, ...
@@ -1053,7 +1083,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
                     bulk_g2s_a(dst + r * kRowBytes, src + (int64_t)t * kWTile, kRowBytes, bar, pol);
                 }
             }
-            if (rows == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
+            if (streamed == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
         }
     };
     for (int st = 0; st < kDStages; ++st) issue(st);
@@ -1067,7 +1097,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
     c.has = false;
     c.pend = 0;
 #endif
-    uint32_t phase = 0u;
+    uint32_t phase = 0u, rphase = 0u;
     int t_cons = (int)blockIdx.x * kSW + wid;
     for (int st = 0;; st = st + 1 == kDStages ? 0 : st + 1) {
         int t;
@@ -1100,7 +1130,15 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
             __syncwarp();
         }
         CNT(0, 1);
-        depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views);
+        LazyR lr;
+        lr.bar = rbar_s + 8u * st;
+        lr.dst = pos_s + kStageBytes * st + 3 * kRowBytes;
+        lr.src = (kLazyR && staged_r && t < nfull) ? a.radius + base : nullptr;  // (a ragged tile loaded row 3)
+        lr.parity = (rphase >> st) & 1u;
+        const bool r_pending = lr.src != nullptr;
+        depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, pre_views,
+                                     lr);
+        if (r_pending && !lr.src) rphase ^= 1u << st;
         __syncwarp();  // every lane is done with stage st
         issue(st);
         __syncwarp();
@@ -1110,6 +1148,123 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
         mv_close(a, c, lane);        // lane w: the rest of view w's chunk
     else
         rec_reserve(a, c, lane, false);  // mark this warp's unused slots dead
+}
+
+// --------------------------------------------------------------------------- //
+// depth pass with a CTA-wide pool of stages (launches without tile culling or dynamic claiming): the CTA's k-th
+// warp tile is tile k G + b (G CTAs; all CTAs sweep the cloud as one
+// front) and lands in stage k mod kPool.  A warp claims the next k of its CTA, waits for that stage, processes
+// the tile and refills the stage with tile k + kPool.  Unlike the per-warp rings, a loaded stage never waits
+// for a particular warp: a warp busy with a visible tile holds one stage, every other loaded stage goes to the
+// next free warp (the per-warp rings left the busy warp's prefetched tile idle).
+// --------------------------------------------------------------------------- //
+constexpr int kPool = 2 * kSW;
+struct PoolSmem {
+    float pos[kPool][4][kWTile];
+    uint64_t bar[kPool];
+    int filled[kPool];  // the k whose copy into the stage was issued last (phase-unambiguous waits)
+    int next;
+    WarpQueue q[kSW];
+    uint8_t cand[kSW][kWTile];
+};
+static_assert(sizeof(PoolSmem) + 1024 <= 228 * 1024 / kDCTAs, "pooled depth sweep: kDCTAs CTAs per SM must fit");
+
+template <int MODEL, int VM, bool DISC>
+__global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constant__ RasterArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    const int ntiles = a.ntiles, nfull = a.nfull;
+    const bool staged_r = a.discard && a.radius != nullptr;
+    const int rows = staged_r ? 4 : 3;
+    const int G = (int)gridDim.x, b = (int)blockIdx.x;
+    if (tid < kPool) {
+        mbar_init(&sm.bar[tid], 1);
+        sm.filled[tid] = -1;
+    }
+    if (tid == 0) sm.next = 0;
+    fence_mbar_init();
+    __syncthreads();
+    constexpr uint32_t kStageBytes = sizeof(sm.pos[0]), kRowBytes = kWTile * sizeof(float);
+    const uint32_t bar0 = smem_addr(&sm.bar[0]), pos0 = smem_addr(&sm.pos[0][0][0]);
+    const uint32_t txb = (uint32_t)rows * kRowBytes;
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int k) {  // lane 0: stream the CTA's k-th tile into stage k mod kPool
+        const int t = k * G + b;
+        if (t >= ntiles) return;
+        const int s = k % kPool;
+        const uint32_t bar = bar0 + 8u * s, dst = pos0 + kStageBytes * s;
+        *(volatile int *)&sm.filled[s] = k;
+        if (t >= nfull) {  // ragged last tile: its consumer loads it; the arrival only releases the stage
+            mbar_arrive_a(bar);
+            return;
+        }
+        mbar_expect_tx_a(bar, txb);
+        if (a.use_tmap) {
+            tensor_g2s_2d_a(dst, &a.tmap, t * kWTile, 0, bar, pol);
+        } else {
+            for (int r = 0; r < 3; ++r) {
+                const float *src = r == 0 ? a.x : (r == 1 ? a.y : a.z);
+                bulk_g2s_a(dst + r * kRowBytes, src + (int64_t)t * kWTile, kRowBytes, bar, pol);
+            }
+        }
+        if (rows == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
+    };
+    if (lane == 0) {
+        issue(wid);
+        issue(wid + kSW);
+    }
+    __syncwarp();
+    WarpQueue &q = sm.q[wid];
+    int qn = 0;
+    RecChunk c;
+    c.base = 0;
+    c.left = 0;
+#if ADOP_CHUNK_PREFETCH
+    c.has = false;
+    c.pend = 0;
+#endif
+    LazyR lr;
+    lr.src = nullptr;
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&sm.next, 1);
+        k = __shfl_sync(kFull, k, 0);
+        const int t = k * G + b;
+        if (t >= ntiles) break;
+        const int s = k % kPool;
+        const int64_t base = (int64_t)t * kWTile;
+        const float *rp[4] = {sm.pos[s][0], sm.pos[s][1], sm.pos[s][2], sm.pos[s][3]};
+        // the stage's barrier alternates parity per use: wait until tile k's copy was issued (tile k - kPool is then
+        // done with the stage), so the parity names tile k's phase and not a later or earlier one
+        while (*(volatile int *)&sm.filled[s] != k) __nanosleep(64);
+        mbar_wait_a(bar0 + 8u * s, (uint32_t)(k / kPool) & 1u);
+        int vmask = 0xFF;
+        if (t >= nfull) {  // ragged last tile: guarded loads into the released stage
+            const float *src[4] = {a.x, a.y, a.z, a.radius};
+            vmask = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
+                const bool in = base + e < a.n;
+                for (int r = 0; r < 4; ++r) sm.pos[s][r][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                vmask |= (in ? 1 : 0) << j;
+            }
+            __syncwarp();
+        }
+        CNT(0, 1);
+        depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt,
+                                     0xFFFFFFFFu, lr);
+        __syncwarp();  // every lane is done with stage s
+        if (lane == 0) issue(k + kPool);
+        __syncwarp();
+    }
+    if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
+    if (VM == 2 && a.mv_lists)
+        mv_close(a, c, lane);
+    else
+        rec_reserve(a, c, lane, false);
 }
 
 // Shared-pyramid reset (adop_clear_pyramid): keys <- sentinel, accum / count <- 0.
@@ -2416,8 +2571,32 @@ int launch_clear(const RasterArgs &a, int what, void *stream) {
     return (int)cudaGetLastError();
 }
 
+static bool depth_pool_enabled() {  // ADOP_DEPTH_POOL=0: the per-warp-ring depth sweep instead (A/B)
+    static int env = -1;
+    if (env < 0) {
+        const char *e = std::getenv("ADOP_DEPTH_POOL");
+        env = e ? std::atoi(e) : 1;
+    }
+    return env != 0;
+}
+
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
+    if (depth_pool_enabled() && !a.tbounds && !(a.dyn_tiles & 1)) {
+        auto kp = a.discard ? k_depth_pool<MODEL, VM, true> : k_depth_pool<MODEL, VM, false>;
+        if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PoolSmem)) !=
+            cudaSuccess)
+            return (int)cudaGetLastError();
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, kST, sizeof(PoolSmem));
+        if (per_sm < 1) per_sm = 1;
+        int64_t g = (int64_t)sms * per_sm;
+        const int64_t tiles = (a.n + kWTile - 1) / kWTile;
+        if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
+        if (g < 1) g = 1;
+        kp<<<(unsigned)g, kST, sizeof(PoolSmem), (cudaStream_t)stream>>>(a);
+        return (int)cudaGetLastError();
+    }
     auto k = a.discard ? k_depth_async<MODEL, VM, true> : k_depth_async<MODEL, VM, false>;
     // the dynamic shared-memory limit is a per-device (context) attribute: raised once per device and
     // instance (two threads racing here both set the same value)
