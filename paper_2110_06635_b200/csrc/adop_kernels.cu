@@ -2326,15 +2326,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
     }
 }
 
-struct BwdSmem {
-    float pos[kStages][kSW][4][kWTile];
-    uint64_t bar[kSW][kStages];
-    long long tile[kSW][kStages];
+struct BwdSmem {  // CTA-wide pool of kPool stages, claimed like k_depth_pool's
+    float pos[kPool][4][kWTile];
+    uint64_t bar[kPool];
+    int filled[kPool];
+    int next;
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
     uint8_t gl[kSW][kWTile];  // mode 1: compacted ghost points of the warp tile (tile offsets)
 };
 
 static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 3, "backward sweep: 3 CTAs per SM must fit in shared memory");
+static_assert(kPool == 2 * kSW, "the sweeps' initial fills issue two stages per warp");
 
 // GO (ghosts only) is launched for mode 1, !GO for mode 0; the instance not matching the mode exits.
 template <int MODEL, int CT, bool MV, bool GO>
@@ -2353,54 +2355,58 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
     const int rows = staged_r ? 4 : 3;
     const float *src[4] = {a.x, a.y, a.z, a.radius};
     init_layer_descs(a, sm.ld);
-    if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(&sm.bar[wid][st], 1);
-        fence_mbar_init();
+    if (tid < kPool) {
+        mbar_init(&sm.bar[tid], 1);
+        sm.filled[tid] = -1;
     }
+    if (tid == 0) sm.next = 0;
+    fence_mbar_init();
     __syncthreads();
+    const long long G = gridDim.x, bk = blockIdx.x;
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
-    TileClaim tc;
-    if (lane == 0)
-        tc.init(&a.hdr->tiles_bwd, ntiles, (long long)gridDim.x * kSW, (long long)blockIdx.x * kSW + wid,
-                (a.dyn_tiles >> 1) & 1);
-    auto issue = [&](int st) {
-        if (lane == 0) {
-            const long long t = tc.take(&a.hdr->tiles_bwd);
-            sm.tile[wid][st] = t;
-            if (t < ntiles && full_tile(t)) {
-                const uint64_t pol = policy_evict_first();
-                mbar_expect_tx(&sm.bar[wid][st], (uint32_t)(rows * kWTile * sizeof(float)));
-                if (a.use_tmap) {  // x, y, z rows in one 2-D tensor copy, r_world in a 1-D bulk copy
-                    tensor_g2s_2d(sm.pos[st][wid][0], &a.tmap, (int)(t * kWTile), 0, &sm.bar[wid][st], pol);
-                    if (rows == 4)
-                        bulk_g2s(sm.pos[st][wid][3], src[3] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
-                } else {
-                    for (int r = 0; r < rows; ++r)
-                        bulk_g2s(sm.pos[st][wid][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[wid][st], pol);
-                }
-            }
+    auto issue = [&](int k) {  // lane 0: the CTA's k-th tile (k G + b) into stage k mod kPool
+        const long long t = (long long)k * G + bk;
+        if (t >= ntiles) return;
+        const int st = k % kPool;
+        *(volatile int *)&sm.filled[st] = k;
+        if (!full_tile(t)) {  // ragged last tile: its consumer loads it; the arrival only releases the stage
+            mbar_arrive_a(smem_addr(&sm.bar[st]));
+            return;
+        }
+        const uint64_t pol = policy_evict_first();
+        mbar_expect_tx(&sm.bar[st], (uint32_t)(rows * kWTile * sizeof(float)));
+        if (a.use_tmap) {  // x, y, z rows in one 2-D tensor copy, r_world in a 1-D bulk copy
+            tensor_g2s_2d(sm.pos[st][0], &a.tmap, (int)(t * kWTile), 0, &sm.bar[st], pol);
+            if (rows == 4) bulk_g2s(sm.pos[st][3], src[3] + t * kWTile, kWTile * sizeof(float), &sm.bar[st], pol);
+        } else {
+            for (int r = 0; r < rows; ++r)
+                bulk_g2s(sm.pos[st][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[st], pol);
         }
     };
-    for (int st = 0; st < kStages; ++st) issue(st);
+    if (lane == 0) {
+        issue(wid);
+        issue(wid + kSW);
+    }
     __syncwarp();
-    uint32_t phase = 0u;
-    for (int64_t k = 0;; ++k) {
-        const int st = (int)(k % kStages);
-        const long long t = *(volatile long long *)&sm.tile[wid][st];
+    for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(&sm.next, 1);
+        k = __shfl_sync(kFull, k, 0);
+        const long long t = (long long)k * G + bk;
         if (t >= ntiles) break;
+        const int st = k % kPool;
         const int64_t base = t * kWTile;
-        const float *rp[4] = {sm.pos[st][wid][0], sm.pos[st][wid][1], sm.pos[st][wid][2], sm.pos[st][wid][3]};
+        const float *rp[4] = {sm.pos[st][0], sm.pos[st][1], sm.pos[st][2], sm.pos[st][3]};
+        while (*(volatile int *)&sm.filled[st] != k) __nanosleep(64);  // (see k_depth_pool)
+        mbar_wait(&sm.bar[st], (uint32_t)(k / kPool) & 1u);
         int vmask = 0xFF;
-        if (full_tile(t)) {
-            mbar_wait(&sm.bar[wid][st], (phase >> st) & 1u);
-            phase ^= 1u << st;
-        } else {
+        if (!full_tile(t)) {
             vmask = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int e = (j >> 2) * 128 + 4 * lane + (j & 3);
                 const bool in = base + e < a.n;
-                for (int r = 0; r < 4; ++r) sm.pos[st][wid][r][e] = (in && r < rows) ? src[r][base + e] : 0.f;
+                for (int r = 0; r < 4; ++r) sm.pos[st][r][e] = (in && r < rows) ? src[r][base + e] : 0.f;
                 vmask |= (in ? 1 : 0) << j;
             }
             __syncwarp();
@@ -2459,9 +2465,8 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                     }
                 }
             }
-            __syncwarp();  // the ghost list is rewritten by the next tile
-            __syncwarp();
-            issue(st);
+            __syncwarp();  // the ghost list is rewritten by the next tile; every lane is done with the stage
+            if (lane == 0) issue(k + kPool);
             __syncwarp();
             continue;
         }
@@ -2503,7 +2508,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             }
         }
         __syncwarp();
-        issue(st);
+        if (lane == 0) issue(k + kPool);
         __syncwarp();
     }
     list_close<false>(a, ct, lane);
