@@ -311,6 +311,9 @@ constexpr int kDStages = ADOP_DSTAGES;  // depth sweep ring depth (tiles in flig
 #ifndef ADOP_DRAIN_NOINLINE
 #define ADOP_DRAIN_NOINLINE 0
 #endif
+#ifndef ADOP_PREREDUCE
+#define ADOP_PREREDUCE 0
+#endif
 #ifndef ADOP_COUNTERS  // profiling build only: per-stage work counts of the depth sweep (scripts/depth_counters.py)
 #define ADOP_COUNTERS 0
 #endif
@@ -686,7 +689,19 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
         const int loc = l < nk ? layer_pixel(v, p, l, pu, pv) : -1;
         const bool hit = loc >= 0;
         const uint32_t pix = (uint32_t)(v.off[l] + loc);
+#if ADOP_PREREDUCE
+        // warp-level pre-reduction (measured, see profiles/r02/evolution.md): lanes hitting the same (view, pixel)
+        // min-reduce their keys with two 32-bit REDUX steps and only the group's winner issues the L2 reduction
+        {
+            const unsigned grp = __match_any_sync(kFull, hit ? (((unsigned long long)vs << 32) | pix) : ~0ull);
+            const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+            const unsigned mhi = __reduce_min_sync(grp, hi);
+            const unsigned mlo = __reduce_min_sync(grp, hi == mhi ? lo : 0xFFFFFFFFu);
+            if (hit && hi == mhi && lo == mlo) red_min_u64_keep(v.keys + pix, key, policy_evict_last());
+        }
+#else
         if (hit) red_min_u64_keep(v.keys + pix, key, policy_evict_last());
+#endif
         const unsigned b = __ballot_sync(kFull, hit);
         if (b == 0u) {
             if (!__any_sync(kFull, l + 1 < nk)) break;
