@@ -44,6 +44,13 @@ def parse():
     ap.add_argument("--comm", choices=["nccl", "p2p"], default="nccl",
                     help="N > 1 point sharding: NCCL all-reduces of private pyramids, or every shard reducing "
                          "straight into rank 0's pyramid over peer memory (DESIGN.md section 8)")
+    ap.add_argument("--keys32", action="store_true",
+                    help="N > 1 point sharding (nccl): MIN-exchange only the 32-bit depth words (11 MB/view instead of "
+                         "22 MB; the winner indices stay shard-local; DESIGN.md section 8)")
+    ap.add_argument("--mode", choices=["point", "view"], default="point",
+                    help="point: configs[3] forward, point-sharded over N ranks (the headline); view: configs[4] "
+                         "training step (fwd+bwd, 16 views) view-sharded over N ranks with one SUM all-reduce of the "
+                         "point gradients and an all-gather of the pose rows")
     ap.add_argument("--cpu-sample", type=int, default=25_000_000)
     ap.add_argument("--ref-sample", type=int, default=4_000_000)
     return ap.parse_args()
@@ -213,7 +220,11 @@ def run_ours(args, rank, world, local_rank):
             ev[1].record(s)
         if world > 1:
             for p in pyrs:
-                dist.all_reduce(p.keys, op=dist.ReduceOp.MIN)
+                if args.keys32:
+                    from paper_2110_06635_b200 import parallel as PL
+                    PL.min_depth_words(p.keys)
+                else:
+                    dist.all_reduce(p.keys, op=dist.ReduceOp.MIN)
         if ev is not None:
             ev[2].record(s)
         A.forward_blend(pts_, cams, poses, ap, pyrs, ws, s, cl(pts_))
@@ -335,7 +346,8 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": WORKLOAD, "points_per_gpu": N, "points_total": N * world, "channels": C,
                        "layers": prm.layers, "resolution": "1920x1080", "views": 1, "discard": True,
                        "gamma": prm.gamma, "alpha": prm.alpha,
-                       "parallelism": (f"point-sharded x{world} ({args.comm})" if world > 1 else "single GPU"),
+                       "parallelism": (f"point-sharded x{world} ({args.comm}{', 32-bit depth words' if args.keys32 else ''})"
+                                       if world > 1 else "single GPU"),
                        "l2": "inputs (1.6 GB/GPU positions+radii) exceed the 126 MB L2; no flush needed",
                        "record_slots_per_frame": records, "record_overflow": overflow},
             "timing": ("CUDA graph replays (depth | blend+resolve) with an event pair around each depth phase"
@@ -540,6 +552,143 @@ def time_preprocess(cloud):
 
 
 # --------------------------------------------------------------------------- #
+# --mode view: the configs[4] training step, view-sharded
+# --------------------------------------------------------------------------- #
+VIEW_METRIC = "point-views/sec and ms/step, 50M pts x 16 views 1024^2 OpenCV8, 5 layers, fwd+bwd training step"
+VIEW_WORKLOAD = ("room50M_16view_fwdbwd (BASELINE.json configs[4]): 50M pts, C=4, 16 views 1024^2 OpenCV8, 5 layers, "
+                 "discard on, ghosts 0.25, forward + backward (d_feat, d_pos, d_pose)")
+
+
+def run_view(args, rank, world, local_rank):
+    import dataclasses
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_06635_b200 import adop as A
+    from paper_2110_06635_b200 import parallel as PL
+    from paper_2110_06635_b200 import scene as S
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    w = S.workload(4, device=dev)
+    V = len(w.cameras)
+    a, b = PL.view_range(V, world, rank)
+    prm = dataclasses.replace(w.params, view_id_base=a)
+    cams, poses = w.cameras[a:b], w.poses[a:b]
+    N, C = w.cloud.n, w.cloud.channels
+    r = A.Renderer(w.cloud, cams, poses, prm)
+    buf, d_feat, d_pos = PL.grad_buffer(N, C, dev)  # one SUM all-reduce of d_feat ++ d_pos
+    r.d_feat, r.d_pos = d_feat, d_pos
+    r.d_pose = torch.empty(b - a, 6, dtype=torch.float64, device=dev)
+    P = A.pyramid_pixels(cams[0].width, cams[0].height, prm.layers)
+    Gt = S.grad_pyramid(V, C, P, device=dev)[a:b].contiguous()
+    G = [Gt[v] for v in range(b - a)]
+    stream = torch.cuda.current_stream(dev)
+    counts = [PL.view_range(V, world, q) for q in range(world)]
+    width = max(y - x for x, y in counts)
+    pose_buf = torch.zeros(width, 6, dtype=torch.float64, device=dev)
+    gathered = [torch.empty_like(pose_buf) for _ in range(world)]
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        r.forward()
+        if ev is not None:
+            ev[1].record(stream)
+        r.backward(G)
+        if ev is not None:
+            ev[2].record(stream)
+        if world > 1:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+            pose_buf[: b - a].copy_(r.d_pose)
+            dist.all_gather(gathered, pose_buf)
+        if ev is not None:
+            ev[3].record(stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    clocks = Clocks(phys_index(local_rank))
+    clocks.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    per = sorted(e[0].elapsed_time(e[3]) for e in evs)
+    fwd_ms = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+    bwd_ms = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    comm_ms = statistics.median(e[2].elapsed_time(e[3]) for e in evs)
+    # e2e: this rank's upstream gradient pyramids copied from pinned host memory every step, d_pose read back
+    hG = Gt.cpu().pin_memory()
+    hpose = torch.empty(V, 6, dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        Gt.copy_(hG, non_blocking=True)
+        step()
+        hpose[: b - a].copy_(r.d_pose, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    K = max(3, min(args.steps, 10))
+    s0.record(stream)
+    for _ in range(K):
+        e2e_step()
+    s1.record(stream)
+    barrier()
+    te = torch.tensor([s0.elapsed_time(s1) / K], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    out = None
+    if rank == 0:
+        peak, peak_src = peaks()
+        n_blend = int(sum(float(p.count.sum()) for p in r.pyrs))
+        _, n_ghost, _ = r.ws.stats3()
+        Vl = b - a
+        b_fwd = N * 16 + n_blend * 4 * C + Vl * P * (8 + 4 * C + 4)
+        b_bwd = N * 16 + n_ghost * 4 * C + N * (4 * C + 12) + Vl * P * (4 * C + 4 * C + 4 + 8)
+        q = lambda f: per[min(len(per) - 1, int(f * (len(per) - 1) + 0.5))]
+        out = {
+            "metric": VIEW_METRIC, "value": N * V / (ms * 1e-3), "unit": "point-views/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": VIEW_WORKLOAD, "points": N, "views_total": V, "views_per_rank": Vl,
+                       "parallelism": f"view-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (0.8 GB positions+radii, 0.8 GB descriptors) exceed the 126 MB L2"},
+            "phases_ms_median_rank0": {"forward": fwd_ms, "backward": bwd_ms, "grad_allreduce_pose_allgather": comm_ms},
+            "ms_per_step_stats": {"median": statistics.median(per), "p10": q(0.1), "p90": q(0.9), "steps": len(per)},
+            "roofline": {"kernel": "whole fwd+bwd step of rank 0 (SURVEY §8(d) B_fwd + B_bwd)", "bound": "hbm",
+                         "achieved": (b_fwd + b_bwd) / ((fwd_ms + bwd_ms) * 1e-3) / 1e9, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": (b_fwd + b_bwd) / ((fwd_ms + bwd_ms) * 1e-3) / 1e9 / peak,
+                         "algorithmic_bytes": b_fwd + b_bwd, "traffic": None},
+            "gpu_launches": 16 * args.steps,  # 7 forward + 9 backward kernels per step (launch list, profiles/r02)
+            "clocks": clk,
+            "e2e": {"value": N * V / (float(te.item()) * 1e-3), "unit": "point-views/s", "ms_per_step": float(te.item()),
+                    "h2d_bytes_per_step": Gt.numel() * 4, "d2h_bytes_per_step": Vl * 6 * 8,
+                    "h2d_note": "this rank's upstream image-pyramid gradients from pinned host memory; d_pose read back"},
+            "comm": {"allreduce_bytes": buf.numel() * 4 if world > 1 else 0,
+                     "model": "T(G) = T_compute(V/G views) + T_allreduce(1.4 GB) + T_allgather (DESIGN.md section 8)"},
+        }
+    return out
+
+
+# --------------------------------------------------------------------------- #
 # reference arm: the CPU oracle (this tier has no reference implementation)
 # --------------------------------------------------------------------------- #
 def run_reference(args, rank, world):
@@ -588,6 +737,14 @@ def main():
     if world > 1:
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.mode == "view":
+        out = run_view(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     out, ctx = run_ours(args, rank, world, local_rank)
     if not args.no_e2e:
         e2e = run_e2e(args, ctx, rank, world, local_rank)

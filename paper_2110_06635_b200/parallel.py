@@ -47,13 +47,30 @@ def view_range(n_views: int, world: int, rank: int) -> Tuple[int, int]:
     return a, a + per + (1 if rank < extra else 0)
 
 
-def point_sharded_forward(phases, pyramids: Sequence, group=None):
+def min_depth_words(keys: torch.Tensor, group=None, scratch: torch.Tensor = None):
+    """MIN all-reduce of only the 32-bit depth word (bits(z), the high word of every key, R8) -- half the bytes
+    of the 64-bit key exchange (SURVEY §8(e) mitigation 3).  The blend and resolve read only the depth word
+    (Eq. 6's min_z), so counts, sums and images equal the 64-bit exchange's; the low words (winner indices)
+    stay each shard's local winners, i.e. the global winner index is not exchanged (verification-only)."""
+    hi = keys.view(torch.int32)[1::2]  # little endian: word 1 of each key is bits(z)
+    buf = torch.empty_like(hi) if scratch is None else scratch
+    buf.copy_(hi)
+    dist.all_reduce(buf, op=dist.ReduceOp.MIN, group=group)
+    hi.copy_(buf)
+    return buf
+
+
+def point_sharded_forward(phases, pyramids: Sequence, group=None, keys32: bool = False):
     """phases.depth(); MIN(keys); phases.blend(); SUM(accum++count); phases.resolve().
 
-    pyramids: objects with `.keys` (int64 tensor) and `.ac` (accum ++ count tensor) per view."""
+    pyramids: objects with `.keys` (int64 tensor) and `.ac` (accum ++ count tensor) per view.
+    keys32: exchange only the depth words (min_depth_words)."""
     phases.depth()
     for p in pyramids:
-        dist.all_reduce(p.keys, op=dist.ReduceOp.MIN, group=group)
+        if keys32:
+            min_depth_words(p.keys, group)
+        else:
+            dist.all_reduce(p.keys, op=dist.ReduceOp.MIN, group=group)
     phases.blend()
     for p in pyramids:
         dist.all_reduce(p.ac, op=dist.ReduceOp.SUM, group=group)

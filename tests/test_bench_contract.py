@@ -44,3 +44,13 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["os_cpu_count"] == os.cpu_count()
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["unit"] == d["unit"]
+
+
+@pytest.mark.gpu
+def test_bench_view_mode_line():
+    """--mode view: the configs[4] training step (fwd+bwd over 16 views), same JSON contract."""
+    d = _line(["--mode", "view", "--steps", "2", "--warmup", "3"])
+    for k in ("metric", "value", "unit", "n_gpus", "ms_per_step", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["config"]["views_total"] == 16 and d["value"] > 0
+    assert 0 < d["roofline"]["frac"] < 1.2 and d["e2e"]["h2d_bytes_per_step"] > 0

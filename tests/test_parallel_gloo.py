@@ -84,19 +84,23 @@ def _scene():
     return cloud, cams, poses, prm
 
 
-def _point_sharded(rank, world, port, q):
+def _point_sharded(rank, world, port, q, keys32=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     cloud, cams, poses, prm = _scene()
     a, b = PL.shard_range(cloud.n, world, rank, align=256)
     pts = O.Points.from_cloud(cloud.slice(a, b), global_offset=a)
     P = O.pyramid_pixels(96, 64, prm.layers)
     pyrs = [_Pyr(P, 3) for _ in cams]
-    PL.point_sharded_forward(OraclePhases(pts, cams, poses, prm, pyrs), pyrs)
+    PL.point_sharded_forward(OraclePhases(pts, cams, poses, prm, pyrs), pyrs, keys32=keys32)
     if rank == 0:
         q.put(([p.keys.numpy().copy() for p in pyrs], [p.ac.numpy().copy() for p in pyrs],
                [p.image.numpy().copy() for p in pyrs]))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _point_sharded32(rank, world, port, q):
+    _point_sharded(rank, world, port, q, keys32=True)
 
 
 def _view_sharded(rank, world, port, q):
@@ -166,6 +170,19 @@ def test_point_sharded_forward_gloo_ws2_equals_unsharded():
         assert np.array_equal(ac[v][P * 3:], fwd.count[v])
         np.testing.assert_allclose(image[v], fwd.image[v], rtol=1e-12, atol=1e-12)
     assert fwd.count.sum() > 500
+
+
+def test_point_sharded_forward_depth_words_only_gloo_ws2():
+    """32-bit depth-word MIN exchange: depth words, counts and images equal the unsharded forward; the
+    low words are the shard-local winners (not exchanged)."""
+    keys, ac, image = _spawn(_point_sharded32)
+    cloud, cams, poses, prm = _scene()
+    fwd = O.forward(O.Points.from_cloud(cloud), cams, poses, prm)
+    P = fwd.count.shape[1]
+    for v in range(len(cams)):
+        assert np.array_equal(keys[v].view(np.uint64) >> np.uint64(32), fwd.keys[v] >> np.uint64(32))
+        assert np.array_equal(ac[v][P * 3:], fwd.count[v])
+        np.testing.assert_allclose(image[v], fwd.image[v], rtol=1e-12, atol=1e-12)
 
 
 def test_view_sharded_training_gloo_ws2_equals_unsharded():
