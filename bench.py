@@ -617,6 +617,11 @@ def run_view(args, rank, world, local_rank):
     barrier()
     clocks = Clocks(phys_index(local_rank))
     clocks.start()
+    t0 = time.time()
+    while time.time() - t0 < 0.5:  # under the clock sampler (nvidia-smi takes a moment to start)
+        step()
+        torch.cuda.synchronize(dev)
+    barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record(stream)

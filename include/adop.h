@@ -64,10 +64,28 @@ typedef enum {
     ADOP_ERR_SHAPE_MISMATCH = 2,
     ADOP_ERR_UNSUPPORTED = 3,
     ADOP_ERR_WORKSPACE_TOO_SMALL = 4,
-    ADOP_ERR_CUDA = 5
+    ADOP_ERR_CUDA = 5,
+    ADOP_ERR_NCCL = 6
 } adop_status;
 
 enum { ADOP_PINHOLE = 0, ADOP_OPENCV8 = 1, ADOP_FISHEYE = 2 };
+
+/* Multi-GPU communicator (adop_comm_init; NULL everywhere = single GPU).  The two partitionings of the
+ * north star ("well over 100M points"; the paper itself is single-GPU, L811):
+ *  ADOP_SHARD_POINTS: every rank renders its shard of one cloud (disjoint global_offset ranges) into a full
+ *    local pyramid; adop_rasterize_forward MIN-reduces the keys after the depth pass (64-bit keys, or only
+ *    the 32-bit depth words with ADOP_COMM_KEYS32 -- the blend reads only those; the winner indices then
+ *    stay shard-local) and SUM-reduces accum and count after the blend, so every rank resolves the image
+ *    of the whole cloud; adop_rasterize_backward sums d_pose and d_intrinsics over the shards.
+ *  ADOP_SHARD_VIEWS: every rank renders the whole cloud for its range of the batch's views (params
+ *    view_id_base = the range's first view, so the discard draws equal the unsharded batch's); the forward
+ *    is local and adop_rasterize_backward sums d_feat, d_pos and d_env over the ranks (d_pose rows stay
+ *    with their view's rank).
+ * Collectives are NCCL (libnccl.so.2 loaded at run time) on the call's stream; NCCL errors return
+ * ADOP_ERR_NCCL. */
+typedef struct adop_comm adop_comm;
+enum { ADOP_SHARD_POINTS = 0, ADOP_SHARD_VIEWS = 1 };
+enum { ADOP_COMM_KEYS32 = 1 };
 
 #define ADOP_MAX_LAYERS 8
 #define ADOP_MAX_CHANNELS 32
@@ -207,7 +225,7 @@ ADOP_API adop_status adop_forward_resolve(const adop_points *points, int32_t n_v
 /* Phases 1-3 in order (single GPU). */
 ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                    const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
-                                   void *workspace, size_t workspace_bytes, void *stream);
+                                   void *workspace, size_t workspace_bytes, adop_comm *comm, void *stream);
 
 /* Backward (§4.2-4.5): re-renders every point (L361) against the forward's
  * keys/count/accum/image (which must be unmodified) and the upstream gradient
@@ -236,7 +254,8 @@ ADOP_API adop_status adop_rasterize_backward(const adop_points *points, int32_t 
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image,
                                     float *d_feat, float *d_pos, double *d_pose, double *d_intrinsics,
-                                    float *d_env, void *workspace, size_t workspace_bytes, void *stream);
+                                    float *d_env, void *workspace, size_t workspace_bytes, adop_comm *comm,
+                                    void *stream);
 
 /* Debug / parity: per point and view, bit l (l < L) = valid, in bounds and kept
  * by the discard test at layer l; bit 7 = ghost.  mask: device uint8 [V][n]. */
@@ -255,6 +274,21 @@ ADOP_API adop_status adop_workspace_stats(const void *workspace, size_t workspac
 /* Bounding box of every 256-point tile of `points` (lo x, y, z, 0, hi x, y, z, 0; NaN coordinates
  * ignored): bounds = device float [ceil(n/256)][8], 16-byte aligned.  Enqueued on `stream`. */
 ADOP_API adop_status adop_tile_bounds(const adop_points *points, float *bounds, void *stream);
+
+/* A fresh NCCL unique id (128 bytes) on one rank, to be broadcast to the others (e.g. with
+ * torch.distributed.broadcast_object_list).  Errors: ADOP_ERR_INVALID_ARGUMENT, ADOP_ERR_NCCL. */
+ADOP_API adop_status adop_comm_unique_id(uint8_t id[128]);
+
+/* Collective over nranks processes (one per GPU, the CURRENT device of the calling thread): mode
+ * ADOP_SHARD_POINTS or ADOP_SHARD_VIEWS, flags 0 or ADOP_COMM_KEYS32.  Every rank calls it with the same
+ * id.  The communicator owns its NCCL communicator and (with ADOP_COMM_KEYS32) a device scratch buffer of
+ * the largest view's P int32 -- the only device memory the library allocates.  Errors:
+ * ADOP_ERR_INVALID_ARGUMENT (rank not in [0, nranks), bad mode or flags), ADOP_ERR_CUDA, ADOP_ERR_NCCL. */
+ADOP_API adop_status adop_comm_init(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t mode, int32_t flags,
+                                    adop_comm **comm);
+
+/* Frees the communicator (NULL: no-op).  The caller ensures no enqueued call still uses it. */
+ADOP_API adop_status adop_comm_destroy(adop_comm *comm);
 
 /* Host-only diagnostic of the OpenCV8 candidate window (no GPU work): the box [xlo, xhi] x [ylo, yhi]
  * in undistorted normalized coordinates that contains every point n with |n|^2 <= r2_max whose

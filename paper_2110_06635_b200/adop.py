@@ -80,14 +80,22 @@ def lib():
         P = C.POINTER
         common = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params), P(adop_pyramid),
                   C.c_void_p, C.c_size_t, C.c_void_p]
-        for name in ("adop_forward_depth", "adop_forward_blend", "adop_forward_resolve", "adop_rasterize_forward"):
+        for name in ("adop_forward_depth", "adop_forward_blend", "adop_forward_resolve"):
             f = getattr(L, name)
             f.restype, f.argtypes = C.c_int, common
+        L.adop_rasterize_forward.restype = C.c_int
+        L.adop_rasterize_forward.argtypes = common[:-1] + [C.c_void_p, C.c_void_p]  # ..., comm, stream
         L.adop_rasterize_backward.restype = C.c_int
         L.adop_rasterize_backward.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose),
                                               P(adop_params), P(adop_pyramid), P(C.c_void_p), C.c_void_p,
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                              C.c_size_t, C.c_void_p]
+                                              C.c_size_t, C.c_void_p, C.c_void_p]
+        L.adop_comm_unique_id.restype = C.c_int
+        L.adop_comm_unique_id.argtypes = [C.c_char_p]
+        L.adop_comm_init.restype = C.c_int
+        L.adop_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.c_int32, C.c_int32, P(C.c_void_p)]
+        L.adop_comm_destroy.restype = C.c_int
+        L.adop_comm_destroy.argtypes = [C.c_void_p]
         L.adop_point_masks.restype = C.c_int
         L.adop_point_masks.argtypes = [P(adop_points), C.c_int32, P(adop_camera), P(adop_pose), P(adop_params),
                                        C.c_void_p, C.c_void_p]
@@ -396,22 +404,49 @@ def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None, call=Non
     _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream, call)
 
 
-def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None, call=None):
-    _phase("adop_rasterize_forward", points, cams, poses, params, pyrs, ws, stream, call)
+def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None, call=None, comm=None):
+    """Fused forward; comm: a Comm (multi-GPU collectives between the phases) or None."""
+    c = _Call(points, cams, poses, params, pyrs) if call is None else call
+    _check(lib().adop_rasterize_forward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, ws.ptr,
+                                        ws.nbytes, None if comm is None else comm.ptr, _stream(stream)))
+
+
+SHARD_POINTS, SHARD_VIEWS, COMM_KEYS32 = 0, 1, 1
+
+
+class Comm:
+    """The library's NCCL communicator (adop_comm_init): ADOP_SHARD_POINTS or ADOP_SHARD_VIEWS collectives run
+    inside adop_rasterize_forward / _backward.  Rank 0 creates the id (unique_id()), every rank passes it."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().adop_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, mode: int, flags: int = 0):
+        p = C.c_void_p()
+        _check(lib().adop_comm_init(int(nranks), int(rank), C.create_string_buffer(uid, 128), int(mode), int(flags),
+                                    C.byref(p)))
+        self.ptr = p
+
+    def close(self):
+        if self.ptr:
+            _check(lib().adop_comm_destroy(self.ptr))
+            self.ptr = None
 
 
 def rasterize_backward(points, cams, poses, params, pyrs, grads: Sequence[torch.Tensor], ws,
                        d_feat: Optional[torch.Tensor], d_pos: Optional[torch.Tensor],
                        d_pose: Optional[torch.Tensor], d_intr: Optional[torch.Tensor] = None,
-                       d_env: Optional[torch.Tensor] = None, stream=None, call=None):
+                       d_env: Optional[torch.Tensor] = None, stream=None, call=None, comm=None):
     """d_intr: optional [V][12] float64 camera-intrinsics gradient (fx, fy, cx, cy, k1..k6, p1, p2);
     d_env: optional [H][W][C] float32 environment-map gradient (needs params.env_map)."""
     c = _Call(points, cams, poses, params, pyrs) if call is None else call
     g = (C.c_void_p * c.V)(*[t.data_ptr() for t in grads])
     _check(lib().adop_rasterize_backward(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs, g,
                                          _ptr(d_feat), _ptr(d_pos), _ptr(d_pose), _ptr(d_intr), _ptr(d_env), ws.ptr,
-                                         ws.nbytes,
-                                         _stream(stream)))
+                                         ws.nbytes, None if comm is None else comm.ptr, _stream(stream)))
 
 
 def point_masks(points, cams, poses, params, mask: torch.Tensor, stream=None):
@@ -483,8 +518,9 @@ class Renderer:
     """
 
     def __init__(self, cloud, cams, poses, params, global_offset: int = 0, record_capacity: Optional[int] = None,
-                 device=None, intrinsics: bool = False):
+                 device=None, intrinsics: bool = False, comm: Optional["Comm"] = None):
         device = cloud.pos.device if device is None else device
+        self.comm = comm  # multi-GPU collectives inside the fused calls (Comm) or None
         self.cams, self.poses, self.sparams = list(cams), list(poses), params
         self.points = Points.from_cloud(cloud, global_offset)
         self.C = self.points.channels
@@ -526,7 +562,8 @@ class Renderer:
         return self._c
 
     def forward(self, stream=None):
-        rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream, self._call())
+        rasterize_forward(self.points, self.cams, self.poses, self.params, self.pyrs, self.ws, stream, self._call(),
+                          self.comm)
         return self.pyrs
 
     def alloc_grads(self):
@@ -546,7 +583,8 @@ class Renderer:
         if self.d_feat is None:
             self.alloc_grads()
         rasterize_backward(self.points, self.cams, self.poses, self.params, self.pyrs, grads, self.ws,
-                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, self.d_env, stream, self._call())
+                           self.d_feat, self.d_pos, self.d_pose, self.d_intr, self.d_env, stream, self._call(),
+                           self.comm)
         return self.d_feat, self.d_pos, self.d_pose
 
     def masks(self, stream=None) -> torch.Tensor:

@@ -125,7 +125,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     target = LIB if out is None else out
     tmp = target + f".tmp{os.getpid()}"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs,
-           "-cudart", "static"]
+           "-cudart", "static", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -785,13 +785,20 @@ adop_status adop_forward_resolve(const adop_points *points, int32_t n_views, con
 
 adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                    const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
-                                   void *workspace, size_t workspace_bytes, void *stream) {
+                                   void *workspace, size_t workspace_bytes, adop_comm *comm, void *stream) {
     adop_status s;
     if ((s = check_points(points, true))) return s;
+    if ((s = comm_check(comm))) return s;
+    if (comm && params && params->shared_pyramid)
+        return fail(ADOP_ERR_INVALID_ARGUMENT, "a communicator and a shared pyramid exclude each other");
     if ((s = adop_forward_depth(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream)))
         return s;
+    int64_t pixels[ADOP_MAX_VIEWS_PER_LAUNCH];
+    for (int v = 0; v < n_views; ++v) pixels[v] = adop_pyramid_pixels(cameras[v].width, cameras[v].height, params->layers);
+    if ((s = comm_keys(comm, views, pixels, n_views, stream))) return s;  // point sharding: MIN of the keys
     if ((s = adop_forward_blend(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream)))
         return s;
+    if ((s = comm_sums(comm, views, pixels, n_views, points->channels, stream))) return s;  // SUM of accum, count
     return adop_forward_resolve(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, stream);
 }
 
@@ -799,8 +806,10 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
                                     const adop_pose *poses, const adop_params *params,
                                     const adop_pyramid *fwd_views, const float *const *grad_image, float *d_feat,
                                     float *d_pos, double *d_pose, double *d_intrinsics, float *d_env,
-                                    void *workspace, size_t workspace_bytes, void *stream) {
+                                    void *workspace, size_t workspace_bytes, adop_comm *comm, void *stream) {
     Ws ws;
+    adop_status cs = comm_check(comm);
+    if (cs) return cs;
     adop_status s = prologue(points, n_views, cameras, poses, params, fwd_views, workspace, workspace_bytes, true, ws);
     if (s) return s;
     if (!grad_image) return fail(ADOP_ERR_INVALID_ARGUMENT, "grad_image is NULL");
@@ -839,10 +848,14 @@ adop_status adop_rasterize_backward(const adop_points *points, int32_t n_views, 
             int e = launch_env_grad(a, stream);
             if (e) return cuda_status(e, "env gradient launch");
         }
-        return ok();
+    } else {
+        int e = launch_backward(a, model, vec_path(points), device_sms(), kMaxBwdBlocks, d_pose, stream);
+        if (e) return cuda_status(e, "backward launch");
     }
-    int e = launch_backward(a, model, vec_path(points), device_sms(), kMaxBwdBlocks, d_pose, stream);
-    if (e) return cuda_status(e, "backward launch");
+    const int64_t n_env = d_env ? (int64_t)params->env_width * params->env_height * points->channels : 0;
+    adop_status st = comm_grads(comm, points->n, points->channels, n_views, d_feat, d_pos, d_pose, d_intrinsics, d_env,
+                                n_env, stream);
+    if (st) return st;
     return ok();
 }
 

@@ -164,6 +164,13 @@ int launch_env_grad(const RasterArgs &a, void *stream);  // d_env only (zeroed f
 int launch_clear_pyr(uint64_t *keys, float *accum, float *count, int64_t P, int C, void *stream);
 int launch_tile_bounds(const float *x, const float *y, const float *z, int64_t n, float *out, void *stream);
 adop_status set_status(adop_status s, const char *msg);  // thread-local last-error message (adop_api.cu)
+// collectives of a communicator between the fused entry points' phases (adop_comm.cu; comm NULL: no-ops)
+adop_status comm_check(const adop_comm *comm);
+adop_status comm_keys(adop_comm *comm, const adop_pyramid *views, const int64_t *pixels, int32_t n_views, void *stream);
+adop_status comm_sums(adop_comm *comm, const adop_pyramid *views, const int64_t *pixels, int32_t n_views, int32_t C,
+                      void *stream);
+adop_status comm_grads(adop_comm *comm, int64_t n, int32_t C, int32_t n_views, float *d_feat, float *d_pos,
+                       double *d_pose, double *d_intr, float *d_env, int64_t n_env, void *stream);
 int backward_grid(int sms);
 
 }  // namespace adop

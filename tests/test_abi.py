@@ -62,7 +62,7 @@ def _call(points, cams, poses, params, pyrs, ws_ptr=256 * 1024, ws_bytes=1 << 30
     pa = (A.adop_pose * V)(*[A.pose_struct(p) for p in poses])
     py = (A.adop_pyramid * V)(*pyrs) if pyrs is not None else None
     st = A.lib().adop_rasterize_forward(C.byref(points), V, ca, pa, C.byref(params), py, C.c_void_p(ws_ptr),
-                                        ws_bytes, None)
+                                        ws_bytes, None, None)
     return st, A.lib().adop_last_error().decode()
 
 
@@ -106,7 +106,7 @@ def test_invalid_arguments_rejected_before_launch(mutate, expect):
     pa = (A.adop_pose * V)(*[A.pose_struct(p) for p in poses])
     py = (A.adop_pyramid * V)(*pyrs)
     st = A.lib().adop_rasterize_forward(C.byref(pts), V, ca, pa, C.byref(prm), py, C.c_void_p(256 * 1024),
-                                        1 << 30, None)
+                                        1 << 30, None, None)
     assert st == 1, st
     assert expect in A.lib().adop_last_error().decode()
 
@@ -149,3 +149,14 @@ def test_shared_pyramid_and_ipc_arguments_rejected():
     assert L.adop_ipc_open(None, 0, C.byref(b), C.byref(p)) == 1
     assert L.adop_ipc_open(h.raw, 0, None, C.byref(p)) == 1
     assert L.adop_ipc_close(None) == 1
+
+
+def test_comm_arguments_rejected_without_a_gpu():
+    """adop_comm_init validates its arguments before touching NCCL or the GPU."""
+    p = C.c_void_p()
+    uid = C.create_string_buffer(128)
+    assert A.lib().adop_comm_init(2, 2, uid, 0, 0, C.byref(p)) == 1 and not p.value
+    assert A.lib().adop_comm_init(0, 0, uid, 0, 0, C.byref(p)) == 1
+    assert A.lib().adop_comm_init(1, 0, uid, 7, 0, C.byref(p)) == 1
+    assert A.lib().adop_comm_init(1, 0, uid, 0, 4, C.byref(p)) == 1
+    assert A.lib().adop_comm_destroy(None) == 0
