@@ -987,6 +987,10 @@ adop_status adop_workspace_stats(const void *workspace, size_t workspace_bytes, 
 
 const char *adop_last_error(void) { return g_err; }
 
-const char *adop_version(void) { return "adop-b200 0.1 (sm_100a)"; }
+#if defined(ADOP_CHECKS) && ADOP_CHECKS
+const char *adop_version(void) { return "adop-b200 0.2 (sm_100a, bounds-checked)"; }
+#else
+const char *adop_version(void) { return "adop-b200 0.2 (sm_100a)"; }
+#endif
 
 }  // extern "C"

@@ -16,6 +16,7 @@
 // cloud in warp chunks of 128 points (4 consecutive points per lane, float4 loads
 // of the SoA rows), so every warp-collective below is warp-uniform.
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <atomic>
 #include <cstdlib>
@@ -23,6 +24,28 @@
 #include "adop_device.cuh"
 
 namespace adop {
+
+// Bounds-checked build (ADOP_CHECKS=1, scripts/build_variants.py chk=ADOP_CHECKS=1): every index into a pyramid,
+// a point array, the record region, the chunk tables or a shared-memory list is checked on the device; a
+// violation prints the check and traps (the run fails).  compute-sanitizer is closed on this GPU pool; the GPU
+// test suite runs against this build instead.
+#ifndef ADOP_CHECKS
+#define ADOP_CHECKS 0
+#endif
+#if ADOP_CHECKS
+#define ADOP_CHECK(cond)                                                                                         \
+    do {                                                                                                         \
+        if (!(cond)) {                                                                                           \
+            printf("ADOP_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                                 \
+            __trap();                                                                                            \
+        }                                                                                                        \
+    } while (0)
+#else
+#define ADOP_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -181,6 +204,7 @@ __device__ __forceinline__ void flush_records(const RasterArgs &a, Record *buf, 
 template <bool VEC4>
 __device__ __forceinline__ void accumulate_feature(const RasterArgs &a, const ViewDesc &v, int64_t idx,
                                                    uint32_t pix) {
+    ADOP_CHECK(idx >= 0 && idx < a.n && pix < (uint32_t)v.pixels);
     const int C = a.channels;
     const float *f = a.feat + idx * C;
     float *acc = v.accum + (int64_t)pix * C;
@@ -563,6 +587,7 @@ struct RecChunk {  // warp-uniform (pend: lane 0)
 
 // A chunk that could not be reserved has base = capacity: its records are dropped (overflow is set).
 __device__ __forceinline__ void put_record(const RasterArgs &a, unsigned long long slot, uint4 r) {
+    ADOP_CHECK(r.w == 0xFFFFFFFFu || (r.w < (uint32_t)a.nviews && r.x < (uint32_t)a.v[r.w].pixels && r.z < (uint64_t)a.n));
     if (slot < (unsigned long long)a.rec_capacity) reinterpret_cast<uint4 *>(a.records)[slot] = r;
 }
 
@@ -700,6 +725,8 @@ __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDes
             if (hit && hi == mhi && lo == mlo) red_min_u64_keep(v.keys + pix, key, policy_evict_last());
         }
 #else
+        ADOP_CHECK(!hit || (loc < v.wl[l] * v.hl[l] && (l + 1 >= ADOP_MAX_LAYERS || pix < (uint32_t)v.off[l + 1] ||
+                                                         l + 1 >= a.layers)));
         if (hit) red_min_u64_keep(v.keys + pix, key, policy_evict_last());
 #endif
         const unsigned b = __ballot_sync(kFull, hit);
@@ -783,6 +810,7 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
     if (b == 0u) return;
     if (nk > 0) {
         const int slot = qn + __popc(b & lt);
+        ADOP_CHECK(slot < kQCap && vs < 16);
         q.e[slot] = make_float4(p.u0, p.v0, p.D, __uint_as_float((uint32_t)i));
         q.meta[slot] = (uint8_t)(nk | (vs << 4));
     }
@@ -971,6 +999,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         for (int j = 0; j < 8; ++j) {
             const bool bit = (m >> j) & 1u;
             const unsigned b = __ballot_sync(kFull, bit);
+            ADOP_CHECK(!bit || cn + __popc(b & lt) < kWTile);
             if (bit) cl[cn + __popc(b & lt)] = (uint8_t)((j >> 2) * 128 + 4 * lane + (j & 3));
             cn += __popc(b);
         }
@@ -1427,6 +1456,7 @@ __device__ __forceinline__ void for_ordered(const RasterArgs &a, int list, F &&f
     const int lane = threadIdx.x & 31;
     for (unsigned long long j = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nch; j += W) {
         const unsigned long long base = (unsigned long long)a.corder[list][j] * kListChunk;
+        ADOP_CHECK(base + kListChunk <= (unsigned long long)a.rec_capacity);
 #pragma unroll
         for (int k = 0; k < kListChunk / (32 * STEP); ++k) f(base + (unsigned long long)STEP * (k * 32 + lane));
     }
@@ -1434,8 +1464,10 @@ __device__ __forceinline__ void for_ordered(const RasterArgs &a, int list, F &&f
 
 template <bool VEC4>
 __device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long long r) {
+    ADOP_CHECK(r < (unsigned long long)a.rec_capacity);
     const uint4 rec = __ldcs(reinterpret_cast<const uint4 *>(a.records) + r);
     if (rec.w == kDeadView) return;
+    ADOP_CHECK(rec.w < (uint32_t)a.nviews && rec.x < (uint32_t)a.v[rec.w].pixels && rec.z < (uint64_t)a.n);
     const ViewDesc &v = a.v[rec.w];
     const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(v.keys) + rec.x);
     if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
@@ -1987,6 +2019,7 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
             if (z > fmul(a.onepa, m)) continue;                       // case 2: behind
             factor = fmul(z, a.onepa) < m ? 1.0f : __frcp_rn(nq + 1.0f);  // case 3 / case 4
         }
+        ADOP_CHECK(q[k] < v.pixels);
         d[k] = factor * (row_dot<CT>(v.prow + (int64_t)q[k] * a.prow + 4, tau, C) - __uint_as_float(e[k].z));
     }
     const float sc = 0.5f * pow2_neg(l);  // layer-l pixels -> layer-0 pixels (R17)
@@ -2108,6 +2141,7 @@ __device__ __forceinline__ void red_add_row(float *dst, const float *src, int C,
 
 // texture gradient of one rendered hit (R24): fuzzy membership against the forward's key, G / |Lambda|
 __device__ __forceinline__ void tex_hit(const RasterArgs &a, const ViewDesc &v, uint32_t q, float z, int64_t idx) {
+    ADOP_CHECK(q < (uint32_t)v.pixels && idx >= 0 && idx < a.n);
     const float *row = v.prow + (int64_t)q * a.prow;
     const uint4 e = __ldcg(reinterpret_cast<const uint4 *>(row));
     if (!(z <= fmul(a.onepa, __uint_as_float(e.x)))) return;  // fuzzy test (Eq. 6, R9)
@@ -2295,6 +2329,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
                 const uint4 e0 = __ldcs(ent);
                 vs = (int)(e1.z & 0xFF);
                 const int nk = (int)(e1.z >> 8);
+                ADOP_CHECK(vs < a.nviews && nk >= 1 && nk <= a.layers && e1.y < (uint64_t)a.n);
                 const ViewDesc &v = a.v[vs];
                 Proj p;
                 p.u0 = __uint_as_float(e0.x);
