@@ -1,20 +1,21 @@
 // adop_kernels.cu -- sm_100a kernels of the ADOP one-pixel point rasterizer.
 //
-//   k_clear    keys <- sentinel, accum/count <- 0                          (§4.5 setup)
-//   k_stream   <DEPTH>  all points: project (Eq. 2), round (Eq. 3), bounds (Eq. 4),
-//                       ghost split (§4.3), discard (Eq. 12), 64-bit red.min of the packed
-//                       key per layer (§4.5 depth-only pass, min_z of Eq. 6), survivor records
-//              <BLEND>  overflow fallback: same sweep, fuzzy test + accumulate
-//              <MASKS>  debug/parity: per point per view layer mask
-//   k_blend    survivors: fuzzy test (Eq. 6) + vector red.add of tau and the count (§4.5)
-//   k_resolve  per pixel: Eq. 7 mean or background, planar NCHW output
-//   k_backward all points: texture gradient (R24) and ghost gradient Eqs. 9-11 + chain rule
-//              (Eq. 8) into d_pos and per-block tangent pose partials (Eq. 17)
-//   k_pose_reduce  deterministic fp64 sum of the per-block pose partials
+//   k_clear          keys <- sentinel + header / plane / layer tables (phase 1); accum, count <- 0 (phase 2)
+//   k_depth_pool     the depth-only pass (§4.5, min_z of Eq. 6) -- the hot kernel: TMA-streamed warp tiles from
+//                    a CTA-wide pool of stages; lane-box cull, hash-first discard prefilter (Eq. 12), exact
+//                    projection (Eqs. 2-4), 64-bit red.min of the packed keys (R8), survivor records
+//   k_depth_async    the same pass with per-warp 2-stage rings (tile culling / dynamic claiming; A/B reference)
+//   k_stream         fallback sweep for unaligned inputs <DEPTH>, the blend's overflow re-stream <BLEND>,
+//                    the per-point masks <MASKS>
+//   k_chunk_hist / k_chunk_scatter   view-major order of the multi-view lists' 64-slot chunks
+//   k_blend          survivor records: fuzzy test (Eq. 6) + vector red.add of tau and the count (§4.5)
+//   k_resolve        per pixel: Eq. 7 mean or background (constant or environment map), planar NCHW output
+//   k_fill / k_bwd_prep / k_bwd_sweep / k_bwd_tex / k_bwd_ghost / k_pose_reduce   the backward: zero fill and
+//                    mode choice, per-pixel tables, the re-render sweep (ghost list; texture list only when the
+//                    forward's records cannot be reused), texture gradient (R24), ghost gradient (Eqs. 9-11 +
+//                    chain rule, Eq. 8, Eq. 17), fixed-order fp64 pose reduction
+//   k_backward       fused planar backward for unaligned inputs
 //
-// Streaming kernels are persistent (grid = SMs x resident blocks) and walk the
-// cloud in warp chunks of 128 points (4 consecutive points per lane, float4 loads
-// of the SoA rows), so every warp-collective below is warp-uniform.
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -301,22 +302,24 @@ __global__ void __launch_bounds__(kThreads) k_stream(const __grid_constant__ Ras
 }
 
 // --------------------------------------------------------------------------- //
-// depth pass, async-copy pipelined (the hot kernel of the forward)
+// depth pass, TMA pipelined (k_depth_pool; k_depth_async with per-warp rings)
 //
-// Work unit = a warp tile of 256 consecutive (blocked-Morton ordered) points; warp w of the grid
-// takes tiles w, w + W, w + 2W, ...  Each lane owns 8 consecutive points and streams its own 16-byte
-// pieces of the x, y, z (and r_world) rows into a private 2-deep shared-memory ring with cp.async
-// (L2 evict-first): the next tile is in flight while the current one is processed, with no registers,
-// barriers or coupling between lanes or warps.  Per tile and view:
+// Work unit = a warp tile of 256 consecutive (blocked-Morton ordered) points.  Lane 0 of a warp streams a
+// tile's x, y, z rows with one 2-D TMA tensor copy (cp.async.bulk.tensor; 1-D bulk copies without a tensor
+// map) and the r_world row with a 1-D bulk copy (L2 evict-first) into a shared-memory stage guarded by an
+// mbarrier; the lane owns points h*128 + 4*lane + j so every LDS.128 of a row is one contiguous 512-B access.
+// k_depth_pool: the CTA's tiles k G + b cycle through a pool of kPool stages (see there); k_depth_async:
+// warp w of the grid takes tiles w, w + W, ... through a private 2-stage ring.  Per tile and view:
 //   1. lane-box cull: a lane whose 8-point bounding box lies outside one of 5 conservative world-space
-//      half-spaces skips its points; a warp whose lanes all agree skips the tile;
-//   2. per point, branch-free: FMA pre-cull + a conservative early discard test (Eq. 12 evaluated on
-//      a lower bound of z) -> candidate bit mask;
-//   3. candidates, one per lane per iteration: pinned transform (R1), validity (R7), exact discard
+//      half-spaces (pinhole frustum, or the OpenCV8 image window in normalized coordinates) skips its points;
+//      a warp whose lanes all agree skips the tile;
+//   2. discard on: the hash-first prefilter (Eq. 12 on the lane box's depth bound: one hash compare per
+//      point); discard off: a branch-free FMA pre-cull per point -> candidate bit mask, compacted per warp;
+//   3. candidates, 32 per iteration: pinned transform (R1), validity (R7), OpenCV8 window test, exact discard
 //      (R10), exact projection (R2/R6); kept points go to a warp queue;
 //   4. the queue is drained 32 at a time: per layer round + bounds (Eqs. 3-4), 64-bit red.min of the
-//      packed key (§4.5, R8) and survivor records, written straight to global memory into per-warp
-//      chunks of kChunk slots reserved with one atomic (unused slots are marked dead).
+//      packed key (§4.5, R8) and survivor records written straight to global memory into per-warp chunks
+//      (multi-view launches: per-view 64-slot chunks from a warp pool; unused slots are marked dead).
 // --------------------------------------------------------------------------- //
 constexpr int kStages = 2;   // backward sweep ring depth
 #ifndef ADOP_DSTAGES
@@ -1203,6 +1206,9 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
 // next free warp (the per-warp rings left the busy warp's prefetched tile idle).
 // --------------------------------------------------------------------------- //
 constexpr int kPool = 2 * kSW;
+#ifndef ADOP_POOL_SLEEP
+#define ADOP_POOL_SLEEP 64  // ns between polls of a stage whose refill is not issued yet
+#endif
 struct PoolSmem {
     float pos[kPool][4][kWTile];
     uint64_t bar[kPool];
@@ -1282,7 +1288,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
         const float *rp[4] = {sm.pos[s][0], sm.pos[s][1], sm.pos[s][2], sm.pos[s][3]};
         // the stage's barrier alternates parity per use: wait until tile k's copy was issued (tile k - kPool is then
         // done with the stage), so the parity names tile k's phase and not a later or earlier one
-        while (*(volatile int *)&sm.filled[s] != k) __nanosleep(64);
+        while (*(volatile int *)&sm.filled[s] != k) __nanosleep(ADOP_POOL_SLEEP);
         mbar_wait_a(bar0 + 8u * s, (uint32_t)(k / kPool) & 1u);
         int vmask = 0xFF;
         if (t >= nfull) {  // ragged last tile: guarded loads into the released stage
@@ -2447,7 +2453,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         const int st = k % kPool;
         const int64_t base = t * kWTile;
         const float *rp[4] = {sm.pos[st][0], sm.pos[st][1], sm.pos[st][2], sm.pos[st][3]};
-        while (*(volatile int *)&sm.filled[st] != k) __nanosleep(64);  // (see k_depth_pool)
+        while (*(volatile int *)&sm.filled[st] != k) __nanosleep(ADOP_POOL_SLEEP);  // (see k_depth_pool)
         mbar_wait(&sm.bar[st], (uint32_t)(k / kPool) & 1u);
         int vmask = 0xFF;
         if (!full_tile(t)) {
