@@ -481,19 +481,24 @@ void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const ado
         a.corder[1] = ws->corder1;
         a.ccount = ws->ccount;
         // per-view chunk lists for multi-view launches (the chunk slot index must fit 32 bits)
+        // (only for large launches: the chunk ordering costs three small launches, more than the view-major
+        // consumers save on configs[1]'s 4M point-views; configs[4] has 800M)
+        const bool large = pts->n * (int64_t)n_views >= ((int64_t)1 << 26);
         a.mv_lists = (n_views > 2 && vec_path(pts) && ws->capacity >= 64 * kListChunk &&
-                      ws->capacity < ((int64_t)1 << 32) - 256) ? 1 : 0;
+                      ws->capacity < ((int64_t)1 << 32) - 256) ? (large ? 1 : 2) : 0;  // 2: small launch
         {
-            // ADOP_MV_LISTS (A/B measurements): bit 0 lists on, bit 1 view-major texture consumer, bit 2
-            // view-major ghost consumer.  Default 5: the texture gradient keeps the lists' chunk order, in which
-            // a point's records of different views sit close together (its d_feat row is reused), while the
-            // blend and the ghost consumer gain more from one view's pixel state staying in L2.
+            // ADOP_MV_LISTS (A/B measurements, tests): bit 0 lists on, bit 1 view-major texture consumer, bit 2
+            // view-major ghost consumer, bit 3 also for small launches.  Default 5: the texture gradient keeps the
+            // lists' chunk order, in which a point's records of different views sit close together (its d_feat
+            // row is reused), while the blend and the ghost consumer gain more from one view's pixel state
+            // staying in L2.
             static int env = -1;
             if (env < 0) {
                 const char *e = std::getenv("ADOP_MV_LISTS");
                 env = e ? std::atoi(e) : 5;
             }
-            a.mv_lists = (a.mv_lists && (env & 1)) ? (env & 7) : 0;
+            const bool on = a.mv_lists == 1 || (a.mv_lists == 2 && (env & 8));
+            a.mv_lists = (on && (env & 1)) ? (env & 7) : 0;
         }
         a.tables = ws->tables;
         a.pose_partials = ws->partials;

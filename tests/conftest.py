@@ -8,6 +8,12 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# the multi-view chunk lists switch on only for large launches (n x views >= 2^26); the GPU tests force them for
+# every multi-view launch (ADOP_MV_LISTS bit 3) so the small parity cases exercise them too
+# (test_multi_view_list_orders runs the default and the flat lists in subprocesses)
+os.environ.setdefault("ADOP_MV_LISTS", "13")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: longer CPU test")
