@@ -727,6 +727,21 @@ def run_reference(args, rank, world):
             "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def nccl_summary(path):
+    """Whether NCCL set up NVLink SHARP (NVLS) and which algorithms its tuner reported (rank 0's log)."""
+    try:
+        txt = open(path).read()
+    except OSError:
+        return {"log": None}
+    lines = [l.strip() for l in txt.splitlines()]
+    nvls = [l for l in lines if "NVLS" in l]
+    return {"log": path, "nvls_lines": len(nvls), "nvls_enabled": any("NVLS" in l and ("enabled" in l.lower() or
+                                                                                       "multicast" in l.lower() or
+                                                                                       "comm" in l.lower())
+                                                                       for l in nvls),
+            "nvls_sample": nvls[:3], "version": next((l for l in lines if "NCCL version" in l), None)}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -739,12 +754,19 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    nccl_log = None
     if world > 1:
+        # NCCL's own log (to a file, not stdout) tells whether the collectives ran on NVLink SHARP (NVLS)
+        if "NCCL_DEBUG" not in os.environ:
+            nccl_log = f"/tmp/adop_bench_nccl_{os.getpid()}_rank{rank}.log"
+            os.environ.update({"NCCL_DEBUG": "INFO", "NCCL_DEBUG_SUBSYS": "INIT,TUNING", "NCCL_DEBUG_FILE": nccl_log})
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.mode == "view":
         out = run_view(args, rank, world, local_rank)
         if rank == 0:
+            if nccl_log:
+                out["nccl"] = nccl_summary(nccl_log)
             print(json.dumps(out), flush=True)
         if world > 1:
             dist.barrier()
@@ -762,6 +784,8 @@ def main():
             dev = ctx[0]
             del ctx
             out["secondary"] = run_secondary(args, dev)
+        if nccl_log:
+            out["nccl"] = nccl_summary(nccl_log)
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -637,6 +637,53 @@ __device__ __forceinline__ void rec_reserve(const RasterArgs &a, RecChunk &c, in
     c.left = kChunk;
 }
 
+// ---- work lists shared by the sweeps (front: records; back: ghost entries / depth candidates) ----
+constexpr uint32_t kDead = 0xFFFFFFFFu;
+
+struct ListChunk {  // warp-uniform per-warp chunk of a work list
+    unsigned long long base;  // slot of the next free item
+    int left;                 // items left in the chunk; -1: the list is full (process inline)
+};
+
+// Mark the chunk's unused items dead (front: Record.view, back: GhostEntry.vsnk).
+template <bool BACK>
+__device__ __forceinline__ void list_close(const RasterArgs &a, const ListChunk &c, int lane) {
+    uint4 *r = reinterpret_cast<uint4 *>(a.records);
+    for (int k = lane; k < c.left; k += 32) {
+        if (BACK)
+            r[c.base + 2ull * k + 1] = make_uint4(0u, 0u, kDead, kDead);
+        else
+            r[c.base + k] = make_uint4(0u, 0u, 0u, kDead);
+    }
+}
+
+// Slots for the lanes in ballot b (front: 1 slot per item, back: 2); returns the lane's slot, or kNoSlot
+// when the record region is full (the caller processes its item inline).  Warp-collective.
+template <bool BACK>
+__device__ __forceinline__ unsigned long long list_take(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
+                                                        int lane, unsigned lt) {
+    constexpr int W = BACK ? 2 : 1;
+    const int nb = __popc(b);
+    if (c.left >= 0 && nb > c.left) {
+        list_close<BACK>(a, c, lane);
+        unsigned long long s = 0;
+        if (lane == 0) s = resv_take<BACK>(a, kChunk, false);
+        s = __shfl_sync(kFull, s, 0);
+        if (s == kNoSlot) {
+            c.left = -1;
+        } else {
+            c.base = s;
+            c.left = kChunk / W;
+        }
+    }
+    if (c.left < 0) return kNoSlot;
+    const unsigned long long slot = c.base + (unsigned long long)W * __popc(b & lt);
+    c.base += (unsigned long long)W * nb;
+    c.left -= nb;
+    return mine ? slot : kNoSlot;
+}
+
+
 // Multi-view lists (RasterArgs::mv_lists): every kListChunk-slot chunk of the survivor list holds one view's
 // records.  Lane w of the warp keeps view w's open chunk in c.base (the next free slot; a multiple of
 // kListChunk means no room left).  The lanes of ballot b (record `rec` each, view `vs`) append to their
@@ -912,10 +959,11 @@ __device__ __forceinline__ void ensure_r(LazyR &r, int lane) {
 
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
-template <int MODEL, int VM, bool DISC>
+template <int MODEL, int VM, bool DISC, bool SPLIT = false>
 __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
-                                            uint8_t *cl, int lane, unsigned lt, uint32_t pre_views, LazyR &lr) {
+                                            uint8_t *cl, int lane, unsigned lt, uint32_t pre_views, LazyR &lr,
+                                            ListChunk *cc = nullptr) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     // ghosts take no part in the depth test (§4.3): their mask is hashed at the tile's first visible view
     uint32_t live = (uint32_t)vmask;
@@ -1009,9 +1057,20 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         __syncwarp();
         CNT(2, cn);
         for (int i0 = 0; i0 < cn; i0 += 32) {
-            const bool ok = i0 + lane < cn;
+            bool ok = i0 + lane < cn;
             const int e = ok ? cl[i0 + lane] : 0;
             const float rw = staged_r ? rows[3][e] : a.radius_uniform;
+            if (SPLIT) {  // hand the candidate to k_depth_exact: {x, y, z, r_world}, {index, view, live} in the back list
+                const unsigned long long slot = list_take<true>(a, *cc, __ballot_sync(kFull, ok), ok, lane, lt);
+                if (ok && slot != kNoSlot) {
+                    uint4 *r = reinterpret_cast<uint4 *>(a.records) + slot;
+                    r[0] = make_uint4(__float_as_uint(rows[0][e]), __float_as_uint(rows[1][e]), __float_as_uint(rows[2][e]),
+                                      __float_as_uint(rw));
+                    r[1] = make_uint4((uint32_t)(base + e), (uint32_t)vs, 0u, 0u);
+                    ok = false;
+                }
+                if (!__any_sync(kFull, ok)) continue;  // (the region is full: the rest is processed here)
+            }
             depth_candidate<MODEL, VM != 0 || MODEL != 0, VM == 2>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
                                    a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
         }
@@ -1219,7 +1278,7 @@ struct PoolSmem {
 };
 static_assert(sizeof(PoolSmem) + 1024 <= 228 * 1024 / kDCTAs, "pooled depth sweep: kDCTAs CTAs per SM must fit");
 
-template <int MODEL, int VM, bool DISC>
+template <int MODEL, int VM, bool DISC, bool SPLIT>
 __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
@@ -1277,6 +1336,9 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
 #endif
     LazyR lr;
     lr.src = nullptr;
+    ListChunk cc;  // SPLIT: this warp's chunk of the candidate list
+    cc.base = 0;
+    cc.left = 0;
     for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(&sm.next, 1);
@@ -1304,17 +1366,65 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
             __syncwarp();
         }
         CNT(0, 1);
-        depth_lane8<MODEL, VM, DISC>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt,
-                                     0xFFFFFFFFu, lr);
+        depth_lane8<MODEL, VM, DISC, SPLIT>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt,
+                                            0xFFFFFFFFu, lr, &cc);
         __syncwarp();  // every lane is done with stage s
         if (lane == 0) issue(k + kPool);
         __syncwarp();
     }
+    if (SPLIT) list_close<true>(a, cc, lane);
     if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
     if (VM == 2 && a.mv_lists)
         mv_close(a, c, lane);
     else
         rec_reserve(a, c, lane, false);
+}
+
+// The exact part of a split depth pass (ADOP_DEPTH_SPLIT): the candidates k_depth_pool<SPLIT> compacted into the
+// back list -- 32 per warp iteration, every warp busy -- through the same exact path, queue and drains.  The cull
+// kernel then streams the cloud with little per-tile work and no long visible-tile latency chains, which kept
+// its loaded stages waiting; the candidates (1.57M on configs[3]) cost 32 B written and read each.
+struct ExactSmem {
+    WarpQueue q[kWarps];
+};
+template <int MODEL, int VM>
+__global__ void __launch_bounds__(kThreads) k_depth_exact(const __grid_constant__ RasterArgs a) {
+    __shared__ ExactSmem sm;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    const unsigned long long back = *(volatile unsigned long long *)&a.hdr->back_ok;
+    const uint4 *list = reinterpret_cast<const uint4 *>(a.records) + ((unsigned long long)a.rec_capacity - back);
+    const unsigned long long total = back / 2;
+    WarpQueue &q = sm.q[wid];
+    int qn = 0;
+    RecChunk c;
+    c.base = 0;
+    c.left = 0;
+#if ADOP_CHUNK_PREFETCH
+    c.has = false;
+    c.pend = 0;
+#endif
+    const unsigned long long W = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp
+    for (unsigned long long j0 = gw * 32; j0 < total; j0 += W * 32) {
+        const unsigned long long j = j0 + lane;
+        bool ok = j < total;
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = make_uint4(0u, 0u, kDead, 0u);
+        if (ok) {
+            e1 = __ldcs(list + 2 * j + 1);
+            ok = e1.z != kDead;
+            if (ok) e0 = __ldcs(list + 2 * j);
+        }
+        const int vs = ok ? (int)e1.y : 0;
+        ADOP_CHECK(!ok || (vs < a.nviews && e1.x < (uint64_t)a.n));
+        // (single-view instances: vs = 0 for every candidate, so the warp-uniform view argument holds)
+        depth_candidate<MODEL, VM != 0 || MODEL != 0, VM == 2>(a, a.v[VM == 0 ? 0 : vs], vs, ok, __uint_as_float(e0.x),
+                                                               __uint_as_float(e0.y), __uint_as_float(e0.z),
+                                                               __uint_as_float(e0.w), (int64_t)e1.x, a.goff + e1.x,
+                                                               a.ldesc, q, qn, c, lane, lt);
+    }
+    if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
+    rec_reserve(a, c, lane, false);
 }
 
 // Shared-pyramid reset (adop_clear_pyramid): keys <- sentinel, accum / count <- 0.
@@ -1481,6 +1591,10 @@ __device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long 
 
 template <int MODEL, bool VEC, bool VEC4, bool HOCC>
 __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_constant__ RasterArgs a) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // a split depth pass's candidate list is consumed: drop it
+        a.hdr->back_ok = 0ull;
+        a.hdr->resv = *(volatile unsigned long long *)&a.hdr->front_ok;
+    }
     if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
         stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
         return;
@@ -2036,51 +2150,6 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
 // ---- record-driven backward: work lists in the record region, two balanced kernels consume them ----
 // Texture list = the front list (Record layout): the depth pass's survivor records (mode 1) or the
 // sweep's rendered hits (mode 0).  Ghost list = the back list (GhostEntry layout), written by the sweep.
-constexpr uint32_t kDead = 0xFFFFFFFFu;
-
-struct ListChunk {  // warp-uniform per-warp chunk of a work list
-    unsigned long long base;  // slot of the next free item
-    int left;                 // items left in the chunk; -1: the list is full (process inline)
-};
-
-// Mark the chunk's unused items dead (front: Record.view, back: GhostEntry.vsnk).
-template <bool BACK>
-__device__ __forceinline__ void list_close(const RasterArgs &a, const ListChunk &c, int lane) {
-    uint4 *r = reinterpret_cast<uint4 *>(a.records);
-    for (int k = lane; k < c.left; k += 32) {
-        if (BACK)
-            r[c.base + 2ull * k + 1] = make_uint4(0u, 0u, kDead, kDead);
-        else
-            r[c.base + k] = make_uint4(0u, 0u, 0u, kDead);
-    }
-}
-
-// Slots for the lanes in ballot b (front: 1 slot per item, back: 2); returns the lane's slot, or kNoSlot
-// when the record region is full (the caller processes its item inline).  Warp-collective.
-template <bool BACK>
-__device__ __forceinline__ unsigned long long list_take(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
-                                                        int lane, unsigned lt) {
-    constexpr int W = BACK ? 2 : 1;
-    const int nb = __popc(b);
-    if (c.left >= 0 && nb > c.left) {
-        list_close<BACK>(a, c, lane);
-        unsigned long long s = 0;
-        if (lane == 0) s = resv_take<BACK>(a, kChunk, false);
-        s = __shfl_sync(kFull, s, 0);
-        if (s == kNoSlot) {
-            c.left = -1;
-        } else {
-            c.base = s;
-            c.left = kChunk / W;
-        }
-    }
-    if (c.left < 0) return kNoSlot;
-    const unsigned long long slot = c.base + (unsigned long long)W * __popc(b & lt);
-    c.base += (unsigned long long)W * nb;
-    c.left -= nb;
-    return mine ? slot : kNoSlot;
-}
-
 // Multi-view ghost list (RasterArgs::mv_lists): like mv_put for the back list -- lane vs keeps view vs's open
 // chunk in c.base (next free slot; 2 slots per ghost entry); all items of a call share the warp-uniform view
 // slot vs.  Returns the lane's slot or kNoSlot (region full: processed inline).  Warp-collective.
@@ -2641,10 +2710,21 @@ static bool depth_pool_enabled() {  // ADOP_DEPTH_POOL=0: the per-warp-ring dept
     return env != 0;
 }
 
+static bool depth_split_enabled() {  // ADOP_DEPTH_SPLIT=1: cull kernel + exact kernel (single-view launches)
+    static int env = -1;
+    if (env < 0) {
+        const char *e = std::getenv("ADOP_DEPTH_SPLIT");
+        env = e ? std::atoi(e) : 0;
+    }
+    return env != 0;
+}
+
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
     if (depth_pool_enabled() && !a.tbounds && !(a.dyn_tiles & 1)) {
-        auto kp = a.discard ? k_depth_pool<MODEL, VM, true> : k_depth_pool<MODEL, VM, false>;
+        const bool split = VM == 0 && depth_split_enabled();
+        auto kp = split ? (a.discard ? k_depth_pool<MODEL, VM, true, true> : k_depth_pool<MODEL, VM, false, true>)
+                        : (a.discard ? k_depth_pool<MODEL, VM, true, false> : k_depth_pool<MODEL, VM, false, false>);
         if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PoolSmem)) !=
             cudaSuccess)
             return (int)cudaGetLastError();
@@ -2656,6 +2736,13 @@ static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
         if ((tiles + kSW - 1) / kSW < g) g = (tiles + kSW - 1) / kSW;
         if (g < 1) g = 1;
         kp<<<(unsigned)g, kST, sizeof(PoolSmem), (cudaStream_t)stream>>>(a);
+        if (split) {
+            if constexpr (VM == 0) {
+                int pe = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pe, k_depth_exact<MODEL, VM>, kThreads, 0);
+                k_depth_exact<MODEL, VM><<<(unsigned)(sms * (pe < 1 ? 1 : pe)), kThreads, 0, (cudaStream_t)stream>>>(a);
+            }
+        }
         return (int)cudaGetLastError();
     }
     auto k = a.discard ? k_depth_async<MODEL, VM, true> : k_depth_async<MODEL, VM, false>;
