@@ -959,11 +959,19 @@ __device__ __forceinline__ void ensure_r(LazyR &r, int lane) {
 
 // The lane's 8 points of one warp tile (tile base index `base`, valid-point bit mask `vmask`), all views,
 // read from the warp tile's shared-memory rows.
-template <int MODEL, int VM, bool DISC, bool SPLIT = false>
-__device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
+struct NoRelease {
+    __device__ __forceinline__ void operator()() const {}
+};
+// EARLY (single-view pool kernel): a tile with at most kCBuf candidates copies their x, y, z, r_world into the warp's
+// candidate buffer `cbuf` and calls release() -- the stage is refilled while the exact path runs from the copy, so a
+// visible tile no longer holds its stage through the latency-bound exact path and drains.  Returns true if
+// release() was called.
+constexpr int kCBuf = 64;
+template <int MODEL, int VM, bool DISC, bool SPLIT = false, bool EARLY = false, typename Rel = NoRelease>
+__device__ __forceinline__ bool depth_lane8(const RasterArgs &a, const float *const *rows, int64_t base, int vmask,
                                             bool staged_r, const LayerDesc *ld, WarpQueue &q, int &qn, RecChunk &c,
                                             uint8_t *cl, int lane, unsigned lt, uint32_t pre_views, LazyR &lr,
-                                            ListChunk *cc = nullptr) {
+                                            ListChunk *cc = nullptr, float4 *cbuf = nullptr, Rel &&release = Rel()) {
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     // ghosts take no part in the depth test (§4.3): their mask is hashed at the tile's first visible view
     uint32_t live = (uint32_t)vmask;
@@ -1056,6 +1064,25 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         }
         __syncwarp();
         CNT(2, cn);
+        if constexpr (EARLY && VM == 0) {
+            if (cn <= kCBuf) {
+                for (int k = lane; k < cn; k += 32) {
+                    const int e = cl[k];
+                    cbuf[k] = make_float4(rows[0][e], rows[1][e], rows[2][e], staged_r ? rows[3][e] : a.radius_uniform);
+                }
+                __syncwarp();
+                release();  // the stage is free: refilled while the exact path runs from the copy
+                for (int i0 = 0; i0 < cn; i0 += 32) {
+                    const bool ok = i0 + lane < cn;
+                    const int e = ok ? cl[i0 + lane] : 0;
+                    const float4 pc = cbuf[ok ? i0 + lane : 0];
+                    depth_candidate<MODEL, MODEL != 0, false>(a, v, vs, ok, pc.x, pc.y, pc.z, pc.w, base + e,
+                                                              a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
+                }
+                __syncwarp();
+                return true;
+            }
+        }
         for (int i0 = 0; i0 < cn; i0 += 32) {
             bool ok = i0 + lane < cn;
             const int e = ok ? cl[i0 + lane] : 0;
@@ -1076,6 +1103,7 @@ __device__ __forceinline__ void depth_lane8(const RasterArgs &a, const float *co
         }
         __syncwarp();  // the list is rewritten by the next view / tile
     }
+    return false;
 }
 
 static_assert(sizeof(DepthSmem) + 1024 <= 228 * 1024 / kDCTAs, "depth sweep: kDCTAs CTAs per SM must fit in shared memory");
@@ -1264,7 +1292,13 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
 // for a particular warp: a warp busy with a visible tile holds one stage, every other loaded stage goes to the
 // next free warp (the per-warp rings left the busy warp's prefetched tile idle).
 // --------------------------------------------------------------------------- //
-constexpr int kPool = 2 * kSW;
+#ifndef ADOP_POOL_STAGES
+#define ADOP_POOL_STAGES 16  // (14 with the early-release candidate buffers)
+#endif
+#ifndef ADOP_EARLY_RELEASE
+#define ADOP_EARLY_RELEASE 0  // measured: no gain (profiles/r02/evolution.md)
+#endif
+constexpr int kPool = ADOP_POOL_STAGES;
 #ifndef ADOP_POOL_SLEEP
 #define ADOP_POOL_SLEEP 64  // ns between polls of a stage whose refill is not issued yet
 #endif
@@ -1275,6 +1309,9 @@ struct PoolSmem {
     int next;
     WarpQueue q[kSW];
     uint8_t cand[kSW][kWTile];
+#if ADOP_EARLY_RELEASE
+    float4 cbuf[kSW][kCBuf];  // early release: the warp's candidates of its current tile
+#endif
 };
 static_assert(sizeof(PoolSmem) + 1024 <= 228 * 1024 / kDCTAs, "pooled depth sweep: kDCTAs CTAs per SM must fit");
 
@@ -1322,7 +1359,7 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
     };
     if (lane == 0) {
         issue(wid);
-        issue(wid + kSW);
+        if (wid + kSW < kPool) issue(wid + kSW);
     }
     __syncwarp();
     WarpQueue &q = sm.q[wid];
@@ -1366,11 +1403,21 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
             __syncwarp();
         }
         CNT(0, 1);
-        depth_lane8<MODEL, VM, DISC, SPLIT>(a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt,
-                                            0xFFFFFFFFu, lr, &cc);
+        constexpr bool kEarly = ADOP_EARLY_RELEASE && VM == 0 && !SPLIT;
+        auto rel = [&]() {
+            if (lane == 0) issue(k + kPool);
+            __syncwarp();
+        };
+        const bool released = depth_lane8<MODEL, VM, DISC, SPLIT, kEarly>(
+            a, rp, base, vmask, staged_r, a.ldesc, q, qn, c, sm.cand[wid], lane, lt, 0xFFFFFFFFu, lr, &cc,
+#if ADOP_EARLY_RELEASE
+            sm.cbuf[wid],
+#else
+            nullptr,
+#endif
+            rel);
         __syncwarp();  // every lane is done with stage s
-        if (lane == 0) issue(k + kPool);
-        __syncwarp();
+        if (!released) rel();
     }
     if (SPLIT) list_close<true>(a, cc, lane);
     if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
@@ -2461,7 +2508,7 @@ struct BwdSmem {  // CTA-wide pool of kPool stages, claimed like k_depth_pool's
 };
 
 static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 3, "backward sweep: 3 CTAs per SM must fit in shared memory");
-static_assert(kPool == 2 * kSW, "the sweeps' initial fills issue two stages per warp");
+static_assert(kPool >= kSW && kPool <= 2 * kSW, "the sweeps' initial fills issue at most two stages per warp");
 
 // GO (ghosts only) is launched for mode 1, !GO for mode 0; the instance not matching the mode exits.
 template <int MODEL, int CT, bool MV, bool GO>
@@ -2510,7 +2557,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
     };
     if (lane == 0) {
         issue(wid);
-        issue(wid + kSW);
+        if (wid + kSW < kPool) issue(wid + kSW);
     }
     __syncwarp();
     for (;;) {
