@@ -1299,13 +1299,18 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_async(const __grid_consta
 #define ADOP_EARLY_RELEASE 0  // measured: no gain (profiles/r02/evolution.md)
 #endif
 constexpr int kPool = ADOP_POOL_STAGES;
+#ifndef ADOP_PCTAS
+#define ADOP_PCTAS 3  // pooled depth sweep CTAs per SM
+#endif
+constexpr int kPCTAs = ADOP_PCTAS;
 #ifndef ADOP_POOL_SLEEP
 #define ADOP_POOL_SLEEP 64  // ns between polls of a stage whose refill is not issued yet
 #endif
-struct PoolSmem {
-    float pos[kPool][4][kWTile];
-    uint64_t bar[kPool];
-    int filled[kPool];  // the k whose copy into the stage was issued last (phase-unambiguous waits)
+template <int NP>
+struct PoolSmemT {
+    float pos[NP][4][kWTile];
+    uint64_t bar[NP];
+    int filled[NP];  // the k whose copy into the stage was issued last (phase-unambiguous waits)
     int next;
     WarpQueue q[kSW];
     uint8_t cand[kSW][kWTile];
@@ -1313,10 +1318,17 @@ struct PoolSmem {
     float4 cbuf[kSW][kCBuf];  // early release: the warp's candidates of its current tile
 #endif
 };
-static_assert(sizeof(PoolSmem) + 1024 <= 228 * 1024 / kDCTAs, "pooled depth sweep: kDCTAs CTAs per SM must fit");
+// Single-view launches: 4 CTAs x 11 stages per SM (32 warps; headline depth -2%); multi-view ones keep 3 x 16
+// (configs[4] forward +5% with 4 x 11): profiles/r02/evolution.md.
+constexpr int kPoolSV = 11, kPoolMV = kPool;
+template <int NP> constexpr int pool_ctas() { return NP == kPoolSV ? 4 : kPCTAs; }
+static_assert(sizeof(PoolSmemT<kPoolSV>) + 1024 <= 228 * 1024 / 4, "pooled depth sweep: 4 CTAs x 11 stages per SM");
+static_assert(sizeof(PoolSmemT<kPoolMV>) + 1024 <= 228 * 1024 / kPCTAs, "pooled depth sweep: kPCTAs CTAs per SM must fit");
 
-template <int MODEL, int VM, bool DISC, bool SPLIT>
-__global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constant__ RasterArgs a) {
+template <int MODEL, int VM, bool DISC, bool SPLIT, int NP>
+__global__ void __launch_bounds__(kST, pool_ctas<NP>()) k_depth_pool(const __grid_constant__ RasterArgs a) {
+    constexpr int kPool = NP;
+    using PoolSmem = PoolSmemT<NP>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1357,10 +1369,8 @@ __global__ void __launch_bounds__(kST, kDCTAs) k_depth_pool(const __grid_constan
         }
         if (rows == 4) bulk_g2s_a(dst + 3 * kRowBytes, a.radius + (int64_t)t * kWTile, kRowBytes, bar, pol);
     };
-    if (lane == 0) {
-        issue(wid);
-        if (wid + kSW < kPool) issue(wid + kSW);
-    }
+    if (lane == 0)
+        for (int k0 = wid; k0 < kPool; k0 += kSW) issue(k0);
     __syncwarp();
     WarpQueue &q = sm.q[wid];
     int qn = 0;
@@ -2498,17 +2508,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_bwd_ghost(const __grid_constant
     }
 }
 
-struct BwdSmem {  // CTA-wide pool of kPool stages, claimed like k_depth_pool's
-    float pos[kPool][4][kWTile];
-    uint64_t bar[kPool];
-    int filled[kPool];
+constexpr int kBPool = 2 * kSW;  // backward sweep stage pool
+struct BwdSmem {  // CTA-wide pool of kBPool stages, claimed like k_depth_pool's
+    float pos[kBPool][4][kWTile];
+    uint64_t bar[kBPool];
+    int filled[kBPool];
     int next;
     LayerDesc ld[ADOP_MAX_VIEWS_PER_LAUNCH];
     uint8_t gl[kSW][kWTile];  // mode 1: compacted ghost points of the warp tile (tile offsets)
 };
 
 static_assert(sizeof(BwdSmem) + 1024 <= 228 * 1024 / 3, "backward sweep: 3 CTAs per SM must fit in shared memory");
-static_assert(kPool >= kSW && kPool <= 2 * kSW, "the sweeps' initial fills issue at most two stages per warp");
+static_assert(kBPool >= kSW && kBPool <= 3 * kSW, "the sweeps' initial fills issue at most three stages per warp");
 
 // GO (ghosts only) is launched for mode 1, !GO for mode 0; the instance not matching the mode exits.
 template <int MODEL, int CT, bool MV, bool GO>
@@ -2527,7 +2538,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
     const int rows = staged_r ? 4 : 3;
     const float *src[4] = {a.x, a.y, a.z, a.radius};
     init_layer_descs(a, sm.ld);
-    if (tid < kPool) {
+    if (tid < kBPool) {
         mbar_init(&sm.bar[tid], 1);
         sm.filled[tid] = -1;
     }
@@ -2536,10 +2547,10 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
     __syncthreads();
     const long long G = gridDim.x, bk = blockIdx.x;
     auto full_tile = [&](long long t) { return (t + 1) * kWTile <= a.n; };
-    auto issue = [&](int k) {  // lane 0: the CTA's k-th tile (k G + b) into stage k mod kPool
+    auto issue = [&](int k) {  // lane 0: the CTA's k-th tile (k G + b) into stage k mod kBPool
         const long long t = (long long)k * G + bk;
         if (t >= ntiles) return;
-        const int st = k % kPool;
+        const int st = k % kBPool;
         *(volatile int *)&sm.filled[st] = k;
         if (!full_tile(t)) {  // ragged last tile: its consumer loads it; the arrival only releases the stage
             mbar_arrive_a(smem_addr(&sm.bar[st]));
@@ -2555,10 +2566,8 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                 bulk_g2s(sm.pos[st][r], src[r] + t * kWTile, kWTile * sizeof(float), &sm.bar[st], pol);
         }
     };
-    if (lane == 0) {
-        issue(wid);
-        if (wid + kSW < kPool) issue(wid + kSW);
-    }
+    if (lane == 0)
+        for (int k0 = wid; k0 < kBPool; k0 += kSW) issue(k0);
     __syncwarp();
     for (;;) {
         int k = 0;
@@ -2566,11 +2575,11 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
         k = __shfl_sync(kFull, k, 0);
         const long long t = (long long)k * G + bk;
         if (t >= ntiles) break;
-        const int st = k % kPool;
+        const int st = k % kBPool;
         const int64_t base = t * kWTile;
         const float *rp[4] = {sm.pos[st][0], sm.pos[st][1], sm.pos[st][2], sm.pos[st][3]};
         while (*(volatile int *)&sm.filled[st] != k) __nanosleep(ADOP_POOL_SLEEP);  // (see k_depth_pool)
-        mbar_wait(&sm.bar[st], (uint32_t)(k / kPool) & 1u);
+        mbar_wait(&sm.bar[st], (uint32_t)(k / kBPool) & 1u);
         int vmask = 0xFF;
         if (!full_tile(t)) {
             vmask = 0;
@@ -2638,7 +2647,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
                 }
             }
             __syncwarp();  // the ghost list is rewritten by the next tile; every lane is done with the stage
-            if (lane == 0) issue(k + kPool);
+            if (lane == 0) issue(k + kBPool);
             __syncwarp();
             continue;
         }
@@ -2680,7 +2689,7 @@ __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ Ra
             }
         }
         __syncwarp();
-        if (lane == 0) issue(k + kPool);
+        if (lane == 0) issue(k + kBPool);
         __syncwarp();
     }
     list_close<false>(a, ct, lane);
@@ -2769,9 +2778,11 @@ static bool depth_split_enabled() {  // ADOP_DEPTH_SPLIT=1: cull kernel + exact 
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
     if (depth_pool_enabled() && !a.tbounds && !(a.dyn_tiles & 1)) {
+        constexpr int NP = VM == 0 ? kPoolSV : kPoolMV;
+        using PoolSmem = PoolSmemT<NP>;
         const bool split = VM == 0 && depth_split_enabled();
-        auto kp = split ? (a.discard ? k_depth_pool<MODEL, VM, true, true> : k_depth_pool<MODEL, VM, false, true>)
-                        : (a.discard ? k_depth_pool<MODEL, VM, true, false> : k_depth_pool<MODEL, VM, false, false>);
+        auto kp = split ? (a.discard ? k_depth_pool<MODEL, VM, true, true, NP> : k_depth_pool<MODEL, VM, false, true, NP>)
+                        : (a.discard ? k_depth_pool<MODEL, VM, true, false, NP> : k_depth_pool<MODEL, VM, false, false, NP>);
         if (cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PoolSmem)) !=
             cudaSuccess)
             return (int)cudaGetLastError();
