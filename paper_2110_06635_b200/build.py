@@ -38,8 +38,9 @@ SPLIT = 16
 ROUNDS = 3
 SPILL_OK = 300  # every hot instance within its limit (an instance over its limit adds 100000)
 HOT = {  # hot instances -> accepted spill-store bytes (tests/test_build_spills.py checks the kept build)
-    "_ZN4adop13k_depth_asyncILi0ELi0ELb1EEEvNS_10RasterArgsE": 0,     # configs[3] headline depth sweep
-    "_ZN4adop13k_depth_asyncILi1ELi2ELb1EEEvNS_10RasterArgsE": 32,    # configs[4] multi-view depth sweep
+    "_ZN4adop12k_depth_poolILi0ELi0ELb1ELb0ELi11EEEvNS_10RasterArgsE": 0,   # configs[3] headline depth sweep
+    "_ZN4adop12k_depth_poolILi1ELi0ELb1ELb0ELi11EEEvNS_10RasterArgsE": 0,   # configs[2] depth sweep
+    "_ZN4adop12k_depth_poolILi1ELi2ELb1ELb0ELi16EEEvNS_10RasterArgsE": 32,  # configs[4] multi-view depth sweep
     "_ZN4adop11k_bwd_sweepILi1ELi4ELb1ELb1EEEvNS_10RasterArgsE": 0,   # configs[4] ghost-only backward sweep
     "_ZN4adop11k_bwd_sweepILi1ELi8ELb0ELb1EEEvNS_10RasterArgsE": 40,  # configs[2] ghost-only backward sweep
     "_ZN4adop11k_bwd_ghostILi1ELi4ELi6EEEvNS_10RasterArgsE": 0,       # configs[4] ghost consumer
