@@ -784,6 +784,18 @@ def main():
             dev = ctx[0]
             del ctx
             out["secondary"] = run_secondary(args, dev)
+    if world > 1 and not args.no_secondary:
+        # the other partitioning of the north star in the same N-GPU run: the configs[4] training step,
+        # view-sharded (16 views over N ranks, SUM of the point gradients), so the driver's scaling run measures both
+        ctx = None
+        torch.cuda.empty_cache()
+        vargs = argparse.Namespace(**{**vars(args), "steps": min(args.steps, 10), "warmup": 3})
+        vout = run_view(vargs, rank, world, local_rank)
+        if rank == 0:
+            keep = ("metric", "value", "unit", "ms_per_step", "phases_ms_median_rank0", "ms_per_step_stats",
+                    "roofline", "config", "comm")
+            out["view_sharded"] = {k: vout[k] for k in keep if k in vout}
+    if rank == 0:
         if nccl_log:
             out["nccl"] = nccl_summary(nccl_log)
         print(json.dumps(out), flush=True)
