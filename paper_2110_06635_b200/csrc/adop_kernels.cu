@@ -1306,6 +1306,7 @@ constexpr int kPCTAs = ADOP_PCTAS;
 #ifndef ADOP_POOL_SLEEP
 #define ADOP_POOL_SLEEP 64  // ns between polls of a stage whose refill is not issued yet
 #endif
+constexpr int kPoolSV = 11, kPoolMV = kPool;
 template <int NP>
 struct PoolSmemT {
     float pos[NP][4][kWTile];
@@ -1320,7 +1321,6 @@ struct PoolSmemT {
 };
 // Single-view launches: 4 CTAs x 11 stages per SM (32 warps; headline depth -2%); multi-view ones keep 3 x 16
 // (configs[4] forward +5% with 4 x 11): profiles/r02/evolution.md.
-constexpr int kPoolSV = 11, kPoolMV = kPool;
 template <int NP> constexpr int pool_ctas() { return NP == kPoolSV ? 4 : kPCTAs; }
 static_assert(sizeof(PoolSmemT<kPoolSV>) + 1024 <= 228 * 1024 / 4, "pooled depth sweep: 4 CTAs x 11 stages per SM");
 static_assert(sizeof(PoolSmemT<kPoolMV>) + 1024 <= 228 * 1024 / kPCTAs, "pooled depth sweep: kPCTAs CTAs per SM must fit");
@@ -1646,6 +1646,12 @@ __device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long 
     if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
 }
 
+// The record list's overflow fallback out of line: its registers do not weigh on the record path's allocation.
+template <int MODEL, bool VEC, bool VEC4>
+__device__ __noinline__ void blend_overflow(const RasterArgs &a) {
+    stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
+}
+
 template <int MODEL, bool VEC, bool VEC4, bool HOCC>
 __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_constant__ RasterArgs a) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // a split depth pass's candidate list is consumed: drop it
@@ -1653,7 +1659,7 @@ __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_c
         a.hdr->resv = *(volatile unsigned long long *)&a.hdr->front_ok;
     }
     if (*(volatile int32_t *)&a.hdr->overflow) {  // record list overflowed: re-stream every point instead
-        stream_sweep<MODEL, VEC, MODE_BLEND, VEC4>(a);
+        blend_overflow<MODEL, VEC, VEC4>(a);
         return;
     }
     if (a.mv_lists) {  // multi-view: the survivor chunks view by view (keys and accumulators stay in L2)
