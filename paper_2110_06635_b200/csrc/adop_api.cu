@@ -746,6 +746,8 @@ adop_status adop_forward_depth(const adop_points *points, int32_t n_views, const
     if (vec_path(points)) encode_pos_tmap(a, points);
     // only the pipelined depth kernel (vector path) writes the ghost list the backward can consume
     a.tag = vec_path(points) ? call_tag(points, n_views, cameras, poses, params, views, workspace_bytes) : 0ull;
+    // with ghosts (rho > 0) the pooled depth pass also lists them for the backward, which then needs no sweep
+    a.ghost_fwd = (a.tag != 0ull && a.ghost_thr != 0u && depth_lists_ghosts(a)) ? 1 : 0;
     int e = launch_clear(a, 0, stream);
     if (e) return cuda_status(e, "clear launch");
     if (points->n > 0) {

@@ -74,6 +74,8 @@ struct WsHeader {
     unsigned long long tiles_read; // tile culling: tiles the depth pass loaded
     unsigned long long tiles_fwd;  // dynamic tile counters of the depth and backward sweeps
     unsigned long long tiles_bwd;
+    int32_t ghosts_fwd;            // 1: the depth pass listed every ghost (back list), the backward needs no sweep
+    int32_t pad_;
 };
 
 // Frustum half-spaces of every view in the workspace (written by k_clear<KEYS> of the depth phase;
@@ -149,12 +151,14 @@ struct RasterArgs {
     uint32_t *ccount;      // [2][64]: per-view chunk counts [0..16], cursors [32..48], total [63]
     int32_t mv_lists;      // bit 0: the sweeps write per-view chunks (the blend walks them view-major);
                            // bit 1: the texture consumer walks them view-major too; bit 2: the ghost consumer
+    int32_t ghost_fwd;     // the depth pass also lists the ghosts (back of the record region) for the backward
 };
 constexpr int kListChunk = 64;  // record slots per chunk of the chunk table (a 64-aligned unit of every list)
 
 // Launchers (adop_kernels.cu).  Return cudaError_t as int.
 int launch_clear(const RasterArgs &a, int what, void *stream);  // 0 keys+header, 1 accum+count
 int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream);
+bool depth_lists_ghosts(const RasterArgs &a);  // the depth launch for `a` runs k_depth_pool (it can list ghosts)
 int launch_blend(const RasterArgs &a, int model, bool vec, int sms, void *stream);
 int launch_resolve(const RasterArgs &a, void *stream);
 int launch_chunk_order(const RasterArgs &a, int list, int sms, void *stream);  // multi-view lists (mv_lists)

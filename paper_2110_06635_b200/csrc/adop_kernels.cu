@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ Rast
             a.hdr->tag = a.tag;
             a.hdr->tiles_fwd = 0ull;
             a.hdr->tiles_read = 0ull;
+            a.hdr->ghosts_fwd = a.ghost_fwd;  // cleared by the depth pass if a ghost did not fit the list
         }
         if (blockIdx.x == 0 && threadIdx.x < 5) {  // this view's frustum planes for tile_views
             const int k = threadIdx.x;
@@ -744,6 +745,58 @@ __device__ __forceinline__ void mv_close(const RasterArgs &a, const RecChunk &c,
     for (unsigned long long s = c.base; (s & (kListChunk - 1)) != 0; ++s) put_record(a, s, make_uint4(0u, 0u, 0u, kDeadView));
 }
 
+// Multi-view ghost list (RasterArgs::mv_lists): like mv_put for the back list -- lane vs keeps view vs's open
+// chunk in c.base (next free slot; 2 slots per ghost entry); all items of a call share the warp-uniform view
+// slot vs.  Returns the lane's slot or kNoSlot (region full: processed inline).  Warp-collective.
+__device__ __forceinline__ unsigned long long mv_take_back(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
+                                                           int vs, int lane, unsigned lt) {
+    const int nb = __popc(b);
+    const unsigned long long st = __shfl_sync(kFull, c.base, vs);
+    const int used = (int)(st & (kListChunk - 1));
+    const int room = used ? (kListChunk - used) / 2 : 0;
+    unsigned long long nbase = 0;
+    if (nb > room) {  // a fresh list chunk from the warp's pool (lane kPoolLane), refilled one back reservation at a time
+        unsigned long long pb = __shfl_sync(kFull, c.base, kPoolLane);
+        int pl = __shfl_sync(kFull, c.left, kPoolLane);
+        if (pl <= 0) {
+            if (lane == 0) pb = resv_take<true>(a, kChunk, false);
+            pb = __shfl_sync(kFull, pb, 0);
+            pl = pb == kNoSlot ? 0 : kChunk / kListChunk;
+        }
+        if (pl > 0) {
+            nbase = pb;
+            pb += kListChunk;
+            --pl;
+            if (lane == 0) a.cview[nbase / kListChunk] = (uint8_t)vs;
+        } else {
+            nbase = kNoSlot;  // region full: the items are processed inline
+        }
+        if (lane == kPoolLane) {
+            c.base = pb;
+            c.left = pl;
+        }
+    }
+    const int off = __popc(b & lt);
+    const unsigned long long slot =
+        off < room ? st + 2ull * off : (nbase == kNoSlot ? kNoSlot : nbase + 2ull * (off - room));
+    if (lane == vs) c.base = nb <= room ? st + 2ull * nb : (nbase == kNoSlot ? 0ull : nbase + 2ull * (nb - room));
+    return mine ? slot : kNoSlot;
+}
+
+// End of a multi-view backward sweep: lane w marks the rest of view w's ghost chunk dead.
+__device__ __forceinline__ void mv_close_back(const RasterArgs &a, const ListChunk &c, int lane) {
+    uint4 *r = reinterpret_cast<uint4 *>(a.records);
+    if (lane == kPoolLane) {
+        for (int k = 0; k < c.left; ++k) {
+            const unsigned long long b = c.base + (unsigned long long)k * kListChunk;
+            a.cview[b / kListChunk] = 0xFF;
+            for (int j = 0; j < kListChunk; j += 2) r[b + j + 1] = make_uint4(0u, 0u, kDead, kDead);
+        }
+        return;
+    }
+    for (unsigned long long s = c.base; (s & (kListChunk - 1)) != 0; s += 2) r[s + 1] = make_uint4(0u, 0u, kDead, kDead);
+}
+
 // Layers of one kept point per lane (nk = 0: idle lane).  Warp-collective.
 template <bool MV>
 __device__ __forceinline__ void depth_layers(const RasterArgs &a, const LayerDesc &v, int vs, int nk, float u0,
@@ -826,10 +879,18 @@ void drain(const RasterArgs &a, const LayerDesc *ld, WarpQueue &q, int &qn, int 
 // are dropped before the queue (configs[4]: a quarter of the kept point-views; with distortion the pre-cull
 // planes bound the whole valid cone, well beyond the image).  On the single-view pinhole headline the extra
 // compares cost more than the few out-of-image points they save.
+//
+// Forward ghost listing (RasterArgs::ghost_fwd, R13 / R22): a candidate that is a ghost (`ghost`) takes the same exact
+// test -- plus the in-bounds test of some kept layer, as the backward sweep's ghost emission (bwd_emit) -- and, if it
+// passes, goes to the ghost list at the back of the record region instead of the depth test, so the backward
+// consumes it without re-streaming the cloud.  A ghost whose slot cannot be reserved clears hdr->ghosts_fwd (the
+// backward then re-finds every ghost with its sweep).  One exact path for both (a second inlined copy of it doubled
+// the configs[4] depth pass: instruction-cache misses, 26% of the stall samples).
 template <int MODEL, bool PRECHECK, bool MV>
 __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewDesc &v, int vs, bool ok, float x,
                                                 float y, float z, float rw, int64_t i, uint32_t gi, const LayerDesc *ld,
-                                                WarpQueue &q, int &qn, RecChunk &c, int lane, unsigned lt) {
+                                                WarpQueue &q, int &qn, RecChunk &c, int lane, unsigned lt,
+                                                bool ghost = false, ListChunk *cg = nullptr) {
     Proj p;
     int nk = 0;
 #if ADOP_COUNTERS
@@ -855,7 +916,26 @@ __device__ __forceinline__ void depth_candidate(const RasterArgs &a, const ViewD
         CNT(7, __popc(b_proj));
     }
 #endif
-    if (nk > 0 && !(project_uv<MODEL>(v, p) && (!PRECHECK || any_layer_in_bounds(v, p, nk)))) nk = 0;
+    if (nk > 0 && !(project_uv<MODEL>(v, p) && ((!PRECHECK && !ghost) || any_layer_in_bounds(v, p, nk)))) nk = 0;
+    if (cg && __any_sync(kFull, ghost)) {  // ghost candidates: to the ghost list (GhostEntry, as bwd_emit)
+        const bool gh = ghost && nk > 0;
+        const unsigned bg = __ballot_sync(kFull, gh);
+        if (bg != 0u) {
+            const unsigned long long slot = (MV && a.mv_lists) ? mv_take_back(a, *cg, bg, gh, vs, lane, lt)
+                                                               : list_take<true>(a, *cg, bg, gh, lane, lt);
+            if (gh) {
+                if (slot != kNoSlot) {
+                    uint4 *r = reinterpret_cast<uint4 *>(a.records) + slot;
+                    r[0] = make_uint4(__float_as_uint(p.u0), __float_as_uint(p.v0), __float_as_uint(p.X),
+                                      __float_as_uint(p.Y));
+                    r[1] = make_uint4(__float_as_uint(p.Z), (uint32_t)i, (uint32_t)(vs | (nk << 8)), __float_as_uint(p.D));
+                } else {
+                    *(volatile int32_t *)&a.hdr->ghosts_fwd = 0;
+                }
+            }
+        }
+        if (ghost) nk = 0;  // ghosts take no part in the depth test (§4.3)
+    }
     const unsigned b = __ballot_sync(kFull, nk > 0);
     if (b == 0u) return;
     if (nk > 0) {
@@ -975,7 +1055,8 @@ __device__ __forceinline__ bool depth_lane8(const RasterArgs &a, const float *co
     auto pidx = [&](int j) { return base + (j >> 2) * 128 + 4 * lane + (j & 3); };
     // ghosts take no part in the depth test (§4.3): their mask is hashed at the tile's first visible view
     uint32_t live = (uint32_t)vmask;
-    bool live_done = a.ghost_thr == 0u;
+    const bool gf = !SPLIT && !EARLY && a.ghost_fwd;  // this pass lists the ghosts (ghost_thr != 0)
+    bool live_done = a.ghost_thr == 0u || gf;
     const Box box = lane_box(rows, lane, vmask);
     uint32_t views = pre_views != 0xFFFFFFFFu ? pre_views
                      : (VM == 2 ? tile_views(a, box, lane) : (VM == 0 ? 1u : (1u << a.nviews) - 1u));
@@ -1049,7 +1130,7 @@ __device__ __forceinline__ bool depth_lane8(const RasterArgs &a, const float *co
                 if (h24(a.ghost_salt, a.goff + (uint32_t)pidx(j)) < a.ghost_thr) live &= ~(1u << j);
             live_done = true;
         }
-        m &= live;
+        m &= gf ? (uint32_t)vmask : live;  // (listing ghosts: they stay candidates, flagged per candidate below)
         if (!__any_sync(kFull, m != 0u)) continue;
         // compact the warp's candidates into a list of tile offsets, then run the exact path 32 at a time
         // with every lane busy (a per-lane loop would idle the lanes whose points are all rejected)
@@ -1098,8 +1179,10 @@ __device__ __forceinline__ bool depth_lane8(const RasterArgs &a, const float *co
                 }
                 if (!__any_sync(kFull, ok)) continue;  // (the region is full: the rest is processed here)
             }
+            const uint32_t gi = a.goff + (uint32_t)(base + e);
+            const bool ghost = gf && ok && h24(a.ghost_salt, gi) < a.ghost_thr;
             depth_candidate<MODEL, VM != 0 || MODEL != 0, VM == 2>(a, v, vs, ok, rows[0][e], rows[1][e], rows[2][e], rw, base + e,
-                                   a.goff + (uint32_t)(base + e), ld, q, qn, c, lane, lt);
+                                   gi, ld, q, qn, c, lane, lt, ghost, gf ? cc : nullptr);
         }
         __syncwarp();  // the list is rewritten by the next view / tile
     }
@@ -1430,6 +1513,12 @@ __global__ void __launch_bounds__(kST, pool_ctas<NP>()) k_depth_pool(const __gri
         if (!released) rel();
     }
     if (SPLIT) list_close<true>(a, cc, lane);
+    if (!SPLIT && a.ghost_fwd) {  // the rest of this warp's ghost-list chunk(s)
+        if (VM == 2 && a.mv_lists)
+            mv_close_back(a, cc, lane);
+        else
+            list_close<true>(a, cc, lane);
+    }
     if (qn > 0) drain<VM == 2>(a, a.ldesc, q, qn, qn, c, lane, lt);
     if (VM == 2 && a.mv_lists)
         mv_close(a, c, lane);
@@ -1654,7 +1743,8 @@ __device__ __noinline__ void blend_overflow(const RasterArgs &a) {
 
 template <int MODEL, bool VEC, bool VEC4, bool HOCC>
 __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_constant__ RasterArgs a) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // a split depth pass's candidate list is consumed: drop it
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !*(volatile int32_t *)&a.hdr->ghosts_fwd) {
+        // a split depth pass's candidate list is consumed: drop it (a ghost list of the depth pass stays)
         a.hdr->back_ok = 0ull;
         a.hdr->resv = *(volatile unsigned long long *)&a.hdr->front_ok;
     }
@@ -2120,20 +2210,26 @@ __global__ void __launch_bounds__(kThreads) k_backward(const __grid_constant__ R
 // the sweep re-renders every point into fresh lists (mode 0).  Either way the ghost list starts empty.
 __global__ void __launch_bounds__(kThreads) k_fill(float *p, int64_t n, float *q, int64_t m, float *r, int64_t rn,
                                                    WsHeader *hdr,
-                                                   double *inline_row, int inline_len, unsigned long long tag) {
+                                                   double *inline_row, int inline_len, unsigned long long tag,
+                                                   int fwd_ghosts_ok) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid == 0 && hdr) {
         const bool reuse = tag != 0ull && hdr->tag == tag && hdr->overflow == 0;
-        hdr->mode = reuse ? 1 : 0;
-        if (reuse) {  // keep the survivor records, drop an earlier backward's ghost list
-            hdr->resv = hdr->front_ok;
-        } else {      // the sweep's lists overwrite the record region
-            hdr->tag = 0ull;
-            hdr->resv = 0ull;
-            hdr->front_ok = 0ull;
-            hdr->overflow = 0;
+        // mode 2: the depth pass also listed every ghost (and nothing has replaced its list since): no sweep
+        const bool ghosts = reuse && fwd_ghosts_ok && hdr->ghosts_fwd == 1;
+        hdr->mode = ghosts ? 2 : (reuse ? 1 : 0);
+        if (!ghosts) {
+            if (reuse) {  // keep the survivor records, drop the ghost list (an earlier backward's or the depth pass's)
+                hdr->resv = hdr->front_ok;
+            } else {      // the sweep's lists overwrite the record region
+                hdr->tag = 0ull;
+                hdr->resv = 0ull;
+                hdr->front_ok = 0ull;
+                hdr->overflow = 0;
+            }
+            hdr->back_ok = 0ull;
+            hdr->ghosts_fwd = 0;
         }
-        hdr->back_ok = 0ull;
         hdr->tiles_bwd = 0ull;
     }
     if (inline_row && tid < inline_len) inline_row[tid] = 0.0;
@@ -2213,58 +2309,6 @@ __device__ __forceinline__ void ghost_layer(const RasterArgs &a, const ViewDesc 
 // ---- record-driven backward: work lists in the record region, two balanced kernels consume them ----
 // Texture list = the front list (Record layout): the depth pass's survivor records (mode 1) or the
 // sweep's rendered hits (mode 0).  Ghost list = the back list (GhostEntry layout), written by the sweep.
-// Multi-view ghost list (RasterArgs::mv_lists): like mv_put for the back list -- lane vs keeps view vs's open
-// chunk in c.base (next free slot; 2 slots per ghost entry); all items of a call share the warp-uniform view
-// slot vs.  Returns the lane's slot or kNoSlot (region full: processed inline).  Warp-collective.
-__device__ __forceinline__ unsigned long long mv_take_back(const RasterArgs &a, ListChunk &c, unsigned b, bool mine,
-                                                           int vs, int lane, unsigned lt) {
-    const int nb = __popc(b);
-    const unsigned long long st = __shfl_sync(kFull, c.base, vs);
-    const int used = (int)(st & (kListChunk - 1));
-    const int room = used ? (kListChunk - used) / 2 : 0;
-    unsigned long long nbase = 0;
-    if (nb > room) {  // a fresh list chunk from the warp's pool (lane kPoolLane), refilled one back reservation at a time
-        unsigned long long pb = __shfl_sync(kFull, c.base, kPoolLane);
-        int pl = __shfl_sync(kFull, c.left, kPoolLane);
-        if (pl <= 0) {
-            if (lane == 0) pb = resv_take<true>(a, kChunk, false);
-            pb = __shfl_sync(kFull, pb, 0);
-            pl = pb == kNoSlot ? 0 : kChunk / kListChunk;
-        }
-        if (pl > 0) {
-            nbase = pb;
-            pb += kListChunk;
-            --pl;
-            if (lane == 0) a.cview[nbase / kListChunk] = (uint8_t)vs;
-        } else {
-            nbase = kNoSlot;  // region full: the items are processed inline
-        }
-        if (lane == kPoolLane) {
-            c.base = pb;
-            c.left = pl;
-        }
-    }
-    const int off = __popc(b & lt);
-    const unsigned long long slot =
-        off < room ? st + 2ull * off : (nbase == kNoSlot ? kNoSlot : nbase + 2ull * (off - room));
-    if (lane == vs) c.base = nb <= room ? st + 2ull * nb : (nbase == kNoSlot ? 0ull : nbase + 2ull * (nb - room));
-    return mine ? slot : kNoSlot;
-}
-
-// End of a multi-view backward sweep: lane w marks the rest of view w's ghost chunk dead.
-__device__ __forceinline__ void mv_close_back(const RasterArgs &a, const ListChunk &c, int lane) {
-    uint4 *r = reinterpret_cast<uint4 *>(a.records);
-    if (lane == kPoolLane) {
-        for (int k = 0; k < c.left; ++k) {
-            const unsigned long long b = c.base + (unsigned long long)k * kListChunk;
-            a.cview[b / kListChunk] = 0xFF;
-            for (int j = 0; j < kListChunk; j += 2) r[b + j + 1] = make_uint4(0u, 0u, kDead, kDead);
-        }
-        return;
-    }
-    for (unsigned long long s = c.base; (s & (kListChunk - 1)) != 0; s += 2) r[s + 1] = make_uint4(0u, 0u, kDead, kDead);
-}
-
 __device__ __forceinline__ void red_add_row(float *dst, const float *src, int C, float scale) {
     if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
         for (int c = 0; c < C; c += 4) {
@@ -2429,7 +2473,7 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
 // texture list consumer: one thread per hit (balanced), vector reductions into d_feat.
 __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
     const uint4 *list = reinterpret_cast<const uint4 *>(a.records);
-    if ((a.mv_lists & 2) && *(volatile int32_t *)&a.hdr->mode == 1) {  // the forward's per-view chunks, view by view
+    if ((a.mv_lists & 2) && *(volatile int32_t *)&a.hdr->mode >= 1) {  // the forward's per-view chunks, view by view
         for_ordered<1>(a, 0, [&](unsigned long long r) {
             const uint4 e = __ldcs(list + r);
             if (e.w != kDead) tex_hit(a, a.v[e.w], e.x, __uint_as_float(e.y), (int64_t)e.z);
@@ -2532,7 +2576,8 @@ template <int MODEL, int CT, bool MV, bool GO>
 __global__ void __launch_bounds__(kST, 3) k_bwd_sweep(const __grid_constant__ RasterArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
-    if ((*(volatile int32_t *)&a.hdr->mode == 1) != GO) return;
+    const int32_t mode = *(volatile int32_t *)&a.hdr->mode;
+    if (mode == 2 || (mode == 1) != GO) return;  // mode 2: the depth pass listed the ghosts
     constexpr bool tex_on = !GO;  // mode 1: the survivor records are the texture list
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned lt = lanemask_lt();
@@ -2781,6 +2826,23 @@ static bool depth_split_enabled() {  // ADOP_DEPTH_SPLIT=1: cull kernel + exact 
     return env != 0;
 }
 
+static bool ghost_fwd_enabled() {  // ADOP_GHOST_FWD=0: ghosts found by the backward's sweep instead (A/B)
+    static int env = -1;
+    if (env < 0) {
+        const char *e = std::getenv("ADOP_GHOST_FWD");
+        env = e ? std::atoi(e) : 1;
+    }
+    return env != 0;
+}
+
+// The depth launch for `a` is the pooled, unsplit sweep (launch_depth_async's first branch on the vector path),
+// the only one that lists ghosts.
+bool depth_lists_ghosts(const RasterArgs &a) {
+    return ghost_fwd_enabled() && depth_pool_enabled() && !a.tbounds && !(a.dyn_tiles & 1) &&
+           !(a.nviews == 1 && depth_split_enabled()) && (reinterpret_cast<uintptr_t>(a.x) & 15) == 0 &&
+           !ADOP_EARLY_RELEASE;
+}
+
 template <int MODEL, int VM>
 static int launch_depth_async(const RasterArgs &a, int sms, void *stream) {
     if (depth_pool_enabled() && !a.tbounds && !(a.dyn_tiles & 1)) {
@@ -3015,7 +3077,7 @@ static int launch_backward_t(const RasterArgs &a, int sms, int grid_cap, double 
         k_fill<<<(unsigned)bx, kThreads, 0, s>>>(nf ? a.d_feat : nullptr, nf, np ? a.d_pos : nullptr, np,
                                                 ne ? a.d_env : nullptr, ne, a.hdr,
                                                 a.pose_partials + (int64_t)gg * a.nviews * a.nterms, a.nviews * a.nterms,
-                                                a.tag);
+                                                a.tag, a.spatial_rendered ? 0 : 1);
     }
     {   // per-pixel tables
         int64_t bx = (maxP + kThreads - 1) / kThreads;

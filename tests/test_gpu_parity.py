@@ -310,12 +310,18 @@ def test_precull_is_conservative_at_frustum_borders(model, tight):
 
 def _hdr(ws):
     """WsHeader fields (adop_internal.h): resv u64 @0, overflow i32 @8, mode i32 @12, tag u64 @16,
-    front_ok u64 @24, back_ok u64 @32."""
+    front_ok u64 @24, back_ok u64 @32, tiles_read / tiles_fwd / tiles_bwd u64 @40..64, ghosts_fwd i32 @64."""
     off = ws.ptr - ws.buf.data_ptr()
-    h = ws.buf[off:off + 40].cpu().numpy()
+    h = ws.buf[off:off + 72].cpu().numpy()
     u = lambda a, b: int(h[a:b].view(np.uint64)[0])
     return {"resv": u(0, 8), "overflow": int(h[8:12].view(np.int32)[0]), "mode": int(h[12:16].view(np.int32)[0]),
-            "tag": u(16, 24), "front_ok": u(24, 32), "back_ok": u(32, 40)}
+            "tag": u(16, 24), "front_ok": u(24, 32), "back_ok": u(32, 40),
+            "ghosts_fwd": int(h[64:68].view(np.int32)[0])}
+
+
+def _set_hdr_i32(ws, byte_off, value):
+    off = ws.ptr - ws.buf.data_ptr() + byte_off
+    ws.buf[off:off + 4] = torch.from_numpy(np.array([value], dtype=np.int32).view(np.uint8)).to(ws.buf.device)
 
 
 @pytest.mark.parametrize("idx,n,views,cap", [(2, 120_000, None, 3000), (4, 60_000, 16, 8192)])
@@ -334,17 +340,26 @@ def test_backward_work_lists_overflow_to_inline(idx, n, views, cap):
 
 
 def test_backward_consumes_forward_lists_or_resweeps():
-    """The backward's texture list is the depth pass's survivor records when the workspace holds them for
-    the same inputs (mode 1: the sweep only collects ghosts); with the header's fingerprint cleared it
-    re-renders every point (mode 0).  Both agree with the oracle; a second backward after a re-render
-    re-sweeps again."""
+    """With ghosts (rho > 0) the depth pass lists them too (back of the record region), and the backward
+    consumes both of its lists when the workspace holds them for the same inputs (mode 2: no sweep); with the
+    header's ghost flag cleared (a ghost that did not fit the forward's list) the sweep re-finds the ghosts and
+    keeps the survivor records (mode 1); with the fingerprint cleared it re-renders every point (mode 0).  All
+    three agree with the oracle; a second backward after a re-render re-sweeps again."""
     w = S.workload(2, n=150_000)
     dev = torch.device("cuda")
     G = [g.to(dev) for g in grads_for(w.cameras, w.params.layers, w.cloud.channels)]
     r = A.Renderer(w.cloud.to(dev), w.cameras, w.poses, w.params)
     r.forward()
     h = _hdr(r.ws)
-    assert h["tag"] != 0 and h["overflow"] == 0 and h["back_ok"] == 0 and h["front_ok"] == h["resv"] > 0
+    front = h["resv"] & ((1 << 40) - 1)
+    assert h["tag"] != 0 and h["overflow"] == 0 and h["ghosts_fwd"] == 1 and h["front_ok"] == front > 0
+    assert h["back_ok"] == (h["resv"] >> 40) * 256 > 0  # the depth pass wrote the ghost list
+    listed = [t.clone() for t in r.backward(G)]
+    h0 = _hdr(r.ws)
+    assert h0["mode"] == 2 and h0["back_ok"] == h["back_ok"] and h0["front_ok"] == h["front_ok"]
+    r.backward(G)  # the lists stay consumable
+    assert _hdr(r.ws)["mode"] == 2
+    _set_hdr_i32(r.ws, 64, 0)  # as if a ghost had not fitted the forward's list
     reuse = [t.clone() for t in r.backward(G)]
     h1 = _hdr(r.ws)
     assert h1["mode"] == 1 and h1["back_ok"] == (h1["resv"] >> 40) * 256 > 0  # the sweep wrote the ghost list
@@ -357,12 +372,31 @@ def test_backward_consumes_forward_lists_or_resweeps():
     assert _hdr(r.ws)["mode"] == 0
     torch.cuda.synchronize()
     _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=[g.cpu() for g in G])
-    for name, res in (("reuse", reuse), ("sweep", sweep)):
+    for name, res in (("listed", listed), ("reuse", reuse), ("sweep", sweep)):
         r.d_feat.copy_(res[0]); r.d_pos.copy_(res[1]); r.d_pose.copy_(res[2])
         compare_backward(r, bwd, ctx=name)
     r.forward()  # a fresh forward makes the lists consumable again
     r.backward(G)
-    assert _hdr(r.ws)["mode"] == 1
+    assert _hdr(r.ws)["mode"] == 2
+
+
+@pytest.mark.parametrize("idx,n,views", [(2, 150_000, None), (4, 60_000, 16)])
+def test_forward_ghost_list_overflow(idx, n, views):
+    """A record region with room for the survivor records but not for every ghost: the depth pass clears its
+    ghost flag and the backward re-finds the ghosts with its sweep (mode 1; mode 0 if the survivors did not fit
+    either) -- same results.  The 16-view case runs the per-view ghost chunks."""
+    w = S.workload(idx, n=n, n_views=views)
+    G = grads_for(w.cameras, w.params.layers, w.cloud.channels)
+    full = run_gpu(w.cloud, w.cameras, w.poses, w.params, grads=None)
+    hf = _hdr(full.ws)
+    assert hf["ghosts_fwd"] == 1 and hf["back_ok"] > 0
+    cap = int(hf["front_ok"] + hf["back_ok"] // 3)
+    small = run_gpu(w.cloud, w.cameras, w.poses, w.params, grads=G, record_capacity=cap)
+    hs = _hdr(small.ws)
+    assert hs["mode"] in (0, 1) and hs["ghosts_fwd"] == 0
+    _, fwd, bwd = run_oracle(w.cloud, w.cameras, w.poses, w.params, grads=G)
+    compare_forward(small, fwd, ctx="ghost overflow")
+    compare_backward(small, bwd, ctx="ghost overflow")
 
 
 # --------------------------------------------------------------------------- #
