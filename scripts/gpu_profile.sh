@@ -16,9 +16,9 @@ full() {  # name kernel-regex skip command...
   bash scripts/ncu_stalls.sh /tmp/$name.ncu-rep > $T/${name}_stalls.txt 2>&1
   python scripts/ncu_lines_cuda.py /tmp/$name.ncu-rep 40 > $T/${name}_lines.txt 2>&1
 }
-full cfg3_depth '^k_depth_async' 3 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary
+full cfg3_depth '^k_depth_(pool|async)' 3 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary
 full cfg3_blend '^k_blend' 3 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-secondary
 full cfg2_ghost '^k_bwd_ghost' 3 python scripts/run_config.py 2 5
-full cfg2_sweep '^k_bwd_sweep' 7 python scripts/run_config.py 2 5
+full cfg4_ghost '^k_bwd_ghost' 1 python scripts/run_config.py 4 2
 full cfg2_tex '^k_bwd_tex' 3 python scripts/run_config.py 2 5
-full cfg4_depth '^k_depth_async' 0 python scripts/run_config.py 4 1
+full cfg4_depth '^k_depth_(pool|async)' 0 python scripts/run_config.py 4 1

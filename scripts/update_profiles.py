@@ -55,9 +55,10 @@ for c in ("cfg3", "cfg2", "cfg4"):
     for n, k, us, rd, wr in setup:
         md += [f"(not in the shares: `{n}`, the tile-culled variant's one-time per-tile bounds, {us:.1f} us)", ""]
     if c == "cfg3":
-        dep = [x for x in t if "k_depth_async" in x[0] or x[0].endswith("k_clear<0>")]
+        isdep = lambda name: "k_depth_pool" in name or "k_depth_async" in name
+        dep = [x for x in t if isdep(x[0]) or x[0].endswith("k_clear<0>")]
         traffic = {"depth_phase_bytes": int(sum(x[3] + x[4] for x in dep)),
-                   "k_depth_async_bytes": int(sum(x[3] + x[4] for x in t if "k_depth_async" in x[0])),
+                   "depth_kernel_bytes": int(sum(x[3] + x[4] for x in t if isdep(x[0]))),
                    "source": f"profiles/{rnd}/launches_summary.md (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)"}
 open(f"{dst}/launches_summary.md", "w").write("\n".join(md) + "\n")
 for f in sorted(os.listdir(src)):
