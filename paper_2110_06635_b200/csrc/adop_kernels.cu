@@ -63,9 +63,14 @@ enum { MODE_DEPTH = 0, MODE_BLEND = 1, MODE_MASKS = 2 };
 // CLEAR_ACC  (phase 2): accum, count <- 0 right before the blend, so the blend's reductions and the
 //                        resolve find these 55 MB (configs[3]) still in L2.
 enum { CLEAR_KEYS = 0, CLEAR_ACC = 1 };
+#ifndef ADOP_CLEAR_REVERSE
+#define ADOP_CLEAR_REVERSE 1
+#endif
 template <int WHAT>
 __global__ void __launch_bounds__(kThreads) k_clear(const __grid_constant__ RasterArgs a) {
-    const ViewDesc &v = a.v[blockIdx.y];
+    // CLEAR_ACC clears the views last-to-first (blocks are scheduled in blockIdx.y order): the view-major blend
+    // starts on view 0, whose freshly zeroed lines are then the ones still in L2
+    const ViewDesc &v = a.v[WHAT == CLEAR_ACC && ADOP_CLEAR_REVERSE ? gridDim.y - 1 - blockIdx.y : blockIdx.y];
     const int64_t P = v.pixels;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1735,6 +1740,54 @@ __device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long 
     if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
 }
 
+// U records per thread with their loads staged (all records, then all depth words, then all descriptors, then the
+// reductions): the per-record chain record -> key -> descriptor -> reduction is latency-bound (configs[4]: 90% of
+// the stall samples long-scoreboard, 15% issue), and the reductions' memory clobbers keep the compiler from
+// overlapping two chains on its own.  slot[u] = kNoSlot: no record.
+#ifndef ADOP_BLEND_U
+#define ADOP_BLEND_U 1  // measured: 2 slows the configs[4] blend (fwd 5.25 -> 5.46 ms: more random gathers in flight thrash L2)
+#endif
+template <bool VEC4, int U>
+__device__ __forceinline__ void blend_records(const RasterArgs &a, const unsigned long long (&slot)[U]) {
+    uint4 rec[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        rec[u] = make_uint4(0u, 0u, 0u, kDeadView);
+        if (slot[u] != kNoSlot) {
+            ADOP_CHECK(slot[u] < (unsigned long long)a.rec_capacity);
+            rec[u] = __ldcs(reinterpret_cast<const uint4 *>(a.records) + slot[u]);
+        }
+    }
+    bool pass[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        pass[u] = false;
+        if (rec[u].w != kDeadView) {
+            ADOP_CHECK(rec[u].w < (uint32_t)a.nviews && rec[u].x < (uint32_t)a.v[rec[u].w].pixels && rec[u].z < (uint64_t)a.n);
+            const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(a.v[rec[u].w].keys) + rec[u].x);
+            pass[u] = fuzzy_pass(__uint_as_float(rec[u].y), key, a.onepa);
+        }
+    }
+    if (VEC4 && a.channels == 4 && !a.log_desc) {
+        const uint64_t pol = policy_evict_first();
+        float4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pass[u]) t[u] = ld_once4(a.feat + (int64_t)rec[u].z * 4, pol);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pass[u]) {
+                const ViewDesc &v = a.v[rec[u].w];
+                red_add_v4(v.accum + (int64_t)rec[u].x * 4, t[u]);
+                red_add(v.count + rec[u].x, 1.0f);
+            }
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (pass[u]) accumulate_feature<VEC4>(a, a.v[rec[u].w], rec[u].z, rec[u].x);
+}
+
 // The record list's overflow fallback out of line: its registers do not weigh on the record path's allocation.
 template <int MODEL, bool VEC, bool VEC4>
 __device__ __noinline__ void blend_overflow(const RasterArgs &a) {
@@ -1753,11 +1806,35 @@ __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_c
         return;
     }
     if (a.mv_lists) {  // multi-view: the survivor chunks view by view (keys and accumulators stay in L2)
-        for_ordered<1>(a, 0, [&](unsigned long long r) { blend_record<VEC4>(a, r); });
+        if constexpr (ADOP_BLEND_U >= 2 && !HOCC) {  // the chunk's two items per lane, loads staged
+            static_assert(kListChunk == 64, "blend: two items per lane of a 64-slot chunk");
+            unsigned long long c0, c1;
+            list_chunks(a, 0, c0, c1);
+            const unsigned long long nch = c1 - c0;
+            const unsigned long long W = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+            const int lane = threadIdx.x & 31;
+            for (unsigned long long j = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nch;
+                 j += W) {
+                const unsigned long long base = (unsigned long long)a.corder[0][j] * kListChunk;
+                ADOP_CHECK(base + kListChunk <= (unsigned long long)a.rec_capacity);
+                const unsigned long long s[2] = {base + lane, base + 32 + lane};
+                blend_records<VEC4, 2>(a, s);
+            }
+        } else {
+            for_ordered<1>(a, 0, [&](unsigned long long r) { blend_record<VEC4>(a, r); });
+        }
         return;
     }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    if constexpr (ADOP_BLEND_U >= 2 && !HOCC) {  // two records per thread, loads staged
+        for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+             r += 2 * stride) {
+            const unsigned long long s[2] = {r, r + stride < total ? r + stride : kNoSlot};
+            blend_records<VEC4, 2>(a, s);
+        }
+        return;
+    }
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride)
         blend_record<VEC4>(a, r);
 }
@@ -1783,12 +1860,19 @@ __device__ __forceinline__ void env_bg4(const RasterArgs &a, const ViewDesc &v, 
 // Groups of 4 consecutive pixels of one layer (host guarantees off_l and h_l*w_l are multiples of 4
 // when VEC4): one 16-B count load, accum read only for covered pixels, one 16-B store per channel plane.
 // ENV: empty pixels sample the environment map (NEXT-2); a separate instance keeps the plain path lean.
+#ifndef ADOP_RESOLVE_SPARSE
+#define ADOP_RESOLVE_SPARSE 1
+#endif
 template <bool VEC4, bool ENV>
 __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ RasterArgs a) {
     const ViewDesc &v = a.v[blockIdx.y];
     const int C = a.channels;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (VEC4) {
+        // Multi-view launches: the views' accumulators do not stay in L2 after the blend (configs[1]: 4 x 55 MB), so
+        // a pixel's accumulator is read only if its count is non-zero -- an empty pixel's 32-B sector is never
+        // fetched (configs[1]: ~6% of the pixels are covered).  One view: loaded with the counts (L2 hits).
+        const bool sparse = a.nviews > 1 && ADOP_RESOLVE_SPARSE;
         for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < v.pixels / 4; g += stride) {
             const int64_t p = 4 * g;
             int l = 0;
@@ -1805,7 +1889,9 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
 #pragma unroll
                 float4 acc[4];  // loaded with the counts (L2-resident after the blend): one round trip
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0));
+                for (int q = 0; q < 4; ++q)
+                    acc[q] = (!sparse || cn[q] > 0.0f) ? __ldcs(reinterpret_cast<const float4 *>(v.accum + (p + q) * C + c0))
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float av[4] = {acc[q].x, acc[q].y, acc[q].z, acc[q].w};
@@ -2343,7 +2429,18 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
                                             int64_t idx, int nt, double *tt, float *g = nullptr) {
     const int C = CT > 0 ? CT : a.channels;
     float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
-    for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + idx * C + c));  // linear space
+    if (CT > 0 && (CT & 3) == 0 && (reinterpret_cast<uintptr_t>(a.feat) & 15) == 0) {  // one 16-B load per 4 channels
+#pragma unroll
+        for (int c = 0; c < (CT > 0 ? CT : 4); c += 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4 *>(a.feat + idx * C + c));
+            tau[c] = desc_lin(a, t.x);
+            tau[c + 1] = desc_lin(a, t.y);
+            tau[c + 2] = desc_lin(a, t.z);
+            tau[c + 3] = desc_lin(a, t.w);
+        }
+    } else {
+        for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + idx * C + c));  // linear space
+    }
     float gu = 0.f, gv = 0.f;
     bool gc = false;
     for (int l = 0; l < nk; ++l) {
@@ -2471,6 +2568,9 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
 }
 
 // texture list consumer: one thread per hit (balanced), vector reductions into d_feat.
+#ifndef ADOP_TEX_U
+#define ADOP_TEX_U 1  // measured: 2 is neutral on configs[4] (bwd 3.24 vs 3.27 ms)
+#endif
 __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
     const uint4 *list = reinterpret_cast<const uint4 *>(a.records);
     if ((a.mv_lists & 2) && *(volatile int32_t *)&a.hdr->mode >= 1) {  // the forward's per-view chunks, view by view
@@ -2482,6 +2582,36 @@ __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ Ra
     }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    if (ADOP_TEX_U >= 2 && a.channels == 4 && !a.log_desc && (reinterpret_cast<uintptr_t>(a.d_feat) & 15) == 0 &&
+        a.prow == 8) {
+        // two records per thread, loads staged (records, then both halves of both pixel-table rows, then the
+        // reductions): the chain record -> row header -> row G -> reduction was latency-bound (configs[4]: 91%
+        // long-scoreboard stalls, 20% issue); the header and G halves share one 32-B sector
+        for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+             r += 2 * stride) {
+            uint4 e[2];
+            e[0] = __ldcs(list + r);
+            e[1] = r + stride < total ? __ldcs(list + r + stride) : make_uint4(0u, 0u, 0u, kDead);
+            uint4 h[2];
+            float4 g[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (e[u].w != kDead) {
+                    ADOP_CHECK(e[u].w < (uint32_t)a.nviews && e[u].x < (uint32_t)a.v[e[u].w].pixels && e[u].z < (uint32_t)a.n);
+                    const float *row = a.v[e[u].w].prow + (int64_t)e[u].x * 8;
+                    h[u] = __ldcg(reinterpret_cast<const uint4 *>(row));
+                    g[u] = __ldcg(reinterpret_cast<const float4 *>(row + 4));
+                }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (e[u].w != kDead && __uint_as_float(e[u].y) <= fmul(a.onepa, __uint_as_float(h[u].x))) {  // Eq. 6, R9
+                    const float s = __uint_as_float(h[u].y);
+                    red_add_v4(a.d_feat + (int64_t)e[u].z * 4, make_float4(__fdiv_rn(g[u].x, s), __fdiv_rn(g[u].y, s),
+                                                                        __fdiv_rn(g[u].z, s), __fdiv_rn(g[u].w, s)));
+                }
+        }
+        return;
+    }
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
         const uint4 e = __ldcs(list + r);
         if (e.w == kDead) continue;
