@@ -1740,54 +1740,6 @@ __device__ __forceinline__ void blend_record(const RasterArgs &a, unsigned long 
     if (fuzzy_pass(__uint_as_float(rec.y), key, a.onepa)) accumulate_feature<VEC4>(a, v, rec.z, rec.x);
 }
 
-// U records per thread with their loads staged (all records, then all depth words, then all descriptors, then the
-// reductions): the per-record chain record -> key -> descriptor -> reduction is latency-bound (configs[4]: 90% of
-// the stall samples long-scoreboard, 15% issue), and the reductions' memory clobbers keep the compiler from
-// overlapping two chains on its own.  slot[u] = kNoSlot: no record.
-#ifndef ADOP_BLEND_U
-#define ADOP_BLEND_U 1  // measured: 2 slows the configs[4] blend (fwd 5.25 -> 5.46 ms: more random gathers in flight thrash L2)
-#endif
-template <bool VEC4, int U>
-__device__ __forceinline__ void blend_records(const RasterArgs &a, const unsigned long long (&slot)[U]) {
-    uint4 rec[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        rec[u] = make_uint4(0u, 0u, 0u, kDeadView);
-        if (slot[u] != kNoSlot) {
-            ADOP_CHECK(slot[u] < (unsigned long long)a.rec_capacity);
-            rec[u] = __ldcs(reinterpret_cast<const uint4 *>(a.records) + slot[u]);
-        }
-    }
-    bool pass[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        pass[u] = false;
-        if (rec[u].w != kDeadView) {
-            ADOP_CHECK(rec[u].w < (uint32_t)a.nviews && rec[u].x < (uint32_t)a.v[rec[u].w].pixels && rec[u].z < (uint64_t)a.n);
-            const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long *>(a.v[rec[u].w].keys) + rec[u].x);
-            pass[u] = fuzzy_pass(__uint_as_float(rec[u].y), key, a.onepa);
-        }
-    }
-    if (VEC4 && a.channels == 4 && !a.log_desc) {
-        const uint64_t pol = policy_evict_first();
-        float4 t[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (pass[u]) t[u] = ld_once4(a.feat + (int64_t)rec[u].z * 4, pol);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (pass[u]) {
-                const ViewDesc &v = a.v[rec[u].w];
-                red_add_v4(v.accum + (int64_t)rec[u].x * 4, t[u]);
-                red_add(v.count + rec[u].x, 1.0f);
-            }
-        return;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-        if (pass[u]) accumulate_feature<VEC4>(a, a.v[rec[u].w], rec[u].z, rec[u].x);
-}
-
 // The record list's overflow fallback out of line: its registers do not weigh on the record path's allocation.
 template <int MODEL, bool VEC, bool VEC4>
 __device__ __noinline__ void blend_overflow(const RasterArgs &a) {
@@ -1806,35 +1758,11 @@ __global__ void __launch_bounds__(kThreads, HOCC ? 6 : 1) k_blend(const __grid_c
         return;
     }
     if (a.mv_lists) {  // multi-view: the survivor chunks view by view (keys and accumulators stay in L2)
-        if constexpr (ADOP_BLEND_U >= 2 && !HOCC) {  // the chunk's two items per lane, loads staged
-            static_assert(kListChunk == 64, "blend: two items per lane of a 64-slot chunk");
-            unsigned long long c0, c1;
-            list_chunks(a, 0, c0, c1);
-            const unsigned long long nch = c1 - c0;
-            const unsigned long long W = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-            const int lane = threadIdx.x & 31;
-            for (unsigned long long j = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nch;
-                 j += W) {
-                const unsigned long long base = (unsigned long long)a.corder[0][j] * kListChunk;
-                ADOP_CHECK(base + kListChunk <= (unsigned long long)a.rec_capacity);
-                const unsigned long long s[2] = {base + lane, base + 32 + lane};
-                blend_records<VEC4, 2>(a, s);
-            }
-        } else {
-            for_ordered<1>(a, 0, [&](unsigned long long r) { blend_record<VEC4>(a, r); });
-        }
+        for_ordered<1>(a, 0, [&](unsigned long long r) { blend_record<VEC4>(a, r); });
         return;
     }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    if constexpr (ADOP_BLEND_U >= 2 && !HOCC) {  // two records per thread, loads staged
-        for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
-             r += 2 * stride) {
-            const unsigned long long s[2] = {r, r + stride < total ? r + stride : kNoSlot};
-            blend_records<VEC4, 2>(a, s);
-        }
-        return;
-    }
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride)
         blend_record<VEC4>(a, r);
 }
@@ -2568,9 +2496,6 @@ __device__ __forceinline__ void bwd_emit(const RasterArgs &a, const ViewDesc &v,
 }
 
 // texture list consumer: one thread per hit (balanced), vector reductions into d_feat.
-#ifndef ADOP_TEX_U
-#define ADOP_TEX_U 1  // measured: 2 is neutral on configs[4] (bwd 3.24 vs 3.27 ms)
-#endif
 __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ RasterArgs a) {
     const uint4 *list = reinterpret_cast<const uint4 *>(a.records);
     if ((a.mv_lists & 2) && *(volatile int32_t *)&a.hdr->mode >= 1) {  // the forward's per-view chunks, view by view
@@ -2582,36 +2507,6 @@ __global__ void __launch_bounds__(kThreads) k_bwd_tex(const __grid_constant__ Ra
     }
     const unsigned long long total = *(volatile unsigned long long *)&a.hdr->front_ok;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    if (ADOP_TEX_U >= 2 && a.channels == 4 && !a.log_desc && (reinterpret_cast<uintptr_t>(a.d_feat) & 15) == 0 &&
-        a.prow == 8) {
-        // two records per thread, loads staged (records, then both halves of both pixel-table rows, then the
-        // reductions): the chain record -> row header -> row G -> reduction was latency-bound (configs[4]: 91%
-        // long-scoreboard stalls, 20% issue); the header and G halves share one 32-B sector
-        for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total;
-             r += 2 * stride) {
-            uint4 e[2];
-            e[0] = __ldcs(list + r);
-            e[1] = r + stride < total ? __ldcs(list + r + stride) : make_uint4(0u, 0u, 0u, kDead);
-            uint4 h[2];
-            float4 g[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-                if (e[u].w != kDead) {
-                    ADOP_CHECK(e[u].w < (uint32_t)a.nviews && e[u].x < (uint32_t)a.v[e[u].w].pixels && e[u].z < (uint32_t)a.n);
-                    const float *row = a.v[e[u].w].prow + (int64_t)e[u].x * 8;
-                    h[u] = __ldcg(reinterpret_cast<const uint4 *>(row));
-                    g[u] = __ldcg(reinterpret_cast<const float4 *>(row + 4));
-                }
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-                if (e[u].w != kDead && __uint_as_float(e[u].y) <= fmul(a.onepa, __uint_as_float(h[u].x))) {  // Eq. 6, R9
-                    const float s = __uint_as_float(h[u].y);
-                    red_add_v4(a.d_feat + (int64_t)e[u].z * 4, make_float4(__fdiv_rn(g[u].x, s), __fdiv_rn(g[u].y, s),
-                                                                        __fdiv_rn(g[u].z, s), __fdiv_rn(g[u].w, s)));
-                }
-        }
-        return;
-    }
     for (unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r < total; r += stride) {
         const uint4 e = __ldcs(list + r);
         if (e.w == kDead) continue;
@@ -3045,14 +2940,14 @@ int launch_depth(const RasterArgs &a, int model, bool vec, int sms, void *stream
 template <int MODEL, bool VEC, bool VEC4>
 static int launch_blend_t(const RasterArgs &a, int sms, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (a.clear_pyr) {  // a shared pyramid was reset by its owner (adop_clear_pyramid)
-        int e = launch_clear(a, CLEAR_ACC, stream);
-        if (e) return e;
-    }
     auto k = k_blend<MODEL, VEC, VEC4, false>;
     if constexpr (VEC && VEC4)
         if (a.nviews == 1) k = k_blend<MODEL, VEC, VEC4, true>;
     int g = resident_grid(k, sms, kWarps * 128, a.n > 0 ? a.n : 1);
+    if (a.clear_pyr) {  // a shared pyramid was reset by its owner (adop_clear_pyramid)
+        int e = launch_clear(a, CLEAR_ACC, stream);
+        if (e) return e;
+    }
     k<<<g, kThreads, 0, s>>>(a);
     return (int)cudaGetLastError();
 }
