@@ -34,7 +34,14 @@ NVCC_FLAGS = [
 # without -split-compile it is deterministic but always spills 68 B there; profiles/r01/evolution.md).
 # So adop_kernels.cu is compiled twice concurrently per round, the copy with the fewest spill bytes in the
 # hot instances is kept, and another round runs (up to ROUNDS) while that is above SPILL_OK.
-SPLIT = 16
+SPLIT = int(os.environ.get("ADOP_SPLIT", "16"))  # 0: no -split-compile
+# The split-compile partition also changes what ptxas makes of the kernels (r02: two code-generation modes --
+# e.g. a 6 x 6-stage headline depth kernel of 2624 instructions, 0.296 ms, with 4-60 B of spills in the multi-view
+# depth sweep and the ghost consumer (configs[4] forward +6%), or 2984 instructions, 0.324 ms, with none;
+# profiles/r02/evolution.md).  The hot TU is compiled with two partition counts per round; the copy with the
+# fewest hot-instance spill bytes is kept, ties broken by the shorter headline kernel.
+SPLIT_COPIES = ((16, 12), (8, 32), (20, 24))
+HEADLINE = "_ZN4adop12k_depth_poolILi0ELi0ELb1ELb0ELi11EEEvNS_10RasterArgsE"
 ROUNDS = 3
 SPILL_OK = 300  # every hot instance within its limit (an instance over its limit adds 100000)
 HOT = {  # hot instances -> accepted spill-store bytes (tests/test_build_spills.py checks the kept build)
@@ -59,6 +66,17 @@ def hot_spills(ptxas_log: str) -> dict:
         if m and cur in HOT:
             out[cur] = int(m.group(1))
     return out
+
+
+def sass_size(obj: str, fn: str) -> int:
+    """Instruction count of kernel `fn` in object `obj` (cuobjdump), or a large number if it cannot be read."""
+    try:
+        r = subprocess.run([os.path.join(os.path.dirname(NVCC), "cuobjdump"), "-sass", "-fun", fn, obj],
+                           capture_output=True, text=True, timeout=300)
+        n = len(re.findall(r"^\s+/\*[0-9a-f]{4}\*/", r.stdout, re.M))
+        return n if n > 0 else 1 << 30
+    except Exception:  # noqa: BLE001
+        return 1 << 30
 
 
 def hot_spill_bytes(ptxas_log: str) -> int:
@@ -98,11 +116,12 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
                 (os.path.basename(src) == "adop_kernels.cu" and best[src][0] > SPILL_OK)]
         if not todo:
             break
-        for src in todo:  # the translation units (and the hot TU's two copies) compile concurrently
-            copies = 2 if os.path.basename(src) == "adop_kernels.cu" else 1
-            for k in range(copies):
+        for src in todo:  # the translation units (and the hot TU's copies) compile concurrently
+            hot_tu = os.path.basename(src) == "adop_kernels.cu"
+            splits = SPLIT_COPIES[rnd % len(SPLIT_COPIES)] if (hot_tu and SPLIT) else (SPLIT,)
+            for k, sp in enumerate(splits):
                 obj = os.path.join(bdir, os.path.basename(src) + f".r{rnd}c{k}.o")
-                cmd = [NVCC, *NVCC_FLAGS, f"-split-compile={SPLIT}", *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+                cmd = [NVCC, *NVCC_FLAGS, *([f"-split-compile={sp}"] if sp else []), *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
                 procs.append((src, rnd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                                               text=True)))
         for src, r, obj, p in procs:
@@ -111,17 +130,18 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
                 sys.stderr.write(so + se)
                 raise RuntimeError(f"nvcc failed on {src}")
             score = hot_spill_bytes(so + se)
-            if src not in best or score < best[src][0]:
-                best[src] = (score, r, obj, so + se)
+            size = sass_size(obj, HEADLINE) if os.path.basename(src) == "adop_kernels.cu" else 0
+            if src not in best or (score, size) < (best[src][0], best[src][4]):
+                best[src] = (score, r, obj, so + se, size)
         procs = []
     for src in sources():
-        score, r, obj, log = best[src]
+        score, r, obj, log, size = best[src]
         if score > SPILL_OK:  # still a hot instance over its limit after ROUNDS attempts: say which, loudly
             # (linked anyway -- a correct but slower library beats no library; tests/test_build_spills.py fails)
             over = {k: v for k, v in hot_spills(log).items() if v > HOT[k]}
             sys.stderr.write(f"WARNING build: {os.path.basename(src)} kept with hot instances over their spill "
                              f"limits after {ROUNDS} rounds: {over}\n")
-        logs.append(f"// {os.path.basename(src)}: round {r} (hot-instance spill bytes {score})\n" + log)
+        logs.append(f"// {os.path.basename(src)}: round {r} (hot-instance spill bytes {score}, headline kernel {size} instructions)\n" + log)
         objs.append(obj)
     target = LIB if out is None else out
     tmp = target + f".tmp{os.getpid()}"
