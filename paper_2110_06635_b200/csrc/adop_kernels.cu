@@ -2357,18 +2357,7 @@ __device__ __forceinline__ bool ghost_point(const RasterArgs &a, const ViewDesc 
                                             int64_t idx, int nt, double *tt, float *g = nullptr) {
     const int C = CT > 0 ? CT : a.channels;
     float tau[CT > 0 ? CT : ADOP_MAX_CHANNELS];
-    if (CT > 0 && (CT & 3) == 0 && (reinterpret_cast<uintptr_t>(a.feat) & 15) == 0) {  // one 16-B load per 4 channels
-#pragma unroll
-        for (int c = 0; c < (CT > 0 ? CT : 4); c += 4) {
-            const float4 t = __ldg(reinterpret_cast<const float4 *>(a.feat + idx * C + c));
-            tau[c] = desc_lin(a, t.x);
-            tau[c + 1] = desc_lin(a, t.y);
-            tau[c + 2] = desc_lin(a, t.z);
-            tau[c + 3] = desc_lin(a, t.w);
-        }
-    } else {
-        for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + idx * C + c));  // linear space
-    }
+    for (int c = 0; c < C; ++c) tau[c] = desc_lin(a, __ldg(a.feat + idx * C + c));  // linear space
     float gu = 0.f, gv = 0.f;
     bool gc = false;
     for (int l = 0; l < nk; ++l) {
