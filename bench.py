@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--comm", choices=["nccl", "p2p"], default="nccl",
                     help="N > 1 point sharding: NCCL all-reduces of private pyramids, or every shard reducing "
                          "straight into rank 0's pyramid over peer memory (DESIGN.md section 8)")
+    ap.add_argument("--scatter", action="store_true",
+                    help="N > 1 point sharding (nccl): reduce-scatter accum/count (one packed collective per view) "
+                         "and resolve only this rank's pixel slice, instead of the SUM all-reduce (DESIGN.md section 8)")
     ap.add_argument("--keys32", action="store_true",
                     help="N > 1 point sharding (nccl): MIN-exchange only the 32-bit depth words (11 MB/view instead of "
                          "22 MB; the winner indices stay shard-local; DESIGN.md section 8)")
@@ -174,6 +177,12 @@ def run_ours(args, rank, world, local_rank):
             pyrs = [A.PeerPyramid(A.ipc_open(*k), A.ipc_open(*a), A.ipc_open(*c), q.image.data_ptr(), q.width,
                                   q.height, q.layers) for (k, a, c), q in zip(obj[0], own)]
 
+    rs_scratch = None
+    if world > 1 and args.scatter and not p2p:
+        from paper_2110_06635_b200 import parallel as PL
+        Pp = pyrs[0].count.numel()
+        rs_scratch = torch.empty(world * PL.pixel_chunk(Pp, world) * (C + 1), dtype=torch.float32, device=dev)
+
     calls = {}
 
     def cl(p):  # marshalled descriptors per points object, built once (no per-phase host marshalling)
@@ -230,12 +239,20 @@ def run_ours(args, rank, world, local_rank):
         A.forward_blend(pts_, cams, poses, ap, pyrs, ws, s, cl(pts_))
         if ev is not None:
             ev[3].record(s)
+        sl = None
         if world > 1:
-            for p in pyrs:
-                dist.all_reduce(p.ac, op=dist.ReduceOp.SUM)
+            from paper_2110_06635_b200 import parallel as PL
+            if args.scatter:
+                sl = PL.reduce_scatter_accum(pyrs, scratch=rs_scratch)
+            else:
+                for p in pyrs:
+                    dist.all_reduce(p.ac, op=dist.ReduceOp.SUM)
         if ev is not None:
             ev[4].record(s)
-        A.forward_resolve(pts_, cams, poses, ap, pyrs, ws, s, cl(pts_))
+        if sl is not None:
+            A.forward_resolve_range(pts_, cams, poses, ap, pyrs, ws, sl[0], sl[1], s, cl(pts_))
+        else:
+            A.forward_resolve(pts_, cams, poses, ap, pyrs, ws, s, cl(pts_))
         if ev is not None:
             ev[5].record(s)
 
@@ -326,6 +343,13 @@ def run_ours(args, rank, world, local_rank):
     culled_ms = cs.elapsed_time(ce) / args.steps
     culled_depth = statistics.mean(e[0].elapsed_time(e[1]) for e in cevs)
     pts.s.tile_bounds = None  # back to the full sweep for the e2e leg
+    nb_scatter = None
+    if world > 1 and args.scatter:  # each rank holds the global counts of its pixel slice only (collective)
+        from paper_2110_06635_b200 import parallel as PL
+        a_, b_ = PL.pixel_range(pyrs[0].count.numel(), world, rank)
+        nb = torch.tensor([float(sum(float(p.count[a_:b_].sum()) for p in pyrs))], device=dev)
+        dist.all_reduce(nb)
+        nb_scatter = int(nb.item())
     out = {}
     if rank == 0:
         P = A.pyramid_pixels(cams[0].width, cams[0].height, prm.layers)
@@ -334,7 +358,7 @@ def run_ours(args, rank, world, local_rank):
         #   keys 8 B per pixel written once (survivor records are this design's intermediate, not counted);
         #   frame: B_fwd = N (12 + 4) + N_blend 4C + P (8 + 4C + 4), N_blend = sum of the counts.
         alg = N * 16 + P * 8
-        n_blend = int(sum(float(p.count.sum()) for p in rd_pyrs))
+        n_blend = nb_scatter if nb_scatter is not None else int(sum(float(p.count.sum()) for p in rd_pyrs))
         alg_frame = N * 16 + n_blend * 4 * C + P * (8 + 4 * C + 4)
         peak, peak_src = peaks()
         achieved = alg / (depth_ms * 1e-3) / 1e9
@@ -346,7 +370,8 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": WORKLOAD, "points_per_gpu": N, "points_total": N * world, "channels": C,
                        "layers": prm.layers, "resolution": "1920x1080", "views": 1, "discard": True,
                        "gamma": prm.gamma, "alpha": prm.alpha,
-                       "parallelism": (f"point-sharded x{world} ({args.comm}{', 32-bit depth words' if args.keys32 else ''})"
+                       "parallelism": (f"point-sharded x{world} ({args.comm}{', 32-bit depth words' if args.keys32 else ''}"
+                                        f"{', reduce-scatter + slice resolve' if args.scatter else ''})"
                                        if world > 1 else "single GPU"),
                        "l2": "inputs (1.6 GB/GPU positions+radii) exceed the 126 MB L2; no flush needed",
                        "record_slots_per_frame": records, "record_overflow": overflow},

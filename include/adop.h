@@ -222,6 +222,17 @@ ADOP_API adop_status adop_forward_resolve(const adop_points *points, int32_t n_v
                                  const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
                                  void *workspace, size_t workspace_bytes, void *stream);
 
+/* Phase 3 over a pixel range (point sharding with a reduce-scatter, DESIGN.md section 8;
+ * SURVEY §8(e)): as adop_forward_resolve, but only pyramid pixels [p0, p1) of every
+ * view -- pixel p of the concatenated layers 0..L-1 (layout above) -- are normalized
+ * and written; the rest of the image is left untouched.  p1 is clipped to each view's
+ * pixel count.  After a reduce-scatter of accum and count, rank r resolves its own
+ * slice.  Ranges whose ends are multiples of 4 (or p1 >= P) take the vector path.
+ * Errors: ADOP_ERR_INVALID_ARGUMENT (p0 < 0 or p1 < p0), as adop_forward_resolve. */
+ADOP_API adop_status adop_forward_resolve_range(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                       const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                       int64_t p0, int64_t p1, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Phases 1-3 in order (single GPU). */
 ADOP_API adop_status adop_rasterize_forward(const adop_points *points, int32_t n_views, const adop_camera *cameras,
                                    const adop_pose *poses, const adop_params *params, const adop_pyramid *views,

@@ -5,7 +5,7 @@ for device memory and streams.  There is no CPU fallback: if libadop.so is
 missing or no CUDA device is present, the calls raise.
 
 Names follow the C-ABI without the `adop_` prefix:
-    pyramid_pixels, workspace_size, forward_depth, forward_blend, forward_resolve,
+    pyramid_pixels, workspace_size, forward_depth, forward_blend, forward_resolve, forward_resolve_range,
     rasterize_forward, rasterize_backward, point_masks, workspace_stats.
 """
 from __future__ import annotations
@@ -83,6 +83,8 @@ def lib():
         for name in ("adop_forward_depth", "adop_forward_blend", "adop_forward_resolve"):
             f = getattr(L, name)
             f.restype, f.argtypes = C.c_int, common
+        L.adop_forward_resolve_range.restype = C.c_int
+        L.adop_forward_resolve_range.argtypes = common[:6] + [C.c_int64, C.c_int64] + common[6:]
         L.adop_rasterize_forward.restype = C.c_int
         L.adop_rasterize_forward.argtypes = common[:-1] + [C.c_void_p, C.c_void_p]  # ..., comm, stream
         L.adop_rasterize_backward.restype = C.c_int
@@ -402,6 +404,13 @@ def forward_blend(points, cams, poses, params, pyrs, ws, stream=None, call=None)
 
 def forward_resolve(points, cams, poses, params, pyrs, ws, stream=None, call=None):
     _phase("adop_forward_resolve", points, cams, poses, params, pyrs, ws, stream, call)
+
+
+def forward_resolve_range(points, cams, poses, params, pyrs, ws, p0: int, p1: int, stream=None, call=None):
+    """Phase 3 over pyramid pixels [p0, p1) of every view (adop_forward_resolve_range)."""
+    c = _Call(points, cams, poses, params, pyrs) if call is None else call
+    _check(lib().adop_forward_resolve_range(C.byref(points.s), c.V, c.cams, c.poses, C.byref(params.s), c.pyrs,
+                                            int(p0), int(p1), ws.ptr, ws.nbytes, _stream(stream)))
 
 
 def rasterize_forward(points, cams, poses, params, pyrs, ws, stream=None, call=None, comm=None):

@@ -427,6 +427,8 @@ bool vec_path(const adop_points *pts) {
 void fill_args(RasterArgs &a, const adop_points *pts, int32_t n_views, const adop_camera *cams,
                const adop_pose *poses, const adop_params *pr, const adop_pyramid *views, const Ws *ws) {
     std::memset(&a, 0, sizeof(a));
+    a.res_p0 = 0;
+    a.res_p1 = INT64_MAX;  // adop_forward_resolve: every pixel
     a.x = pts->pos;
     a.y = pts->pos ? pts->pos + pts->pos_stride : nullptr;
     a.z = pts->pos ? pts->pos + 2 * pts->pos_stride : nullptr;
@@ -785,6 +787,23 @@ adop_status adop_forward_resolve(const adop_points *points, int32_t n_views, con
     if (s) return s;
     static thread_local RasterArgs a;
     fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    int e = launch_resolve(a, stream);
+    if (e) return cuda_status(e, "resolve launch");
+    return ok();
+}
+
+adop_status adop_forward_resolve_range(const adop_points *points, int32_t n_views, const adop_camera *cameras,
+                                       const adop_pose *poses, const adop_params *params, const adop_pyramid *views,
+                                       int64_t p0, int64_t p1, void *workspace, size_t workspace_bytes, void *stream) {
+    if (p0 < 0 || p1 < p0) return fail(ADOP_ERR_INVALID_ARGUMENT, "resolve range: need 0 <= p0 <= p1");
+    Ws ws;
+    adop_status s = prologue(points, n_views, cameras, poses, params, views, workspace, workspace_bytes, false, ws);
+    if (s) return s;
+    static thread_local RasterArgs a;
+    fill_args(a, points, n_views, cameras, poses, params, views, &ws);
+    a.res_p0 = p0;
+    a.res_p1 = p1;
+    if (p0 == p1) return ok();
     int e = launch_resolve(a, stream);
     if (e) return cuda_status(e, "resolve launch");
     return ok();

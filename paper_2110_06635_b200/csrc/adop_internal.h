@@ -152,6 +152,7 @@ struct RasterArgs {
     int32_t mv_lists;      // bit 0: the sweeps write per-view chunks (the blend walks them view-major);
                            // bit 1: the texture consumer walks them view-major too; bit 2: the ghost consumer
     int32_t ghost_fwd;     // the depth pass also lists the ghosts (back of the record region) for the backward
+    int64_t res_p0, res_p1;  // resolve only pyramid pixels [res_p0, res_p1) of every view (adop_forward_resolve_range)
 };
 constexpr int kListChunk = 64;  // record slots per chunk of the chunk table (a 64-aligned unit of every list)
 

@@ -1801,7 +1801,8 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
         // a pixel's accumulator is read only if its count is non-zero -- an empty pixel's 32-B sector is never
         // fetched (configs[1]: ~6% of the pixels are covered).  One view: loaded with the counts (L2 hits).
         const bool sparse = a.nviews > 1 && ADOP_RESOLVE_SPARSE;
-        for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < v.pixels / 4; g += stride) {
+        const int64_t g0 = a.res_p0 / 4, g1 = (a.res_p1 < v.pixels ? a.res_p1 : v.pixels) / 4;  // (range: multiples of 4)
+        for (int64_t g = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < g1; g += stride) {
             const int64_t p = 4 * g;
             int l = 0;
 #pragma unroll
@@ -1836,7 +1837,8 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
         }
         return;
     }
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < v.pixels; p += stride) {
+    const int64_t p1 = a.res_p1 < v.pixels ? a.res_p1 : v.pixels;
+    for (int64_t p = a.res_p0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < p1; p += stride) {
         int l = 0;
 #pragma unroll
         for (int k = 1; k < ADOP_MAX_LAYERS; ++k)
@@ -1857,7 +1859,8 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const __grid_constant__ Ra
             }
             continue;
         }
-        for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fdiv_rn(acc[c], cnt) : a.bg[c]);
+        const float inv = __frcp_rn(cnt);  // as the vector path: sum x (1/n), so any pixel range resolves identically
+        for (int c = 0; c < C; ++c) __stcs(img + c * hw, cnt > 0.0f ? __fmul_rn(acc[c], inv) : a.bg[c]);
     }
 }
 
@@ -2979,6 +2982,7 @@ int launch_resolve(const RasterArgs &a, void *stream) {
             if ((a.v[v].off[l] & 3) || (((int64_t)a.v[v].wl[l] * a.v[v].hl[l]) & 3)) v4 = false;
         if (a.v[v].pixels & 3) v4 = false;
     }
+    if ((a.res_p0 & 3) || ((a.res_p1 & 3) && a.res_p1 < maxP)) v4 = false;  // a range resolved 4 pixels at a time
     cudaStream_t s = (cudaStream_t)stream;
     if (a.env) {
         if (v4) k_resolve<true, true><<<grid, kThreads, 0, s>>>(a);

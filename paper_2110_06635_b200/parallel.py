@@ -77,6 +77,73 @@ def point_sharded_forward(phases, pyramids: Sequence, group=None, keys32: bool =
     phases.resolve()
 
 
+def pixel_chunk(P: int, world: int, align: int = 4) -> int:
+    """Pixels per rank of the reduce-scatter: ceil(P / world) rounded up to `align` (the resolve's vector width)."""
+    return max(align, -(-(-(-P // world)) // align) * align)
+
+
+def pixel_range(P: int, world: int, rank: int, align: int = 4) -> Tuple[int, int]:
+    """Slice [a, b) of a view's P pyramid pixels that `rank` receives and resolves (equal chunks of
+    pixel_chunk pixels; the last is shorter or empty)."""
+    c = pixel_chunk(P, world, align)
+    return min(P, rank * c), min(P, (rank + 1) * c)
+
+
+def reduce_scatter_accum(pyramids: Sequence, group=None, scratch=None) -> Tuple[int, int]:
+    """The SUM exchange of point_sharded_forward_rs: accum and count of every view packed rank-major
+    ([rank][accum slice | count slice]) and reduce-scattered in one collective per view; this rank's slice of
+    its own accum / count then holds the global sums.  Returns the rank's (a, b) pixel slice."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    P = pyramids[0].count.numel()
+    C = pyramids[0].accum.numel() // P
+    ch = pixel_chunk(P, world)
+    full = P // ch  # ranks whose slice is a whole chunk
+    a, b = pixel_range(P, world, rank)
+    for p in pyramids:
+        acc, cnt = p.accum, p.count
+        n = world * ch * (C + 1)
+        buf = torch.zeros(n, dtype=acc.dtype, device=acc.device) if scratch is None else scratch[:n]
+        if scratch is not None:
+            buf.zero_()
+        rows = buf.view(world, ch * (C + 1))
+        if full:
+            rows[:full, : ch * C].copy_(acc[: full * ch * C].view(full, ch * C))
+            rows[:full, ch * C:].copy_(cnt[: full * ch].view(full, ch))
+        if full < world and full * ch < P:  # the short last slice
+            t = P - full * ch
+            rows[full, : t * C].copy_(acc[full * ch * C:])
+            rows[full, ch * C: ch * C + t].copy_(cnt[full * ch:])
+        out = torch.empty(ch * (C + 1), dtype=acc.dtype, device=acc.device)
+        dist.reduce_scatter_tensor(out, buf, op=dist.ReduceOp.SUM, group=group)
+        if a < b:
+            acc[a * C: b * C].copy_(out[: (b - a) * C])
+            cnt[a:b].copy_(out[ch * C: ch * C + (b - a)])
+    return a, b
+
+
+def point_sharded_forward_rs(phases, pyramids: Sequence, group=None, keys32: bool = False, scratch=None):
+    """Point sharding with a reduce-scatter instead of the SUM all-reduce (SURVEY §8(e)): phases.depth();
+    MIN(keys); phases.blend(); accum and count are packed rank-major ([rank][accum slice | count slice], one
+    copy per part) and reduce-scattered in ONE collective -- (G-1)/G of the all-reduce's bus traffic -- so rank
+    r holds the sums of its pixel slice (pixel_range); phases.resolve_range(a_r, b_r) writes that slice of the
+    image, which stays distributed by pixel slice.  Forward only: outside its slice a rank's accum / count
+    are its shard's partial sums (like the peer-memory mode's non-owners, it must not run a backward).
+
+    pyramids: objects with `.keys`, `.accum` ([P * C] view) and `.count` ([P] view) per view.
+    scratch: optional flat buffer of >= world * pixel_chunk(P, world) * (C + 1) elements (allocated if None).
+    Returns this rank's (a, b) pixel slice."""
+    phases.depth()
+    for p in pyramids:
+        if keys32:
+            min_depth_words(p.keys, group)
+        else:
+            dist.all_reduce(p.keys, op=dist.ReduceOp.MIN, group=group)
+    phases.blend()
+    a, b = reduce_scatter_accum(pyramids, group, scratch)
+    phases.resolve_range(a, b)
+    return a, b
+
+
 def point_sharded_backward(phases, d_pose: torch.Tensor, group=None):
     """Per-shard backward against the reduced pyramid; point gradients stay with their shard, the
     per-view pose gradient is the sum over shards."""
@@ -175,6 +242,11 @@ class CudaPhases:
         from . import adop as A
         r = self.r
         A.forward_resolve(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, call=r._call())
+
+    def resolve_range(self, p0: int, p1: int):
+        from . import adop as A
+        r = self.r
+        A.forward_resolve_range(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, p0, p1, call=r._call())
 
     def clear(self):
         from . import adop as A

@@ -160,3 +160,17 @@ def test_comm_arguments_rejected_without_a_gpu():
     assert A.lib().adop_comm_init(1, 0, uid, 7, 0, C.byref(p)) == 1
     assert A.lib().adop_comm_init(1, 0, uid, 0, 4, C.byref(p)) == 1
     assert A.lib().adop_comm_destroy(None) == 0
+
+
+def test_resolve_range_rejects_bad_ranges_before_launch():
+    """adop_forward_resolve_range: p0 < 0 or p1 < p0 is an invalid argument (checked before any device work)."""
+    pts, cams, poses, prm, pyrs = _valid()
+    V = 1
+    ca = (A.adop_camera * V)(*[A.camera_struct(c) for c in cams])
+    pa = (A.adop_pose * V)(*[A.pose_struct(p) for p in poses])
+    py = (A.adop_pyramid * V)(*pyrs)
+    for p0, p1 in ((-4, 8), (16, 8)):
+        st = A.lib().adop_forward_resolve_range(C.byref(pts), V, ca, pa, C.byref(prm), py, p0, p1,
+                                                C.c_void_p(256 * 1024), 1 << 30, None)
+        assert st == 1, st
+        assert "resolve range" in A.lib().adop_last_error().decode()

@@ -213,6 +213,91 @@ def test_phase_split_point_sharding_on_one_gpu():
         torch.testing.assert_close(pyrs0[v].image, full.pyrs[v].image, rtol=1e-5, atol=1e-6)
 
 
+def _image_idx(width, height, layers, C, p0, p1, device):
+    """Indices into the planar layer-concatenated image of pyramid pixels [p0, p1) (include/adop.h layout)."""
+    out, off = [], 0
+    for l in range(layers):
+        wl, hl = -(-width // (1 << l)), -(-height // (1 << l))
+        hw = wl * hl
+        a, b = max(p0, off), min(p1, off + hw)
+        if a < b:
+            for c in range(C):
+                out.append(torch.arange(C * off + c * hw + (a - off), C * off + c * hw + (b - off), device=device))
+        off += hw
+    return torch.cat(out) if out else torch.empty(0, dtype=torch.int64, device=device)
+
+
+def test_resolve_range_matches_full_resolve():
+    """adop_forward_resolve_range: the vector path (ends at multiples of 4), the scalar path (odd ends) and the
+    empty range write exactly the full resolve's values on their pixels and leave the rest untouched."""
+    w = S.workload(1, n=120_000, n_views=2)
+    r = run_gpu(w.cloud, w.cameras, w.poses, w.params)
+    cam, L, C = w.cameras[0], w.params.layers, w.cloud.channels
+    P = r.pyrs[0].count.numel()
+    full = [p.image.clone() for p in r.pyrs]
+    for p0, p1 in ((0, P), (4, 2_000_004), (7, 1_234_567), (P - 5, P + 100), (11, 11)):
+        for p in r.pyrs:
+            p.image.fill_(-7.0)
+        A.forward_resolve_range(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, p0, p1)
+        torch.cuda.synchronize()
+        idx = _image_idx(cam.width, cam.height, L, C, p0, min(p1, P), r.pyrs[0].image.device)
+        for v in range(2):
+            img = r.pyrs[v].image
+            assert torch.equal(img[idx], full[v][idx]), (p0, p1)
+            mask = torch.ones_like(img, dtype=torch.bool)
+            mask[idx] = False
+            assert bool((img[mask] == -7.0).all()), (p0, p1)
+    with pytest.raises(RuntimeError):
+        A.forward_resolve_range(r.points, r.cams, r.poses, r.params, r.pyrs, r.ws, 10, 5)
+
+
+def test_reduce_scatter_point_sharding_on_one_gpu():
+    """Point sharding with a reduce-scatter (parallel.point_sharded_forward_rs, §8e) on one GPU: 3 shards,
+    keys min-combined, each shard r receives the sums of ITS pixel slice only and resolves it with
+    adop_forward_resolve_range; the slices together equal the unsharded forward (counts exact, image within
+    the fp32 summation tolerance)."""
+    from paper_2110_06635_b200 import parallel as PL
+    w = S.workload(1, n=120_000, n_views=2)
+    dev = torch.device("cuda")
+    cloud = w.cloud.to(dev)
+    C = cloud.channels
+    ap = A.Params(w.params, C)
+    full = A.Renderer(cloud, w.cameras, w.poses, w.params)
+    full.forward()
+    bounds = [0, 37_001, 80_000, cloud.n]
+    G = len(bounds) - 1
+    shards = []
+    for a, b in zip(bounds, bounds[1:]):
+        pts = A.Points.from_cloud(cloud.slice(a, b), global_offset=a)
+        pyrs = A.alloc_pyramids(w.cameras, w.params.layers, C, dev)
+        ws = A.Workspace(pts, w.cameras, ap, dev)
+        A.forward_depth(pts, w.cameras, w.poses, ap, pyrs, ws)
+        shards.append((pts, pyrs, ws))
+    for v in range(2):
+        kmin = torch.stack([s[1][v].keys for s in shards]).amin(0)
+        for s in shards:
+            s[1][v].keys.copy_(kmin)
+    for pts, pyrs, ws in shards:
+        A.forward_blend(pts, w.cameras, w.poses, ap, pyrs, ws)
+    P = shards[0][1][0].count.numel()
+    ranges = [PL.pixel_range(P, G, r) for r in range(G)]
+    for v in range(2):  # the reduce to rank r of slice r (accum and count), as the NCCL reduces do
+        for r, (a, b) in enumerate(ranges):
+            shards[r][1][v].accum[a * C:b * C] = torch.stack([s[1][v].accum[a * C:b * C] for s in shards]).sum(0)
+            shards[r][1][v].count[a:b] = torch.stack([s[1][v].count[a:b] for s in shards]).sum(0)
+    for r, (a, b) in enumerate(ranges):
+        pts, pyrs, ws = shards[r]
+        A.forward_resolve_range(pts, w.cameras, w.poses, ap, pyrs, ws, a, b)
+    torch.cuda.synchronize()
+    cam = w.cameras[0]
+    assert ranges[0][0] == 0 and ranges[-1][1] == P and all(a % 4 == 0 for a, _ in ranges)
+    for r, (a, b) in enumerate(ranges):
+        idx = _image_idx(cam.width, cam.height, w.params.layers, C, a, b, dev)
+        for v in range(2):
+            assert torch.equal(shards[r][1][v].count[a:b], full.pyrs[v].count[a:b])
+            torch.testing.assert_close(shards[r][1][v].image[idx], full.pyrs[v].image[idx], rtol=1e-5, atol=1e-6)
+
+
 def test_view_id_base_matches_per_view_calls():
     """beta is keyed by the global view id: rendering views 2..3 of a batch alone (view_id_base=2)
     gives the same pyramids as the 4-view call (view sharding)."""

@@ -25,6 +25,14 @@ class _Pyr:
         self.ac = torch.zeros(P * (C + 1), dtype=torch.float64)
         self.image = torch.zeros(C * P, dtype=torch.float64)
 
+    @property
+    def accum(self):
+        return self.ac[: self.P * self.C]
+
+    @property
+    def count(self):
+        return self.ac[self.P * self.C:]
+
 
 class OraclePhases:
     """Oracle phase functions behind the CudaPhases interface (test stand-in for the GPU)."""
@@ -59,6 +67,15 @@ class OraclePhases:
         for v, p in enumerate(self.pyrs):
             p.image.copy_(torch.from_numpy(img[v]))
 
+    def resolve_range(self, p0, p1):
+        """The oracle resolves every pixel; only the image entries of pyramid pixels [p0, p1) are written (what
+        adop_forward_resolve_range leaves touched)."""
+        acc, cnt = self._ac()
+        img = O.forward_resolve(self.cams, self.prm, self.C, acc, cnt, self.prm.background)
+        idx = _image_indices(self.cams[0], self.prm.layers, self.C, p0, p1)
+        for v, p in enumerate(self.pyrs):
+            p.image[idx] = torch.from_numpy(img[v][idx.numpy()])
+
     def forward(self):
         self.depth()
         self.blend()
@@ -71,6 +88,19 @@ class OraclePhases:
         self.d_feat.copy_(torch.from_numpy(b.dtau))
         self.d_pos.copy_(torch.from_numpy(b.dx))
         self.d_pose.copy_(torch.from_numpy(b.dpose))
+
+
+def _image_indices(cam, layers, C, p0, p1):
+    """Indices into the planar layer-concatenated image of pyramid pixels [p0, p1) (layout of include/adop.h)."""
+    out, off = [], 0
+    for l in range(layers):
+        w, h = -(-cam.width // 2 ** l), -(-cam.height // 2 ** l)  # ceil (oracle layer_w)
+        hw = w * h
+        a, b = max(p0, off), min(p1, off + hw)
+        for c in range(C):
+            out.append(np.arange(C * off + c * hw + (a - off), C * off + c * hw + (b - off)) if a < b else [])
+        off += hw
+    return torch.from_numpy(np.concatenate([np.asarray(x, dtype=np.int64) for x in out]))
 
 
 def _scene():
@@ -95,6 +125,19 @@ def _point_sharded(rank, world, port, q, keys32=False):
     if rank == 0:
         q.put(([p.keys.numpy().copy() for p in pyrs], [p.ac.numpy().copy() for p in pyrs],
                [p.image.numpy().copy() for p in pyrs]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _point_sharded_rs(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    cloud, cams, poses, prm = _scene()
+    a, b = PL.shard_range(cloud.n, world, rank, align=256)
+    pts = O.Points.from_cloud(cloud.slice(a, b), global_offset=a)
+    P = O.pyramid_pixels(96, 64, prm.layers)
+    pyrs = [_Pyr(P, 3) for _ in cams]
+    p0, p1 = PL.point_sharded_forward_rs(OraclePhases(pts, cams, poses, prm, pyrs), pyrs)
+    q.put((rank, p0, p1, [p.count[p0:p1].numpy().copy() for p in pyrs], [p.image.numpy().copy() for p in pyrs]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -133,14 +176,14 @@ def _free_port():
     return p
 
 
-def _spawn(fn, world=2):
+def _spawn(fn, world=2, nres=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=fn, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
+    res = q.get(timeout=300) if nres == 1 else [q.get(timeout=300) for _ in range(nres)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
@@ -169,6 +212,22 @@ def test_point_sharded_forward_gloo_ws2_equals_unsharded():
         assert np.array_equal(keys[v].view(np.uint64), fwd.keys[v])
         assert np.array_equal(ac[v][P * 3:], fwd.count[v])
         np.testing.assert_allclose(image[v], fwd.image[v], rtol=1e-12, atol=1e-12)
+    assert fwd.count.sum() > 500
+
+
+def test_point_sharded_forward_reduce_scatter_gloo_ws2():
+    """Reduce-scatter variant: each rank's pixel slice of counts and image equals the unsharded
+    forward's; the slices partition the pyramid."""
+    res = sorted(_spawn(_point_sharded_rs, nres=2), key=lambda r: r[0])
+    cloud, cams, poses, prm = _scene()
+    fwd = O.forward(O.Points.from_cloud(cloud), cams, poses, prm)
+    P = fwd.count.shape[1]
+    assert res[0][1] == 0 and res[0][2] == res[1][1] and res[1][2] == P and res[0][1] < res[0][2] < P
+    for rank, p0, p1, counts, images in res:
+        idx = _image_indices(cams[0], prm.layers, 3, p0, p1).numpy()
+        for v in range(len(cams)):
+            assert np.array_equal(counts[v], fwd.count[v][p0:p1])
+            np.testing.assert_allclose(images[v][idx], fwd.image[v][idx], rtol=1e-12, atol=1e-12)
     assert fwd.count.sum() > 500
 
 
