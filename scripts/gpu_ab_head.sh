@@ -9,7 +9,7 @@ for order in "$*" "$REV" "$*"; do
 import json
 for l in open('gpurun_out/head_$v.log'):
     if l.startswith('{'):
-        d=json.loads(l); p=d['phases_ms']; print('$v', round(d['ms_per_step'],4), 'median', round(d['ms_per_step_stats']['median'],4), 'depth', round(p['depth'],4), 'frac', round(d['roofline']['frac'],4))" >> gpurun_out/ab_head.txt
+        d=json.loads(l); p=d['phases_ms']; print('$v', round(d['ms_per_step'],4), 'median', round(d['ms_per_step_stats']['median'],4), 'depth', round(p['depth'],4), 'blend', round(p['blend'],4), 'frac', round(d['roofline']['frac'],4))" >> gpurun_out/ab_head.txt
   done
 done
 echo done >> gpurun_out/ab_head.txt
