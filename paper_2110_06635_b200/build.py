@@ -40,9 +40,9 @@ SPLIT = int(os.environ.get("ADOP_SPLIT", "16"))  # 0: no -split-compile
 # depth sweep and the ghost consumer (configs[4] forward +6%), or 2984 instructions, 0.324 ms, with none;
 # profiles/r02/evolution.md).  The hot TU is compiled with two partition counts per round; the copy with the
 # fewest hot-instance spill bytes is kept, ties broken by the shorter headline kernel.
-SPLIT_COPIES = ((16, 12), (8, 32), (20, 24))
+SPLIT_COPIES = ((16, 12), (8, 32), (20, 24), (10, 14))
 HEADLINE = "_ZN4adop12k_depth_poolILi0ELi0ELb1ELb0ELi11EEEvNS_10RasterArgsE"
-ROUNDS = 3
+ROUNDS = 4
 SPILL_OK = 300  # every hot instance within its limit (an instance over its limit adds 100000)
 HOT = {  # hot instances -> accepted spill-store bytes (tests/test_build_spills.py checks the kept build)
     "_ZN4adop12k_depth_poolILi0ELi0ELb1ELb0ELi11EEEvNS_10RasterArgsE": 0,   # configs[3] headline depth sweep
